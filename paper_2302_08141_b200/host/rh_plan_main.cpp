@@ -1,0 +1,183 @@
+// rh_plan — plan a program with the UNCHANGED reference planner and emit the lowered program.
+//
+// This is the `parashard plan` path (proj/tools/parashard_main.cpp:56-125: LoadGraph -> plan)
+// with RunPlan's tail replaced by strategy recovery + lowering (rh_lower.h).  The output JSON
+// ("rhino-lowered/1") is what the executor consumes through the C-ABI (include/rhino_exec.h).
+//
+//   rh_plan (--text F | --json F | --fixture family:layers:hidden:batch)
+//           [--devices N | --machines M --gpus G] [--equal-bw] [--ilp-time-limit S]
+//           [--random-choice SEED --mesh d0[,d1]] [--dtype f32|bf16] [--name NAME]
+//           [--plan-out PLAN.json] -o OUT.json
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <iostream>
+#include <random>
+#include <sstream>
+#include <string>
+
+#include "nlohmann/json.hpp"
+#include "parashard/fixtures.h"
+#include "parashard/parser.h"
+#include "parashard/planner.h"
+#include "rh_lower.h"
+
+using namespace parashard;
+using json = nlohmann::ordered_json;
+
+namespace {
+
+std::string ReadFile(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw std::runtime_error("cannot read " + path);
+  std::stringstream ss;
+  ss << in.rdbuf();
+  return ss.str();
+}
+
+std::vector<int> ParseInts(const std::string& s, char sep) {
+  std::vector<int> out;
+  std::stringstream ss(s);
+  std::string tok;
+  while (std::getline(ss, tok, sep)) out.push_back(std::stoi(tok));
+  return out;
+}
+
+// Random but legal partitioned program: per axis, a uniformly random candidate per op from
+// generate_candidates (proj/src/sharding.cpp:405-491); later axes see the composed shapes
+// (EffectiveShapes, :390-403) exactly as the planner's searches do.
+rhino::LoweredProgram RandomChoice(const TensorProgram& g, const std::vector<int>& mesh,
+                                   uint64_t seed) {
+  std::mt19937_64 rng(seed);
+  std::vector<std::vector<AxisSpec>> chosen;
+  std::vector<int> chosen_d;
+  std::vector<std::vector<OpStrategy>> strat(mesh.size(), std::vector<OpStrategy>(g.size()));
+  for (size_t axis = 0; axis < mesh.size(); ++axis) {
+    int d = mesh[axis];
+    auto shapes = EffectiveShapes(g, chosen, chosen_d);
+    CandidateMap cand = generate_candidates(g, shapes, d, 0.0, static_cast<int>(axis));
+    std::vector<AxisSpec> specs(g.size());
+    for (int i = 0; i < g.size(); ++i) {
+      const auto& c = cand[i];
+      strat[axis][i] = c[rng() % c.size()];
+      specs[i] = strat[axis][i].output_spec;
+    }
+    chosen.push_back(specs);
+    chosen_d.push_back(d);
+  }
+  return rhino::StrategiesFromChoice(g, mesh, chosen, strat);
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  std::string text_path, json_path, fixture, out_path, plan_out, name, dtype = "f32", mesh_s;
+  int devices = 0, machines = 0, gpus = 0;
+  bool equal_bw = false;
+  long long random_seed = -1;
+  double ilp_limit = 60.0;
+  for (int i = 1; i < argc; ++i) {
+    std::string a = argv[i];
+    auto next = [&]() -> std::string {
+      if (i + 1 >= argc) throw std::runtime_error("missing value for " + a);
+      return argv[++i];
+    };
+    if (a == "--text") text_path = next();
+    else if (a == "--json") json_path = next();
+    else if (a == "--fixture") fixture = next();
+    else if (a == "--devices") devices = std::stoi(next());
+    else if (a == "--machines") machines = std::stoi(next());
+    else if (a == "--gpus") gpus = std::stoi(next());
+    else if (a == "--equal-bw") equal_bw = true;
+    else if (a == "--ilp-time-limit") ilp_limit = std::stod(next());
+    else if (a == "--random-choice") random_seed = std::stoll(next());
+    else if (a == "--mesh") mesh_s = next();
+    else if (a == "--dtype") dtype = next();
+    else if (a == "--name") name = next();
+    else if (a == "--plan-out") plan_out = next();
+    else if (a == "-o") out_path = next();
+    else {
+      std::cerr << "unknown argument " << a << "\n";
+      return 2;
+    }
+  }
+  try {
+    TensorProgram g;
+    if (!text_path.empty()) {
+      g = parse_program(ReadFile(text_path));
+    } else if (!json_path.empty()) {
+      g = ParseProgramJson(ReadFile(json_path));
+    } else if (!fixture.empty()) {
+      std::stringstream ss(fixture);
+      FixtureSpec fs;
+      std::string tok;
+      std::getline(ss, fs.family, ':');
+      std::getline(ss, tok, ':');
+      fs.layers = std::stoi(tok);
+      std::getline(ss, tok, ':');
+      fs.hidden = std::stoi(tok);
+      std::getline(ss, tok, ':');
+      fs.batch = std::stoi(tok);
+      g = generate(fs);
+    } else {
+      throw std::runtime_error("one of --text/--json/--fixture is required");
+    }
+    if (name.empty()) name = fixture.empty() ? (text_path.empty() ? json_path : text_path) : fixture;
+
+    rhino::LoweredProgram lp;
+    json extra;
+    auto t0 = std::chrono::steady_clock::now();
+    if (random_seed >= 0) {
+      lp = RandomChoice(g, ParseInts(mesh_s, ','), static_cast<uint64_t>(random_seed));
+    } else {
+      ClusterConfig cluster;
+      if (devices > 0) {
+        cluster.machines = 1;
+        cluster.gpus_per_machine = devices;
+      } else {
+        cluster.machines = machines > 0 ? machines : 1;
+        cluster.gpus_per_machine = gpus > 0 ? gpus : 1;
+      }
+      if (equal_bw) {
+        cluster.inter_bandwidth = cluster.intra_bandwidth;
+        cluster.inter_alpha = cluster.intra_alpha;
+      }
+      PlanOptions opts;
+      opts.pipeline_stages = -1;  // SPMD plans (pipeline execution is SURVEY §8f-1)
+      opts.ilp_time_limit = ilp_limit;
+      ExecutionPlan p = plan(g, cluster, opts);
+      auto t1 = std::chrono::steady_clock::now();
+      lp = rhino::RecoverStrategies(g, p, opts);
+      extra["plan_seconds"] = std::chrono::duration<double>(t1 - t0).count();
+      extra["cost_report"] = {{"communication_bytes", p.cost.communication_bytes},
+                              {"communication_seconds", p.cost.communication_seconds},
+                              {"computation_seconds", p.cost.computation_seconds},
+                              {"collective_counts", p.cost.collective_counts}};
+      json sh = json::array();
+      for (const auto& axis : p.sharding) {
+        json a = json::array();
+        for (const auto& s : axis) a.push_back(s.ToString());
+        sh.push_back(a);
+      }
+      extra["plan_sharding"] = sh;
+      if (!plan_out.empty()) {
+        std::ofstream(plan_out) << PlanToJsonText(p, g);
+      }
+    }
+    json j = json::parse(rhino::LoweredToJson(g, lp, name, dtype));
+    for (auto it = extra.begin(); it != extra.end(); ++it) j[it.key()] = it.value();
+    std::string text = j.dump(1) + "\n";
+    if (out_path.empty()) {
+      std::cout << text;
+    } else {
+      std::ofstream(out_path) << text;
+    }
+    std::cerr << "rh_plan: " << name << " mesh=" << json(lp.mesh).dump() << " ops=" << g.size()
+              << " descriptor=" << lp.descriptor << "\n";
+  } catch (const std::exception& e) {
+    std::cerr << "rh_plan: error: " << e.what() << "\n";
+    return 1;
+  }
+  return 0;
+}
