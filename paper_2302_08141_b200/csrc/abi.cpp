@@ -1,0 +1,768 @@
+// abi.cpp — the extern "C" entry points of include/rhino_exec.h: runtime / mesh creation,
+// program load (lowering + symmetric arena + CUDA-IPC peer mapping), execution, timing and
+// host I/O.  No C++ exception crosses this boundary.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "executor.h"
+
+namespace rh {
+void LowerProgram(rh_program* p);
+}
+
+using rh::Fail;
+
+namespace {
+
+thread_local std::string g_err;
+
+#define RH_NCCL(x)                                                                        \
+  do {                                                                                    \
+    ncclResult_t r_ = (x);                                                                \
+    if (r_ != ncclSuccess)                                                                \
+      ::rh::Fail(std::string("NCCL: ") + ncclGetErrorString(r_) + " (" #x ")", RH_ERR_NCCL); \
+  } while (0)
+
+template <typename F>
+int Guard(F&& f) {
+  try {
+    f();
+    return RH_OK;
+  } catch (const rh::Error& e) {
+    g_err = e.what();
+    return e.status;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RH_ERR_INVALID;
+  }
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (dev != prev) RH_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int64_t Prod(const Dims& d) {
+  int64_t n = 1;
+  for (auto x : d) n *= x;
+  return n;
+}
+
+rh::ComposedMap MakeComposed(const rh_program* p, const rh::Tensor& t, int global_rank) {
+  rh::ComposedMap m{};
+  m.nd = static_cast<int>(t.gdims.size());
+  for (int k = 0; k < m.nd; ++k) {
+    m.gdims[k] = t.gdims[k];
+    m.ldims[k] = t.ldims[k];
+  }
+  const std::vector<int> c = p->mesh->Coords(global_rank);
+  for (int a = 0; a < p->n_axes; ++a) {
+    if (t.specs[a].kind != RH_SHARD) continue;
+    auto& x = m.ax[m.nshard++];
+    x.dim = t.specs[a].dim;
+    x.d = p->mesh->dims[a];
+    x.stride = t.specs[a].stride;
+    x.coord = c[a];
+  }
+  return m;
+}
+
+bool SameStream(const rh_runtime* rt) { return rt->streams.size() == 1; }
+
+// Cross-rank ordering around a transition that reads peer buffers.
+void GroupSync(rh_program* p, int axis) {
+  rh_runtime* rt = p->mesh->rt;
+  if (rt->dist) {
+    if (rt->world == 1) return;
+    const int g = rt->first_rank;
+    const std::vector<int> members = p->mesh->Group(axis, g);
+    rh::BarrierArgs b{};
+    b.d = static_cast<int>(members.size());
+    for (int k = 0; k < b.d; ++k) {
+      b.members[k] = members[k];
+      b.peer_flags[k] = reinterpret_cast<uint32_t*>(p->peer_base[members[k]] + p->flags_off);
+    }
+    b.my_flags = reinterpret_cast<uint32_t*>(p->base[0] + p->flags_off);
+    b.counter = reinterpret_cast<uint32_t*>(p->base[0] + p->counter_off);
+    b.me = g;
+    rh::LaunchBarrier(b, rt->streams[0]);
+    return;
+  }
+  if (SameStream(rt)) return;  // emulated ranks on one GPU share one in-order stream
+  // Several GPUs in one process: join every stream (events).
+  std::vector<cudaEvent_t> ev(rt->streams.size());
+  for (size_t i = 0; i < rt->streams.size(); ++i) {
+    DeviceGuard dg(rt->devs[i]);
+    RH_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    RH_CUDA(cudaEventRecord(ev[i], rt->streams[i]));
+  }
+  for (size_t i = 0; i < rt->streams.size(); ++i) {
+    DeviceGuard dg(rt->devs[i]);
+    for (size_t j = 0; j < ev.size(); ++j)
+      if (i != j) RH_CUDA(cudaStreamWaitEvent(rt->streams[i], ev[j], 0));
+  }
+  for (auto e : ev) cudaEventDestroy(e);
+}
+
+// One run of the schedule.  `prof` (optional): event pairs around every step on local rank 0's
+// stream.
+int64_t RunOnce(rh_program* p, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* prof) {
+  rh_runtime* rt = p->mesh->rt;
+  int64_t launches = 0;
+  const bool multi_dev = rt->devs.size() > 1;
+  for (size_t si = 0; si < p->steps.size(); ++si) {
+    rh::Step& st = p->steps[si];
+    if (prof) RH_CUDA(cudaEventRecord((*prof)[si].first, rt->streams[0]));
+    if (st.p2p) GroupSync(p, st.axis);
+    for (int li = 0; li < rt->n_local(); ++li) {
+      if (multi_dev) RH_CUDA(cudaSetDevice(rt->device_of(li)));
+      launches += st.run(li, rt->stream_of(li));
+    }
+    if (st.p2p) GroupSync(p, st.axis);
+    if (prof) RH_CUDA(cudaEventRecord((*prof)[si].second, rt->streams[0]));
+  }
+  if (multi_dev) RH_CUDA(cudaSetDevice(rt->devs[0]));
+  return launches;
+}
+
+void SyncAll(rh_runtime* rt) {
+  for (size_t i = 0; i < rt->streams.size(); ++i) {
+    DeviceGuard dg(rt->devs[i]);
+    RH_CUDA(cudaStreamSynchronize(rt->streams[i]));
+  }
+}
+
+// Host-side barrier over the world communicator (dist) — used around setup only.
+void HostBarrier(rh_runtime* rt) {
+  if (!rt->dist || rt->world == 1) return;
+  float* buf = nullptr;
+  RH_CUDA(cudaMalloc(&buf, 4));
+  RH_NCCL(ncclAllReduce(buf, buf, 1, ncclFloat32, ncclSum, rt->world_comm, rt->streams[0]));
+  RH_CUDA(cudaStreamSynchronize(rt->streams[0]));
+  cudaFree(buf);
+}
+
+void Allocate(rh_program* p) {
+  rh_runtime* rt = p->mesh->rt;
+  const size_t bytes = std::max<size_t>(p->arena_bytes, 256);
+  p->base.assign(rt->n_local(), nullptr);
+  for (int li = 0; li < rt->n_local(); ++li) {
+    DeviceGuard dg(rt->device_of(li));
+    void* ptr = nullptr;
+    RH_CUDA(cudaMalloc(&ptr, bytes));
+    RH_CUDA(cudaMemset(ptr, 0, bytes));
+    p->base[li] = static_cast<char*>(ptr);
+    p->owned.push_back(ptr);
+  }
+  p->peer_base.assign(rt->world, nullptr);
+  if (!rt->dist) {
+    for (int li = 0; li < rt->n_local(); ++li) p->peer_base[rt->first_rank + li] = p->base[li];
+    return;
+  }
+  p->peer_base[rt->first_rank] = p->base[0];
+  if (rt->world == 1) return;
+  // Exchange CUDA IPC handles of the symmetric arenas over the world communicator.
+  cudaIpcMemHandle_t mine;
+  RH_CUDA(cudaIpcGetMemHandle(&mine, p->base[0]));
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  char* dev = nullptr;
+  RH_CUDA(cudaMalloc(&dev, hb * (rt->world + 1)));
+  RH_CUDA(cudaMemcpy(dev + hb * rt->world, &mine, hb, cudaMemcpyHostToDevice));
+  RH_NCCL(ncclAllGather(dev + hb * rt->world, dev, hb, ncclChar, rt->world_comm, rt->streams[0]));
+  RH_CUDA(cudaStreamSynchronize(rt->streams[0]));
+  std::vector<cudaIpcMemHandle_t> all(rt->world);
+  RH_CUDA(cudaMemcpy(all.data(), dev, hb * rt->world, cudaMemcpyDeviceToHost));
+  cudaFree(dev);
+  for (int r = 0; r < rt->world; ++r) {
+    if (r == rt->first_rank) continue;
+    void* ptr = nullptr;
+    RH_CUDA(cudaIpcOpenMemHandle(&ptr, all[r], cudaIpcMemLazyEnablePeerAccess));
+    p->peer_base[r] = static_cast<char*>(ptr);
+  }
+  p->ipc_opened = true;
+  HostBarrier(rt);  // every arena zeroed (flags included) before any barrier kernel runs
+}
+
+void DestroyProgram(rh_program* p) {
+  if (!p) return;
+  rh_runtime* rt = p->mesh->rt;
+  try {
+    SyncAll(rt);
+  } catch (...) {
+  }
+  if (p->ipc_opened) {
+    HostBarrier(rt);
+    for (int r = 0; r < rt->world; ++r)
+      if (r != rt->first_rank && p->peer_base[r]) cudaIpcCloseMemHandle(p->peer_base[r]);
+  }
+  for (int li = 0; li < rt->n_local() && li < static_cast<int>(p->owned.size()); ++li) {
+    DeviceGuard dg(rt->device_of(li));
+    cudaFree(p->owned[li]);
+  }
+  delete p;
+}
+
+// Host full tensor -> every local rank's buffer of tensor t (H2D staging + slice kernel).
+void WriteFull(rh_program* p, const rh::Tensor& t, const void* src, size_t bytes,
+               std::vector<void*>* stage_cache) {
+  rh_runtime* rt = p->mesh->rt;
+  for (int li = 0; li < rt->n_local(); ++li) {
+    DeviceGuard dg(rt->device_of(li));
+    cudaStream_t s = rt->stream_of(li);
+    const int g = rt->first_rank + li;
+    bool all_rep = true;
+    for (auto& sp : t.specs) all_rep = all_rep && sp.kind == RH_REPLICATED;
+    if (all_rep) {
+      RH_CUDA(cudaMemcpyAsync(p->base[li] + t.offset, src, bytes, cudaMemcpyHostToDevice, s));
+      continue;
+    }
+    void* stage = nullptr;
+    if (stage_cache && static_cast<int>(stage_cache->size()) > li && (*stage_cache)[li]) {
+      stage = (*stage_cache)[li];
+    } else {
+      RH_CUDA(cudaMallocAsync(&stage, bytes, s));
+    }
+    RH_CUDA(cudaMemcpyAsync(stage, src, bytes, cudaMemcpyHostToDevice, s));
+    bool partial_zero = false;
+    const std::vector<int> c = p->mesh->Coords(g);
+    for (int a = 0; a < p->n_axes; ++a)
+      if (t.specs[a].kind == RH_PARTIAL && c[a] != 0) partial_zero = true;
+    if (partial_zero) {
+      rh::LaunchZero(p->base[li] + t.offset, t.bytes, s);
+    } else {
+      rh::LaunchSliceComposed(p->base[li] + t.offset, stage, MakeComposed(p, t, g), t.elems(),
+                              t.dtype, s);
+    }
+    if (!(stage_cache && static_cast<int>(stage_cache->size()) > li && (*stage_cache)[li]))
+      RH_CUDA(cudaFreeAsync(stage, s));
+  }
+}
+
+uint16_t F2Bf(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u && (u & 0x7fffffu)) return static_cast<uint16_t>((u | 0x400000u) >> 16);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+float Bf2F(uint16_t x) {
+  uint32_t u = static_cast<uint32_t>(x) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rh_last_error(void) { return g_err.c_str(); }
+const char* rh_version(void) { return "rhino-b200 0.1 (sm_100a)"; }
+
+int rh_get_unique_id(uint8_t uid[RH_UID_BYTES]) {
+  return Guard([&] {
+    static_assert(sizeof(ncclUniqueId) == RH_UID_BYTES, "uid size");
+    ncclUniqueId id;
+    RH_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(uid, &id, RH_UID_BYTES);
+  });
+}
+
+int rh_runtime_create(int n_ranks, const int* cuda_ids, rh_runtime** out) {
+  return Guard([&] {
+    if (n_ranks < 1) Fail("rh_runtime_create: n_ranks must be >= 1");
+    auto rt = std::make_unique<rh_runtime>();
+    rt->world = n_ranks;
+    rt->dist = false;
+    for (int i = 0; i < n_ranks; ++i) {
+      auto it = std::find(rt->devs.begin(), rt->devs.end(), cuda_ids[i]);
+      if (it == rt->devs.end()) {
+        rt->devs.push_back(cuda_ids[i]);
+        rt->rank_dev.push_back(static_cast<int>(rt->devs.size()) - 1);
+      } else {
+        rt->rank_dev.push_back(static_cast<int>(it - rt->devs.begin()));
+      }
+    }
+    for (int dev : rt->devs) {
+      DeviceGuard dg(dev);
+      cudaStream_t s;
+      RH_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      rt->streams.push_back(s);
+      for (int other : rt->devs) {
+        if (other == dev) continue;
+        int ok = 0;
+        RH_CUDA(cudaDeviceCanAccessPeer(&ok, dev, other));
+        if (!ok) Fail("rh_runtime_create: no peer access between devices");
+        cudaError_t e = cudaDeviceEnablePeerAccess(other, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) RH_CUDA(e);
+        cudaGetLastError();
+      }
+    }
+    RH_CUDA(cudaSetDevice(rt->devs[0]));
+    *out = rt.release();
+  });
+}
+
+int rh_runtime_create_dist(int world, int rank, int cuda_id, const uint8_t uid[RH_UID_BYTES],
+                           rh_runtime** out) {
+  return Guard([&] {
+    if (world < 1 || rank < 0 || rank >= world) Fail("rh_runtime_create_dist: bad world/rank");
+    auto rt = std::make_unique<rh_runtime>();
+    rt->world = world;
+    rt->dist = true;
+    rt->first_rank = rank;
+    rt->devs = {cuda_id};
+    rt->rank_dev = {0};
+    RH_CUDA(cudaSetDevice(cuda_id));
+    cudaStream_t s;
+    RH_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    rt->streams = {s};
+    ncclUniqueId id;
+    std::memcpy(&id, uid, RH_UID_BYTES);
+    RH_NCCL(ncclCommInitRank(&rt->world_comm, world, id, rank));
+    *out = rt.release();
+  });
+}
+
+int rh_runtime_world(const rh_runtime* rt, int* world, int* first_local_rank, int* n_local) {
+  return Guard([&] {
+    *world = rt->world;
+    *first_local_rank = rt->first_rank;
+    *n_local = rt->n_local();
+  });
+}
+
+void rh_runtime_destroy(rh_runtime* rt) {
+  if (!rt) return;
+  for (size_t i = 0; i < rt->streams.size(); ++i) {
+    cudaSetDevice(rt->devs[i]);
+    cudaStreamSynchronize(rt->streams[i]);
+    cudaStreamDestroy(rt->streams[i]);
+  }
+  if (rt->world_comm) ncclCommDestroy(rt->world_comm);
+  delete rt;
+}
+
+int rh_mesh_create(rh_runtime* rt, int n_axes, const int* dims, rh_mesh** out) {
+  return Guard([&] {
+    if (n_axes < 1 || n_axes > RH_MAX_AXES) Fail("rh_mesh_create: 1..4 axes");
+    auto m = std::make_unique<rh_mesh>();
+    m->rt = rt;
+    m->dims.assign(dims, dims + n_axes);
+    int64_t prod = 1;
+    for (int d : m->dims) {
+      if (d < 1 || d > rh::kMaxGroup) Fail("rh_mesh_create: axis size must be 1..8");
+      prod *= d;
+    }
+    if (prod != rt->world) Fail("rh_mesh_create: prod(dims) != world size");
+    if (rt->dist) {
+      const std::vector<int> c = m->Coords(rt->first_rank);
+      for (int a = 0; a < n_axes; ++a) {
+        int color = 0;
+        for (int b = 0; b < n_axes; ++b)
+          if (b != a) color = color * m->dims[b] + c[b];
+        ncclComm_t comm = nullptr;
+        RH_NCCL(ncclCommSplit(rt->world_comm, color, c[a], &comm, nullptr));
+        m->axis_comm.push_back(comm);
+      }
+    }
+    *out = m.release();
+  });
+}
+
+void rh_mesh_destroy(rh_mesh* mesh) {
+  if (!mesh) return;
+  for (auto c : mesh->axis_comm)
+    if (c) ncclCommDestroy(c);
+  delete mesh;
+}
+
+int rh_program_load(rh_mesh* mesh, const rh_op* ops, int n_ops, const int* outputs, int n_out,
+                    uint32_t flags, rh_program** out) {
+  rh_program* raw = nullptr;
+  int rc = Guard([&] {
+    auto p = std::make_unique<rh_program>();
+    p->mesh = mesh;
+    p->flags = flags;
+    p->n_axes = static_cast<int>(mesh->dims.size());
+    p->ops.assign(ops, ops + n_ops);
+    p->inputs.resize(n_ops);
+    p->in_specs.resize(n_ops);
+    p->out_specs.resize(n_ops);
+    for (int i = 0; i < n_ops; ++i) {
+      const rh_op& op = ops[i];
+      if (op.rank < 1 || op.rank > RH_MAX_RANK) Fail("op " + std::to_string(i) + ": bad rank");
+      if (op.dtype != RH_F32 && op.dtype != RH_BF16) Fail("op " + std::to_string(i) + ": bad dtype");
+      p->inputs[i].assign(op.inputs, op.inputs + op.n_in);
+      for (int s : p->inputs[i])
+        if (s < 0 || s >= n_ops) Fail("op " + std::to_string(i) + ": bad input index");
+      p->out_specs[i].assign(op.out_spec, op.out_spec + p->n_axes);
+      p->in_specs[i].assign(op.n_in, Specs(p->n_axes));
+      for (int a = 0; a < p->n_axes; ++a)
+        for (int s = 0; s < op.n_in; ++s) p->in_specs[i][s][a] = op.in_specs[a * op.n_in + s];
+      p->ops[i].inputs = nullptr;
+      p->ops[i].in_specs = nullptr;
+    }
+    p->outputs.assign(outputs, outputs + n_out);
+    // Kahn order with index tie-break (ops are pure: any topological order gives the same
+    // values; the reference's own order is TopoOrderIndices, proj/src/ir.cpp:381-412).
+    std::vector<int> indeg(n_ops, 0);
+    std::vector<std::vector<int>> cons(n_ops);
+    for (int i = 0; i < n_ops; ++i)
+      for (int s : p->inputs[i]) {
+        ++indeg[i];
+        cons[s].push_back(i);
+      }
+    std::vector<int> q;
+    for (int i = 0; i < n_ops; ++i)
+      if (!indeg[i]) q.push_back(i);
+    for (size_t h = 0; h < q.size(); ++h)
+      for (int c : cons[q[h]])
+        if (--indeg[c] == 0) q.push_back(c);
+    if (static_cast<int>(q.size()) != n_ops) Fail("program has a cycle");
+    p->order = q;
+    rh::LowerProgram(p.get());
+    Allocate(p.get());
+    raw = p.release();
+  });
+  if (rc == RH_OK) *out = raw;
+  return rc;
+}
+
+void rh_program_destroy(rh_program* prog) { DestroyProgram(prog); }
+
+int rh_program_init_synthetic(rh_program* p, uint64_t seed) {
+  return Guard([&] {
+    rh_runtime* rt = p->mesh->rt;
+    for (size_t i = 0; i < p->ops.size(); ++i) {
+      const rh_op& op = p->ops[i];
+      if (op.kind != RH_OP_PARAMETER && op.kind != RH_OP_INPUT) continue;
+      const rh::Tensor& t = p->tensors[p->out_tensor[i]];
+      const float scale = op.kind == RH_OP_PARAMETER
+                              ? static_cast<float>(std::sqrt(3.0 / static_cast<double>(op.dims[0])))
+                              : 1.0f;
+      for (int li = 0; li < rt->n_local(); ++li) {
+        DeviceGuard dg(rt->device_of(li));
+        const int g = rt->first_rank + li;
+        bool zero = false;
+        const std::vector<int> c = p->mesh->Coords(g);
+        for (int a = 0; a < p->n_axes; ++a)
+          if (t.specs[a].kind == RH_PARTIAL && c[a] != 0) zero = true;
+        if (zero) {
+          rh::LaunchZero(p->base[li] + t.offset, t.bytes, rt->stream_of(li));
+        } else {
+          rh::LaunchSynthetic(p->base[li] + t.offset, MakeComposed(p, t, g), t.elems(), seed,
+                              static_cast<uint32_t>(i), scale, t.dtype, rt->stream_of(li));
+        }
+      }
+    }
+    SyncAll(rt);
+  });
+}
+
+int rh_program_write_full(rh_program* p, int op, const void* src, size_t bytes) {
+  return Guard([&] {
+    if (op < 0 || op >= static_cast<int>(p->ops.size())) Fail("bad op index");
+    if (p->ops[op].kind != RH_OP_PARAMETER && p->ops[op].kind != RH_OP_INPUT)
+      Fail("rh_program_write_full: op is not a source");
+    const rh::Tensor& t = p->tensors[p->out_tensor[op]];
+    if (bytes != static_cast<size_t>(Prod(t.gdims)) * rh::ElemBytes(t.dtype)) Fail("size mismatch");
+    WriteFull(p, t, src, bytes, nullptr);
+    SyncAll(p->mesh->rt);
+  });
+}
+
+int rh_program_run(rh_program* p, int iters, double* ms_per_iter) {
+  return Guard([&] {
+    rh_runtime* rt = p->mesh->rt;
+    SyncAll(rt);
+    std::vector<cudaEvent_t> ev0(rt->streams.size()), ev1(rt->streams.size());
+    for (size_t i = 0; i < rt->streams.size(); ++i) {
+      DeviceGuard dg(rt->devs[i]);
+      RH_CUDA(cudaEventCreate(&ev0[i]));
+      RH_CUDA(cudaEventCreate(&ev1[i]));
+      RH_CUDA(cudaEventRecord(ev0[i], rt->streams[i]));
+    }
+    for (int it = 0; it < iters; ++it) RunOnce(p, nullptr);
+    float worst = 0;
+    for (size_t i = 0; i < rt->streams.size(); ++i) {
+      DeviceGuard dg(rt->devs[i]);
+      RH_CUDA(cudaEventRecord(ev1[i], rt->streams[i]));
+      RH_CUDA(cudaEventSynchronize(ev1[i]));
+      float ms = 0;
+      RH_CUDA(cudaEventElapsedTime(&ms, ev0[i], ev1[i]));
+      worst = std::max(worst, ms);
+      cudaEventDestroy(ev0[i]);
+      cudaEventDestroy(ev1[i]);
+    }
+    if (ms_per_iter) *ms_per_iter = iters > 0 ? worst / iters : 0.0;
+  });
+}
+
+int rh_program_profile(rh_program* p, int iters, double* ms_per_iter) {
+  return Guard([&] {
+    rh_runtime* rt = p->mesh->rt;
+    SyncAll(rt);
+    DeviceGuard dg(rt->devs[0]);
+    const size_t n = p->steps.size();
+    std::vector<double> acc(n, 0.0);
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev(n);
+    for (auto& e : ev) {
+      RH_CUDA(cudaEventCreate(&e.first));
+      RH_CUDA(cudaEventCreate(&e.second));
+    }
+    cudaEvent_t t0, t1;
+    RH_CUDA(cudaEventCreate(&t0));
+    RH_CUDA(cudaEventCreate(&t1));
+    double total = 0;
+    for (int it = 0; it < iters; ++it) {
+      RH_CUDA(cudaEventRecord(t0, rt->streams[0]));
+      RunOnce(p, &ev);
+      RH_CUDA(cudaEventRecord(t1, rt->streams[0]));
+      RH_CUDA(cudaEventSynchronize(t1));
+      SyncAll(rt);
+      for (size_t i = 0; i < n; ++i) {
+        float ms = 0;
+        RH_CUDA(cudaEventElapsedTime(&ms, ev[i].first, ev[i].second));
+        acc[i] += ms;
+      }
+      float ms = 0;
+      RH_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+      total += ms;
+    }
+    for (size_t i = 0; i < n; ++i) p->steps[i].ms = iters > 0 ? acc[i] / iters : 0.0;
+    for (auto& e : ev) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    if (ms_per_iter) *ms_per_iter = iters > 0 ? total / iters : 0.0;
+  });
+}
+
+int rh_program_step_host(rh_program* p, int n_in, const int* in_ops, const void* const* in_ptrs,
+                         int n_outs, void* const* out_ptrs, double* ms) {
+  return Guard([&] {
+    rh_runtime* rt = p->mesh->rt;
+    SyncAll(rt);
+    DeviceGuard dg(rt->devs[0]);
+    cudaEvent_t e0, e1;
+    RH_CUDA(cudaEventCreate(&e0));
+    RH_CUDA(cudaEventCreate(&e1));
+    RH_CUDA(cudaEventRecord(e0, rt->streams[0]));
+    auto h0 = std::chrono::steady_clock::now();
+    for (int k = 0; k < n_in; ++k) {
+      const int op = in_ops[k];
+      const rh::Tensor& t = p->tensors[p->out_tensor[op]];
+      WriteFull(p, t, in_ptrs[k], static_cast<size_t>(Prod(t.gdims)) * rh::ElemBytes(t.dtype), nullptr);
+    }
+    RunOnce(p, nullptr);
+    if (n_outs > static_cast<int>(p->outputs.size())) Fail("too many output buffers");
+    for (int k = 0; k < n_outs; ++k) {
+      const int op = p->outputs[k];
+      const int ti = p->mat_tensor[op] >= 0 ? p->mat_tensor[op] : -1;
+      if (ti < 0) Fail("output not materialized (RH_FLAG_NO_MATERIALIZE)");
+      const rh::Tensor& t = p->tensors[ti];
+      RH_CUDA(cudaMemcpyAsync(out_ptrs[k], p->base[0] + t.offset, t.bytes, cudaMemcpyDeviceToHost,
+                              rt->streams[0]));
+    }
+    RH_CUDA(cudaEventRecord(e1, rt->streams[0]));
+    SyncAll(rt);
+    RH_CUDA(cudaEventSynchronize(e1));
+    float dev_ms = 0;
+    RH_CUDA(cudaEventElapsedTime(&dev_ms, e0, e1));
+    const double host_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (ms) *ms = std::max<double>(dev_ms, host_ms);
+  });
+}
+
+int rh_program_local_bytes(const rh_program* p, int op, int rank, size_t* bytes) {
+  return Guard([&] {
+    (void)rank;
+    if (op < 0 || op >= static_cast<int>(p->ops.size())) Fail("bad op index");
+    if (p->out_tensor[op] < 0) Fail("op was fused into its consumer's kernel (use RH_FLAG_NO_FUSION)");
+    *bytes = p->tensors[p->out_tensor[op]].bytes;
+  });
+}
+
+int rh_program_read_local(rh_program* p, int op, int rank, void* dst, size_t bytes) {
+  return Guard([&] {
+    if (op < 0 || op >= static_cast<int>(p->ops.size())) Fail("bad op index");
+    if (p->out_tensor[op] < 0) Fail("op was fused into its consumer's kernel (use RH_FLAG_NO_FUSION)");
+    const rh::Tensor& t = p->tensors[p->out_tensor[op]];
+    if (bytes != t.bytes) Fail("rh_program_read_local: size mismatch");
+    const int li = p->LocalIndex(rank);
+    SyncAll(p->mesh->rt);
+    DeviceGuard dg(p->mesh->rt->device_of(li));
+    RH_CUDA(cudaMemcpy(dst, p->base[li] + t.offset, bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
+int rh_program_read_full(rh_program* p, int op, void* dst, size_t bytes) {
+  return Guard([&] {
+    if (op < 0 || op >= static_cast<int>(p->ops.size())) Fail("bad op index");
+    rh_runtime* rt = p->mesh->rt;
+    SyncAll(rt);
+    const int dtype = p->ops[op].dtype;
+    const int eb = rh::ElemBytes(dtype);
+    Dims g(p->ops[op].dims, p->ops[op].dims + p->ops[op].rank);
+    const int64_t n = Prod(g);
+    if (bytes != static_cast<size_t>(n) * eb) Fail("rh_program_read_full: size mismatch");
+    if (p->mat_tensor[op] >= 0) {
+      const rh::Tensor& t = p->tensors[p->mat_tensor[op]];
+      DeviceGuard dg(rt->device_of(0));
+      RH_CUDA(cudaMemcpy(dst, p->base[0] + t.offset, bytes, cudaMemcpyDeviceToHost));
+      return;
+    }
+    if (p->out_tensor[op] < 0) Fail("op was fused into its consumer's kernel (use RH_FLAG_NO_FUSION)");
+    if (rt->n_local() != rt->world) Fail("rh_program_read_full: non-output op needs every rank local");
+    const rh::Tensor& t = p->tensors[p->out_tensor[op]];
+    std::vector<float> full(n, 0.0f);
+    bool any_partial = false;
+    for (auto& s : t.specs) any_partial = any_partial || s.kind == RH_PARTIAL;
+    std::vector<char> loc(t.bytes);
+    for (int r = 0; r < rt->world; ++r) {
+      const std::vector<int> c = p->mesh->Coords(r);
+      bool skip = false, first = true;
+      for (int a = 0; a < p->n_axes; ++a) {
+        if (t.specs[a].kind == RH_REPLICATED && c[a] != 0) skip = true;
+        if (t.specs[a].kind == RH_PARTIAL && c[a] != 0) first = false;
+      }
+      if (skip) continue;
+      {
+        DeviceGuard dg(rt->device_of(r));
+        RH_CUDA(cudaMemcpy(loc.data(), p->base[r] + t.offset, t.bytes, cudaMemcpyDeviceToHost));
+      }
+      const rh::ComposedMap m = MakeComposed(p, t, r);
+      for (int64_t l = 0; l < t.elems(); ++l) {
+        const int64_t f = rh::ComposedLocalToGlobal(m, l);
+        float v;
+        if (eb == 4) std::memcpy(&v, &loc[l * 4], 4);
+        else {
+          uint16_t h;
+          std::memcpy(&h, &loc[l * 2], 2);
+          v = Bf2F(h);
+        }
+        full[f] = first ? v : full[f] + v;
+      }
+    }
+    if (eb == 4) {
+      std::memcpy(dst, full.data(), bytes);
+    } else {
+      uint16_t* o = static_cast<uint16_t*>(dst);
+      for (int64_t i = 0; i < n; ++i) o[i] = F2Bf(full[i]);
+    }
+    (void)any_partial;
+  });
+}
+
+int rh_program_num_steps(const rh_program* p, int* n) {
+  return Guard([&] { *n = static_cast<int>(p->steps.size()); });
+}
+
+int rh_program_step_info(const rh_program* p, int i, rh_step_info* out) {
+  return Guard([&] {
+    if (i < 0 || i >= static_cast<int>(p->steps.size())) Fail("bad step index");
+    const rh::Step& s = p->steps[i];
+    std::memset(out, 0, sizeof(*out));
+    std::strncpy(out->name, s.name.c_str(), sizeof(out->name) - 1);
+    out->kind = s.kind;
+    out->launches = s.launches;
+    out->alg_bytes = s.alg_bytes;
+    out->alg_flops = s.alg_flops;
+    out->wire_bytes = s.wire_bytes;
+    out->ms = s.ms;
+  });
+}
+
+int rh_program_launch_count(const rh_program* p, int64_t* launches) {
+  return Guard([&] {
+    int64_t n = 0;
+    for (const auto& s : p->steps) n += static_cast<int64_t>(s.launches) * p->mesh->rt->n_local();
+    for (const auto& s : p->steps)
+      if (s.p2p && p->mesh->rt->dist && p->mesh->rt->world > 1) n += 2;  // group barriers
+    *launches = n;
+  });
+}
+
+int rh_reshard(rh_mesh* mesh, int axis, rh_spec from, rh_spec to, int ndim, const int64_t* dims,
+               int dtype, void* const* src, void* const* dst, uint32_t flags, int iters, double* ms) {
+  return Guard([&] {
+    if (axis < 0 || axis >= static_cast<int>(mesh->dims.size())) Fail("rh_reshard: bad axis");
+    if (from.kind == RH_PARTIAL && to.kind == RH_PARTIAL) Fail("rh_reshard: identity");
+    const int na = static_cast<int>(mesh->dims.size());
+    // Program: x = input (spec `from` on `axis`, Replicated elsewhere) -> y = identity(x) with
+    // input demanded in `to`.  Only the transition step is timed.
+    std::vector<rh_spec> xs(na, rh_spec{RH_REPLICATED, -1, 0}), ys = xs;
+    xs[axis] = from;
+    ys[axis] = to;
+    rh_op ops[2];
+    std::memset(ops, 0, sizeof(ops));
+    int32_t in0[1] = {0};
+    for (int k = 0; k < 2; ++k) {
+      ops[k].dtype = dtype;
+      ops[k].rank = ndim;
+      for (int i = 0; i < ndim; ++i) ops[k].dims[i] = dims[i];
+    }
+    ops[0].kind = RH_OP_INPUT;
+    for (int a = 0; a < na; ++a) ops[0].out_spec[a] = xs[a];
+    ops[1].kind = RH_OP_UNARY;
+    ops[1].fn = RH_FN_IDENTITY;
+    ops[1].n_in = 1;
+    ops[1].inputs = in0;
+    for (int a = 0; a < na; ++a) ops[1].out_spec[a] = ys[a];
+    ops[1].in_specs = ys.data();
+    int outs[1] = {1};
+    rh_program* p = nullptr;
+    int rc = rh_program_load(mesh, ops, 2, outs, 1, flags | RH_FLAG_NO_MATERIALIZE, &p);
+    if (rc != RH_OK) throw rh::Error(rc, g_err);
+    std::unique_ptr<rh_program, void (*)(rh_program*)> guard(p, DestroyProgram);
+    rh_runtime* rt = mesh->rt;
+    const rh::Tensor& x = p->tensors[p->out_tensor[0]];
+    int ti = -1;  // the transition's destination tensor
+    for (size_t k = 0; k < p->tensors.size(); ++k)
+      if (p->tensors[k].op == 0 && k != static_cast<size_t>(p->out_tensor[0])) ti = static_cast<int>(k);
+    if (ti < 0) Fail("rh_reshard: no transition was scheduled");
+    const rh::Tensor& y = p->tensors[ti];
+    for (int li = 0; li < rt->n_local(); ++li) {
+      DeviceGuard dg(rt->device_of(li));
+      RH_CUDA(cudaMemcpy(p->base[li] + x.offset, src[li], x.bytes, cudaMemcpyDeviceToDevice));
+    }
+    HostBarrier(rt);
+    // warm-up, then time the transition steps only
+    p->steps.erase(std::remove_if(p->steps.begin(), p->steps.end(),
+                                  [](const rh::Step& s) { return s.kind != rh::Step::kTransition; }),
+                   p->steps.end());
+    RunOnce(p, nullptr);
+    SyncAll(rt);
+    HostBarrier(rt);
+    double t = 0;
+    rc = rh_program_run(p, std::max(iters, 1), &t);
+    if (rc != RH_OK) throw rh::Error(rc, g_err);
+    for (int li = 0; li < rt->n_local(); ++li) {
+      DeviceGuard dg(rt->device_of(li));
+      RH_CUDA(cudaMemcpy(dst[li], p->base[li] + y.offset, y.bytes, cudaMemcpyDeviceToDevice));
+    }
+    if (ms) *ms = t;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,704 @@
+// executor.cpp — lowering a partitioned program (rh_op records) into a static schedule of
+// sm_100a kernels and resharding transitions, and running it.
+//
+// Semantics followed (reference files):
+//   local-op rules          proj/src/sharding.cpp:225-388 (FollowInput / ProduceOutput)
+//   pin fallback            proj/src/sharding.cpp:477-487 (compute replicated, then slice)
+//   transitions             proj/src/sharding.cpp:104-142 (reshard_cost's collective table)
+//   axis composition        proj/src/sharding.cpp:390-403 (EffectiveShapes)
+//   reshape pass-through    proj/src/sharding.cpp:144-160 (metadata only: buffers alias)
+//   per-edge transitions    proj/src/spmd.cpp:1033-1045 (CollectStrategyStats' edge loop)
+#include "executor.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <sstream>
+
+using rh::Fail;
+using rh::Step;
+using rh::Tensor;
+
+std::vector<int> rh_mesh::Coords(int rank) const {
+  std::vector<int> c(dims.size());
+  for (int a = static_cast<int>(dims.size()) - 1; a >= 0; --a) {
+    c[a] = rank % dims[a];
+    rank /= dims[a];
+  }
+  return c;
+}
+
+std::vector<int> rh_mesh::Group(int axis, int rank) const {
+  std::vector<int> c = Coords(rank);
+  std::vector<int> out;
+  for (int k = 0; k < dims[axis]; ++k) {
+    c[axis] = k;
+    int r = 0;
+    for (size_t a = 0; a < dims.size(); ++a) r = r * dims[a] + c[a];
+    out.push_back(r);
+  }
+  return out;
+}
+
+int rh_program::LocalIndex(int global_rank) const {
+  int li = global_rank - mesh->rt->first_rank;
+  if (li < 0 || li >= mesh->rt->n_local()) Fail("rank " + std::to_string(global_rank) + " is not local");
+  return li;
+}
+
+namespace rh {
+namespace {
+
+int64_t Prod(const Dims& d) {
+  int64_t n = 1;
+  for (auto x : d) n *= x;
+  return n;
+}
+int64_t Inner(const Dims& d, int dim) {
+  int64_t n = 1;
+  for (size_t i = dim + 1; i < d.size(); ++i) n *= d[i];
+  return n;
+}
+bool SpecEq(const rh_spec& a, const rh_spec& b) {
+  if (a.kind != b.kind) return false;
+  return a.kind != RH_SHARD || (a.dim == b.dim && a.stride == b.stride);
+}
+bool SpecsEq(const Specs& a, const Specs& b) {
+  for (size_t i = 0; i < a.size(); ++i)
+    if (!SpecEq(a[i], b[i])) return false;
+  return true;
+}
+std::string SpecStr(const rh_spec& s) {
+  if (s.kind == RH_REPLICATED) return "R";
+  if (s.kind == RH_PARTIAL) return "P";
+  return "S(" + std::to_string(s.dim) + "," + std::to_string(s.stride) + ")";
+}
+std::string SpecsStr(const Specs& s) {
+  std::string k;
+  for (size_t i = 0; i < s.size(); ++i) k += (i ? "," : "") + SpecStr(s[i]);
+  return k;
+}
+rh_spec Rep() { return rh_spec{RH_REPLICATED, -1, 0}; }
+rh_spec Par() { return rh_spec{RH_PARTIAL, -1, 0}; }
+rh_spec Sh(int dim, int64_t s) { return rh_spec{RH_SHARD, dim, s}; }
+
+// SpecValidForShape (sharding.cpp:47-53)
+bool Valid(const rh_spec& s, const Dims& d, int n) {
+  if (s.kind != RH_SHARD) return true;
+  if (s.dim < 0 || s.dim >= static_cast<int>(d.size()) || s.stride < 1) return false;
+  return d[s.dim] % (n * s.stride) == 0;
+}
+
+Dims LocalDims(const Dims& g, const Specs& specs, const std::vector<int>& mesh, size_t upto) {
+  Dims l = g;
+  for (size_t a = 0; a < upto && a < specs.size(); ++a)
+    if (specs[a].kind == RH_SHARD) l[specs[a].dim] /= mesh[a];
+  return l;
+}
+
+bool Passthrough(const Dims& in, const Dims& out, const rh_spec& s, int d, rh_spec* res) {
+  if (s.kind == RH_REPLICATED) {
+    *res = s;
+    return true;
+  }
+  if (s.kind == RH_PARTIAL || !Valid(s, in, d)) return false;
+  const int64_t run = Inner(in, s.dim) * s.stride;
+  for (int dim = 0; dim < static_cast<int>(out.size()); ++dim) {
+    const int64_t inner = Inner(out, dim);
+    if (run % inner != 0) continue;
+    rh_spec c = Sh(dim, run / inner);
+    if (Valid(c, out, d)) {
+      *res = c;
+      return true;
+    }
+  }
+  return false;
+}
+
+std::vector<int> EffPerm(const rh_op& op, int rank) {
+  std::vector<int> p(rank);
+  for (int i = 0; i < rank; ++i) p[i] = op.has_perm ? op.perm[i] : rank - 1 - i;
+  return p;
+}
+
+const char* KindName(int k) {
+  static const char* names[] = {"param", "input", "matmul", "add", "mul", "unary",
+                                "reshape", "transpose", "reduce_sum", "broadcast", "concat"};
+  return (k >= 0 && k <= 10) ? names[k] : "?";
+}
+
+// The output spec (one mesh axis) the local computation produces from the given input specs.
+rh_spec Natural(const rh_op& op, const std::vector<rh_spec>& in, const std::vector<Dims>& in_dims,
+                const Dims& out_dims, int d) {
+  auto bad = [&]() -> rh_spec {
+    std::string m = std::string("no local rule for ") + KindName(op.kind) + " with inputs";
+    for (auto& s : in) m += " " + SpecStr(s);
+    Fail(m);
+  };
+  bool all_rep = true;
+  for (auto& s : in) all_rep = all_rep && s.kind == RH_REPLICATED;
+  if (all_rep) return Rep();
+  for (auto& s : in)
+    if (s.kind == RH_PARTIAL) bad();
+  switch (op.kind) {
+    case RH_OP_MATMUL: {  // MatMulLayout (sharding.cpp:202-212) + rules :277-292, :376-384
+      const int a_m = op.transpose_a ? 1 : 0, a_k = 1 - a_m;
+      const int b_k = op.transpose_b ? 1 : 0, b_n = 1 - b_k;
+      const rh_spec &A = in[0], &B = in[1];
+      if (A.kind == RH_SHARD && A.dim == a_m && B.kind == RH_REPLICATED) return Sh(0, A.stride);
+      if (A.kind == RH_REPLICATED && B.kind == RH_SHARD && B.dim == b_n) return Sh(1, B.stride);
+      if (A.kind == RH_SHARD && B.kind == RH_SHARD && A.dim == a_k && B.dim == b_k &&
+          A.stride == B.stride)
+        return Par();
+      return bad();
+    }
+    case RH_OP_ADD:
+    case RH_OP_MUL:
+      if (SpecEq(in[0], in[1])) return in[0];
+      return bad();
+    case RH_OP_UNARY:
+      if (op.fn == RH_FN_SOFTMAX && in[0].dim == static_cast<int>(out_dims.size()) - 1)
+        Fail("softmax over a sharded last dim is not executable as a local op");
+      return in[0];
+    case RH_OP_RESHAPE: {
+      rh_spec r;
+      if (!Passthrough(in_dims[0], out_dims, in[0], d, &r)) Fail("reshape without a pass-through spec");
+      return r;
+    }
+    case RH_OP_TRANSPOSE: {
+      auto perm = EffPerm(op, static_cast<int>(in_dims[0].size()));
+      for (size_t p = 0; p < perm.size(); ++p)
+        if (perm[p] == in[0].dim) return Sh(static_cast<int>(p), in[0].stride);
+      return bad();
+    }
+    case RH_OP_REDUCE_SUM:
+      if (in[0].dim == op.axis) return Par();
+      return Sh(in[0].dim - (in[0].dim > op.axis ? 1 : 0), in[0].stride);
+    case RH_OP_BROADCAST:
+      return Sh(in[0].dim + static_cast<int>(out_dims.size() - in_dims[0].size()), in[0].stride);
+    case RH_OP_CONCAT:
+      for (auto& s : in)
+        if (!SpecEq(s, in[0]) || s.dim == op.axis) bad();
+      return in[0];
+    default:
+      return bad();
+  }
+}
+
+// Reshard wire bytes of one single-axis transition (sharding.cpp:113-135).
+double WireBytes(const rh_spec& from, const rh_spec& to, double S, int d) {
+  const double frac = static_cast<double>(d - 1) / d;
+  if (from.kind == RH_PARTIAL) return to.kind == RH_REPLICATED ? 2.0 * frac * S : frac * S;
+  if (from.kind == RH_SHARD) {
+    if (to.kind == RH_SHARD) return S / d * frac;
+    return frac * S;
+  }
+  return 0.0;
+}
+
+const char* CollectiveName(const rh_spec& from, const rh_spec& to) {
+  if (from.kind == RH_PARTIAL) return to.kind == RH_REPLICATED ? "all_reduce" : "reduce_scatter";
+  if (from.kind == RH_SHARD) return to.kind == RH_SHARD ? "all_to_all" : "all_gather";
+  return to.kind == RH_PARTIAL ? "zero_fill" : "slice";
+}
+
+ncclDataType_t NcclType(int dtype) { return dtype == RH_BF16 ? ncclBfloat16 : ncclFloat32; }
+
+#define RH_NCCL(x)                                                                        \
+  do {                                                                                    \
+    ncclResult_t r_ = (x);                                                                \
+    if (r_ != ncclSuccess)                                                                \
+      ::rh::Fail(std::string("NCCL: ") + ncclGetErrorString(r_) + " (" #x ")", RH_ERR_NCCL); \
+  } while (0)
+
+class Lowerer {
+ public:
+  explicit Lowerer(rh_program* p) : p_(p), mesh_(p->mesh->dims), rt_(p->mesh->rt) {}
+
+  void Lower() {
+    const int n = static_cast<int>(p_->ops.size());
+    p_->out_tensor.assign(n, -1);
+    p_->mat_tensor.assign(n, -1);
+    // flags + barrier counter live at the front of the arena
+    p_->flags_off = Alloc(static_cast<size_t>(rt_->world) * 4);
+    p_->counter_off = Alloc(4);
+    ValidateSpecs();
+    PlanFusion();
+    for (int i : p_->order) {
+      const rh_op& op = p_->ops[i];
+      if (op.kind == RH_OP_PARAMETER || op.kind == RH_OP_INPUT) {
+        p_->out_tensor[i] = NewTensor(i, p_->out_specs[i]);
+        continue;
+      }
+      if (absorbed_[i]) continue;  // computed by its chain head's kernel
+      EmitOp(i);
+    }
+    if (!(p_->flags & RH_FLAG_NO_MATERIALIZE)) {
+      for (int o : p_->outputs) {
+        Specs rep(p_->n_axes, Rep());
+        p_->mat_tensor[o] = GetTensor(o, rep, "materialize");
+      }
+    }
+    p_->arena_bytes = arena_;
+  }
+
+ private:
+  size_t Alloc(size_t bytes) {
+    const size_t off = arena_;
+    arena_ += (bytes + 255) / 256 * 256;
+    return off;
+  }
+
+  Dims GDims(int i) const { return Dims(p_->ops[i].dims, p_->ops[i].dims + p_->ops[i].rank); }
+
+  int NewTensor(int op, const Specs& specs, bool alloc = true) {
+    Tensor t;
+    t.op = op;
+    t.specs = specs;
+    t.gdims = GDims(op);
+    t.ldims = LocalDims(t.gdims, specs, mesh_, specs.size());
+    t.dtype = p_->ops[op].dtype;
+    t.bytes = static_cast<size_t>(t.elems()) * ElemBytes(t.dtype);
+    if (alloc) t.offset = Alloc(t.bytes);
+    p_->tensors.push_back(t);
+    const int idx = static_cast<int>(p_->tensors.size()) - 1;
+    cache_[Key(op, specs)] = idx;
+    return idx;
+  }
+
+  static std::string Key(int op, const Specs& s) { return std::to_string(op) + "|" + SpecsStr(s); }
+
+  void ValidateSpecs() {
+    for (size_t i = 0; i < p_->ops.size(); ++i) {
+      const Dims g = GDims(static_cast<int>(i));
+      auto check = [&](const Specs& s, const Dims& dims, const std::string& what) {
+        for (int a = 0; a < p_->n_axes; ++a) {
+          if (!Valid(s[a], LocalDims(dims, s, mesh_, a), mesh_[a]))
+            Fail("op " + std::to_string(i) + ": " + what + " spec " + SpecStr(s[a]) +
+                 " invalid on axis " + std::to_string(a));
+        }
+      };
+      check(p_->out_specs[i], g, "output");
+      for (size_t s = 0; s < p_->inputs[i].size(); ++s)
+        check(p_->in_specs[i][s], GDims(p_->inputs[i][s]), "input");
+    }
+  }
+
+  Specs NaturalSpecs(int i, const std::vector<Specs>& ins) {
+    const rh_op& op = p_->ops[i];
+    Specs nat(p_->n_axes);
+    for (int a = 0; a < p_->n_axes; ++a) {
+      std::vector<rh_spec> in_a;
+      std::vector<Dims> in_d;
+      for (size_t s = 0; s < ins.size(); ++s) {
+        in_a.push_back(ins[s][a]);
+        in_d.push_back(LocalDims(GDims(p_->inputs[i][s]), ins[s], mesh_, a));
+      }
+      nat[a] = Natural(op, in_a, in_d, LocalDims(GDims(i), nat, mesh_, a), mesh_[a]);
+    }
+    return nat;
+  }
+
+  bool IsElementwiseUnary(int i) const {
+    return p_->ops[i].kind == RH_OP_UNARY && p_->ops[i].fn != RH_FN_SOFTMAX;
+  }
+
+  // Fusion of comm-free unary chains into one kernel, and into the epilogue of the GEMM /
+  // add / mul that produces them.  Op u is absorbed into its producer's kernel when u is an
+  // elementwise unary whose single input edge needs no resharding and whose producer has no
+  // other consumer and is not a program output.
+  void PlanFusion() {
+    const int n = static_cast<int>(p_->ops.size());
+    absorbed_.assign(n, false);
+    chain_.assign(n, {});
+    if (p_->flags & RH_FLAG_NO_FUSION) return;
+    std::vector<int> uses(n, 0);
+    std::vector<int> consumer(n, -1);
+    for (int i = 0; i < n; ++i)
+      for (int s : p_->inputs[i]) {
+        ++uses[s];
+        consumer[s] = i;
+      }
+    std::vector<bool> is_out(n, false);
+    for (int o : p_->outputs) is_out[o] = true;
+    auto natural_ok = [&](int i) {
+      try {
+        return SpecsEq(NaturalSpecs(i, p_->in_specs[i]), p_->out_specs[i]);
+      } catch (const Error&) {
+        return false;
+      }
+    };
+    auto no_partial = [&](const Specs& s) {
+      for (auto& x : s)
+        if (x.kind == RH_PARTIAL) return false;
+      return true;
+    };
+    for (int h : p_->order) {
+      const rh_op& op = p_->ops[h];
+      const bool head_kind = IsElementwiseUnary(h) || op.kind == RH_OP_MATMUL ||
+                             op.kind == RH_OP_ADD || op.kind == RH_OP_MUL;
+      if (!head_kind || absorbed_[h]) continue;
+      int cur = h;
+      while (true) {
+        if (uses[cur] != 1 || is_out[cur]) break;
+        const int v = consumer[cur];
+        if (!IsElementwiseUnary(v) || p_->ops[v].dtype != op.dtype) break;
+        if (!SpecsEq(p_->in_specs[v][0], p_->out_specs[cur])) break;
+        if (!no_partial(p_->out_specs[cur]) || !natural_ok(cur) || !natural_ok(v)) break;
+        if (static_cast<int>(chain_[h].size()) + 1 >= kMaxChain) break;
+        chain_[h].push_back(v);
+        absorbed_[v] = true;
+        cur = v;
+      }
+    }
+  }
+
+  int UnaryFn(int i) const {
+    int fn = p_->ops[i].fn;
+    if (fn == RH_FN_UNLABELED)
+      fn = (p_->flags & RH_FLAG_UNLABELED_IDENTITY) ? RH_FN_IDENTITY : RH_FN_TANH;
+    return fn;
+  }
+
+  ChainArgs ChainOf(int h, bool include_head) const {
+    ChainArgs c{};
+    if (include_head) c.fns[c.n_fn++] = UnaryFn(h);
+    for (int v : chain_[h]) c.fns[c.n_fn++] = UnaryFn(v);
+    return c;
+  }
+
+  std::string OpName(int i) const { return "op" + std::to_string(i); }
+
+  void AddStep(Step s) { p_->steps.push_back(std::move(s)); }
+
+  void EmitOp(int i) {
+    const rh_op& op = p_->ops[i];
+    const int nin = static_cast<int>(p_->inputs[i].size());
+    std::vector<int> in_t(nin);
+    for (int s = 0; s < nin; ++s)
+      in_t[s] = GetTensor(p_->inputs[i][s], p_->in_specs[i][s], "edge");
+    const Specs nat = NaturalSpecs(i, p_->in_specs[i]);
+    const int tail = chain_[i].empty() ? i : chain_[i].back();
+    const bool direct = SpecsEq(nat, p_->out_specs[i]);
+    if (!chain_[i].empty() && !direct) Fail("internal: fused head without a natural spec");
+    // Reshape: pass-through layouts keep the local buffer byte-identical -> alias, no kernel.
+    if (op.kind == RH_OP_RESHAPE) {
+      int t = NewTensor(i, nat, /*alloc=*/false);
+      p_->tensors[t].offset = p_->tensors[in_t[0]].offset;
+      p_->out_tensor[i] = t;
+      if (!direct) p_->out_tensor[i] = GetTensor(i, p_->out_specs[i], "pin");
+      return;
+    }
+    const int out_t = NewTensor(tail, nat);
+    if (tail != i) {  // intermediate members of the chain have no buffer
+      p_->tensors[out_t].gdims = GDims(i);
+    }
+    EmitKernel(i, in_t, out_t);
+    p_->out_tensor[tail] = out_t;
+    if (!direct) {  // pinned op without a rule: computed replicated, then sliced (sharding.cpp:477-487)
+      p_->out_tensor[i] = out_t;
+      p_->out_tensor[i] = GetTensor(i, p_->out_specs[i], "pin");
+    }
+  }
+
+  void EmitKernel(int i, const std::vector<int>& in_t, int out_t) {
+    rh_program* P = p_;
+    const rh_op& op = P->ops[i];
+    const int first = rt_->first_rank;
+    const Tensor& T = P->tensors[out_t];
+    const int dtype = op.dtype;
+    const int eb = ElemBytes(dtype);
+    Step st;
+    st.kind = Step::kKernel;
+    st.launches = 1;
+    const int64_t n_out = T.elems();
+    double in_bytes = 0;
+    for (int t : in_t) in_bytes += static_cast<double>(P->tensors[t].bytes);
+    st.alg_bytes = in_bytes + static_cast<double>(T.bytes);
+    const std::string id = OpName(i);
+    switch (op.kind) {
+      case RH_OP_MATMUL: {
+        const Dims ad = P->tensors[in_t[0]].ldims, bd = P->tensors[in_t[1]].ldims;
+        GemmArgs g{};
+        g.m = op.transpose_a ? ad[1] : ad[0];
+        g.k = op.transpose_a ? ad[0] : ad[1];
+        g.n = op.transpose_b ? bd[0] : bd[1];
+        if ((op.transpose_b ? bd[1] : bd[0]) != g.k) Fail("matmul " + id + ": local k mismatch");
+        if (T.ldims[0] != g.m || T.ldims[1] != g.n) Fail("matmul " + id + ": local output shape mismatch");
+        g.ta = op.transpose_a;
+        g.tb = op.transpose_b;
+        g.dtype = dtype;
+        g.epi = ChainOf(i, false);
+        const bool tc = !(P->flags & RH_FLAG_SIMT_GEMM) && GemmTcSupported(g);
+        st.name = std::string(tc ? "gemm_tc " : "gemm_simt ") + id;
+        st.alg_flops = 2.0 * g.m * g.n * g.k;
+        const int ta = in_t[0], tb = in_t[1];
+        st.run = [P, g, ta, tb, out_t, first, tc](int li, cudaStream_t s) {
+          GemmArgs a = g;
+          const int r = first + li;
+          a.a = P->Ptr(P->tensors[ta], r);
+          a.b = P->Ptr(P->tensors[tb], r);
+          a.c = P->Ptr(P->tensors[out_t], r);
+          if (tc) LaunchGemmTc(a, s);
+          else LaunchGemmSimt(a, s);
+          return 1;
+        };
+        break;
+      }
+      case RH_OP_ADD:
+      case RH_OP_MUL: {
+        const bool mul = op.kind == RH_OP_MUL;
+        const ChainArgs c = ChainOf(i, false);
+        st.name = std::string(mul ? "mul " : "add ") + id + (c.n_fn ? "+chain" : "");
+        st.alg_flops = static_cast<double>(n_out) * (1 + c.n_fn);
+        const int ta = in_t[0], tb = in_t[1];
+        st.run = [P, ta, tb, out_t, first, n_out, mul, c, dtype](int li, cudaStream_t s) {
+          const int r = first + li;
+          LaunchBinary(P->Ptr(P->tensors[out_t], r), P->Ptr(P->tensors[ta], r),
+                       P->Ptr(P->tensors[tb], r), n_out, mul, c, dtype, s);
+          return 1;
+        };
+        break;
+      }
+      case RH_OP_UNARY: {
+        const int ti = in_t[0];
+        if (op.fn == RH_FN_SOFTMAX) {
+          const int64_t cols = T.ldims.back();
+          const int64_t rows = n_out / cols;
+          st.name = "softmax " + id;
+          st.alg_flops = 4.0 * n_out;
+          st.run = [P, ti, out_t, first, rows, cols, dtype](int li, cudaStream_t s) {
+            const int r = first + li;
+            LaunchSoftmaxRows(P->Ptr(P->tensors[out_t], r), P->Ptr(P->tensors[ti], r), rows, cols,
+                              dtype, s);
+            return 1;
+          };
+        } else {
+          const ChainArgs c = ChainOf(i, true);
+          st.name = "unary_chain[" + std::to_string(c.n_fn) + "] " + id;
+          st.alg_flops = static_cast<double>(n_out) * c.n_fn;
+          st.run = [P, ti, out_t, first, n_out, c, dtype](int li, cudaStream_t s) {
+            const int r = first + li;
+            LaunchUnaryChain(P->Ptr(P->tensors[out_t], r), P->Ptr(P->tensors[ti], r), n_out, c,
+                             dtype, s);
+            return 1;
+          };
+        }
+        break;
+      }
+      case RH_OP_TRANSPOSE: {
+        const int ti = in_t[0];
+        const Dims id_ = P->tensors[ti].ldims;
+        const std::vector<int> perm = EffPerm(op, static_cast<int>(id_.size()));
+        st.name = "transpose " + id;
+        st.run = [P, ti, out_t, first, id_, perm, dtype](int li, cudaStream_t s) {
+          const int r = first + li;
+          LaunchTranspose(P->Ptr(P->tensors[out_t], r), P->Ptr(P->tensors[ti], r),
+                          static_cast<int>(id_.size()), id_.data(), perm.data(), dtype, s);
+          return 1;
+        };
+        break;
+      }
+      case RH_OP_REDUCE_SUM: {
+        const int ti = in_t[0];
+        const Dims id_ = P->tensors[ti].ldims;
+        int64_t outer = 1;
+        for (int k = 0; k < op.axis; ++k) outer *= id_[k];
+        const int64_t e = id_[op.axis], inner = Inner(id_, op.axis);
+        st.name = "reduce_sum " + id;
+        st.alg_flops = static_cast<double>(outer * e * inner);
+        st.run = [P, ti, out_t, first, outer, e, inner, dtype](int li, cudaStream_t s) {
+          const int r = first + li;
+          LaunchReduceSum(P->Ptr(P->tensors[out_t], r), P->Ptr(P->tensors[ti], r), outer, e, inner,
+                          dtype, s);
+          return 1;
+        };
+        break;
+      }
+      case RH_OP_BROADCAST: {
+        const int ti = in_t[0];
+        const int64_t n_in = P->tensors[ti].elems();
+        st.name = "broadcast " + id;
+        st.run = [P, ti, out_t, first, n_out, n_in, dtype](int li, cudaStream_t s) {
+          const int r = first + li;
+          LaunchBroadcast(P->Ptr(P->tensors[out_t], r), P->Ptr(P->tensors[ti], r), n_out, n_in,
+                          dtype, s);
+          return 1;
+        };
+        break;
+      }
+      case RH_OP_CONCAT: {
+        const int ax = op.axis;
+        const Dims od = T.ldims;
+        int64_t outer = 1;
+        for (int k = 0; k < ax; ++k) outer *= od[k];
+        const int64_t orow = od[ax] * Inner(od, ax);
+        std::vector<int64_t> rows, offs;
+        int64_t off = 0;
+        for (int t : in_t) {
+          const Dims ld = P->tensors[t].ldims;
+          rows.push_back(ld[ax] * Inner(ld, ax));
+          offs.push_back(off);
+          off += rows.back();
+        }
+        if (off != orow) Fail("concat " + id + ": local shapes do not add up");
+        st.name = "concat " + id;
+        st.launches = static_cast<int>(in_t.size());
+        const std::vector<int> ins = in_t;
+        st.run = [P, ins, out_t, first, outer, orow, rows, offs, dtype](int li, cudaStream_t s) {
+          const int r = first + li;
+          for (size_t k = 0; k < ins.size(); ++k)
+            LaunchConcatPiece(P->Ptr(P->tensors[out_t], r), P->Ptr(P->tensors[ins[k]], r), outer,
+                              rows[k], orow, offs[k], dtype, s);
+          return static_cast<int>(ins.size());
+        };
+        break;
+      }
+      default:
+        Fail(std::string("cannot execute op kind ") + KindName(op.kind));
+    }
+    (void)eb;
+    AddStep(std::move(st));
+  }
+
+  // Producer `p` in the per-axis layout `want`, inserting single-axis transitions as needed.
+  int GetTensor(int p, const Specs& want, const char* why) {
+    auto it = cache_.find(Key(p, want));
+    if (it != cache_.end()) return it->second;
+    int cur = p_->out_tensor[p];
+    if (cur < 0) Fail("internal: producer " + std::to_string(p) + " has no buffer");
+    Specs cs = p_->tensors[cur].specs;
+    if (SpecsEq(cs, want)) return cur;
+    int m = 0;
+    while (SpecEq(cs[m], want[m])) ++m;
+    // Gather later sharded axes first so every single-axis move sees Replicated/Partial beyond
+    // its own axis (its buffers are then exactly the axis-local tensor).
+    for (int j = p_->n_axes - 1; j > m; --j) {
+      if (cs[j].kind == RH_SHARD) {
+        cs[j] = Rep();
+        cur = Move(cur, j, cs, why);
+      }
+    }
+    cs[m] = want[m];
+    cur = Move(cur, m, cs, why);
+    for (int j = m + 1; j < p_->n_axes; ++j) {
+      if (!SpecEq(cs[j], want[j])) {
+        cs[j] = want[j];
+        cur = Move(cur, j, cs, why);
+      }
+    }
+    return cur;
+  }
+
+  int Move(int src, int axis, const Specs& to_specs, const char* why) {
+    auto it = cache_.find(Key(p_->tensors[src].op, to_specs));
+    if (it != cache_.end()) return it->second;
+    const Tensor X = p_->tensors[src];
+    const int dst = NewTensor(X.op, to_specs);
+    const Tensor Y = p_->tensors[dst];
+    const int d = mesh_[axis];
+    const Dims D = LocalDims(X.gdims, X.specs, mesh_, axis);  // axis-local tensor
+    const rh_spec from = X.specs[axis], to = to_specs[axis];
+    if (!Valid(to, D, d)) Fail("reshard: target spec " + SpecStr(to) + " invalid on axis " + std::to_string(axis));
+    const AxisView fv = MakeAxisView(from, static_cast<int>(D.size()), D.data(), d);
+    const AxisView tv = MakeAxisView(to, static_cast<int>(D.size()), D.data(), d);
+    const int eb = ElemBytes(X.dtype);
+    const double S = static_cast<double>(Prod(D)) * eb;
+    Step st;
+    st.kind = Step::kTransition;
+    st.axis = axis;
+    st.name = std::string(CollectiveName(from, to)) + " op" + std::to_string(X.op) + " " +
+              SpecStr(from) + "->" + SpecStr(to) + "@" + std::to_string(axis) + " (" + why + ")";
+    st.wire_bytes = WireBytes(from, to, S, d);
+    const double n_dst = static_cast<double>(Y.elems());
+    st.alg_bytes = n_dst * eb * (from.kind == RH_PARTIAL ? d + 1 : 2);
+    if (to.kind == RH_PARTIAL) st.alg_bytes = n_dst * eb * 2;
+    st.launches = 1;
+    rh_program* P = p_;
+    const int first = rt_->first_rank;
+    const int dtype = X.dtype;
+    const bool remote = from.kind != RH_REPLICATED && d > 1;
+    const bool nccl = (P->flags & RH_FLAG_TRANSPORT_NCCL) && rt_->dist && remote;
+    st.p2p = remote && !nccl;
+    if (!nccl) {
+      st.run = [P, src, dst, axis, fv, tv, dtype](int li, cudaStream_t s) {
+        const int g = P->mesh->rt->first_rank + li;
+        const std::vector<int> members = P->mesh->Group(axis, g);
+        const int coord = P->mesh->Coords(g)[axis];
+        PullArgs a{};
+        a.dst = P->Ptr(P->tensors[dst], g);
+        for (size_t k = 0; k < members.size(); ++k) a.src[k] = P->Ptr(P->tensors[src], members[k]);
+        a.from = fv;
+        a.to = tv;
+        a.coord = coord;
+        a.n_dst = P->tensors[dst].elems();
+        a.dtype = dtype;
+        return LaunchPull(a, s);
+      };
+    } else {
+      // Baseline: NCCL collective on this axis's communicator (+ pack/unpack pull kernels).
+      const size_t chunk = static_cast<size_t>(Prod(LocalDims(D, {from.kind == RH_SHARD ? from : to}, {d}, 1)));
+      const size_t stage_off = Alloc(static_cast<size_t>(Prod(D)) * eb);
+      st.name += " [nccl]";
+      st.run = [P, src, dst, axis, fv, tv, dtype, from, to, d, chunk, stage_off, eb, first](int li, cudaStream_t s) {
+        const int g = first + li;
+        ncclComm_t comm = P->mesh->axis_comm[axis];
+        const int coord = P->mesh->Coords(g)[axis];
+        char* x = P->Ptr(P->tensors[src], g);
+        char* y = P->Ptr(P->tensors[dst], g);
+        char* stage = P->peer_base[g] + stage_off;
+        const int64_t ny = P->tensors[dst].elems();
+        int launches = 0;
+        if (from.kind == RH_PARTIAL && to.kind == RH_REPLICATED) {
+          RH_NCCL(ncclAllReduce(x, y, ny, NcclType(dtype), ncclSum, comm, s));
+          return 1;
+        }
+        if (from.kind == RH_PARTIAL) {  // pack each member's chunk, reduce-scatter
+          AxisView rep = fv;
+          rep.kind = RH_REPLICATED;
+          for (int k = 0; k < d; ++k) {
+            PullArgs a{};
+            a.dst = stage + static_cast<size_t>(k) * chunk * eb;
+            a.src[coord] = x;
+            a.from = rep;
+            a.to = tv;
+            a.coord = k;
+            a.n_dst = static_cast<int64_t>(chunk);
+            a.dtype = dtype;
+            launches += LaunchPull(a, s);
+          }
+          RH_NCCL(ncclReduceScatter(stage, y, chunk, NcclType(dtype), ncclSum, comm, s));
+          return launches + 1;
+        }
+        // Shard source: all-gather the shards, then one pull from the staging chunks.
+        RH_NCCL(ncclAllGather(x, stage, chunk, NcclType(dtype), comm, s));
+        PullArgs a{};
+        a.dst = y;
+        for (int k = 0; k < d; ++k) a.src[k] = stage + static_cast<size_t>(k) * chunk * eb;
+        a.from = fv;
+        a.to = tv;
+        a.coord = coord;
+        a.n_dst = ny;
+        a.dtype = dtype;
+        return 1 + LaunchPull(a, s);
+      };
+    }
+    AddStep(std::move(st));
+    return dst;
+  }
+
+  rh_program* p_;
+  std::vector<int> mesh_;
+  rh_runtime* rt_;
+  size_t arena_ = 0;
+  std::map<std::string, int> cache_;
+  std::vector<bool> absorbed_;
+  std::vector<std::vector<int>> chain_;
+};
+
+}  // namespace
+
+void LowerProgram(rh_program* p) { Lowerer(p).Lower(); }
+
+}  // namespace rh

@@ -1,0 +1,97 @@
+// executor.h — runtime, mesh and partitioned-program structures behind the C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "kernels.h"
+
+using Dims = std::vector<int64_t>;
+using Specs = std::vector<rh_spec>;  // one per mesh axis
+
+struct rh_runtime {
+  int world = 1;
+  bool dist = false;          // one process per GPU (torchrun)
+  int first_rank = 0;         // global rank of local rank 0
+  std::vector<int> rank_dev;  // local rank -> index into devs
+  std::vector<int> devs;      // distinct CUDA device ids
+  std::vector<cudaStream_t> streams;  // one per distinct device
+  ncclComm_t world_comm = nullptr;    // dist only
+  int n_local() const { return static_cast<int>(rank_dev.size()); }
+  cudaStream_t stream_of(int li) const { return streams[rank_dev[li]]; }
+  int device_of(int li) const { return devs[rank_dev[li]]; }
+};
+
+struct rh_mesh {
+  rh_runtime* rt = nullptr;
+  std::vector<int> dims;
+  std::vector<ncclComm_t> axis_comm;  // dist only: this process's communicator per axis
+  std::vector<int> Coords(int rank) const;
+  // Global ranks of `rank`'s group along `axis`, ordered by their coordinate on that axis.
+  std::vector<int> Group(int axis, int rank) const;
+};
+
+namespace rh {
+
+struct Tensor {
+  int op = -1;
+  Specs specs;
+  Dims gdims;   // global shape
+  Dims ldims;   // composed local shape
+  int dtype = RH_F32;
+  size_t bytes = 0;   // local bytes per rank
+  size_t offset = 0;  // arena offset (identical on every rank: the arena is symmetric)
+  int64_t elems() const {
+    int64_t n = 1;
+    for (auto x : ldims) n *= x;
+    return n;
+  }
+};
+
+struct Step {
+  enum Kind { kKernel = 0, kTransition = 1, kSync = 2 };
+  int kind = kKernel;
+  std::string name;
+  int axis = -1;             // transitions: mesh axis (group) that must be synchronised
+  bool p2p = false;          // transition reads peer buffers (needs pre/post group sync)
+  double alg_bytes = 0, alg_flops = 0, wire_bytes = 0;
+  int launches = 0;          // per rank per run
+  double ms = 0;             // from the last profile
+  // Enqueue this step for local rank `li` on stream `s`; returns the launches issued.
+  std::function<int(int li, cudaStream_t s)> run;
+};
+
+}  // namespace rh
+
+struct rh_program {
+  rh_mesh* mesh = nullptr;
+  uint32_t flags = 0;
+  int n_axes = 0;
+  std::vector<rh_op> ops;
+  std::vector<std::vector<int>> inputs;
+  std::vector<std::vector<Specs>> in_specs;  // [op][slot] -> per axis
+  std::vector<Specs> out_specs;
+  std::vector<int> outputs;
+  std::vector<int> order;
+
+  std::vector<rh::Tensor> tensors;
+  std::vector<int> out_tensor;  // op -> tensor index (-1: fused into a successor's kernel)
+  std::vector<int> mat_tensor;  // op -> materialized Replicated tensor (outputs)
+  std::vector<rh::Step> steps;
+
+  // memory
+  size_t arena_bytes = 0;
+  size_t flags_off = 0, counter_off = 0;
+  std::vector<char*> base;       // per local rank
+  std::vector<char*> peer_base;  // per global rank (dist: IPC-mapped; local: = base)
+  bool ipc_opened = false;
+  std::vector<void*> owned;      // device allocations to free (per distinct device)
+
+  char* Ptr(const rh::Tensor& t, int global_rank) const { return peer_base[global_rank] + t.offset; }
+  int LocalIndex(int global_rank) const;
+};

@@ -1,0 +1,357 @@
+// k_elementwise.cu — local (per-rank) non-GEMM operators: K2 add/mul, K3 fused unary chains,
+// softmax rows, K4 reduce_sum, K5 transpose, K6 broadcast, K7 concat.  All HBM-bound: 16-byte
+// vector loads/stores, grid-stride loops sized to the 148 SMs.
+//
+// Unary semantics (the reference leaves them undefined, include/parashard/ir.h:87; DESIGN.md
+// §Semantics): evaluated in fp32 with the expression order below (explicit _rn intrinsics so
+// no FMA contraction changes the rounding); bf16 outputs are rounded after every op.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "kernels.h"
+
+namespace rh {
+namespace {
+
+__device__ __forceinline__ float ApplyFn(int fn, float x) {
+  switch (fn) {
+    case RH_FN_RELU: return x > 0.0f ? x : 0.0f;
+    case RH_FN_GELU: {
+      const float x3 = __fmul_rn(__fmul_rn(x, x), x);
+      const float inner = __fmul_rn(0.7978845608028654f, __fadd_rn(x, __fmul_rn(0.044715f, x3)));
+      return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.0f, tanhf(inner)));
+    }
+    case RH_FN_TANH: return tanhf(x);
+    case RH_FN_EXP: return expf(x);
+    case RH_FN_SIGMOID: return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x)));
+    case RH_FN_NEG: return -x;
+    case RH_FN_RSQRT: return __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(fabsf(x), 1e-6f)));
+    default: return x;  // identity
+  }
+}
+
+__device__ __forceinline__ float RoundBf16(float x) {
+  return __bfloat162float(__float2bfloat16_rn(x));
+}
+
+template <bool kBf16>
+__device__ __forceinline__ float ApplyChain(const ChainArgs& c, float x) {
+  for (int i = 0; i < c.n_fn; ++i) {
+    x = ApplyFn(c.fns[i], x);
+    if (kBf16) x = RoundBf16(x);
+  }
+  return x;
+}
+
+// 16-byte packets: 4 fp32 or 8 bf16.
+template <bool kBf16>
+struct Pack {
+  static constexpr int E = kBf16 ? 8 : 4;
+  float v[E];
+  __device__ __forceinline__ void Load(const void* p, int64_t i) {
+    uint4 u = reinterpret_cast<const uint4*>(p)[i];
+    if (kBf16) {
+      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = __bfloat162float(b[e]);
+    } else {
+      const float* f = reinterpret_cast<const float*>(&u);
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = f[e];
+    }
+  }
+  __device__ __forceinline__ void Store(void* p, int64_t i) const {
+    uint4 u;
+    if (kBf16) {
+      __nv_bfloat16* b = reinterpret_cast<__nv_bfloat16*>(&u);
+#pragma unroll
+      for (int e = 0; e < E; ++e) b[e] = __float2bfloat16_rn(v[e]);
+    } else {
+      float* f = reinterpret_cast<float*>(&u);
+#pragma unroll
+      for (int e = 0; e < E; ++e) f[e] = v[e];
+    }
+    reinterpret_cast<uint4*>(p)[i] = u;
+  }
+};
+
+template <bool kBf16>
+__device__ __forceinline__ float LoadScalar(const void* p, int64_t i) {
+  if (kBf16) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]);
+  return reinterpret_cast<const float*>(p)[i];
+}
+template <bool kBf16>
+__device__ __forceinline__ void StoreScalar(void* p, int64_t i, float x) {
+  if (kBf16) {
+    reinterpret_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(x);
+  } else {
+    reinterpret_cast<float*>(p)[i] = x;
+  }
+}
+
+template <bool kBf16>
+__global__ void __launch_bounds__(256) UnaryChainKernel(void* out, const void* in, int64_t n,
+                                                        ChainArgs c) {
+  constexpr int E = Pack<kBf16>::E;
+  const int64_t nv = n / E;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nv; i += stride) {
+    Pack<kBf16> p;
+    p.Load(in, i);
+#pragma unroll
+    for (int e = 0; e < E; ++e) p.v[e] = ApplyChain<kBf16>(c, p.v[e]);
+    p.Store(out, i);
+  }
+  for (int64_t i = nv * E + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride)
+    StoreScalar<kBf16>(out, i, ApplyChain<kBf16>(c, LoadScalar<kBf16>(in, i)));
+}
+
+template <bool kBf16>
+__global__ void __launch_bounds__(256) BinaryKernel(void* out, const void* a, const void* b,
+                                                    int64_t n, bool mul, ChainArgs c) {
+  constexpr int E = Pack<kBf16>::E;
+  const int64_t nv = n / E;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nv; i += stride) {
+    Pack<kBf16> x, y;
+    x.Load(a, i);
+    y.Load(b, i);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      float r = mul ? __fmul_rn(x.v[e], y.v[e]) : __fadd_rn(x.v[e], y.v[e]);
+      if (kBf16) r = RoundBf16(r);
+      x.v[e] = ApplyChain<kBf16>(c, r);
+    }
+    x.Store(out, i);
+  }
+  for (int64_t i = nv * E + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    float xa = LoadScalar<kBf16>(a, i), xb = LoadScalar<kBf16>(b, i);
+    float r = mul ? __fmul_rn(xa, xb) : __fadd_rn(xa, xb);
+    if (kBf16) r = RoundBf16(r);
+    StoreScalar<kBf16>(out, i, ApplyChain<kBf16>(c, r));
+  }
+}
+
+template <bool kBf16>
+__global__ void __launch_bounds__(256) SoftmaxRowsKernel(void* out, const void* in, int64_t cols) {
+  const int64_t row = blockIdx.x;
+  const int64_t base = row * cols;
+  __shared__ float red[32];
+  float mx = -INFINITY;
+  for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) mx = fmaxf(mx, LoadScalar<kBf16>(in, base + j));
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : -INFINITY;
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  mx = red[0];
+  __syncthreads();
+  float s = 0.0f;
+  for (int64_t j = threadIdx.x; j < cols; j += blockDim.x)
+    s += expf(__fsub_rn(LoadScalar<kBf16>(in, base + j), mx));
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  s = red[0];
+  for (int64_t j = threadIdx.x; j < cols; j += blockDim.x)
+    StoreScalar<kBf16>(out, base + j, __fdiv_rn(expf(__fsub_rn(LoadScalar<kBf16>(in, base + j), mx)), s));
+}
+
+// Column sums: one thread per (outer, inner) column, coalesced across `inner`.
+template <bool kBf16>
+__global__ void __launch_bounds__(256) ReduceColsKernel(void* out, const void* in, int64_t outer,
+                                                        int64_t e, int64_t inner) {
+  const int64_t n = outer * inner;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t o = t / inner, i = t - o * inner;
+    const int64_t base = o * e * inner + i;
+    float s = 0.0f;
+    for (int64_t c = 0; c < e; ++c) s = __fadd_rn(s, LoadScalar<kBf16>(in, base + c * inner));
+    StoreScalar<kBf16>(out, t, s);
+  }
+}
+
+// Row sums (inner == 1): one warp per row, shuffle tree.
+template <bool kBf16>
+__global__ void __launch_bounds__(256) ReduceRowsKernel(void* out, const void* in, int64_t rows,
+                                                        int64_t e) {
+  const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  float s = 0.0f;
+  for (int64_t c = lane; c < e; c += 32) s += LoadScalar<kBf16>(in, warp * e + c);
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) StoreScalar<kBf16>(out, warp, s);
+}
+
+// 2-D transpose [R,C] -> [C,R] through a padded shared-memory tile (coalesced both sides).
+template <typename T>
+__global__ void __launch_bounds__(256) Transpose2DKernel(T* out, const T* in, int64_t R, int64_t C) {
+  __shared__ T tile[32][33];
+  const int64_t r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int64_t r = r0 + j, c = c0 + threadIdx.x;
+    if (r < R && c < C) tile[j][threadIdx.x] = in[r * C + c];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int64_t c = c0 + j, r = r0 + threadIdx.x;
+    if (r < R && c < C) out[c * R + r] = tile[threadIdx.x][j];
+  }
+}
+
+struct PermDev {
+  int nd;
+  int64_t odims[RH_MAX_RANK];
+  int64_t istride_of_out[RH_MAX_RANK];
+};
+
+template <typename T>
+__global__ void TransposeNDKernel(T* out, const T* in, PermDev p, int64_t n) {
+  for (int64_t f = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; f < n;
+       f += int64_t(gridDim.x) * blockDim.x) {
+    int64_t t = f, src = 0;
+    for (int i = p.nd - 1; i >= 0; --i) {
+      const int64_t c = t % p.odims[i];
+      t /= p.odims[i];
+      src += c * p.istride_of_out[i];
+    }
+    out[f] = in[src];
+  }
+}
+
+template <typename T>
+__global__ void BroadcastKernel(T* out, const T* in, int64_t n_out, int64_t n_in) {
+  for (int64_t f = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; f < n_out;
+       f += int64_t(gridDim.x) * blockDim.x)
+    out[f] = in[f % n_in];
+}
+
+template <typename T>
+__global__ void ConcatPieceKernel(T* out, const T* in, int64_t outer, int64_t row, int64_t orow,
+                                  int64_t off) {
+  const int64_t n = outer * row;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t o = t / row, j = t - o * row;
+    out[o * orow + off + j] = in[t];
+  }
+}
+
+int Blocks(int64_t n, int per_thread = 1) {
+  return static_cast<int>(
+      std::max<int64_t>(1, std::min<int64_t>((n / per_thread + 255) / 256, 148 * 16)));
+}
+
+}  // namespace
+
+void LaunchUnaryChain(void* out, const void* in, int64_t n, const ChainArgs& c, int dtype,
+                      cudaStream_t s) {
+  if (n == 0) return;
+  if (dtype == RH_BF16) {
+    UnaryChainKernel<true><<<Blocks(n, 8), 256, 0, s>>>(out, in, n, c);
+  } else {
+    UnaryChainKernel<false><<<Blocks(n, 4), 256, 0, s>>>(out, in, n, c);
+  }
+  RH_CUDA(cudaGetLastError());
+}
+
+void LaunchSoftmaxRows(void* out, const void* in, int64_t rows, int64_t cols, int dtype,
+                       cudaStream_t s) {
+  if (rows == 0) return;
+  if (rows > 0x7fffffff) Fail("softmax: too many rows");
+  if (dtype == RH_BF16) {
+    SoftmaxRowsKernel<true><<<static_cast<unsigned>(rows), 256, 0, s>>>(out, in, cols);
+  } else {
+    SoftmaxRowsKernel<false><<<static_cast<unsigned>(rows), 256, 0, s>>>(out, in, cols);
+  }
+  RH_CUDA(cudaGetLastError());
+}
+
+void LaunchBinary(void* out, const void* a, const void* b, int64_t n, bool mul, const ChainArgs& c,
+                  int dtype, cudaStream_t s) {
+  if (n == 0) return;
+  if (dtype == RH_BF16) {
+    BinaryKernel<true><<<Blocks(n, 8), 256, 0, s>>>(out, a, b, n, mul, c);
+  } else {
+    BinaryKernel<false><<<Blocks(n, 4), 256, 0, s>>>(out, a, b, n, mul, c);
+  }
+  RH_CUDA(cudaGetLastError());
+}
+
+void LaunchReduceSum(void* out, const void* in, int64_t outer, int64_t e, int64_t inner, int dtype,
+                     cudaStream_t s) {
+  if (outer * inner == 0) return;
+  const bool bf = dtype == RH_BF16;
+  if (inner == 1) {
+    const int64_t threads = outer * 32;
+    const int blocks = static_cast<int>((threads + 255) / 256);
+    if (bf) ReduceRowsKernel<true><<<blocks, 256, 0, s>>>(out, in, outer, e);
+    else ReduceRowsKernel<false><<<blocks, 256, 0, s>>>(out, in, outer, e);
+  } else {
+    if (bf) ReduceColsKernel<true><<<Blocks(outer * inner), 256, 0, s>>>(out, in, outer, e, inner);
+    else ReduceColsKernel<false><<<Blocks(outer * inner), 256, 0, s>>>(out, in, outer, e, inner);
+  }
+  RH_CUDA(cudaGetLastError());
+}
+
+void LaunchTranspose(void* out, const void* in, int nd, const int64_t* in_dims, const int* perm,
+                     int dtype, cudaStream_t s) {
+  int64_t n = 1;
+  for (int i = 0; i < nd; ++i) n *= in_dims[i];
+  if (n == 0) return;
+  const bool bf = dtype == RH_BF16;
+  if (nd == 2 && perm[0] == 1 && perm[1] == 0) {
+    const int64_t R = in_dims[0], C = in_dims[1];
+    dim3 grid(static_cast<unsigned>((C + 31) / 32), static_cast<unsigned>((R + 31) / 32));
+    dim3 block(32, 8);
+    if (bf) Transpose2DKernel<<<grid, block, 0, s>>>(static_cast<uint16_t*>(out), static_cast<const uint16_t*>(in), R, C);
+    else Transpose2DKernel<<<grid, block, 0, s>>>(static_cast<uint32_t*>(out), static_cast<const uint32_t*>(in), R, C);
+  } else {
+    PermDev p{};
+    p.nd = nd;
+    int64_t istride[RH_MAX_RANK];
+    int64_t st = 1;
+    for (int i = nd - 1; i >= 0; --i) {
+      istride[i] = st;
+      st *= in_dims[i];
+    }
+    for (int i = 0; i < nd; ++i) {
+      p.odims[i] = in_dims[perm[i]];
+      p.istride_of_out[i] = istride[perm[i]];
+    }
+    if (bf) TransposeNDKernel<<<Blocks(n), 256, 0, s>>>(static_cast<uint16_t*>(out), static_cast<const uint16_t*>(in), p, n);
+    else TransposeNDKernel<<<Blocks(n), 256, 0, s>>>(static_cast<uint32_t*>(out), static_cast<const uint32_t*>(in), p, n);
+  }
+  RH_CUDA(cudaGetLastError());
+}
+
+void LaunchBroadcast(void* out, const void* in, int64_t n_out, int64_t n_in, int dtype,
+                     cudaStream_t s) {
+  if (n_out == 0) return;
+  if (dtype == RH_BF16) BroadcastKernel<<<Blocks(n_out), 256, 0, s>>>(static_cast<uint16_t*>(out), static_cast<const uint16_t*>(in), n_out, n_in);
+  else BroadcastKernel<<<Blocks(n_out), 256, 0, s>>>(static_cast<uint32_t*>(out), static_cast<const uint32_t*>(in), n_out, n_in);
+  RH_CUDA(cudaGetLastError());
+}
+
+void LaunchConcatPiece(void* out, const void* in, int64_t outer, int64_t row, int64_t orow,
+                       int64_t off, int dtype, cudaStream_t s) {
+  if (outer * row == 0) return;
+  if (dtype == RH_BF16) ConcatPieceKernel<<<Blocks(outer * row), 256, 0, s>>>(static_cast<uint16_t*>(out), static_cast<const uint16_t*>(in), outer, row, orow, off);
+  else ConcatPieceKernel<<<Blocks(outer * row), 256, 0, s>>>(static_cast<uint32_t*>(out), static_cast<const uint32_t*>(in), outer, row, orow, off);
+  RH_CUDA(cudaGetLastError());
+}
+
+}  // namespace rh

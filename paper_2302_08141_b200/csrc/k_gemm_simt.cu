@@ -1,0 +1,160 @@
+// k_gemm_simt.cu — CUDA-core GEMM (FFMA, fp32 accumulation) for any shape and any of the four
+// transpose layouts of a rank-2 MatMul (proj/src/ir.cpp:121-137).  It is the reference kernel the
+// tcgen05 path is tested against and the path for shapes the tensor-core kernel does not tile.
+#include <cuda_bf16.h>
+
+#include "kernels.h"
+
+namespace rh {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 8;
+
+template <typename T>
+__device__ __forceinline__ float Ld(const T* p, int64_t i);
+template <>
+__device__ __forceinline__ float Ld<float>(const float* p, int64_t i) {
+  return p[i];
+}
+template <>
+__device__ __forceinline__ float Ld<__nv_bfloat16>(const __nv_bfloat16* p, int64_t i) {
+  return __bfloat162float(p[i]);
+}
+
+__device__ __forceinline__ float Fn(int fn, float x) {
+  switch (fn) {
+    case RH_FN_RELU: return x > 0.0f ? x : 0.0f;
+    case RH_FN_GELU: {
+      const float x3 = __fmul_rn(__fmul_rn(x, x), x);
+      const float inner = __fmul_rn(0.7978845608028654f, __fadd_rn(x, __fmul_rn(0.044715f, x3)));
+      return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.0f, tanhf(inner)));
+    }
+    case RH_FN_TANH: return tanhf(x);
+    case RH_FN_EXP: return expf(x);
+    case RH_FN_SIGMOID: return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x)));
+    case RH_FN_NEG: return -x;
+    case RH_FN_RSQRT: return __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(fabsf(x), 1e-6f)));
+    default: return x;
+  }
+}
+
+template <typename T, bool TA, bool TB>
+__global__ void __launch_bounds__(256) GemmSimtKernel(T* __restrict__ C, const T* __restrict__ A,
+                                                      const T* __restrict__ B, int64_t M,
+                                                      int64_t N, int64_t K, ChainArgs epi) {
+  __shared__ __align__(16) float As[BK][BM];
+  __shared__ __align__(16) float Bs[BK][BN];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int64_t m0 = int64_t(blockIdx.y) * BM, n0 = int64_t(blockIdx.x) * BN;
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+
+  for (int64_t k0 = 0; k0 < K; k0 += BK) {
+    // A tile -> As[k][m]
+    if (!TA) {  // A [M,K]: 4 consecutive k per thread
+      const int r = tid / 2, kc = (tid % 2) * 4;
+      const int64_t gm = m0 + r;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t gk = k0 + kc + j;
+        As[kc + j][r] = (gm < M && gk < K) ? Ld<T>(A, gm * K + gk) : 0.0f;
+      }
+    } else {  // A stored [K,M]: 4 consecutive m per thread
+      const int kr = tid / 32, mc = (tid % 32) * 4;
+      const int64_t gk = k0 + kr;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t gm = m0 + mc + j;
+        As[kr][mc + j] = (gm < M && gk < K) ? Ld<T>(A, gk * M + gm) : 0.0f;
+      }
+    }
+    if (!TB) {  // B [K,N]: 4 consecutive n per thread
+      const int kr = tid / 32, nc = (tid % 32) * 4;
+      const int64_t gk = k0 + kr;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t gn = n0 + nc + j;
+        Bs[kr][nc + j] = (gn < N && gk < K) ? Ld<T>(B, gk * N + gn) : 0.0f;
+      }
+    } else {  // B stored [N,K]: 4 consecutive k per thread
+      const int r = tid / 2, kc = (tid % 2) * 4;
+      const int64_t gn = n0 + r;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t gk = k0 + kc + j;
+        Bs[kc + j][r] = (gn < N && gk < K) ? Ld<T>(B, gn * K + gk) : 0.0f;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[8], b[8];
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[kk][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[kk][64 + tx * 4]);
+      a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+      a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+      b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
+      b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t gm = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t gn = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+      if (gn >= N) continue;
+      float v = acc[i][j];
+      if constexpr (sizeof(T) == 2) v = __bfloat162float(__float2bfloat16_rn(v));
+      for (int f = 0; f < epi.n_fn; ++f) {
+        v = Fn(epi.fns[f], v);
+        if constexpr (sizeof(T) == 2) v = __bfloat162float(__float2bfloat16_rn(v));
+      }
+      if constexpr (sizeof(T) == 2) {
+        C[gm * N + gn] = __float2bfloat16_rn(v);
+      } else {
+        C[gm * N + gn] = v;
+      }
+    }
+  }
+}
+
+template <typename T>
+void Dispatch(const GemmArgs& g, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>((g.n + BN - 1) / BN), static_cast<unsigned>((g.m + BM - 1) / BM));
+  T* c = static_cast<T*>(g.c);
+  const T* a = static_cast<const T*>(g.a);
+  const T* b = static_cast<const T*>(g.b);
+  if (!g.ta && !g.tb) GemmSimtKernel<T, false, false><<<grid, 256, 0, s>>>(c, a, b, g.m, g.n, g.k, g.epi);
+  else if (!g.ta && g.tb) GemmSimtKernel<T, false, true><<<grid, 256, 0, s>>>(c, a, b, g.m, g.n, g.k, g.epi);
+  else if (g.ta && !g.tb) GemmSimtKernel<T, true, false><<<grid, 256, 0, s>>>(c, a, b, g.m, g.n, g.k, g.epi);
+  else GemmSimtKernel<T, true, true><<<grid, 256, 0, s>>>(c, a, b, g.m, g.n, g.k, g.epi);
+}
+
+}  // namespace
+
+void LaunchGemmSimt(const GemmArgs& g, cudaStream_t s) {
+  if (g.m == 0 || g.n == 0) return;
+  if (g.k == 0) {
+    RH_CUDA(cudaMemsetAsync(g.c, 0, g.m * g.n * ElemBytes(g.dtype), s));
+    return;
+  }
+  if (g.m / BM >= 65535) Fail("gemm: M too large for the SIMT grid");
+  if (g.dtype == RH_BF16) Dispatch<__nv_bfloat16>(g, s);
+  else Dispatch<float>(g, s);
+  RH_CUDA(cudaGetLastError());
+}
+
+}  // namespace rh

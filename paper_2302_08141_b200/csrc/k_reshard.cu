@@ -1,0 +1,337 @@
+// k_reshard.cu — resharding transitions (K9 slice, K10 all-gather, K11 reduce-scatter,
+// K12 all-reduce, K13 all-to-all, K14 zero-fill), synthetic init (K17) and the cross-GPU
+// group barrier.
+//
+// Every transition of sharding.cpp:104-142 is one "pull" kernel per destination rank: the rank
+// walks its destination buffer in order (coalesced 16-byte stores), maps each 16-byte unit to
+// its global position and reads it from whichever group member owns it (Shard), from its own
+// copy (Replicated) or from all members summed in rank order (Partial).  Sources are device
+// pointers that may live on this GPU, on a peer GPU over NVLink, or in an NCCL staging buffer.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "kernels.h"
+
+namespace rh {
+
+FastDiv MakeFastDiv(uint32_t d) {
+  if (d == 0) Fail("FastDiv: division by zero");
+  FastDiv f{};
+  f.d = d;
+  uint32_t l = 0;
+  while ((uint64_t{1} << l) < d) ++l;  // l = ceil(log2 d)
+  f.mul = static_cast<uint32_t>(((uint64_t{1} << 32) * ((uint64_t{1} << l) - d)) / d + 1);
+  f.s1 = l > 0 ? 1 : 0;
+  f.s2 = l > 0 ? l - 1 : 0;
+  const uint32_t probes[] = {0u, 1u, d - 1, d, d + 1, 2 * d - 1, 0x7fffffffu, 0xfffffffeu, 0xffffffffu};
+  for (uint32_t n : probes) {
+    if (Div(f, n) != n / d) Fail("FastDiv self-check failed");
+  }
+  return f;
+}
+
+namespace {
+
+template <int VB>
+struct VecT;
+template <>
+struct VecT<16> {
+  using T = uint4;
+};
+template <>
+struct VecT<8> {
+  using T = uint2;
+};
+template <>
+struct VecT<4> {
+  using T = uint32_t;
+};
+template <>
+struct VecT<2> {
+  using T = uint16_t;
+};
+
+struct PullDev {
+  char* dst;
+  const char* src[kMaxGroup];
+  int to_shard;
+  FastDiv qst;  // destination run length (units)
+  int from_kind;
+  FastDiv qsf;  // source run length (units)
+  FastDiv dd;   // group size
+  uint32_t coord;
+  uint32_t n;   // destination units
+};
+
+__device__ __forceinline__ uint32_t DstToGlobal(const PullDev& a, uint32_t i) {
+  if (!a.to_shard) return i;
+  const uint32_t p = Div(a.qst, i);
+  const uint32_t u = i - p * a.qst.d;
+  return (p * a.dd.d + a.coord) * a.qst.d + u;
+}
+
+// Shard / Replicated sources: a pure copy of VB-byte units.
+template <int VB, bool kFromShard>
+__global__ void __launch_bounds__(256) PullCopyKernel(PullDev a) {
+  using V = typename VecT<VB>::T;
+  constexpr int U = 4;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i < a.n; i += U * stride) {
+    V v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const uint32_t ii = i + j * stride;
+      if (ii < a.n) {
+        const uint32_t f = DstToGlobal(a, ii);
+        if (kFromShard) {
+          const uint32_t q = Div(a.qsf, f);
+          const uint32_t u = f - q * a.qsf.d;
+          const uint32_t pp = Div(a.dd, q);
+          const uint32_t r = q - pp * a.dd.d;
+          v[j] = reinterpret_cast<const V*>(a.src[r])[pp * a.qsf.d + u];
+        } else {
+          v[j] = reinterpret_cast<const V*>(a.src[a.coord])[f];
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const uint32_t ii = i + j * stride;
+      if (ii < a.n) reinterpret_cast<V*>(a.dst)[ii] = v[j];
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ float ToF(T x);
+template <>
+__device__ __forceinline__ float ToF<float>(float x) {
+  return x;
+}
+template <>
+__device__ __forceinline__ float ToF<__nv_bfloat16>(__nv_bfloat16 x) {
+  return __bfloat162float(x);
+}
+template <typename T>
+__device__ __forceinline__ T FromF(float x);
+template <>
+__device__ __forceinline__ float FromF<float>(float x) {
+  return x;
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 FromF<__nv_bfloat16>(float x) {
+  return __float2bfloat16_rn(x);
+}
+
+// Partial sources: sum of the d members' values at the same global position, rank order.
+template <typename T, int VB>
+__global__ void __launch_bounds__(256) PullSumKernel(PullDev a, int d) {
+  using V = typename VecT<VB>::T;
+  constexpr int E = VB / sizeof(T);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
+    const uint32_t f = DstToGlobal(a, i);
+    float acc[E];
+    for (int k = 0; k < d; ++k) {
+      V v = reinterpret_cast<const V*>(a.src[k])[f];
+      const T* t = reinterpret_cast<const T*>(&v);
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[e] = k == 0 ? ToF<T>(t[e]) : __fadd_rn(acc[e], ToF<T>(t[e]));
+    }
+    V o;
+    T* t = reinterpret_cast<T*>(&o);
+#pragma unroll
+    for (int e = 0; e < E; ++e) t[e] = FromF<T>(acc[e]);
+    reinterpret_cast<V*>(a.dst)[i] = o;
+  }
+}
+
+int Gcd(int64_t a, int64_t b) {
+  while (b) {
+    int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return static_cast<int>(std::min<int64_t>(a, 1 << 30));
+}
+
+template <int VB>
+void LaunchPullVB(const PullArgs& a, PullDev& dv, cudaStream_t s) {
+  const uint32_t n = dv.n;
+  int blocks = static_cast<int>(std::min<int64_t>((n + 1023) / 1024, 148 * 8));
+  blocks = std::max(blocks, 1);
+  if (a.from.kind == RH_PARTIAL) {
+    if (a.dtype == RH_BF16) {
+      if constexpr (VB >= 2) PullSumKernel<__nv_bfloat16, VB><<<blocks * 4, 256, 0, s>>>(dv, a.from.d);
+    } else {
+      if constexpr (VB >= 4) PullSumKernel<float, VB><<<blocks * 4, 256, 0, s>>>(dv, a.from.d);
+    }
+  } else if (a.from.kind == RH_SHARD) {
+    PullCopyKernel<VB, true><<<blocks, 256, 0, s>>>(dv);
+  } else {
+    PullCopyKernel<VB, false><<<blocks, 256, 0, s>>>(dv);
+  }
+  RH_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+int LaunchPull(const PullArgs& a, cudaStream_t s) {
+  const int eb = ElemBytes(a.dtype);
+  if (a.n_dst == 0) return 0;
+  if (a.to.kind == RH_PARTIAL && a.coord != 0) {  // zero-fill (sharding.cpp:132-135)
+    RH_CUDA(cudaMemsetAsync(a.dst, 0, a.n_dst * eb, s));
+    return 1;
+  }
+  // Vector width: the largest power-of-two unit (<= 16 B) that divides every contiguous run and
+  // every buffer alignment.
+  int64_t g = a.n_dst;
+  if (a.to.kind == RH_SHARD) g = Gcd(g, a.to.Qs);
+  if (a.from.kind == RH_SHARD) g = Gcd(g, a.from.Qs);
+  int vb = 16;
+  auto aligned = [&](const void* p) { return (reinterpret_cast<uintptr_t>(p) % vb) == 0; };
+  while (vb > eb) {
+    bool ok = (g * eb) % vb == 0 && aligned(a.dst);
+    const int nsrc = a.from.kind == RH_REPLICATED ? 0 : a.from.d;
+    for (int k = 0; k < nsrc; ++k) ok = ok && aligned(a.src[k]);
+    if (a.from.kind == RH_REPLICATED) ok = ok && aligned(a.src[a.coord]);
+    if (ok) break;
+    vb /= 2;
+  }
+  const int64_t units_per = vb / eb;
+  PullDev dv{};
+  dv.dst = static_cast<char*>(a.dst);
+  for (int k = 0; k < kMaxGroup; ++k) dv.src[k] = static_cast<const char*>(a.src[k]);
+  const int64_t total = a.to.kind == RH_SHARD ? a.n_dst * a.to.d : a.n_dst;
+  if (total / units_per >= (int64_t{1} << 32)) Fail("reshard: tensor too large for 32-bit unit indices");
+  dv.n = static_cast<uint32_t>(a.n_dst / units_per);
+  dv.to_shard = a.to.kind == RH_SHARD;
+  dv.qst = MakeFastDiv(dv.to_shard ? static_cast<uint32_t>(a.to.Qs / units_per) : 1u);
+  dv.from_kind = a.from.kind;
+  dv.qsf = MakeFastDiv(a.from.kind == RH_SHARD ? static_cast<uint32_t>(a.from.Qs / units_per) : 1u);
+  const int d = a.to.kind == RH_SHARD ? a.to.d : a.from.d;
+  dv.dd = MakeFastDiv(static_cast<uint32_t>(std::max(d, 1)));
+  dv.coord = static_cast<uint32_t>(a.coord);
+  switch (vb) {
+    case 16: LaunchPullVB<16>(a, dv, s); break;
+    case 8: LaunchPullVB<8>(a, dv, s); break;
+    case 4: LaunchPullVB<4>(a, dv, s); break;
+    default: LaunchPullVB<2>(a, dv, s); break;
+  }
+  return 1;
+}
+
+// ----------------------------------------------------------------------------------------------
+
+namespace {
+
+template <typename T>
+__global__ void SliceComposedKernel(T* dst, const T* full, ComposedMap m, int64_t n) {
+  for (int64_t l = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; l < n;
+       l += int64_t(gridDim.x) * blockDim.x)
+    dst[l] = full[ComposedLocalToGlobal(m, l)];
+}
+
+__device__ __forceinline__ void Philox(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+    const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+template <typename T>
+__global__ void SyntheticKernel(T* dst, ComposedMap m, int64_t n, uint64_t seed, uint32_t op_index,
+                                float scale) {
+  for (int64_t l = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; l < n;
+       l += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t f = static_cast<uint64_t>(ComposedLocalToGlobal(m, l));
+    const uint64_t blk = f >> 2;
+    uint32_t c[4] = {static_cast<uint32_t>(blk), static_cast<uint32_t>(blk >> 32),
+                     static_cast<uint32_t>(seed >> 32), 0u};
+    Philox(c, static_cast<uint32_t>(seed), op_index);
+    const uint32_t w = c[f & 3];
+    const float v = static_cast<float>(static_cast<int32_t>(w >> 8) - 8388608) * (1.0f / 8388608.0f);
+    const float x = __fmul_rn(v, scale);
+    if constexpr (sizeof(T) == 4) {
+      dst[l] = x;
+    } else {
+      dst[l] = __float2bfloat16_rn(x);
+    }
+  }
+}
+
+__device__ __forceinline__ void StReleaseSys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t LdAcquireSys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void BarrierKernel(BarrierArgs b) {
+  __shared__ uint32_t seq;
+  if (threadIdx.x == 0) {
+    seq = *b.counter + 1;
+    *b.counter = seq;
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < b.d) {
+    __threadfence_system();
+    StReleaseSys(b.peer_flags[t] + b.me, seq);
+    const uint32_t* f = b.my_flags + b.members[t];
+    while (static_cast<int32_t>(LdAcquireSys(f) - seq) < 0) __nanosleep(64);
+  }
+  __syncthreads();
+}
+
+int Blocks(int64_t n) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16))); }
+
+}  // namespace
+
+void LaunchSliceComposed(void* dst, const void* full, const ComposedMap& m, int64_t n, int dtype,
+                         cudaStream_t s) {
+  if (n == 0) return;
+  if (dtype == RH_BF16) {
+    SliceComposedKernel<<<Blocks(n), 256, 0, s>>>(static_cast<uint16_t*>(dst),
+                                                 static_cast<const uint16_t*>(full), m, n);
+  } else {
+    SliceComposedKernel<<<Blocks(n), 256, 0, s>>>(static_cast<uint32_t*>(dst),
+                                                 static_cast<const uint32_t*>(full), m, n);
+  }
+  RH_CUDA(cudaGetLastError());
+}
+
+void LaunchSynthetic(void* dst, const ComposedMap& m, int64_t n, uint64_t seed, uint32_t op_index,
+                     float scale, int dtype, cudaStream_t s) {
+  if (n == 0) return;
+  if (dtype == RH_BF16) {
+    SyntheticKernel<<<Blocks(n), 256, 0, s>>>(static_cast<__nv_bfloat16*>(dst), m, n, seed,
+                                             op_index, scale);
+  } else {
+    SyntheticKernel<<<Blocks(n), 256, 0, s>>>(static_cast<float*>(dst), m, n, seed, op_index, scale);
+  }
+  RH_CUDA(cudaGetLastError());
+}
+
+void LaunchBarrier(const BarrierArgs& b, cudaStream_t s) {
+  BarrierKernel<<<1, 32, 0, s>>>(b);
+  RH_CUDA(cudaGetLastError());
+}
+
+void LaunchZero(void* dst, size_t bytes, cudaStream_t s) {
+  if (bytes) RH_CUDA(cudaMemsetAsync(dst, 0, bytes, s));
+}
+
+}  // namespace rh

@@ -1,0 +1,109 @@
+// kernels.h — launchers of the sm_100a kernels (one translation unit per family).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.h"
+
+namespace rh {
+
+constexpr int kMaxGroup = 8;  // ranks per mesh-axis group (one B200 box)
+
+// Unsigned 32-bit division by an invariant (Granlund & Montgomery 1994, Fig. 4.1): exact for
+// every 32-bit dividend.  Used for the block-cyclic index maps inside the resharding kernels.
+struct FastDiv {
+  uint32_t d, mul, s1, s2;
+};
+FastDiv MakeFastDiv(uint32_t d);
+__host__ __device__ inline uint32_t Div(const FastDiv& f, uint32_t n) {
+#ifdef __CUDA_ARCH__
+  uint32_t t = __umulhi(f.mul, n);
+#else
+  uint32_t t = static_cast<uint32_t>((static_cast<uint64_t>(f.mul) * n) >> 32);
+#endif
+  return (t + ((n - t) >> f.s1)) >> f.s2;
+}
+
+// ------------------------------------ resharding (K9-K14) ------------------------------------
+// One rank's side of a single-axis transition in the pull form: the rank fills its destination
+// buffer (layout `to`, group coordinate `coord`) by reading the d group members' source buffers
+// (layout `from`) directly — device-local, peer (NVLink P2P / CUDA IPC) or, for the NCCL
+// baseline, sub-buffers of a staging buffer.  Partial sources are summed in rank order
+// 0..d-1 in fp32 (bf16 rounded once), matching the oracle bit for bit.
+struct PullArgs {
+  void* dst;
+  const void* src[kMaxGroup];
+  AxisView to, from;
+  int coord;
+  int64_t n_dst;  // destination elements
+  int dtype;
+};
+// Returns the number of kernel launches (0 or 1).
+int LaunchPull(const PullArgs& a, cudaStream_t s);
+
+// dst_local[l] = full[ComposedLocalToGlobal(m, l)]  (R -> any composed spec slice)
+void LaunchSliceComposed(void* dst, const void* full, const ComposedMap& m, int64_t n, int dtype,
+                         cudaStream_t s);
+// Synthetic init of one rank's local buffer (Philox4x32-10 by global flat index).
+void LaunchSynthetic(void* dst, const ComposedMap& m, int64_t n, uint64_t seed, uint32_t op_index,
+                     float scale, int dtype, cudaStream_t s);
+
+// ----------------------------------------- local ops -----------------------------------------
+constexpr int kMaxChain = 64;
+struct ChainArgs {
+  int32_t n_fn;
+  int32_t fns[kMaxChain];
+};
+// Elementwise unary chain (one fused pass).  softmax is not elementwise and has its own kernel.
+void LaunchUnaryChain(void* out, const void* in, int64_t n, const ChainArgs& c, int dtype,
+                      cudaStream_t s);
+void LaunchSoftmaxRows(void* out, const void* in, int64_t rows, int64_t cols, int dtype,
+                       cudaStream_t s);
+// out = a (+|*) b, then an optional unary chain (epilogue fusion).
+void LaunchBinary(void* out, const void* a, const void* b, int64_t n, bool mul, const ChainArgs& c,
+                  int dtype, cudaStream_t s);
+void LaunchReduceSum(void* out, const void* in, int64_t outer, int64_t e, int64_t inner, int dtype,
+                     cudaStream_t s);
+void LaunchTranspose(void* out, const void* in, int nd, const int64_t* in_dims, const int* perm,
+                     int dtype, cudaStream_t s);
+void LaunchBroadcast(void* out, const void* in, int64_t n_out, int64_t n_in, int dtype,
+                     cudaStream_t s);
+// Concat: copies `in` ([outer, row] contiguous) into out at column offset `off` of rows `orow`.
+void LaunchConcatPiece(void* out, const void* in, int64_t outer, int64_t row, int64_t orow,
+                       int64_t off, int dtype, cudaStream_t s);
+void LaunchZero(void* dst, size_t bytes, cudaStream_t s);
+
+// ------------------------------------------ GEMM (K1) ----------------------------------------
+// C[m,n] = op(A)[m,k] . op(B)[k,n]; A stored [m,k] (ta=0) or [k,m] (ta=1), B stored [k,n]
+// (tb=0) or [n,k] (tb=1); fp32 accumulation; C row-major in `dtype`; optional unary chain
+// applied in the epilogue.
+struct GemmArgs {
+  void* c;
+  const void* a;
+  const void* b;
+  int64_t m, n, k;
+  bool ta, tb;
+  int dtype;
+  ChainArgs epi;
+};
+// CUDA-core kernel (any shape/layout); the test reference for the tensor-core path.
+void LaunchGemmSimt(const GemmArgs& g, cudaStream_t s);
+// tcgen05 / TMEM / TMA kernel.  Returns false when the shape/layout is not supported by it.
+bool GemmTcSupported(const GemmArgs& g);
+void LaunchGemmTc(const GemmArgs& g, cudaStream_t s);
+
+// --------------------------------------- cross-GPU sync --------------------------------------
+// Group barrier over CUDA-IPC-mapped flag arrays (one process per GPU only: every member runs on
+// its own GPU, so the spin never waits on a kernel of the same GPU).
+struct BarrierArgs {
+  uint32_t* peer_flags[kMaxGroup];  // member k's flag array (mapped)
+  uint32_t* my_flags;               // this rank's flag array
+  uint32_t* counter;                // this rank's barrier sequence counter (device)
+  int members[kMaxGroup];           // global ranks of the group
+  int d;
+  int me;                           // my global rank
+};
+void LaunchBarrier(const BarrierArgs& b, cudaStream_t s);
+
+}  // namespace rh

@@ -59,8 +59,23 @@ rhino::LoweredProgram RandomChoice(const TensorProgram& g, const std::vector<int
     CandidateMap cand = generate_candidates(g, shapes, d, 0.0, static_cast<int>(axis));
     std::vector<AxisSpec> specs(g.size());
     for (int i = 0; i < g.size(); ++i) {
-      const auto& c = cand[i];
-      strat[axis][i] = c[rng() % c.size()];
+      // Keep only candidates whose demanded input specs are valid on the composed shape the
+      // consumer actually receives (its own input specs on earlier axes).  The planner prices
+      // each axis on the producer's effective shape (EffectiveShapes), so a random mix can
+      // demand a layout that does not exist on the consumer's side of a multi-axis edge.
+      std::vector<const OpStrategy*> ok;
+      for (const auto& c : cand[i]) {
+        bool valid = true;
+        const auto& in_idx = g.input_indices(i);
+        for (size_t slot = 0; slot < in_idx.size() && valid; ++slot) {
+          TensorShape s = g.op(in_idx[slot]).output_shape;
+          for (size_t a = 0; a < axis; ++a) s = LocalShape(s, strat[a][i].input_specs[slot], mesh[a]);
+          valid = SpecValidForShape(c.input_specs[slot], s, d);
+        }
+        if (valid) ok.push_back(&c);
+      }
+      if (ok.empty()) throw std::runtime_error("no consistent candidate for op " + g.op(i).id);
+      strat[axis][i] = *ok[rng() % ok.size()];
       specs[i] = strat[axis][i].output_spec;
     }
     chosen.push_back(specs);

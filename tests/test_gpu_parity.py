@@ -1,0 +1,172 @@
+"""GPU parity: the executor (through the C-ABI) against the CPU oracle on the same partitioned
+programs and the same Philox inputs.
+
+  * placement, index maps and pure data movement: bit-exact (per-rank local buffers);
+  * reductions / GEMM / transcendental chains: normwise max|y - y_ref| / max|y_ref| <= 1e-5 (fp32)
+    or <= 2e-2 (bf16), against the oracle's unpartitioned (single-device) result.
+Multi-rank meshes run as emulated ranks on cuda:0 (several logical ranks share one GPU; their
+collectives are pull kernels over all ranks' buffers).
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from paper_2302_08141_b200.abi import (RH_BF16, RH_FLAG_NO_FUSION, RH_FLAG_SIMT_GEMM,
+                                       RH_FLAG_UNLABELED_IDENTITY)
+from paper_2302_08141_b200.program import PLANS_DIR, LoweredProgram
+
+pytestmark = pytest.mark.gpu
+
+TOL_F32, TOL_BF16 = 1e-5, 2e-2
+SMALL = sorted(os.path.basename(p)[:-5] for p in glob.glob(os.path.join(PLANS_DIR, "*.json"))
+               if not os.path.basename(p).startswith("c3_"))
+DATA_MOVEMENT_KINDS = {0, 1, 6, 7, 9, 10}  # param, input, reshape, transpose, broadcast, concat
+
+
+def normwise(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-30)
+
+
+def as_f32(a, oracle_lib):
+    return oracle_lib.bf16_to_f32(a) if a.dtype == np.uint16 else a
+
+
+@pytest.fixture(scope="module")
+def rx():
+    from paper_2302_08141_b200 import runtime
+    return runtime
+
+
+def load(rx, prog, flags=0):
+    rt = rx.Runtime(devices=[0] * prog.world)
+    mesh = rx.Mesh(rt, prog.mesh)
+    return rt, mesh, rx.Program(mesh, prog, flags)
+
+
+def close(*objs):
+    for o in reversed(objs):
+        o.close()
+
+
+@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("flags", [0, RH_FLAG_NO_FUSION | RH_FLAG_SIMT_GEMM])
+def test_program_outputs(rx, oracle_lib, name, flags):
+    prog = LoweredProgram.load(name)
+    rt, mesh, gp = load(rx, prog, flags)
+    try:
+        gp.init_synthetic(3)
+        gp.run(2)
+        o = oracle_lib.OracleProgram(prog)
+        o.init_synthetic(3)
+        o.run_unpartitioned()
+        for out in prog.outputs:
+            got = gp.read_full(out)
+            want = o.read_full(out, partitioned=False)
+            assert normwise(got, want) <= TOL_F32, (name, prog.ops[out].id)
+    finally:
+        close(rt, mesh, gp)
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_local_buffers(rx, oracle_lib, name):
+    """Every op's per-rank local buffer vs the oracle's partitioned execution: bit-exact for
+    data-movement ops (sources: synthetic init keyed by global index), tolerance otherwise."""
+    prog = LoweredProgram.load(name)
+    rt, mesh, gp = load(rx, prog, RH_FLAG_NO_FUSION | RH_FLAG_SIMT_GEMM)
+    try:
+        gp.init_synthetic(5)
+        gp.run(1)
+        o = oracle_lib.OracleProgram(prog, keep_all=True)
+        o.init_synthetic(5)
+        o.run_partitioned()
+        exact_ops = set()
+        for op in prog.ops:  # an op is pure data movement if its whole cone is
+            if op.kind in DATA_MOVEMENT_KINDS and all(i in exact_ops for i in op.inputs):
+                exact_ops.add(op.index)
+        for op in prog.ops:
+            for r in range(prog.world):
+                got = gp.read_local(op.index, r)
+                want = o.read_local(op.index, r)
+                if op.index in exact_ops:
+                    np.testing.assert_array_equal(got, want, err_msg=f"{name}:{op.id}@{r}")
+                else:
+                    assert got.shape == want.shape
+                    assert normwise(got, want) <= TOL_F32 or np.abs(want).max() == 0, (name, op.id, r)
+    finally:
+        close(rt, mesh, gp)
+
+
+@pytest.mark.parametrize("name", ["c1_mlp_d4", "c2_mlp_reshape_d8", "c2_mlp_pinned_d4",
+                                  "rand_gpt_like_2x2_s2", "moe_small_d2"])
+def test_bf16_programs(rx, oracle_lib, name):
+    prog = LoweredProgram.load(name).with_dtype(RH_BF16)
+    rt, mesh, gp = load(rx, prog)
+    try:
+        gp.init_synthetic(7)
+        gp.run(1)
+        o = oracle_lib.OracleProgram(prog)
+        o.init_synthetic(7)
+        o.run_unpartitioned()
+        for out in prog.outputs:
+            got = oracle_lib.bf16_to_f32(gp.read_full(out))
+            want = oracle_lib.bf16_to_f32(o.read_full(out, partitioned=False))
+            assert normwise(got, want) <= TOL_BF16, name
+    finally:
+        close(rt, mesh, gp)
+
+
+def test_unlabeled_identity_flag(rx, oracle_lib):
+    prog = LoweredProgram.load("gpt_small_d2")
+    rt, mesh, gp = load(rx, prog, RH_FLAG_UNLABELED_IDENTITY)
+    try:
+        gp.init_synthetic(1)
+        gp.run(1)
+        o = oracle_lib.OracleProgram(prog, flags=RH_FLAG_UNLABELED_IDENTITY)
+        o.init_synthetic(1)
+        o.run_unpartitioned()
+        out = prog.outputs[0]
+        assert normwise(gp.read_full(out), o.read_full(out, False)) <= TOL_F32
+    finally:
+        close(rt, mesh, gp)
+
+
+def test_write_full_and_step_host(rx, oracle_lib):
+    prog = LoweredProgram.load("c1_mlp_d4")
+    rt, mesh, gp = load(rx, prog)
+    try:
+        gp.init_synthetic(0)
+        x = prog.op_index("x")
+        xin = np.random.default_rng(0).uniform(-1, 1, prog.ops[x].shape).astype(np.float32)
+        y = np.empty(prog.ops[prog.outputs[0]].shape, np.float32)
+        ms = gp.step_host([x], [xin.ctypes.data], [y.ctypes.data])
+        assert ms > 0
+        o = oracle_lib.OracleProgram(prog)
+        o.init_synthetic(0)
+        o.set_full(x, xin)
+        o.run_unpartitioned()
+        assert normwise(y, o.read_full(prog.outputs[0], False)) <= TOL_F32
+    finally:
+        close(rt, mesh, gp)
+
+
+def test_schedule_reports_transitions(rx):
+    """Wire bytes follow reshard_cost (sharding.cpp:113-135): SPEC.md:145-150 numbers."""
+    prog = LoweredProgram.load("c3_gpt_block_d8")
+    rt, mesh, gp = load(rx, prog)
+    try:
+        steps = gp.steps()
+        names = " ".join(s["name"] for s in steps)
+        for coll in ("reduce_scatter", "all_gather", "all_to_all"):
+            assert coll in names
+        rs = [s for s in steps if s["name"].startswith("reduce_scatter")][0]
+        S = 2048 * 2048 * 4
+        assert abs(rs["wire_bytes"] - 7 / 8 * S) < 1
+        a2a = [s for s in steps if s["name"].startswith("all_to_all")][0]
+        assert abs(a2a["wire_bytes"] - (2048 * 4096 * 4) / 8 * 7 / 8) < 1
+        assert gp.launch_count() > 0
+    finally:
+        close(rt, mesh, gp)
