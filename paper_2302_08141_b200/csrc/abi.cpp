@@ -118,23 +118,23 @@ void GroupSync(rh_program* p, int axis) {
   for (auto e : ev) cudaEventDestroy(e);
 }
 
-// One run of the schedule.  `prof` (optional): event pairs around every step on local rank 0's
-// stream.
-int64_t RunOnce(rh_program* p, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* prof) {
+// One run of the schedule.  `prof` (optional): n_steps + 1 boundary events recorded on local
+// rank 0's stream before every step and after the last.
+int64_t RunOnce(rh_program* p, std::vector<cudaEvent_t>* prof) {
   rh_runtime* rt = p->mesh->rt;
   int64_t launches = 0;
   const bool multi_dev = rt->devs.size() > 1;
   for (size_t si = 0; si < p->steps.size(); ++si) {
     rh::Step& st = p->steps[si];
-    if (prof) RH_CUDA(cudaEventRecord((*prof)[si].first, rt->streams[0]));
+    if (prof) RH_CUDA(cudaEventRecord((*prof)[si], rt->streams[0]));
     if (st.p2p) GroupSync(p, st.axis);
     for (int li = 0; li < rt->n_local(); ++li) {
       if (multi_dev) RH_CUDA(cudaSetDevice(rt->device_of(li)));
       launches += st.run(li, rt->stream_of(li));
     }
     if (st.p2p) GroupSync(p, st.axis);
-    if (prof) RH_CUDA(cudaEventRecord((*prof)[si].second, rt->streams[0]));
   }
+  if (prof) RH_CUDA(cudaEventRecord(prof->back(), rt->streams[0]));
   if (multi_dev) RH_CUDA(cudaSetDevice(rt->devs[0]));
   return launches;
 }
@@ -391,11 +391,16 @@ void rh_mesh_destroy(rh_mesh* mesh) {
   delete mesh;
 }
 
-int rh_program_load(rh_mesh* mesh, const rh_op* ops, int n_ops, const int* outputs, int n_out,
-                    uint32_t flags, rh_program** out) {
+}  // extern "C"
+
+namespace {
+int LoadProgram(rh_mesh* mesh, const rh_op* ops, int n_ops, const int* outputs, int n_out,
+                uint32_t flags, const std::vector<std::pair<int, Specs>>& requests,
+                rh_program** out) {
   rh_program* raw = nullptr;
   int rc = Guard([&] {
     auto p = std::make_unique<rh_program>();
+    p->requests = requests;
     p->mesh = mesh;
     p->flags = flags;
     p->n_axes = static_cast<int>(mesh->dims.size());
@@ -441,6 +446,14 @@ int rh_program_load(rh_mesh* mesh, const rh_op* ops, int n_ops, const int* outpu
   });
   if (rc == RH_OK) *out = raw;
   return rc;
+}
+}  // namespace
+
+extern "C" {
+
+int rh_program_load(rh_mesh* mesh, const rh_op* ops, int n_ops, const int* outputs, int n_out,
+                    uint32_t flags, rh_program** out) {
+  return LoadProgram(mesh, ops, n_ops, outputs, n_out, flags, {}, out);
 }
 
 void rh_program_destroy(rh_program* prog) { DestroyProgram(prog); }
@@ -519,38 +532,24 @@ int rh_program_profile(rh_program* p, int iters, double* ms_per_iter) {
     SyncAll(rt);
     DeviceGuard dg(rt->devs[0]);
     const size_t n = p->steps.size();
+    // Boundary events for every (iteration, step); no host sync inside the timed region.
+    std::vector<std::vector<cudaEvent_t>> ev(std::max(iters, 0), std::vector<cudaEvent_t>(n + 1));
+    for (auto& row : ev)
+      for (auto& e : row) RH_CUDA(cudaEventCreate(&e));
+    for (int it = 0; it < iters; ++it) RunOnce(p, &ev[it]);
+    SyncAll(rt);
     std::vector<double> acc(n, 0.0);
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev(n);
-    for (auto& e : ev) {
-      RH_CUDA(cudaEventCreate(&e.first));
-      RH_CUDA(cudaEventCreate(&e.second));
-    }
-    cudaEvent_t t0, t1;
-    RH_CUDA(cudaEventCreate(&t0));
-    RH_CUDA(cudaEventCreate(&t1));
-    double total = 0;
-    for (int it = 0; it < iters; ++it) {
-      RH_CUDA(cudaEventRecord(t0, rt->streams[0]));
-      RunOnce(p, &ev);
-      RH_CUDA(cudaEventRecord(t1, rt->streams[0]));
-      RH_CUDA(cudaEventSynchronize(t1));
-      SyncAll(rt);
+    for (int it = 0; it < iters; ++it)
       for (size_t i = 0; i < n; ++i) {
         float ms = 0;
-        RH_CUDA(cudaEventElapsedTime(&ms, ev[i].first, ev[i].second));
+        RH_CUDA(cudaEventElapsedTime(&ms, ev[it][i], ev[it][i + 1]));
         acc[i] += ms;
       }
-      float ms = 0;
-      RH_CUDA(cudaEventElapsedTime(&ms, t0, t1));
-      total += ms;
-    }
+    float total = 0;
+    if (iters > 0) RH_CUDA(cudaEventElapsedTime(&total, ev[0][0], ev[iters - 1][n]));
     for (size_t i = 0; i < n; ++i) p->steps[i].ms = iters > 0 ? acc[i] / iters : 0.0;
-    for (auto& e : ev) {
-      cudaEventDestroy(e.first);
-      cudaEventDestroy(e.second);
-    }
-    cudaEventDestroy(t0);
-    cudaEventDestroy(t1);
+    for (auto& row : ev)
+      for (auto& e : row) cudaEventDestroy(e);
     if (ms_per_iter) *ms_per_iter = iters > 0 ? total / iters : 0.0;
   });
 }
@@ -709,49 +708,34 @@ int rh_reshard(rh_mesh* mesh, int axis, rh_spec from, rh_spec to, int ndim, cons
     if (axis < 0 || axis >= static_cast<int>(mesh->dims.size())) Fail("rh_reshard: bad axis");
     if (from.kind == RH_PARTIAL && to.kind == RH_PARTIAL) Fail("rh_reshard: identity");
     const int na = static_cast<int>(mesh->dims.size());
-    // Program: x = input (spec `from` on `axis`, Replicated elsewhere) -> y = identity(x) with
-    // input demanded in `to`.  Only the transition step is timed.
+    // Program: x = input (spec `from` on `axis`, Replicated elsewhere) plus a request for x in
+    // `to`: the schedule is exactly the transition.
     std::vector<rh_spec> xs(na, rh_spec{RH_REPLICATED, -1, 0}), ys = xs;
     xs[axis] = from;
     ys[axis] = to;
-    rh_op ops[2];
-    std::memset(ops, 0, sizeof(ops));
-    int32_t in0[1] = {0};
-    for (int k = 0; k < 2; ++k) {
-      ops[k].dtype = dtype;
-      ops[k].rank = ndim;
-      for (int i = 0; i < ndim; ++i) ops[k].dims[i] = dims[i];
-    }
-    ops[0].kind = RH_OP_INPUT;
-    for (int a = 0; a < na; ++a) ops[0].out_spec[a] = xs[a];
-    ops[1].kind = RH_OP_UNARY;
-    ops[1].fn = RH_FN_IDENTITY;
-    ops[1].n_in = 1;
-    ops[1].inputs = in0;
-    for (int a = 0; a < na; ++a) ops[1].out_spec[a] = ys[a];
-    ops[1].in_specs = ys.data();
-    int outs[1] = {1};
+    rh_op op0;
+    std::memset(&op0, 0, sizeof(op0));
+    op0.kind = RH_OP_INPUT;
+    op0.dtype = dtype;
+    op0.rank = ndim;
+    for (int i = 0; i < ndim; ++i) op0.dims[i] = dims[i];
+    for (int a = 0; a < na; ++a) op0.out_spec[a] = xs[a];
+    int outs[1] = {0};
     rh_program* p = nullptr;
-    int rc = rh_program_load(mesh, ops, 2, outs, 1, flags | RH_FLAG_NO_MATERIALIZE, &p);
+    int rc = LoadProgram(mesh, &op0, 1, outs, 1, flags | RH_FLAG_NO_MATERIALIZE, {{0, ys}}, &p);
     if (rc != RH_OK) throw rh::Error(rc, g_err);
     std::unique_ptr<rh_program, void (*)(rh_program*)> guard(p, DestroyProgram);
     rh_runtime* rt = mesh->rt;
     const rh::Tensor& x = p->tensors[p->out_tensor[0]];
-    int ti = -1;  // the transition's destination tensor
-    for (size_t k = 0; k < p->tensors.size(); ++k)
-      if (p->tensors[k].op == 0 && k != static_cast<size_t>(p->out_tensor[0])) ti = static_cast<int>(k);
-    if (ti < 0) Fail("rh_reshard: no transition was scheduled");
+    const int ti = p->request_tensors.at(0);
+    if (p->steps.empty()) Fail("rh_reshard: no transition was scheduled");
     const rh::Tensor& y = p->tensors[ti];
     for (int li = 0; li < rt->n_local(); ++li) {
       DeviceGuard dg(rt->device_of(li));
       RH_CUDA(cudaMemcpy(p->base[li] + x.offset, src[li], x.bytes, cudaMemcpyDeviceToDevice));
     }
     HostBarrier(rt);
-    // warm-up, then time the transition steps only
-    p->steps.erase(std::remove_if(p->steps.begin(), p->steps.end(),
-                                  [](const rh::Step& s) { return s.kind != rh::Step::kTransition; }),
-                   p->steps.end());
-    RunOnce(p, nullptr);
+    RunOnce(p, nullptr);  // warm-up
     SyncAll(rt);
     HostBarrier(rt);
     double t = 0;

@@ -240,6 +240,7 @@ class Lowerer {
         p_->mat_tensor[o] = GetTensor(o, rep, "materialize");
       }
     }
+    for (const auto& rq : p_->requests) p_->request_tensors.push_back(GetTensor(rq.first, rq.second, "request"));
     p_->arena_bytes = arena_;
   }
 

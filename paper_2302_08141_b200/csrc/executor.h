@@ -82,6 +82,9 @@ struct rh_program {
   std::vector<rh::Tensor> tensors;
   std::vector<int> out_tensor;  // op -> tensor index (-1: fused into a successor's kernel)
   std::vector<int> mat_tensor;  // op -> materialized Replicated tensor (outputs)
+  // Extra layouts requested by the caller (rh_reshard): (op, specs) -> tensor index.
+  std::vector<std::pair<int, Specs>> requests;
+  std::vector<int> request_tensors;
   std::vector<rh::Step> steps;
 
   // memory

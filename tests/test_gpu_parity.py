@@ -170,3 +170,28 @@ def test_schedule_reports_transitions(rx):
         assert gp.launch_count() > 0
     finally:
         close(rt, mesh, gp)
+
+
+@pytest.fixture(scope="module")
+def gpt_block_reference(oracle_lib):
+    """Oracle single-device result of the C3 GPT block (fp32), computed once."""
+    prog = LoweredProgram.load("c3_gpt_block_d1")
+    o = oracle_lib.OracleProgram(prog)
+    o.init_synthetic(11)
+    o.run_unpartitioned()
+    return o.read_full(prog.outputs[0], partitioned=False)
+
+
+@pytest.mark.parametrize("name", ["c3_gpt_block_d1", "c3_gpt_block_d8", "c3_gpt_block_2x4",
+                                  "c3_gpt_block_2x2"])
+def test_gpt_block_fp32(rx, gpt_block_reference, name):
+    """C3 at full size: 893.5 GFLOP, RS + AG + A2A on the 8-rank plans, fp32 at 1e-5."""
+    prog = LoweredProgram.load(name)
+    rt, mesh, gp = load(rx, prog)
+    try:
+        gp.init_synthetic(11)
+        gp.run(1)
+        got = gp.read_full(prog.outputs[0])
+        assert normwise(got, gpt_block_reference) <= TOL_F32, name
+    finally:
+        close(rt, mesh, gp)
