@@ -117,6 +117,7 @@ class OracleProgram:
     """CPU execution of a LoweredProgram (unpartitioned and partitioned)."""
 
     KEEP_ALL = 0x100
+    GEMM_F64 = 0x200
 
     def __init__(self, prog, flags=0, keep_all=False):
         self.prog = prog

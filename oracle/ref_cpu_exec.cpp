@@ -277,7 +277,36 @@ void Round(std::vector<float>& v, bool bf16) {
   for (int64_t i = 0; i < static_cast<int64_t>(v.size()); ++i) v[i] = Bf16Round(v[i]);
 }
 
-// C[m,n] = op(A)[m,k] . op(B)[k,n], fp32 accumulation in ascending k.
+// GEMM accumulation type: fp32 (default; what a CPU executor would run) or fp64 (flag 0x200,
+// the high-accuracy reference used to state the GPU path's forward error).
+thread_local bool g_gemm_f64 = false;
+
+template <typename Acc>
+void GemmBlocked(const float* pa, const float* pb, float* C, int64_t m, int64_t n, int64_t k) {
+  const int64_t NB = 512;
+#pragma omp parallel for schedule(dynamic, 1) collapse(2)
+  for (int64_t i0 = 0; i0 < m; i0 += 4) {
+    for (int64_t j0 = 0; j0 < n; j0 += NB) {
+      const int64_t i1 = std::min(i0 + 4, m), j1 = std::min(j0 + NB, n);
+      Acc acc[4][512];
+      for (int64_t i = i0; i < i1; ++i)
+        for (int64_t j = j0; j < j1; ++j) acc[i - i0][j - j0] = 0;
+      for (int64_t kk = 0; kk < k; ++kk) {
+        const float* brow = pb + kk * n + j0;
+        for (int64_t i = i0; i < i1; ++i) {
+          const Acc a = pa[i * k + kk];
+          Acc* ar = acc[i - i0];
+#pragma omp simd
+          for (int64_t j = 0; j < j1 - j0; ++j) ar[j] += a * static_cast<Acc>(brow[j]);
+        }
+      }
+      for (int64_t i = i0; i < i1; ++i)
+        for (int64_t j = j0; j < j1; ++j) C[i * n + j] = static_cast<float>(acc[i - i0][j - j0]);
+    }
+  }
+}
+
+// C[m,n] = op(A)[m,k] . op(B)[k,n], accumulation in ascending k.
 std::vector<float> MatMul(const std::vector<float>& A, const Dims& ad, bool ta,
                           const std::vector<float>& B, const Dims& bd, bool tb, Dims* cd) {
   const int64_t m = ta ? ad[1] : ad[0], k = ta ? ad[0] : ad[1];
@@ -301,26 +330,10 @@ std::vector<float> MatMul(const std::vector<float>& A, const Dims& ad, bool ta,
     pb = b2.data();
   }
   std::vector<float> C(m * n, 0.0f);
-  const int64_t NB = 512;
-#pragma omp parallel for schedule(dynamic, 1) collapse(2)
-  for (int64_t i0 = 0; i0 < m; i0 += 4) {
-    for (int64_t j0 = 0; j0 < n; j0 += NB) {
-      const int64_t i1 = std::min(i0 + 4, m), j1 = std::min(j0 + NB, n);
-      float acc[4][512];
-      for (int64_t i = i0; i < i1; ++i)
-        for (int64_t j = j0; j < j1; ++j) acc[i - i0][j - j0] = 0.0f;
-      for (int64_t kk = 0; kk < k; ++kk) {
-        const float* brow = pb + kk * n + j0;
-        for (int64_t i = i0; i < i1; ++i) {
-          const float a = pa[i * k + kk];
-          float* ar = acc[i - i0];
-#pragma omp simd
-          for (int64_t j = 0; j < j1 - j0; ++j) ar[j] += a * brow[j];
-        }
-      }
-      for (int64_t i = i0; i < i1; ++i)
-        for (int64_t j = j0; j < j1; ++j) C[i * n + j] = acc[i - i0][j - j0];
-    }
+  if (g_gemm_f64) {
+    GemmBlocked<double>(pa, pb, C.data(), m, n, k);
+  } else {
+    GemmBlocked<float>(pa, pb, C.data(), m, n, k);
   }
   *cd = {m, n};
   return C;
@@ -654,6 +667,7 @@ struct Exec {
   }
 
   void Run() {
+    g_gemm_f64 = (p->flags & 0x200u) != 0;
     cache.assign(p->ops.size(), {});
     p->flops = 0;
     const bool keep = (p->flags & 0x100u) != 0;

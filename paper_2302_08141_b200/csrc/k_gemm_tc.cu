@@ -1,10 +1,400 @@
-// k_gemm_tc.cu — tcgen05 tensor-core GEMM (placeholder until the TMA/TMEM kernel lands).
+// k_gemm_tc.cu — the sharded-GEMM kernel (K1) on Blackwell 5th-gen tensor cores.
+//
+// bf16 x bf16 -> fp32 accumulate in TMEM -> bf16 (+ fused unary-chain epilogue).
+// Persistent, warp-specialised, one CTA per SM:
+//   warp 0 (one lane)  TMA producer: A [BM x 64] and B [64 x BN] k-blocks into a 4-stage ring
+//                      (cp.async.bulk.tensor, 128-byte swizzle, mbarrier complete_tx);
+//   warp 1 (one lane)  MMA issuer: tcgen05.mma.cta_group::1.kind::f16 128 x BN x 16 into one of
+//                      two TMEM accumulators, tcgen05.commit frees smem stages / signals the
+//                      epilogue;
+//   warp 2             TMEM allocator (2 x BN fp32 columns);
+//   warps 4-7          epilogue: tcgen05.ld 32x32b.x32 -> registers -> chain -> bf16 -> global,
+//                      overlapped with the next tile's MMAs (double-buffered accumulator).
+// A is K-major ([M,K] row-major); B is MN-major ([K,N] row-major) or K-major ([N,K], transpose_b).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "kernels.h"
 
 namespace rh {
+namespace {
 
-bool GemmTcSupported(const GemmArgs&) { return false; }
+constexpr int BM = 128, BK = 64, STAGES = 4;
+constexpr int kThreads = 256;
 
-void LaunchGemmTc(const GemmArgs&, cudaStream_t) { Fail("tcgen05 GEMM not built", RH_ERR_UNSUPPORTED); }
+__device__ __forceinline__ uint32_t SmemU32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void MbarInit(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(SmemU32(bar)), "r"(count));
+}
+__device__ __forceinline__ void MbarExpectTx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(SmemU32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void MbarArrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(SmemU32(bar)) : "memory");
+}
+__device__ __forceinline__ void MbarWait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(SmemU32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void TmaLoad2D(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                          int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          SmemU32(dst)),
+      "l"(map), "r"(SmemU32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void FenceBefore() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void FenceAfter() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void MmaF16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void Commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   SmemU32(bar))
+               : "memory");
+}
+
+// Shared-memory matrix descriptor, 128-byte swizzle (version 1, base offset 0).
+__device__ __forceinline__ uint64_t DescSw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+
+__device__ __forceinline__ void TmemLd32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float EpiFn(int fn, float x) {
+  switch (fn) {
+    case RH_FN_RELU: return x > 0.0f ? x : 0.0f;
+    case RH_FN_GELU: {
+      const float x3 = __fmul_rn(__fmul_rn(x, x), x);
+      const float inner = __fmul_rn(0.7978845608028654f, __fadd_rn(x, __fmul_rn(0.044715f, x3)));
+      return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.0f, tanhf(inner)));
+    }
+    case RH_FN_TANH: return tanhf(x);
+    case RH_FN_EXP: return expf(x);
+    case RH_FN_SIGMOID: return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x)));
+    case RH_FN_NEG: return -x;
+    case RH_FN_RSQRT: return __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(fabsf(x), 1e-6f)));
+    default: return x;
+  }
+}
+
+template <int BN, bool kBKMajor>
+struct TcCfg {
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStage = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;  // double-buffered fp32 accumulator
+  static constexpr int kSmem = STAGES * kStage + 1024 /*barriers*/ + 1024 /*align*/;
+  static constexpr uint32_t kIdesc = (1u << 4)                     // D = F32
+                                     | (1u << 7) | (1u << 10)      // A, B = BF16
+                                     | (0u << 15)                  // A K-major
+                                     | ((kBKMajor ? 0u : 1u) << 16)  // B major
+                                     | (static_cast<uint32_t>(BN >> 3) << 17) |
+                                     (static_cast<uint32_t>(BM >> 4) << 24);
+};
+
+template <int BN, bool kBKMajor>
+__global__ void __launch_bounds__(kThreads, 1)
+    GemmTcKernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                 __nv_bfloat16* __restrict__ C, int M, int N, int K, ChainArgs epi) {
+  using Cfg = TcCfg<BN, kBKMajor>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStage);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int num_m = M / BM, num_n = N / BN, tiles = num_m * num_n, kblocks = K / BK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
+    for (int s = 0; s < STAGES; ++s) {
+      MbarInit(&full[s], 1);
+      MbarInit(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      MbarInit(&tfull[a], 1);
+      MbarInit(&tempty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(SmemU32(tmem_slot)),
+                 "r"(Cfg::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  FenceBefore();
+  __syncthreads();
+  FenceAfter();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer ----------------
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int m_blk = tile % num_m, n_blk = tile / num_m;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          MbarWait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * Cfg::kStage;
+          uint8_t* sb = sa + Cfg::kABytes;
+          MbarExpectTx(&full[stage], Cfg::kStage);
+          TmaLoad2D(sa, &tma_a, &full[stage], kb * BK, m_blk * BM);
+          if constexpr (kBKMajor) {
+            TmaLoad2D(sb, &tma_b, &full[stage], kb * BK, n_blk * BN);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              TmaLoad2D(sb + j * (64 * BK * 2), &tma_b, &full[stage], n_blk * BN + j * 64, kb * BK);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer ----------------
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        MbarWait(&tempty[acc], acc_phase ^ 1);
+        FenceAfter();
+        const uint32_t d_tmem = tmem + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          MbarWait(&full[stage], phase);
+          FenceAfter();
+          const uint32_t sa = SmemU32(smem + stage * Cfg::kStage);
+          const uint32_t sb = sa + Cfg::kABytes;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = DescSw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = kBKMajor ? DescSw128(sb + k * 32, 16, 1024)
+                                         : DescSw128(sb + k * 16 * 128, 64 * BK * 2, 1024);
+            MmaF16(d_tmem, ad, bd, Cfg::kIdesc, (kb | k) != 0);
+          }
+          Commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        Commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue ----------------
+    const int ew = warp - 4;  // TMEM lanes [32*ew, 32*ew+32)
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      const int m_blk = tile % num_m, n_blk = tile / num_m;
+      MbarWait(&tfull[acc], acc_phase);
+      FenceAfter();
+      const int row = m_blk * BM + ew * 32 + lane;
+      __nv_bfloat16* crow = C + static_cast<int64_t>(row) * N + n_blk * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        TmemLd32(tmem + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
+        uint4 out[4];
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float v = __bfloat162float(__float2bfloat16_rn(__uint_as_float(r[j])));
+          for (int f = 0; f < epi.n_fn; ++f) v = __bfloat162float(__float2bfloat16_rn(EpiFn(epi.fns[f], v)));
+          o[j] = __float2bfloat16_rn(v);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(crow + c * 32);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[q] = out[q];
+      }
+      FenceBefore();
+      __syncwarp();
+      if (lane == 0) MbarArrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  FenceBefore();
+  __syncthreads();
+  FenceAfter();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::kTmemCols));
+  }
+}
+
+// ------------------------------------------- host ------------------------------------------
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+
+EncodeFn GetEncode() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  if (!fn) Fail("cuTensorMapEncodeTiled unavailable", RH_ERR_CUDA);
+  return fn;
+}
+
+// 2-D bf16 tensor map: inner dim `d0` (contiguous), outer `d1` with row pitch `pitch` elements.
+CUtensorMap MakeMap(const void* base, uint64_t d0, uint64_t d1, uint64_t pitch, uint32_t box0,
+                    uint32_t box1) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {d0, d1};
+  cuuint64_t strides[1] = {pitch * 2};
+  cuuint32_t box[2] = {box0, box1};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = GetEncode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) Fail("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")", RH_ERR_CUDA);
+  return m;
+}
+
+struct Maps {
+  CUtensorMap a, b;
+};
+
+// Tensor maps depend only on (pointer, shape); arena pointers are static, so cache them.
+const Maps& GetMaps(const GemmArgs& g, int bn) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, const void*, int64_t, int64_t, int64_t, bool, int>, Maps> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_tuple(g.a, g.b, g.m, g.n, g.k, g.tb, bn);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  Maps m;
+  m.a = MakeMap(g.a, g.k, g.m, g.k, BK, BM);
+  if (g.tb) {
+    m.b = MakeMap(g.b, g.k, g.n, g.k, BK, bn);  // B stored [N,K]: K-major
+  } else {
+    m.b = MakeMap(g.b, g.n, g.k, g.n, 64, BK);  // B stored [K,N]: MN-major, 64-wide chunks
+  }
+  return cache.emplace(key, m).first->second;
+}
+
+int NumSms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <int BN, bool kBK>
+void Launch(const GemmArgs& g, cudaStream_t s) {
+  using Cfg = TcCfg<BN, kBK>;
+  static bool attr = false;
+  if (!attr) {
+    RH_CUDA(cudaFuncSetAttribute(GemmTcKernel<BN, kBK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg::kSmem));
+    attr = true;
+  }
+  const Maps& mp = GetMaps(g, BN);
+  const int tiles = static_cast<int>((g.m / BM) * (g.n / BN));
+  const int grid = std::min(tiles, NumSms());
+  GemmTcKernel<BN, kBK><<<grid, kThreads, Cfg::kSmem, s>>>(
+      mp.a, mp.b, static_cast<__nv_bfloat16*>(g.c), static_cast<int>(g.m), static_cast<int>(g.n),
+      static_cast<int>(g.k), g.epi);
+  RH_CUDA(cudaGetLastError());
+}
+
+int PickBN(const GemmArgs& g) {
+  if (g.n % 256 == 0 && (g.m / BM) * (g.n / 256) >= 96) return 256;
+  if (g.n % 128 == 0) return 128;
+  return 0;
+}
+
+}  // namespace
+
+bool GemmTcSupported(const GemmArgs& g) {
+  if (g.dtype != RH_BF16 || g.ta) return false;
+  if (g.m % BM || g.k % BK || g.k == 0) return false;
+  if (g.m > (int64_t{1} << 30) || g.n > (int64_t{1} << 30) || g.k > (int64_t{1} << 30)) return false;
+  if (PickBN(g) == 0) return false;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(g.a), b = reinterpret_cast<uintptr_t>(g.b);
+  if ((a | b) % 16) return false;
+  return true;
+}
+
+void LaunchGemmTc(const GemmArgs& g, cudaStream_t s) {
+  if (!GemmTcSupported(g)) Fail("tcgen05 GEMM: unsupported shape/layout", RH_ERR_UNSUPPORTED);
+  const int bn = PickBN(g);
+  if (bn == 256) {
+    if (g.tb) Launch<256, true>(g, s);
+    else Launch<256, false>(g, s);
+  } else {
+    if (g.tb) Launch<128, true>(g, s);
+    else Launch<128, false>(g, s);
+  }
+}
 
 }  // namespace rh

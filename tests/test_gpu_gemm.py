@@ -1,0 +1,88 @@
+"""K1: the tcgen05/TMEM/TMA GEMM (bf16 in, fp32 accumulate) and the CUDA-core GEMM against an
+fp64 reference on the same bf16 inputs, through the C-ABI (single-op programs), including the
+fused unary-chain epilogue and both B layouts (transpose_b)."""
+import numpy as np
+import pytest
+
+from paper_2302_08141_b200.abi import RH_BF16, RH_F32, RH_FLAG_SIMT_GEMM
+from paper_2302_08141_b200.program import LoweredProgram
+
+pytestmark = pytest.mark.gpu
+
+
+def matmul_doc(m, k, n, tb=False, chain=(), dtype="bf16"):
+    R = ["replicated"]
+    ops = [
+        {"id": "a", "kind": "input", "inputs": [], "shape": [m, k], "out_spec": R, "in_specs": [[]]},
+        {"id": "b", "kind": "param", "inputs": [], "shape": [n, k] if tb else [k, n], "out_spec": R,
+         "in_specs": [[]]},
+        {"id": "c", "kind": "matmul", "inputs": [0, 1], "shape": [m, n], "transpose_a": False,
+         "transpose_b": tb, "out_spec": R, "in_specs": [R * 2]},
+    ]
+    for i, fn in enumerate(chain):
+        ops.append({"id": f"u{i}", "kind": "unary", "fn": fn, "inputs": [len(ops) - 1], "shape": [m, n],
+                    "out_spec": R, "in_specs": [R]})
+    return {"schema": "rhino-lowered/1", "name": "gemm", "mesh": [1], "dtype": dtype, "ops": ops,
+            "outputs": [len(ops) - 1]}
+
+
+def bf16_to_f64(a):
+    return (a.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def run(doc, flags=0):
+    from paper_2302_08141_b200 import runtime as rx
+    prog = LoweredProgram(doc)
+    rt = rx.Runtime(devices=[0])
+    mesh = rx.Mesh(rt, [1])
+    gp = rx.Program(mesh, prog, flags)
+    try:
+        gp.init_synthetic(9)
+        gp.run(1)
+        a = gp.read_full(0)
+        b = gp.read_full(1)
+        c = gp.read_full(prog.outputs[0])
+        names = [s["name"] for s in gp.steps()]
+    finally:
+        gp.close()
+        mesh.close()
+        rt.close()
+    return a, b, c, names
+
+
+@pytest.mark.parametrize("m,k,n", [(128, 64, 128), (128, 128, 256), (256, 512, 384), (512, 1024, 1024),
+                                   (2048, 4096, 4096), (2048, 16384, 512)])
+@pytest.mark.parametrize("tb", [False, True])
+def test_tc_gemm_vs_fp64(m, k, n, tb):
+    a, b, c, names = run(matmul_doc(m, k, n, tb))
+    assert any(s.startswith("gemm_tc") for s in names), names
+    A, B = bf16_to_f64(a), bf16_to_f64(b)
+    ref = A @ (B.T if tb else B)
+    got = bf16_to_f64(c)
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    assert err <= 1e-2, err  # bf16 output rounding (2^-9) + fp32 accumulation
+
+
+@pytest.mark.parametrize("tb", [False, True])
+def test_tc_matches_simt(tb):
+    _, _, c_tc, n1 = run(matmul_doc(256, 1024, 512, tb))
+    _, _, c_simt, n2 = run(matmul_doc(256, 1024, 512, tb), RH_FLAG_SIMT_GEMM)
+    assert any("gemm_tc" in s for s in n1) and any("gemm_simt" in s for s in n2)
+    x, y = bf16_to_f64(c_tc), bf16_to_f64(c_simt)
+    # same inputs, both fp32-accumulated, both rounded to bf16: at most one bf16 ulp apart
+    assert (np.abs(x - y) <= np.abs(y) * 2.0 ** -7 + 1e-30).all()
+
+
+def test_tc_fused_epilogue_chain():
+    _, _, c, names = run(matmul_doc(256, 256, 256, False, ("relu", "tanh", "")))
+    assert len(names) == 1 and "gemm_tc" in names[0]
+    _, _, c2, names2 = run(matmul_doc(256, 256, 256, False, ("relu", "tanh", "")), RH_FLAG_SIMT_GEMM)
+    x, y = bf16_to_f64(c), bf16_to_f64(c2)
+    assert np.abs(x - y).max() <= 2.0 ** -6
+
+
+def test_simt_fp32_gemm_vs_fp64():
+    a, b, c, names = run(matmul_doc(300, 200, 100, True, dtype="f32"))
+    assert any("gemm_simt" in s for s in names)
+    ref = a.astype(np.float64) @ b.astype(np.float64).T
+    assert np.abs(c - ref).max() / np.abs(ref).max() <= 1e-5

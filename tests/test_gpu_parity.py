@@ -174,24 +174,54 @@ def test_schedule_reports_transitions(rx):
 
 @pytest.fixture(scope="module")
 def gpt_block_reference(oracle_lib):
-    """Oracle single-device result of the C3 GPT block (fp32), computed once."""
+    """Oracle single-device results of the C3 GPT block (fp32), computed once: GEMMs accumulated
+    in fp64 (the high-accuracy reference) and in fp32 (what a correct fp32 executor computes)."""
     prog = LoweredProgram.load("c3_gpt_block_d1")
-    o = oracle_lib.OracleProgram(prog)
-    o.init_synthetic(11)
-    o.run_unpartitioned()
-    return o.read_full(prog.outputs[0], partitioned=False)
+    out = {}
+    for key, flags in (("f64", oracle_lib.OracleProgram.GEMM_F64), ("f32", 0)):
+        o = oracle_lib.OracleProgram(prog, flags=flags)
+        o.init_synthetic(11)
+        o.run_unpartitioned()
+        out[key] = o.read_full(prog.outputs[0], partitioned=False)
+    return out
 
 
 @pytest.mark.parametrize("name", ["c3_gpt_block_d1", "c3_gpt_block_d8", "c3_gpt_block_2x4",
                                   "c3_gpt_block_2x2"])
 def test_gpt_block_fp32(rx, gpt_block_reference, name):
-    """C3 at full size: 893.5 GFLOP, RS + AG + A2A on the 8-rank plans, fp32 at 1e-5."""
+    """C3 at full size: 893.5 GFLOP, RS + AG + A2A on the 8-rank plans, fp32.
+
+    Tolerance: 108 ops with K up to 16384 put any fp32-accumulating
+    execution ~6e-5 (normwise) away from the fp64-accumulated result — the fp32 oracle itself
+    is.  The executor must be within max(1e-5, 2 x that fp32 oracle error) of the fp64 oracle."""
+    ref = gpt_block_reference["f64"]
+    tol = max(TOL_F32, 2.0 * normwise(gpt_block_reference["f32"], ref))
+    assert tol <= 2e-4
     prog = LoweredProgram.load(name)
     rt, mesh, gp = load(rx, prog)
     try:
         gp.init_synthetic(11)
         gp.run(1)
         got = gp.read_full(prog.outputs[0])
-        assert normwise(got, gpt_block_reference) <= TOL_F32, name
+        assert normwise(got, ref) <= tol, (name, normwise(got, ref), tol)
     finally:
         close(rt, mesh, gp)
+
+
+@pytest.mark.parametrize("name", ["c3_gpt_block_d1", "c3_gpt_block_d8"])
+def test_gpt_block_bf16(rx, oracle_lib, name):
+    """The bench configuration (bf16, tcgen05 GEMMs) against the bf16 oracle at 2e-2."""
+    prog = LoweredProgram.load(name).with_dtype(RH_BF16)
+    rt, mesh, gp = load(rx, prog)
+    try:
+        gp.init_synthetic(13)
+        gp.run(1)
+        got = oracle_lib.bf16_to_f32(gp.read_full(prog.outputs[0]))
+        assert any("gemm_tc" in s["name"] for s in gp.steps())
+    finally:
+        close(rt, mesh, gp)
+    o = oracle_lib.OracleProgram(LoweredProgram.load("c3_gpt_block_d1").with_dtype(RH_BF16))
+    o.init_synthetic(13)
+    o.run_unpartitioned()
+    want = oracle_lib.bf16_to_f32(o.read_full(prog.outputs[0], partitioned=False))
+    assert normwise(got, want) <= TOL_BF16, normwise(got, want)
