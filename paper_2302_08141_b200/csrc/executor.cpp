@@ -352,8 +352,16 @@ class Lowerer {
         absorbed_[v] = true;
         cur = v;
       }
+      // The GEMM epilogue runs on 4 warps per SM: only short chains ride in it; a longer chain
+      // runs as one full-occupancy elementwise kernel instead (same HBM traffic, 10x the issue
+      // rate for its transcendental work).
+      if (op.kind == RH_OP_MATMUL && chain_[h].size() > kMaxGemmEpilogue) {
+        for (int v : chain_[h]) absorbed_[v] = false;
+        chain_[h].clear();
+      }
     }
   }
+  static constexpr size_t kMaxGemmEpilogue = 2;
 
   int UnaryFn(int i) const {
     int fn = p_->ops[i].fn;

@@ -10,38 +10,14 @@
 #include <algorithm>
 
 #include "kernels.h"
+#include "unary.cuh"
 
 namespace rh {
 namespace {
 
-__device__ __forceinline__ float ApplyFn(int fn, float x) {
-  switch (fn) {
-    case RH_FN_RELU: return x > 0.0f ? x : 0.0f;
-    case RH_FN_GELU: {
-      const float x3 = __fmul_rn(__fmul_rn(x, x), x);
-      const float inner = __fmul_rn(0.7978845608028654f, __fadd_rn(x, __fmul_rn(0.044715f, x3)));
-      return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.0f, tanhf(inner)));
-    }
-    case RH_FN_TANH: return tanhf(x);
-    case RH_FN_EXP: return expf(x);
-    case RH_FN_SIGMOID: return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x)));
-    case RH_FN_NEG: return -x;
-    case RH_FN_RSQRT: return __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(fabsf(x), 1e-6f)));
-    default: return x;  // identity
-  }
-}
-
-__device__ __forceinline__ float RoundBf16(float x) {
-  return __bfloat162float(__float2bfloat16_rn(x));
-}
-
 template <bool kBf16>
 __device__ __forceinline__ float ApplyChain(const ChainArgs& c, float x) {
-  for (int i = 0; i < c.n_fn; ++i) {
-    x = ApplyFn(c.fns[i], x);
-    if (kBf16) x = RoundBf16(x);
-  }
-  return x;
+  return ApplyChainFns<kBf16>(c.fns, c.n_fn, x);
 }
 
 // 16-byte packets: 4 fp32 or 8 bf16.

@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 
 #include "kernels.h"
+#include "unary.cuh"
 
 namespace rh {
 namespace {
@@ -19,23 +20,6 @@ __device__ __forceinline__ float Ld<float>(const float* p, int64_t i) {
 template <>
 __device__ __forceinline__ float Ld<__nv_bfloat16>(const __nv_bfloat16* p, int64_t i) {
   return __bfloat162float(p[i]);
-}
-
-__device__ __forceinline__ float Fn(int fn, float x) {
-  switch (fn) {
-    case RH_FN_RELU: return x > 0.0f ? x : 0.0f;
-    case RH_FN_GELU: {
-      const float x3 = __fmul_rn(__fmul_rn(x, x), x);
-      const float inner = __fmul_rn(0.7978845608028654f, __fadd_rn(x, __fmul_rn(0.044715f, x3)));
-      return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.0f, tanhf(inner)));
-    }
-    case RH_FN_TANH: return tanhf(x);
-    case RH_FN_EXP: return expf(x);
-    case RH_FN_SIGMOID: return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x)));
-    case RH_FN_NEG: return -x;
-    case RH_FN_RSQRT: return __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(fabsf(x), 1e-6f)));
-    default: return x;
-  }
 }
 
 template <typename T, bool TA, bool TB>
@@ -117,11 +101,8 @@ __global__ void __launch_bounds__(256) GemmSimtKernel(T* __restrict__ C, const T
       const int64_t gn = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
       if (gn >= N) continue;
       float v = acc[i][j];
-      if constexpr (sizeof(T) == 2) v = __bfloat162float(__float2bfloat16_rn(v));
-      for (int f = 0; f < epi.n_fn; ++f) {
-        v = Fn(epi.fns[f], v);
-        if constexpr (sizeof(T) == 2) v = __bfloat162float(__float2bfloat16_rn(v));
-      }
+      if constexpr (sizeof(T) == 2) v = RoundBf16(v);
+      v = ApplyChainFns<sizeof(T) == 2>(epi.fns, epi.n_fn, v);
       if constexpr (sizeof(T) == 2) {
         C[gm * N + gn] = __float2bfloat16_rn(v);
       } else {

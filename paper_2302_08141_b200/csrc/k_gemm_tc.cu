@@ -20,6 +20,7 @@
 #include <tuple>
 
 #include "kernels.h"
+#include "unary.cuh"
 
 namespace rh {
 namespace {
@@ -105,23 +106,6 @@ __device__ __forceinline__ void TmemLd32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-__device__ __forceinline__ float EpiFn(int fn, float x) {
-  switch (fn) {
-    case RH_FN_RELU: return x > 0.0f ? x : 0.0f;
-    case RH_FN_GELU: {
-      const float x3 = __fmul_rn(__fmul_rn(x, x), x);
-      const float inner = __fmul_rn(0.7978845608028654f, __fadd_rn(x, __fmul_rn(0.044715f, x3)));
-      return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.0f, tanhf(inner)));
-    }
-    case RH_FN_TANH: return tanhf(x);
-    case RH_FN_EXP: return expf(x);
-    case RH_FN_SIGMOID: return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x)));
-    case RH_FN_NEG: return -x;
-    case RH_FN_RSQRT: return __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(fabsf(x), 1e-6f)));
-    default: return x;
-  }
 }
 
 template <int BN, bool kBKMajor>
@@ -255,8 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out);
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          float v = __bfloat162float(__float2bfloat16_rn(__uint_as_float(r[j])));
-          for (int f = 0; f < epi.n_fn; ++f) v = __bfloat162float(__float2bfloat16_rn(EpiFn(epi.fns[f], v)));
+          float v = ApplyChainFns<true>(epi.fns, epi.n_fn, RoundBf16(__uint_as_float(r[j])));
           o[j] = __float2bfloat16_rn(v);
         }
         uint4* dst = reinterpret_cast<uint4*>(crow + c * 32);

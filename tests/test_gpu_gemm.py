@@ -69,8 +69,10 @@ def test_tc_matches_simt(tb):
     _, _, c_simt, n2 = run(matmul_doc(256, 1024, 512, tb), RH_FLAG_SIMT_GEMM)
     assert any("gemm_tc" in s for s in n1) and any("gemm_simt" in s for s in n2)
     x, y = bf16_to_f64(c_tc), bf16_to_f64(c_simt)
-    # same inputs, both fp32-accumulated, both rounded to bf16: at most one bf16 ulp apart
-    assert (np.abs(x - y) <= np.abs(y) * 2.0 ** -7 + 1e-30).all()
+    # same inputs, both fp32-accumulated (different orders), both rounded to bf16: the results
+    # differ by at most one bf16 rounding step relative to the output scale
+    assert np.abs(x - y).max() <= 2.0 ** -8 * np.abs(y).max()
+    assert (x == y).mean() > 0.9
 
 
 def test_tc_fused_epilogue_chain():
