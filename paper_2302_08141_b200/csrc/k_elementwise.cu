@@ -66,21 +66,43 @@ __device__ __forceinline__ void StoreScalar(void* p, int64_t i, float x) {
   }
 }
 
+// Each thread owns two 16-byte packets per iteration (16 bf16 / 8 fp32 elements) so the chain's
+// dependent ops of independent elements interleave.
 template <bool kBf16>
 __global__ void __launch_bounds__(256) UnaryChainKernel(void* out, const void* in, int64_t n,
                                                         ChainArgs c) {
   constexpr int E = Pack<kBf16>::E;
   const int64_t nv = n / E;
+  const int64_t npair = nv / 2;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nv; i += stride) {
-    Pack<kBf16> p;
-    p.Load(in, i);
-#pragma unroll
-    for (int e = 0; e < E; ++e) p.v[e] = ApplyChain<kBf16>(c, p.v[e]);
-    p.Store(out, i);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npair; i += stride) {
+    const uint4 u0 = reinterpret_cast<const uint4*>(in)[2 * i];
+    const uint4 u1 = reinterpret_cast<const uint4*>(in)[2 * i + 1];
+    if constexpr (kBf16) {
+      uint32_t p[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+      ApplyChainPackedBf16<8>(c.fns, c.n_fn, p);
+      reinterpret_cast<uint4*>(out)[2 * i] = make_uint4(p[0], p[1], p[2], p[3]);
+      reinterpret_cast<uint4*>(out)[2 * i + 1] = make_uint4(p[4], p[5], p[6], p[7]);
+    } else {
+      float v[8] = {__uint_as_float(u0.x), __uint_as_float(u0.y), __uint_as_float(u0.z),
+                    __uint_as_float(u0.w), __uint_as_float(u1.x), __uint_as_float(u1.y),
+                    __uint_as_float(u1.z), __uint_as_float(u1.w)};
+      ApplyChainVecF32<8>(c.fns, c.n_fn, v);
+      reinterpret_cast<float4*>(out)[2 * i] = make_float4(v[0], v[1], v[2], v[3]);
+      reinterpret_cast<float4*>(out)[2 * i + 1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
   }
-  for (int64_t i = nv * E + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride)
-    StoreScalar<kBf16>(out, i, ApplyChain<kBf16>(c, LoadScalar<kBf16>(in, i)));
+  for (int64_t i = npair * 2 * E + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    if constexpr (kBf16) {
+      uint32_t p[1] = {static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(in)[i])};
+      ApplyChainPackedBf16<1>(c.fns, c.n_fn, p);
+      reinterpret_cast<uint16_t*>(out)[i] = static_cast<uint16_t>(p[0] & 0xffffu);
+    } else {
+      float v[1] = {reinterpret_cast<const float*>(in)[i]};
+      ApplyChainVecF32<1>(c.fns, c.n_fn, v);
+      reinterpret_cast<float*>(out)[i] = v[0];
+    }
+  }
 }
 
 template <bool kBf16>
@@ -94,12 +116,17 @@ __global__ void __launch_bounds__(256) BinaryKernel(void* out, const void* a, co
     x.Load(a, i);
     y.Load(b, i);
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      float r = mul ? __fmul_rn(x.v[e], y.v[e]) : __fadd_rn(x.v[e], y.v[e]);
-      if (kBf16) r = RoundBf16(r);
-      x.v[e] = ApplyChain<kBf16>(c, r);
+    for (int e = 0; e < E; ++e) x.v[e] = mul ? __fmul_rn(x.v[e], y.v[e]) : __fadd_rn(x.v[e], y.v[e]);
+    if constexpr (kBf16) {
+      uint32_t p[E / 2];
+#pragma unroll
+      for (int e = 0; e < E / 2; ++e) p[e] = PackBf16x2(x.v[2 * e], x.v[2 * e + 1]);
+      ApplyChainPackedBf16<E / 2>(c.fns, c.n_fn, p);
+      reinterpret_cast<uint4*>(out)[i] = make_uint4(p[0], p[1], p[2], p[3]);
+    } else {
+      ApplyChainVecF32<E>(c.fns, c.n_fn, x.v);
+      x.Store(out, i);
     }
-    x.Store(out, i);
   }
   for (int64_t i = nv * E + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
     float xa = LoadScalar<kBf16>(a, i), xb = LoadScalar<kBf16>(b, i);

@@ -53,4 +53,72 @@ __device__ __forceinline__ float ApplyChainFns(const int32_t* fns, int n, float 
   return x;
 }
 
+// fp32 chain over E independent elements: the (warp-uniform) fn switch sits outside the
+// element loop so the E elements' dependency chains interleave (ILP E).
+template <int E>
+__device__ __forceinline__ void ApplyChainVecF32(const int32_t* fns, int n, float (&v)[E]) {
+  for (int i = 0; i < n; ++i) {
+    const int fn = fns[i];
+    switch (fn) {
+      case RH_FN_TANH:
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = tanhf(v[e]);
+        break;
+      case RH_FN_IDENTITY:
+        break;
+      default:
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = ApplyFn<false>(fn, v[e]);
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t TanhBf16x2(uint32_t x) {
+  uint32_t y;
+  asm("tanh.approx.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t ReluBf16x2(uint32_t x) {
+  uint32_t y;
+  asm("max.bf16x2 %0, %1, %2;" : "=r"(y) : "r"(x), "r"(0u));
+  return y;
+}
+__device__ __forceinline__ uint32_t PackBf16x2(float lo, float hi) {
+  uint32_t y;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(y) : "f"(hi), "f"(lo));
+  return y;
+}
+
+// bf16 chain over P packed bf16x2 registers (2P elements).  tanh / relu / neg / identity stay
+// in packed bf16 (tanh.approx.bf16x2: one SFU op per two elements, result already bf16); other
+// fns unpack to fp32, apply, and round back — every op's result is a bf16 value.
+template <int P>
+__device__ __forceinline__ void ApplyChainPackedBf16(const int32_t* fns, int n, uint32_t (&p)[P]) {
+  for (int i = 0; i < n; ++i) {
+    const int fn = fns[i];
+    switch (fn) {
+      case RH_FN_TANH:
+#pragma unroll
+        for (int e = 0; e < P; ++e) p[e] = TanhBf16x2(p[e]);
+        break;
+      case RH_FN_RELU:
+#pragma unroll
+        for (int e = 0; e < P; ++e) p[e] = ReluBf16x2(p[e]);
+        break;
+      case RH_FN_NEG:
+#pragma unroll
+        for (int e = 0; e < P; ++e) p[e] ^= 0x80008000u;
+        break;
+      case RH_FN_IDENTITY:
+        break;
+      default:
+#pragma unroll
+        for (int e = 0; e < P; ++e) {
+          const float lo = __uint_as_float(p[e] << 16), hi = __uint_as_float(p[e] & 0xffff0000u);
+          p[e] = PackBf16x2(ApplyFn<true>(fn, lo), ApplyFn<true>(fn, hi));
+        }
+    }
+  }
+}
+
 }  // namespace rh

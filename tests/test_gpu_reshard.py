@@ -41,6 +41,8 @@ def test_all_transitions_bit_exact(oracle_lib, d, dtype):
             if a == b or (a == "partial" and b == "partial"):
                 continue
             fs, ts = spec_of(a, dims, d), spec_of(b, dims, d)
+            if fs == ts:  # e.g. shard(0,8) == shard(0,max) on 64 rows at d=8
+                continue
             n_src, n_dst = local_elems(fs, dims, d), local_elems(ts, dims, d)
             srcs = []
             for r in range(d):
