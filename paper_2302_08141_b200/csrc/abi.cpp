@@ -205,7 +205,10 @@ void DestroyProgram(rh_program* p) {
   } catch (...) {
   }
   if (p->ipc_opened) {
-    HostBarrier(rt);
+    try {
+      HostBarrier(rt);  // peers must be done reading this arena before it is unmapped/freed
+    } catch (...) {
+    }
     for (int r = 0; r < rt->world; ++r)
       if (r != rt->first_rank && p->peer_base[r]) cudaIpcCloseMemHandle(p->peer_base[r]);
   }
@@ -353,6 +356,9 @@ void rh_runtime_destroy(rh_runtime* rt) {
     cudaStreamSynchronize(rt->streams[i]);
     cudaStreamDestroy(rt->streams[i]);
   }
+  for (auto& e : rt->axis_comms)
+    for (auto c : e.second)
+      if (c) ncclCommDestroy(c);
   if (rt->world_comm) ncclCommDestroy(rt->world_comm);
   delete rt;
 }
@@ -370,14 +376,19 @@ int rh_mesh_create(rh_runtime* rt, int n_axes, const int* dims, rh_mesh** out) {
     }
     if (prod != rt->world) Fail("rh_mesh_create: prod(dims) != world size");
     if (rt->dist) {
-      const std::vector<int> c = m->Coords(rt->first_rank);
-      for (int a = 0; a < n_axes; ++a) {
-        int color = 0;
-        for (int b = 0; b < n_axes; ++b)
-          if (b != a) color = color * m->dims[b] + c[b];
-        ncclComm_t comm = nullptr;
-        RH_NCCL(ncclCommSplit(rt->world_comm, color, c[a], &comm, nullptr));
-        m->axis_comm.push_back(comm);
+      for (const auto& e : rt->axis_comms)
+        if (e.first == m->dims) m->axis_comm = e.second;
+      if (m->axis_comm.empty()) {
+        const std::vector<int> c = m->Coords(rt->first_rank);
+        for (int a = 0; a < n_axes; ++a) {
+          int color = 0;
+          for (int b = 0; b < n_axes; ++b)
+            if (b != a) color = color * m->dims[b] + c[b];
+          ncclComm_t comm = nullptr;
+          RH_NCCL(ncclCommSplit(rt->world_comm, color, c[a], &comm, nullptr));
+          m->axis_comm.push_back(comm);
+        }
+        rt->axis_comms.emplace_back(m->dims, m->axis_comm);
       }
     }
     *out = m.release();
@@ -385,10 +396,7 @@ int rh_mesh_create(rh_runtime* rt, int n_axes, const int* dims, rh_mesh** out) {
 }
 
 void rh_mesh_destroy(rh_mesh* mesh) {
-  if (!mesh) return;
-  for (auto c : mesh->axis_comm)
-    if (c) ncclCommDestroy(c);
-  delete mesh;
+  delete mesh;  // axis communicators belong to the runtime (shared across meshes)
 }
 
 }  // extern "C"

@@ -22,6 +22,9 @@ struct rh_runtime {
   std::vector<int> devs;      // distinct CUDA device ids
   std::vector<cudaStream_t> streams;  // one per distinct device
   ncclComm_t world_comm = nullptr;    // dist only
+  // Mesh-axis communicators (ncclCommSplit of world_comm), created once per (dims, axis) and
+  // shared by every mesh with those dims: communicators are costly (NVLS/P2P resources).
+  std::vector<std::pair<std::vector<int>, std::vector<ncclComm_t>>> axis_comms;
   int n_local() const { return static_cast<int>(rank_dev.size()); }
   cudaStream_t stream_of(int li) const { return streams[rank_dev[li]]; }
   int device_of(int li) const { return devs[rank_dev[li]]; }

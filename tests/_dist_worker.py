@@ -42,9 +42,10 @@ def check(rt, name, flags, dtype=None):
         if key not in _ORACLES:
             o = pyoracle.OracleProgram(prog, keep_all=True)
             o.init_synthetic(21)
-            o.run_unpartitioned()
+            threads = max(1, (os.cpu_count() or 2) // max(1, rt.world))  # torchrun sets OMP=1
+            o.run_unpartitioned(threads)
             if not name.startswith("c3_"):
-                o.run_partitioned()
+                o.run_partitioned(threads)
             _ORACLES[key] = o
         o = _ORACLES[key]
         bf = prog.dtype == RH_BF16
