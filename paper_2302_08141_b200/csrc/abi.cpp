@@ -164,7 +164,9 @@ void Allocate(rh_program* p) {
     DeviceGuard dg(rt->device_of(li));
     void* ptr = nullptr;
     RH_CUDA(cudaMalloc(&ptr, bytes));
-    RH_CUDA(cudaMemset(ptr, 0, bytes));
+    // zero on the rank's own (non-blocking) stream so later work is ordered after it
+    RH_CUDA(cudaMemsetAsync(ptr, 0, bytes, rt->stream_of(li)));
+    RH_CUDA(cudaStreamSynchronize(rt->stream_of(li)));
     p->base[li] = static_cast<char*>(ptr);
     p->owned.push_back(ptr);
   }

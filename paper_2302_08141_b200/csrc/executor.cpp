@@ -669,7 +669,7 @@ class Lowerer {
           for (int k = 0; k < d; ++k) {
             PullArgs a{};
             a.dst = stage + static_cast<size_t>(k) * chunk * eb;
-            a.src[coord] = x;
+            for (int j = 0; j < d; ++j) a.src[j] = x;  // Replicated view: any coordinate reads x
             a.from = rep;
             a.to = tv;
             a.coord = k;

@@ -29,6 +29,7 @@ def normwise(a, b):
 
 
 def check(rt, name, flags, dtype=None):
+    print(f"[dist r{rt.first_rank}] {name} flags={flags} dtype={dtype}", file=sys.stderr, flush=True)
     prog = LoweredProgram.load(name)
     if dtype is not None:
         prog = prog.with_dtype(dtype)
