@@ -36,5 +36,9 @@ def test_dist_parity(world):
     lines = [l for l in r.stdout.splitlines() if l.startswith("DIST_RESULT ")]
     assert r.returncode == 0 and lines, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.loads(lines[0][len("DIST_RESULT "):])
+    out_dir = os.path.join(os.path.dirname(HERE), "gpurun_out")
+    if os.path.isdir(out_dir):
+        with open(os.path.join(out_dir, f"dist_parity_{world}.json"), "w") as f:
+            json.dump(res, f, indent=1)
     bad = [x for x in res if not x["ok"]]
     assert not bad, bad
