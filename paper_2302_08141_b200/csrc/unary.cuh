@@ -3,9 +3,10 @@
 //
 // fp32 programs: IEEE-rounded fp32 arithmetic in the order below (explicit _rn intrinsics, no
 // FMA contraction) and CUDA's accurate tanhf/expf (<= 2 ulp from glibc's).
-// bf16 programs: the same formulas with the SFU approximations (tanh.approx.f32, ex2-based
-// __expf, rsqrtf; relative error <= 2^-10.7, below half a bf16 ulp) and the result of every op
-// rounded to bf16 — the per-op rounding the oracle applies.
+// bf16 programs: the same formulas evaluated to ~2^-20 relative error with SFU-based code
+// (FastTanh below, ex2-based __expf, rsqrtf) and the result of every op rounded to bf16 — the
+// per-op rounding the oracle applies; the bf16 results then equal the oracle's correctly rounded
+// ones except in rare boundary cases.
 #pragma once
 
 #include <cuda_bf16.h>
@@ -14,10 +15,22 @@
 
 namespace rh {
 
+// tanh for the bf16 path: relative error < 2^-20 (an odd Taylor polynomial below |x| = 1/4,
+// 1 - 2 / (1 + 2^(2|x| log2 e)) with the SFU ex2 / rcp above), so rounding the result to bf16
+// reproduces the correctly rounded value except within 2^-20 of a rounding boundary.  The raw
+// tanh.approx.f32 (2^-11) is NOT used: its 1-ulp bf16 misroundings compound through the
+// fixture's 12-36-op tanh chains and the attention GEMMs (measured: 0.3 normwise on the block).
 __device__ __forceinline__ float FastTanh(float x) {
-  float y;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
+  const float ax = fabsf(x);
+  if (ax < 0.25f) {
+    const float x2 = x * x;
+    return x * fmaf(x2, fmaf(x2, fmaf(x2, fmaf(x2, 0.021869488f, -0.053968254f), 0.13333334f),
+                             -0.33333334f), 1.0f);
+  }
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(ax * 2.8853900817779268f));  // 2 log2(e)
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+  return copysignf(fmaf(-2.0f, r, 1.0f), x);
 }
 
 template <bool kFast>
@@ -73,11 +86,6 @@ __device__ __forceinline__ void ApplyChainVecF32(const int32_t* fns, int n, floa
   }
 }
 
-__device__ __forceinline__ uint32_t TanhBf16x2(uint32_t x) {
-  uint32_t y;
-  asm("tanh.approx.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
-  return y;
-}
 __device__ __forceinline__ uint32_t ReluBf16x2(uint32_t x) {
   uint32_t y;
   asm("max.bf16x2 %0, %1, %2;" : "=r"(y) : "r"(x), "r"(0u));
@@ -99,7 +107,10 @@ __device__ __forceinline__ void ApplyChainPackedBf16(const int32_t* fns, int n, 
     switch (fn) {
       case RH_FN_TANH:
 #pragma unroll
-        for (int e = 0; e < P; ++e) p[e] = TanhBf16x2(p[e]);
+        for (int e = 0; e < P; ++e) {
+          const float lo = __uint_as_float(p[e] << 16), hi = __uint_as_float(p[e] & 0xffff0000u);
+          p[e] = PackBf16x2(FastTanh(lo), FastTanh(hi));
+        }
         break;
       case RH_FN_RELU:
 #pragma unroll
