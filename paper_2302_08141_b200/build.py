@@ -45,7 +45,8 @@ def build(verbose=False, force=False):
     inc = ["-I" + os.path.join(REPO, "include"), "-I" + CSRC, "-I" + os.path.join(nr, "include")]
     common = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *ARCH, *inc,
               "-Xptxas", "-warn-spills"]
-    headers = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(REPO, "include", "*.h"))
+    headers = (glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+               + glob.glob(os.path.join(REPO, "include", "*.h")))
     hdr_mtime = max(os.path.getmtime(h) for h in headers)
     objs, jobs = [], []
     for src in sources():
