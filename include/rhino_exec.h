@@ -162,6 +162,9 @@ int rh_program_read_local(rh_program* prog, int op, int rank, void* dst, size_t 
  * from the local shards (every rank must be local). */
 int rh_program_read_full(rh_program* prog, int op, void* dst, size_t bytes);
 int rh_program_local_bytes(const rh_program* prog, int op, int rank, size_t* bytes);
+/* Verification: the full value of the tensor `op` consumed at input `slot` (its producer in the
+ * layout the op's strategy demanded, after resharding), assembled from every rank (all local). */
+int rh_program_read_input_full(rh_program* prog, int op, int slot, void* dst, size_t bytes);
 
 /* Schedule introspection: one record per scheduled step (kernel or collective). */
 typedef struct {

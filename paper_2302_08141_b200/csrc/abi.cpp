@@ -257,6 +257,52 @@ void WriteFull(rh_program* p, const rh::Tensor& t, const void* src, size_t bytes
   }
 }
 
+uint16_t F2Bf(float x);
+float Bf2F(uint16_t x);
+
+// Global value of tensor t from every rank's local buffer (all ranks must be local): Replicated
+// axes read coordinate 0, Partial axes are summed in rank order in fp32 and rounded once.
+void AssembleFull(rh_program* p, const rh::Tensor& t, void* dst) {
+  rh_runtime* rt = p->mesh->rt;
+  if (rt->n_local() != rt->world) Fail("assembling a non-output tensor needs every rank local");
+  const int eb = rh::ElemBytes(t.dtype);
+  const int64_t n = Prod(t.gdims);
+  std::vector<float> full(n, 0.0f);
+  std::vector<char> loc(t.bytes);
+  for (int r = 0; r < rt->world; ++r) {
+    const std::vector<int> c = p->mesh->Coords(r);
+    bool skip = false, first = true;
+    for (int a = 0; a < p->n_axes; ++a) {
+      if (t.specs[a].kind == RH_REPLICATED && c[a] != 0) skip = true;
+      if (t.specs[a].kind == RH_PARTIAL && c[a] != 0) first = false;
+    }
+    if (skip) continue;
+    {
+      DeviceGuard dg(rt->device_of(r));
+      RH_CUDA(cudaMemcpy(loc.data(), p->base[r] + t.offset, t.bytes, cudaMemcpyDeviceToHost));
+    }
+    const rh::ComposedMap m = MakeComposed(p, t, r);
+    for (int64_t l = 0; l < t.elems(); ++l) {
+      const int64_t f = rh::ComposedLocalToGlobal(m, l);
+      float v;
+      if (eb == 4) {
+        std::memcpy(&v, &loc[l * 4], 4);
+      } else {
+        uint16_t h;
+        std::memcpy(&h, &loc[l * 2], 2);
+        v = Bf2F(h);
+      }
+      full[f] = first ? v : full[f] + v;
+    }
+  }
+  if (eb == 4) {
+    std::memcpy(dst, full.data(), static_cast<size_t>(n) * 4);
+  } else {
+    uint16_t* o = static_cast<uint16_t*>(dst);
+    for (int64_t i = 0; i < n; ++i) o[i] = F2Bf(full[i]);
+  }
+}
+
 uint16_t F2Bf(float x) {
   uint32_t u;
   std::memcpy(&u, &x, 4);
@@ -642,44 +688,19 @@ int rh_program_read_full(rh_program* p, int op, void* dst, size_t bytes) {
       return;
     }
     if (p->out_tensor[op] < 0) Fail("op was fused into its consumer's kernel (use RH_FLAG_NO_FUSION)");
-    if (rt->n_local() != rt->world) Fail("rh_program_read_full: non-output op needs every rank local");
-    const rh::Tensor& t = p->tensors[p->out_tensor[op]];
-    std::vector<float> full(n, 0.0f);
-    bool any_partial = false;
-    for (auto& s : t.specs) any_partial = any_partial || s.kind == RH_PARTIAL;
-    std::vector<char> loc(t.bytes);
-    for (int r = 0; r < rt->world; ++r) {
-      const std::vector<int> c = p->mesh->Coords(r);
-      bool skip = false, first = true;
-      for (int a = 0; a < p->n_axes; ++a) {
-        if (t.specs[a].kind == RH_REPLICATED && c[a] != 0) skip = true;
-        if (t.specs[a].kind == RH_PARTIAL && c[a] != 0) first = false;
-      }
-      if (skip) continue;
-      {
-        DeviceGuard dg(rt->device_of(r));
-        RH_CUDA(cudaMemcpy(loc.data(), p->base[r] + t.offset, t.bytes, cudaMemcpyDeviceToHost));
-      }
-      const rh::ComposedMap m = MakeComposed(p, t, r);
-      for (int64_t l = 0; l < t.elems(); ++l) {
-        const int64_t f = rh::ComposedLocalToGlobal(m, l);
-        float v;
-        if (eb == 4) std::memcpy(&v, &loc[l * 4], 4);
-        else {
-          uint16_t h;
-          std::memcpy(&h, &loc[l * 2], 2);
-          v = Bf2F(h);
-        }
-        full[f] = first ? v : full[f] + v;
-      }
-    }
-    if (eb == 4) {
-      std::memcpy(dst, full.data(), bytes);
-    } else {
-      uint16_t* o = static_cast<uint16_t*>(dst);
-      for (int64_t i = 0; i < n; ++i) o[i] = F2Bf(full[i]);
-    }
-    (void)any_partial;
+    AssembleFull(p, p->tensors[p->out_tensor[op]], dst);
+  });
+}
+
+int rh_program_read_input_full(rh_program* p, int op, int slot, void* dst, size_t bytes) {
+  return Guard([&] {
+    if (op < 0 || op >= static_cast<int>(p->ops.size())) Fail("bad op index");
+    if (slot < 0 || slot >= static_cast<int>(p->in_tensor[op].size()) || p->in_tensor[op][slot] < 0)
+      Fail("rh_program_read_input_full: op has no recorded input (source, fused or reshape-free)");
+    SyncAll(p->mesh->rt);
+    const rh::Tensor& t = p->tensors[p->in_tensor[op][slot]];
+    if (bytes != static_cast<size_t>(Prod(t.gdims)) * rh::ElemBytes(t.dtype)) Fail("size mismatch");
+    AssembleFull(p, t, dst);
   });
 }
 

@@ -220,6 +220,7 @@ class Lowerer {
     const int n = static_cast<int>(p_->ops.size());
     p_->out_tensor.assign(n, -1);
     p_->mat_tensor.assign(n, -1);
+    p_->in_tensor.assign(n, {});
     // flags + barrier counter live at the front of the arena
     p_->flags_off = Alloc(static_cast<size_t>(rt_->world) * 4);
     p_->counter_off = Alloc(4);
@@ -387,6 +388,7 @@ class Lowerer {
     std::vector<int> in_t(nin);
     for (int s = 0; s < nin; ++s)
       in_t[s] = GetTensor(p_->inputs[i][s], p_->in_specs[i][s], "edge");
+    p_->in_tensor[i] = in_t;
     const Specs nat = NaturalSpecs(i, p_->in_specs[i]);
     const int tail = chain_[i].empty() ? i : chain_[i].back();
     const bool direct = SpecsEq(nat, p_->out_specs[i]);

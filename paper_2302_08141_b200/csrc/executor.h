@@ -85,6 +85,7 @@ struct rh_program {
   std::vector<rh::Tensor> tensors;
   std::vector<int> out_tensor;  // op -> tensor index (-1: fused into a successor's kernel)
   std::vector<int> mat_tensor;  // op -> materialized Replicated tensor (outputs)
+  std::vector<std::vector<int>> in_tensor;  // [op][slot] -> tensor the op's kernel consumed
   // Extra layouts requested by the caller (rh_reshard): (op, specs) -> tensor index.
   std::vector<std::pair<int, Specs>> requests;
   std::vector<int> request_tensors;

@@ -18,7 +18,7 @@ EXPORTS = [
     "rh_runtime_create_dist", "rh_runtime_world", "rh_runtime_destroy", "rh_mesh_create",
     "rh_mesh_destroy", "rh_program_load", "rh_program_destroy", "rh_program_init_synthetic",
     "rh_program_write_full", "rh_program_run", "rh_program_step_host", "rh_program_read_local",
-    "rh_program_read_full", "rh_program_local_bytes", "rh_program_num_steps",
+    "rh_program_read_full", "rh_program_read_input_full", "rh_program_local_bytes", "rh_program_num_steps",
     "rh_program_step_info", "rh_program_profile", "rh_program_launch_count", "rh_reshard",
 ]
 
@@ -58,6 +58,7 @@ def lib():
     L.rh_program_step_host.argtypes = [vp, i, P(i), P(vp), i, P(vp), P(ctypes.c_double)]
     L.rh_program_read_local.argtypes = [vp, i, i, vp, sz]
     L.rh_program_read_full.argtypes = [vp, i, vp, sz]
+    L.rh_program_read_input_full.argtypes = [vp, i, i, vp, sz]
     L.rh_program_local_bytes.argtypes = [vp, i, i, P(sz)]
     L.rh_program_num_steps.argtypes = [vp, P(i)]
     L.rh_program_step_info.argtypes = [vp, i, P(RhStepInfo)]
@@ -189,6 +190,13 @@ class Program:
     def read_full(self, op):
         out = np.empty(self.prog.ops[op].shape, dtype=_np_dtype(self.prog.dtype))
         check(lib().rh_program_read_full(self.h, op, out.ctypes.data, out.nbytes))
+        return out
+
+    def read_input_full(self, op, slot):
+        """The value op `op` consumed at input `slot` (after resharding), assembled."""
+        src = self.prog.ops[self.prog.ops[op].inputs[slot]]
+        out = np.empty(src.shape, dtype=_np_dtype(self.prog.dtype))
+        check(lib().rh_program_read_input_full(self.h, op, slot, out.ctypes.data, out.nbytes))
         return out
 
     def steps(self):
