@@ -20,6 +20,46 @@ __device__ __forceinline__ float ApplyChain(const ChainArgs& c, float x) {
   return ApplyChainFns<kBf16>(c.fns, c.n_fn, x);
 }
 
+// RNE(tanh) for the bf16 inputs 2^-5 <= x < 4 (see TanhBf16Tab), computed once per device in
+// fp64 and rounded directly from fp64 to bf16 (no double rounding through fp32).
+__device__ uint16_t g_tanh_tab[kTanhTab];
+
+__global__ void InitTanhTableKernel() {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= kTanhTab) return;
+  const uint32_t h = (122u << 7) + i;
+  const double x = static_cast<double>(__uint_as_float(h << 16));
+  const double t = tanh(x);
+  const uint32_t lo = __float_as_uint(static_cast<float>(t)) & 0xffff0000u;  // may be off by one
+  uint32_t best = lo;
+  double bd = 1e300;
+  for (int k = -1; k <= 1; ++k) {
+    const uint32_t c = lo + static_cast<uint32_t>(k) * 0x10000u;
+    const double dv = fabs(static_cast<double>(__uint_as_float(c)) - t);
+    if (dv < bd || (dv == bd && ((c >> 16) & 1u) == 0)) {
+      bd = dv;
+      best = c;
+    }
+  }
+  g_tanh_tab[i] = static_cast<uint16_t>(best >> 16);
+}
+
+void EnsureTanhTable(cudaStream_t s) {
+  static bool done[64] = {};
+  int dev = 0;
+  RH_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && done[dev]) return;
+  InitTanhTableKernel<<<(kTanhTab + 255) / 256, 256, 0, s>>>();
+  RH_CUDA(cudaGetLastError());
+  if (dev < 64) done[dev] = true;
+}
+
+__device__ __forceinline__ const uint16_t* LoadTanhTable(uint16_t* smem) {
+  for (int i = threadIdx.x; i < kTanhTab; i += blockDim.x) smem[i] = g_tanh_tab[i];
+  __syncthreads();
+  return smem;
+}
+
 // 16-byte packets: 4 fp32 or 8 bf16.
 template <bool kBf16>
 struct Pack {
@@ -72,6 +112,8 @@ template <bool kBf16>
 __global__ void __launch_bounds__(256) UnaryChainKernel(void* out, const void* in, int64_t n,
                                                         ChainArgs c) {
   constexpr int E = Pack<kBf16>::E;
+  __shared__ uint16_t tab_s[kBf16 ? kTanhTab : 1];
+  const uint16_t* tab = kBf16 ? LoadTanhTable(tab_s) : nullptr;
   const int64_t nv = n / E;
   const int64_t npair = nv / 2;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -80,7 +122,7 @@ __global__ void __launch_bounds__(256) UnaryChainKernel(void* out, const void* i
     const uint4 u1 = reinterpret_cast<const uint4*>(in)[2 * i + 1];
     if constexpr (kBf16) {
       uint32_t p[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
-      ApplyChainPackedBf16<8>(c.fns, c.n_fn, p);
+      ApplyChainPackedBf16<8>(c.fns, c.n_fn, p, tab);
       reinterpret_cast<uint4*>(out)[2 * i] = make_uint4(p[0], p[1], p[2], p[3]);
       reinterpret_cast<uint4*>(out)[2 * i + 1] = make_uint4(p[4], p[5], p[6], p[7]);
     } else {
@@ -95,7 +137,7 @@ __global__ void __launch_bounds__(256) UnaryChainKernel(void* out, const void* i
   for (int64_t i = npair * 2 * E + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
     if constexpr (kBf16) {
       uint32_t p[1] = {static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(in)[i])};
-      ApplyChainPackedBf16<1>(c.fns, c.n_fn, p);
+      ApplyChainPackedBf16<1>(c.fns, c.n_fn, p, tab);
       reinterpret_cast<uint16_t*>(out)[i] = static_cast<uint16_t>(p[0] & 0xffffu);
     } else {
       float v[1] = {reinterpret_cast<const float*>(in)[i]};
@@ -109,6 +151,8 @@ template <bool kBf16>
 __global__ void __launch_bounds__(256) BinaryKernel(void* out, const void* a, const void* b,
                                                     int64_t n, bool mul, ChainArgs c) {
   constexpr int E = Pack<kBf16>::E;
+  __shared__ uint16_t tab_s[kBf16 ? kTanhTab : 1];
+  const uint16_t* tab = kBf16 ? LoadTanhTable(tab_s) : nullptr;
   const int64_t nv = n / E;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nv; i += stride) {
@@ -121,7 +165,7 @@ __global__ void __launch_bounds__(256) BinaryKernel(void* out, const void* a, co
       uint32_t p[E / 2];
 #pragma unroll
       for (int e = 0; e < E / 2; ++e) p[e] = PackBf16x2(x.v[2 * e], x.v[2 * e + 1]);
-      ApplyChainPackedBf16<E / 2>(c.fns, c.n_fn, p);
+      ApplyChainPackedBf16<E / 2>(c.fns, c.n_fn, p, tab);
       reinterpret_cast<uint4*>(out)[i] = make_uint4(p[0], p[1], p[2], p[3]);
     } else {
       ApplyChainVecF32<E>(c.fns, c.n_fn, x.v);
@@ -264,6 +308,7 @@ void LaunchUnaryChain(void* out, const void* in, int64_t n, const ChainArgs& c, 
                       cudaStream_t s) {
   if (n == 0) return;
   if (dtype == RH_BF16) {
+    EnsureTanhTable(s);
     UnaryChainKernel<true><<<Blocks(n, 8), 256, 0, s>>>(out, in, n, c);
   } else {
     UnaryChainKernel<false><<<Blocks(n, 4), 256, 0, s>>>(out, in, n, c);
@@ -287,6 +332,7 @@ void LaunchBinary(void* out, const void* a, const void* b, int64_t n, bool mul, 
                   int dtype, cudaStream_t s) {
   if (n == 0) return;
   if (dtype == RH_BF16) {
+    EnsureTanhTable(s);
     BinaryKernel<true><<<Blocks(n, 8), 256, 0, s>>>(out, a, b, n, mul, c);
   } else {
     BinaryKernel<false><<<Blocks(n, 4), 256, 0, s>>>(out, a, b, n, mul, c);

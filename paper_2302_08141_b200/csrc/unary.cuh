@@ -97,19 +97,39 @@ __device__ __forceinline__ uint32_t PackBf16x2(float lo, float hi) {
   return y;
 }
 
-// bf16 chain over P packed bf16x2 registers (2P elements).  tanh / relu / neg / identity stay
-// in packed bf16 (tanh.approx.bf16x2: one SFU op per two elements, result already bf16); other
-// fns unpack to fp32, apply, and round back — every op's result is a bf16 value.
+// Correctly rounded bf16 tanh of a bf16 input by table: |x| < 2^-5 -> x (tanh(x)/x > 1 - 2^-11.6
+// never crosses half an ulp), |x| >= 4 -> +-1 (1 - tanh(4) < 2^-9), NaN -> NaN, and the 7
+// binades in between (7 x 128 mantissas) from a 896-entry table of RNE(tanh) computed in fp64.
+constexpr int kTanhTab = 896;
+__device__ __forceinline__ uint32_t TanhBf16Tab(uint32_t h, const uint16_t* tab) {
+  const uint32_t a = h & 0x7fffu, s = h & 0x8000u;
+  const uint32_t e = a >> 7;
+  if (e < 122u) return h;
+  if (a > 0x7f80u) return h;                  // NaN
+  if (e >= 129u) return s | 0x3f80u;         // +-1.0
+  return s | tab[a - (122u << 7)];
+}
+
+// bf16 chain over P packed bf16x2 registers (2P elements).  tanh (table), relu, neg, identity
+// stay in packed bf16; other fns unpack to fp32, apply, and round back — every op's result is a
+// bf16 value.  `tab` (shared memory) may be null: tanh then uses FastTanh + RNE.
 template <int P>
-__device__ __forceinline__ void ApplyChainPackedBf16(const int32_t* fns, int n, uint32_t (&p)[P]) {
+__device__ __forceinline__ void ApplyChainPackedBf16(const int32_t* fns, int n, uint32_t (&p)[P],
+                                                     const uint16_t* tab = nullptr) {
   for (int i = 0; i < n; ++i) {
     const int fn = fns[i];
     switch (fn) {
       case RH_FN_TANH:
+        if (tab) {
 #pragma unroll
-        for (int e = 0; e < P; ++e) {
-          const float lo = __uint_as_float(p[e] << 16), hi = __uint_as_float(p[e] & 0xffff0000u);
-          p[e] = PackBf16x2(FastTanh(lo), FastTanh(hi));
+          for (int e = 0; e < P; ++e)
+            p[e] = TanhBf16Tab(p[e] & 0xffffu, tab) | (TanhBf16Tab(p[e] >> 16, tab) << 16);
+        } else {
+#pragma unroll
+          for (int e = 0; e < P; ++e) {
+            const float lo = __uint_as_float(p[e] << 16), hi = __uint_as_float(p[e] & 0xffff0000u);
+            p[e] = PackBf16x2(FastTanh(lo), FastTanh(hi));
+          }
         }
         break;
       case RH_FN_RELU:
