@@ -102,12 +102,13 @@ __device__ __forceinline__ uint32_t PackBf16x2(float lo, float hi) {
 // binades in between (7 x 128 mantissas) from a 896-entry table of RNE(tanh) computed in fp64.
 constexpr int kTanhTab = 896;
 __device__ __forceinline__ uint32_t TanhBf16Tab(uint32_t h, const uint16_t* tab) {
+  // branch-free: always read a (clamped) table slot, then select
   const uint32_t a = h & 0x7fffu, s = h & 0x8000u;
-  const uint32_t e = a >> 7;
-  if (e < 122u) return h;
-  if (a > 0x7f80u) return h;                  // NaN
-  if (e >= 129u) return s | 0x3f80u;         // +-1.0
-  return s | tab[a - (122u << 7)];
+  const int idx = min(max(static_cast<int>(a) - (122 << 7), 0), kTanhTab - 1);
+  const uint32_t t = tab[idx];
+  uint32_t r = a < (122u << 7) ? a : (a >= (129u << 7) ? 0x3f80u : t);
+  r = a > 0x7f80u ? a : r;  // NaN stays NaN
+  return s | r;
 }
 
 // bf16 chain over P packed bf16x2 registers (2P elements).  tanh (table), relu, neg, identity
