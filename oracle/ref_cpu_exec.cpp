@@ -358,8 +358,55 @@ float Unary(int fn, float x) {
   Fail("unary: bad fn " + std::to_string(fn));
 }
 
+// bf16 programs: each unary op is the correctly rounded bf16 result of the exact function
+// (evaluated in fp64, rounded once from fp64 to bf16 with ties to even).
+double UnaryD(int fn, double x) {
+  switch (fn) {
+    case RH_FN_RELU: return x > 0.0 ? x : 0.0;
+    case RH_FN_GELU: return 0.5 * x * (1.0 + std::tanh(0.7978845608028654 * (x + 0.044715 * x * x * x)));
+    case RH_FN_TANH: return std::tanh(x);
+    case RH_FN_EXP: return std::exp(x);
+    case RH_FN_SIGMOID: return 1.0 / (1.0 + std::exp(-x));
+    case RH_FN_NEG: return -x;
+    case RH_FN_RSQRT: return 1.0 / std::sqrt(std::fabs(x) + 1e-6);
+    case RH_FN_IDENTITY: return x;
+  }
+  Fail("unary: bad fn " + std::to_string(fn));
+}
+
+float Bf16FromDouble(double t) {
+  if (!std::isfinite(t) || t == 0.0) return Bf16Round(static_cast<float>(t));
+  const bool neg = t < 0;
+  const double a = neg ? -t : t;
+  const float f = static_cast<float>(a);
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  const uint32_t lo = u & 0xffff0000u;
+  uint32_t best = lo;
+  double bd = 1e300;
+  for (int k = -1; k <= 1; ++k) {
+    const uint32_t c = lo + static_cast<uint32_t>(k) * 0x10000u;
+    float cf;
+    std::memcpy(&cf, &c, 4);
+    const double dv = std::fabs(static_cast<double>(cf) - a);
+    if (dv < bd || (dv == bd && ((c >> 16) & 1u) == 0)) {
+      bd = dv;
+      best = c;
+    }
+  }
+  float r;
+  std::memcpy(&r, &best, 4);
+  return neg ? -r : r;
+}
+
 std::vector<float> UnaryOp(int fn, const std::vector<float>& in, const Dims& ld, bool bf16) {
   std::vector<float> out(in.size());
+  if (bf16 && fn != RH_FN_SOFTMAX) {
+    const int64_t n = static_cast<int64_t>(in.size());
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) out[i] = Bf16FromDouble(UnaryD(fn, static_cast<double>(in[i])));
+    return out;
+  }
   const int64_t n = static_cast<int64_t>(in.size());
   if (fn == RH_FN_SOFTMAX) {
     const int64_t cols = ld.back(), rows = n / cols;

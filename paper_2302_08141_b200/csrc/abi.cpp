@@ -166,6 +166,9 @@ void Allocate(rh_program* p) {
     RH_CUDA(cudaMalloc(&ptr, bytes));
     // zero on the rank's own (non-blocking) stream so later work is ordered after it
     RH_CUDA(cudaMemsetAsync(ptr, 0, bytes, rt->stream_of(li)));
+    for (const auto& up : p->uploads)  // constant tables (e.g. the bf16 tanh-run tables)
+      RH_CUDA(cudaMemcpyAsync(static_cast<char*>(ptr) + up.first, up.second.data(), up.second.size(),
+                              cudaMemcpyHostToDevice, rt->stream_of(li)));
     RH_CUDA(cudaStreamSynchronize(rt->stream_of(li)));
     p->base[li] = static_cast<char*>(ptr);
     p->owned.push_back(ptr);

@@ -356,7 +356,15 @@ class Lowerer {
       // The GEMM epilogue runs on 4 warps per SM: only short chains ride in it; a longer chain
       // runs as one full-occupancy elementwise kernel instead (same HBM traffic, 10x the issue
       // rate for its transcendental work).
-      if (op.kind == RH_OP_MATMUL && chain_[h].size() > kMaxGemmEpilogue) {
+      // bf16 GEMM epilogues take only the exact packed ops (relu / neg / identity); tanh runs
+      // use the T^k tables of the elementwise kernels.
+      bool epi_ok = chain_[h].size() <= kMaxGemmEpilogue;
+      if (op.dtype == RH_BF16)
+        for (int v : chain_[h]) {
+          const int fn = UnaryFn(v);
+          epi_ok = epi_ok && (fn == RH_FN_RELU || fn == RH_FN_NEG || fn == RH_FN_IDENTITY);
+        }
+      if (op.kind == RH_OP_MATMUL && !epi_ok) {
         for (int v : chain_[h]) absorbed_[v] = false;
         chain_[h].clear();
       }
@@ -371,12 +379,50 @@ class Lowerer {
     return fn;
   }
 
-  ChainArgs ChainOf(int h, bool include_head) const {
+  ChainArgs ChainOf(int h, bool include_head) {
+    std::vector<int> fns;
+    if (include_head) fns.push_back(UnaryFn(h));
+    for (int v : chain_[h]) fns.push_back(UnaryFn(v));
     ChainArgs c{};
-    if (include_head) c.fns[c.n_fn++] = UnaryFn(h);
-    for (int v : chain_[h]) c.fns[c.n_fn++] = UnaryFn(v);
+    const bool bf16 = p_->ops[h].dtype == RH_BF16;
+    for (size_t i = 0; i < fns.size();) {
+      size_t j = i;
+      while (j < fns.size() && fns[j] == RH_FN_TANH) ++j;
+      if (bf16 && j > i && c.n_tab < kMaxTanhRuns) {  // run of tanh -> one T^k lookup
+        c.tab_off[c.n_tab] = TanhTable(static_cast<int>(j - i));
+        c.fns[c.n_fn++] = kFnTanhRun + c.n_tab;
+        ++c.n_tab;
+        i = j;
+      } else {
+        c.fns[c.n_fn++] = fns[i++];
+      }
+    }
     return c;
   }
+
+  // Arena offset of the T^k table (uploaded to every rank's arena after allocation).
+  size_t TanhTable(int k) {
+    auto it = tanh_tables_.find(k);
+    if (it != tanh_tables_.end()) return it->second;
+    std::vector<uint16_t> tab(kTanhRunEntries);
+    TanhRunTable(k, tab.data());
+    const size_t off = Alloc(tab.size() * 2);
+    p_->uploads.emplace_back(off, std::vector<char>(reinterpret_cast<char*>(tab.data()),
+                                                    reinterpret_cast<char*>(tab.data()) + tab.size() * 2));
+    tanh_tables_[k] = off;
+    return off;
+  }
+
+ public:
+  // The chain with its tables' device pointers for global rank r.
+  static ChainArgs Patch(const rh_program* P, const ChainArgs& c, int r) {
+    ChainArgs o = c;
+    for (int t = 0; t < c.n_tab; ++t)
+      o.tab[t] = reinterpret_cast<const uint16_t*>(P->peer_base[r] + c.tab_off[t]);
+    return o;
+  }
+
+ private:
 
   std::string OpName(int i) const { return "op" + std::to_string(i); }
 
@@ -467,7 +513,7 @@ class Lowerer {
         st.run = [P, ta, tb, out_t, first, n_out, mul, c, dtype](int li, cudaStream_t s) {
           const int r = first + li;
           LaunchBinary(P->Ptr(P->tensors[out_t], r), P->Ptr(P->tensors[ta], r),
-                       P->Ptr(P->tensors[tb], r), n_out, mul, c, dtype, s);
+                       P->Ptr(P->tensors[tb], r), n_out, mul, Patch(P, c, r), dtype, s);
           return 1;
         };
         break;
@@ -491,8 +537,8 @@ class Lowerer {
           st.alg_flops = static_cast<double>(n_out) * c.n_fn;
           st.run = [P, ti, out_t, first, n_out, c, dtype](int li, cudaStream_t s) {
             const int r = first + li;
-            LaunchUnaryChain(P->Ptr(P->tensors[out_t], r), P->Ptr(P->tensors[ti], r), n_out, c,
-                             dtype, s);
+            LaunchUnaryChain(P->Ptr(P->tensors[out_t], r), P->Ptr(P->tensors[ti], r), n_out,
+                             Patch(P, c, r), dtype, s);
             return 1;
           };
         }
@@ -706,6 +752,7 @@ class Lowerer {
   std::map<std::string, int> cache_;
   std::vector<bool> absorbed_;
   std::vector<std::vector<int>> chain_;
+  std::map<int, size_t> tanh_tables_;
 };
 
 }  // namespace

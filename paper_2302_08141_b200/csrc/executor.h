@@ -98,6 +98,7 @@ struct rh_program {
   std::vector<char*> peer_base;  // per global rank (dist: IPC-mapped; local: = base)
   bool ipc_opened = false;
   std::vector<void*> owned;      // device allocations to free (per distinct device)
+  std::vector<std::pair<size_t, std::vector<char>>> uploads;  // constant data (arena offset, bytes)
 
   char* Ptr(const rh::Tensor& t, int global_rank) const { return peer_base[global_rank] + t.offset; }
   int LocalIndex(int global_rank) const;

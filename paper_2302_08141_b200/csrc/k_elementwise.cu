@@ -8,6 +8,8 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cmath>
+#include <cstring>
 
 #include "kernels.h"
 #include "unary.cuh"
@@ -20,45 +22,62 @@ __device__ __forceinline__ float ApplyChain(const ChainArgs& c, float x) {
   return ApplyChainFns<kBf16>(c.fns, c.n_fn, x);
 }
 
-// RNE(tanh) for the bf16 inputs 2^-5 <= x < 4 (see TanhBf16Tab), computed once per device in
-// fp64 and rounded directly from fp64 to bf16 (no double rounding through fp32).
-__device__ uint16_t g_tanh_tab[kTanhTab];
+// The chain's T^k tables (kernel arguments, arena-resident) staged into shared memory once per
+// block: n_tab x 897 x 2 bytes.
+__device__ __forceinline__ void LoadRunTables(const ChainArgs& c, uint16_t* smem) {
+  for (int t = 0; t < c.n_tab; ++t)
+    for (int i = threadIdx.x; i < kTanhRunEntries; i += blockDim.x)
+      smem[t * kTanhRunEntries + i] = c.tab[t][i];
+  __syncthreads();
+}
 
-__global__ void InitTanhTableKernel() {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= kTanhTab) return;
-  const uint32_t h = (122u << 7) + i;
-  const double x = static_cast<double>(__uint_as_float(h << 16));
-  const double t = tanh(x);
-  const uint32_t lo = __float_as_uint(static_cast<float>(t)) & 0xffff0000u;  // may be off by one
+// ------------------------------------------ host -------------------------------------------
+
+float Bf16BitsToFloat(uint32_t h) {
+  uint32_t u = h << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+// Round a positive finite double to the nearest bf16 (ties to even), directly (no fp32 step).
+uint16_t RneBf16(double t) {
+  float f = static_cast<float>(t);
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  const uint32_t lo = u & 0xffff0000u;
   uint32_t best = lo;
   double bd = 1e300;
   for (int k = -1; k <= 1; ++k) {
     const uint32_t c = lo + static_cast<uint32_t>(k) * 0x10000u;
-    const double dv = fabs(static_cast<double>(__uint_as_float(c)) - t);
+    const double dv = std::fabs(static_cast<double>(Bf16BitsToFloat(c >> 16)) - t);
     if (dv < bd || (dv == bd && ((c >> 16) & 1u) == 0)) {
       bd = dv;
       best = c;
     }
   }
-  g_tanh_tab[i] = static_cast<uint16_t>(best >> 16);
+  return static_cast<uint16_t>(best >> 16);
 }
 
-void EnsureTanhTable(cudaStream_t s) {
-  static bool done[64] = {};
-  int dev = 0;
-  RH_CUDA(cudaGetDevice(&dev));
-  if (dev < 64 && done[dev]) return;
-  InitTanhTableKernel<<<(kTanhTab + 255) / 256, 256, 0, s>>>();
-  RH_CUDA(cudaGetLastError());
-  if (dev < 64) done[dev] = true;
+// The correctly rounded bf16 tanh (the semantics of one unlabeled/tanh op on a bf16 value).
+uint16_t TanhBf16(uint16_t h) {
+  const uint32_t a = h & 0x7fffu, s = h & 0x8000u;
+  if (a < (122u << 7) || a > 0x7f80u) return h;  // tanh(x) rounds to x below 2^-5; NaN
+  if (a >= (129u << 7)) return static_cast<uint16_t>(s | 0x3f80u);  // |x| >= 4 -> +-1
+  return static_cast<uint16_t>(s | RneBf16(std::tanh(static_cast<double>(Bf16BitsToFloat(a)))));
 }
 
-__device__ __forceinline__ const uint16_t* LoadTanhTable(uint16_t* smem) {
-  for (int i = threadIdx.x; i < kTanhTab; i += blockDim.x) smem[i] = g_tanh_tab[i];
-  __syncthreads();
-  return smem;
+}  // namespace
+
+void TanhRunTable(int k, uint16_t* out) {
+  for (int i = 0; i < kTanhRunEntries; ++i) {
+    uint16_t h = i < 896 ? static_cast<uint16_t>((122u << 7) + i) : static_cast<uint16_t>(129u << 7);
+    for (int j = 0; j < k; ++j) h = TanhBf16(h);
+    out[i] = h;
+  }
 }
+
+namespace {
 
 // 16-byte packets: 4 fp32 or 8 bf16.
 template <bool kBf16>
@@ -112,8 +131,12 @@ template <bool kBf16>
 __global__ void __launch_bounds__(256) UnaryChainKernel(void* out, const void* in, int64_t n,
                                                         ChainArgs c) {
   constexpr int E = Pack<kBf16>::E;
-  __shared__ uint16_t tab_s[kBf16 ? kTanhTab : 1];
-  const uint16_t* tab = kBf16 ? LoadTanhTable(tab_s) : nullptr;
+  __shared__ uint16_t tab_s[kBf16 ? kMaxTanhRuns * kTanhRunEntries : 1];
+  const uint16_t* tab = nullptr;
+  if constexpr (kBf16) {
+    LoadRunTables(c, tab_s);
+    tab = tab_s;
+  }
   const int64_t nv = n / E;
   const int64_t npair = nv / 2;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -151,8 +174,12 @@ template <bool kBf16>
 __global__ void __launch_bounds__(256) BinaryKernel(void* out, const void* a, const void* b,
                                                     int64_t n, bool mul, ChainArgs c) {
   constexpr int E = Pack<kBf16>::E;
-  __shared__ uint16_t tab_s[kBf16 ? kTanhTab : 1];
-  const uint16_t* tab = kBf16 ? LoadTanhTable(tab_s) : nullptr;
+  __shared__ uint16_t tab_s[kBf16 ? kMaxTanhRuns * kTanhRunEntries : 1];
+  const uint16_t* tab = nullptr;
+  if constexpr (kBf16) {
+    LoadRunTables(c, tab_s);
+    tab = tab_s;
+  }
   const int64_t nv = n / E;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nv; i += stride) {
@@ -308,7 +335,6 @@ void LaunchUnaryChain(void* out, const void* in, int64_t n, const ChainArgs& c, 
                       cudaStream_t s) {
   if (n == 0) return;
   if (dtype == RH_BF16) {
-    EnsureTanhTable(s);
     UnaryChainKernel<true><<<Blocks(n, 8), 256, 0, s>>>(out, in, n, c);
   } else {
     UnaryChainKernel<false><<<Blocks(n, 4), 256, 0, s>>>(out, in, n, c);
@@ -332,7 +358,6 @@ void LaunchBinary(void* out, const void* a, const void* b, int64_t n, bool mul, 
                   int dtype, cudaStream_t s) {
   if (n == 0) return;
   if (dtype == RH_BF16) {
-    EnsureTanhTable(s);
     BinaryKernel<true><<<Blocks(n, 8), 256, 0, s>>>(out, a, b, n, mul, c);
   } else {
     BinaryKernel<false><<<Blocks(n, 4), 256, 0, s>>>(out, a, b, n, mul, c);

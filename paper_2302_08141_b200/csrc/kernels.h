@@ -51,10 +51,21 @@ void LaunchSynthetic(void* dst, const ComposedMap& m, int64_t n, uint64_t seed, 
 
 // ----------------------------------------- local ops -----------------------------------------
 constexpr int kMaxChain = 64;
+// bf16 only: a run of k consecutive tanh ops is one lookup in the table of T^k, T = the
+// correctly rounded bf16 tanh (bf16 has 2^16 inputs; T^k composes the per-op-rounded
+// semantics exactly).  fns[i] = kFnTanhRun + j selects table j.
+constexpr int kFnTanhRun = 100;
+constexpr int kMaxTanhRuns = 4;
+constexpr int kTanhRunEntries = 897;  // 896 table binades [2^-5, 4) + the |x| >= 4 constant
 struct ChainArgs {
   int32_t n_fn;
   int32_t fns[kMaxChain];
+  int32_t n_tab;
+  uint64_t tab_off[kMaxTanhRuns];        // arena offsets (host side)
+  const uint16_t* tab[kMaxTanhRuns];     // device pointers, patched per rank at launch
 };
+// Host: T^k table (kTanhRunEntries values) of the correctly rounded bf16 tanh.
+void TanhRunTable(int k, uint16_t* out);
 // Elementwise unary chain (one fused pass).  softmax is not elementwise and has its own kernel.
 void LaunchUnaryChain(void* out, const void* in, int64_t n, const ChainArgs& c, int dtype,
                       cudaStream_t s);

@@ -97,40 +97,40 @@ __device__ __forceinline__ uint32_t PackBf16x2(float lo, float hi) {
   return y;
 }
 
-// Correctly rounded bf16 tanh of a bf16 input by table: |x| < 2^-5 -> x (tanh(x)/x > 1 - 2^-11.6
-// never crosses half an ulp), |x| >= 4 -> +-1 (1 - tanh(4) < 2^-9), NaN -> NaN, and the 7
-// binades in between (7 x 128 mantissas) from a 896-entry table of RNE(tanh) computed in fp64.
-constexpr int kTanhTab = 896;
-__device__ __forceinline__ uint32_t TanhBf16Tab(uint32_t h, const uint16_t* tab) {
-  // branch-free: always read a (clamped) table slot, then select
+// A run of k tanh ops on a bf16 value = one lookup in the table of T^k (T = correctly rounded
+// bf16 tanh): |x| < 2^-5 is a fixed point of T (tanh(x)/x > 1 - 2^-11.6 never crosses half an
+// ulp), |x| >= 4 maps like 4 (T(x) = +-1), NaN stays NaN, and the 7 binades [2^-5, 4) (896
+// entries) are tabulated; T is odd.  Branch-free: the clamped slot is always read.
+__device__ __forceinline__ uint32_t TanhRunLookup(uint32_t h, const uint16_t* tab) {
   const uint32_t a = h & 0x7fffu, s = h & 0x8000u;
-  const int idx = min(max(static_cast<int>(a) - (122 << 7), 0), kTanhTab - 1);
+  const int idx = min(max(static_cast<int>(a) - (122 << 7), 0), kTanhRunEntries - 1);
   const uint32_t t = tab[idx];
-  uint32_t r = a < (122u << 7) ? a : (a >= (129u << 7) ? 0x3f80u : t);
+  uint32_t r = a < (122u << 7) ? a : t;
   r = a > 0x7f80u ? a : r;  // NaN stays NaN
   return s | r;
 }
 
-// bf16 chain over P packed bf16x2 registers (2P elements).  tanh (table), relu, neg, identity
-// stay in packed bf16; other fns unpack to fp32, apply, and round back — every op's result is a
-// bf16 value.  `tab` (shared memory) may be null: tanh then uses FastTanh + RNE.
+// bf16 chain over P packed bf16x2 registers (2P elements).  tanh runs (tables in shared memory,
+// `tabs` = kTanhRunEntries-strided), relu, neg, identity stay in packed bf16; other fns unpack to
+// fp32, apply, and round back — every op's result is a bf16 value.
 template <int P>
 __device__ __forceinline__ void ApplyChainPackedBf16(const int32_t* fns, int n, uint32_t (&p)[P],
-                                                     const uint16_t* tab = nullptr) {
+                                                     const uint16_t* tabs = nullptr) {
   for (int i = 0; i < n; ++i) {
     const int fn = fns[i];
+    if (fn >= kFnTanhRun) {
+      const uint16_t* tab = tabs + (fn - kFnTanhRun) * kTanhRunEntries;
+#pragma unroll
+      for (int e = 0; e < P; ++e)
+        p[e] = TanhRunLookup(p[e] & 0xffffu, tab) | (TanhRunLookup(p[e] >> 16, tab) << 16);
+      continue;
+    }
     switch (fn) {
-      case RH_FN_TANH:
-        if (tab) {
+      case RH_FN_TANH:  // (runs are table-compressed by the lowering; kept for completeness)
 #pragma unroll
-          for (int e = 0; e < P; ++e)
-            p[e] = TanhBf16Tab(p[e] & 0xffffu, tab) | (TanhBf16Tab(p[e] >> 16, tab) << 16);
-        } else {
-#pragma unroll
-          for (int e = 0; e < P; ++e) {
-            const float lo = __uint_as_float(p[e] << 16), hi = __uint_as_float(p[e] & 0xffff0000u);
-            p[e] = PackBf16x2(FastTanh(lo), FastTanh(hi));
-          }
+        for (int e = 0; e < P; ++e) {
+          const float lo = __uint_as_float(p[e] << 16), hi = __uint_as_float(p[e] & 0xffff0000u);
+          p[e] = PackBf16x2(FastTanh(lo), FastTanh(hi));
         }
         break;
       case RH_FN_RELU:
