@@ -109,6 +109,7 @@ typedef struct {
                                            (baseline) instead of the peer-memory kernels */
 #define RH_FLAG_NO_MATERIALIZE 0x8u     /* leave program outputs in their planned spec */
 #define RH_FLAG_SIMT_GEMM 0x10u         /* force the CUDA-core GEMM (test/reference kernel) */
+#define RH_FLAG_NO_GRAPH 0x20u          /* launch eagerly instead of replaying a CUDA graph */
 
 typedef struct rh_runtime rh_runtime;
 typedef struct rh_mesh rh_mesh;

@@ -126,17 +126,64 @@ int64_t RunOnce(rh_program* p, std::vector<cudaEvent_t>* prof) {
   const bool multi_dev = rt->devs.size() > 1;
   for (size_t si = 0; si < p->steps.size(); ++si) {
     rh::Step& st = p->steps[si];
-    if (prof) RH_CUDA(cudaEventRecord((*prof)[si], rt->streams[0]));
+    if (prof) RH_CUDA(cudaEventRecordWithFlags((*prof)[si], rt->streams[0], cudaEventRecordExternal));
     if (st.p2p) GroupSync(p, st.axis);
     for (int li = 0; li < rt->n_local(); ++li) {
       if (multi_dev) RH_CUDA(cudaSetDevice(rt->device_of(li)));
       launches += st.run(li, rt->stream_of(li));
     }
-    if (st.p2p) GroupSync(p, st.axis);
+    if (st.p2p && st.post_sync) GroupSync(p, st.axis);
   }
-  if (prof) RH_CUDA(cudaEventRecord(prof->back(), rt->streams[0]));
+  if (prof) RH_CUDA(cudaEventRecordWithFlags(prof->back(), rt->streams[0], cudaEventRecordExternal));
   if (multi_dev) RH_CUDA(cudaSetDevice(rt->devs[0]));
   return launches;
+}
+
+// CUDA graphs: one stream per process (dist mode, or every emulated rank on one GPU).  The
+// static schedule is captured once and replayed, removing per-kernel launch latency (the GPT
+// block at N>=4 and the MLP configs are launch-bound otherwise).
+bool UseGraph(const rh_program* p) {
+  return p->mesh->rt->streams.size() == 1 && !(p->flags & RH_FLAG_NO_GRAPH);
+}
+
+// Capture `iters` back-to-back runs; `ev` (optional) = iters x (n_steps + 1) boundary events
+// recorded as external event nodes.
+cudaGraphExec_t CaptureRuns(rh_program* p, int iters, std::vector<std::vector<cudaEvent_t>>* ev) {
+  cudaStream_t s = p->mesh->rt->streams[0];
+  RH_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  try {
+    for (int it = 0; it < iters; ++it) RunOnce(p, ev ? &(*ev)[it] : nullptr);
+  } catch (...) {
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(s, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  cudaGraph_t g = nullptr;
+  RH_CUDA(cudaStreamEndCapture(s, &g));
+  cudaGraphExec_t e = nullptr;
+  const cudaError_t r = cudaGraphInstantiate(&e, g, 0);
+  cudaGraphDestroy(g);
+  RH_CUDA(r);
+  return e;
+}
+
+// One run: replay the captured schedule (captured lazily after an eager first run, which also
+// performs one-time setup such as kernel attributes and TMA descriptors).
+void RunStep(rh_program* p) {
+  if (!UseGraph(p)) {
+    RunOnce(p, nullptr);
+    return;
+  }
+  if (!p->graph) {
+    if (!p->warmed) {
+      RunOnce(p, nullptr);
+      p->warmed = true;
+      return;
+    }
+    p->graph = CaptureRuns(p, 1, nullptr);
+  }
+  RH_CUDA(cudaGraphLaunch(static_cast<cudaGraphExec_t>(p->graph), p->mesh->rt->streams[0]));
 }
 
 void SyncAll(rh_runtime* rt) {
@@ -217,6 +264,7 @@ void DestroyProgram(rh_program* p) {
     for (int r = 0; r < rt->world; ++r)
       if (r != rt->first_rank && p->peer_base[r]) cudaIpcCloseMemHandle(p->peer_base[r]);
   }
+  if (p->graph) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(p->graph));
   for (int li = 0; li < rt->n_local() && li < static_cast<int>(p->owned.size()); ++li) {
     DeviceGuard dg(rt->device_of(li));
     cudaFree(p->owned[li]);
@@ -569,7 +617,7 @@ int rh_program_run(rh_program* p, int iters, double* ms_per_iter) {
       RH_CUDA(cudaEventCreate(&ev1[i]));
       RH_CUDA(cudaEventRecord(ev0[i], rt->streams[i]));
     }
-    for (int it = 0; it < iters; ++it) RunOnce(p, nullptr);
+    for (int it = 0; it < iters; ++it) RunStep(p);
     float worst = 0;
     for (size_t i = 0; i < rt->streams.size(); ++i) {
       DeviceGuard dg(rt->devs[i]);
@@ -595,7 +643,15 @@ int rh_program_profile(rh_program* p, int iters, double* ms_per_iter) {
     std::vector<std::vector<cudaEvent_t>> ev(std::max(iters, 0), std::vector<cudaEvent_t>(n + 1));
     for (auto& row : ev)
       for (auto& e : row) RH_CUDA(cudaEventCreate(&e));
-    for (int it = 0; it < iters; ++it) RunOnce(p, &ev[it]);
+    if (UseGraph(p) && iters > 0) {
+      // the whole timed region is one graph: K runs back to back with external event nodes
+      cudaGraphExec_t g = CaptureRuns(p, iters, &ev);
+      RH_CUDA(cudaGraphLaunch(g, rt->streams[0]));
+      SyncAll(rt);
+      cudaGraphExecDestroy(g);
+    } else {
+      for (int it = 0; it < iters; ++it) RunOnce(p, &ev[it]);
+    }
     SyncAll(rt);
     std::vector<double> acc(n, 0.0);
     for (int it = 0; it < iters; ++it)
@@ -629,7 +685,7 @@ int rh_program_step_host(rh_program* p, int n_in, const int* in_ops, const void*
       const rh::Tensor& t = p->tensors[p->out_tensor[op]];
       WriteFull(p, t, in_ptrs[k], static_cast<size_t>(Prod(t.gdims)) * rh::ElemBytes(t.dtype), nullptr);
     }
-    RunOnce(p, nullptr);
+    RunStep(p);
     if (n_outs > static_cast<int>(p->outputs.size())) Fail("too many output buffers");
     for (int k = 0; k < n_outs; ++k) {
       const int op = p->outputs[k];
@@ -731,7 +787,7 @@ int rh_program_launch_count(const rh_program* p, int64_t* launches) {
     int64_t n = 0;
     for (const auto& s : p->steps) n += static_cast<int64_t>(s.launches) * p->mesh->rt->n_local();
     for (const auto& s : p->steps)
-      if (s.p2p && p->mesh->rt->dist && p->mesh->rt->world > 1) n += 2;  // group barriers
+      if (s.p2p && p->mesh->rt->dist && p->mesh->rt->world > 1) n += s.post_sync ? 2 : 1;  // barriers
     *launches = n;
   });
 }

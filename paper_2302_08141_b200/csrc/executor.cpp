@@ -243,6 +243,15 @@ class Lowerer {
     }
     for (const auto& rq : p_->requests) p_->request_tensors.push_back(GetTensor(rq.first, rq.second, "request"));
     p_->arena_bytes = arena_;
+    // Barrier elision: tensors are written once per run (single-assignment arena), so a peer can
+    // only overwrite what a transition reads in the NEXT run.  Every p2p transition but the
+    // last one on its axis can drop its post-barrier: the next p2p transition on that axis
+    // begins with a barrier of the same group, which peers cannot pass before we finished.
+    std::vector<int> last(p_->n_axes, -1);
+    for (size_t i = 0; i < p_->steps.size(); ++i)
+      if (p_->steps[i].p2p) last[p_->steps[i].axis] = static_cast<int>(i);
+    for (size_t i = 0; i < p_->steps.size(); ++i)
+      if (p_->steps[i].p2p) p_->steps[i].post_sync = static_cast<int>(i) == last[p_->steps[i].axis];
   }
 
  private:

@@ -62,6 +62,8 @@ struct Step {
   std::string name;
   int axis = -1;             // transitions: mesh axis (group) that must be synchronised
   bool p2p = false;          // transition reads peer buffers (needs pre/post group sync)
+  bool post_sync = true;     // p2p only: false when a later p2p step on the same axis (same
+                             // iteration) already orders the peers' next writes after our reads
   double alg_bytes = 0, alg_flops = 0, wire_bytes = 0;
   int launches = 0;          // per rank per run
   double ms = 0;             // from the last profile
@@ -99,6 +101,8 @@ struct rh_program {
   bool ipc_opened = false;
   std::vector<void*> owned;      // device allocations to free (per distinct device)
   std::vector<std::pair<size_t, std::vector<char>>> uploads;  // constant data (arena offset, bytes)
+  void* graph = nullptr;  // cudaGraphExec_t of one captured run (single-stream runtimes)
+  bool warmed = false;    // one eager run precedes capture
 
   char* Ptr(const rh::Tensor& t, int global_rank) const { return peer_base[global_rank] + t.offset; }
   int LocalIndex(int global_rank) const;
