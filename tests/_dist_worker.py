@@ -40,7 +40,7 @@ def check(rt, name, flags, dtype=None):
         gp.init_synthetic(21)
         gp.run(3)
         key = (name, prog.dtype)
-        if key not in _ORACLES:
+        if key not in _ORACLES and not (prog.dtype == RH_BF16 and name.startswith("c3_")):
             o = pyoracle.OracleProgram(prog, keep_all=True)
             o.init_synthetic(21)
             threads = max(1, (os.cpu_count() or 2) // max(1, rt.world))  # torchrun sets OMP=1
@@ -48,16 +48,38 @@ def check(rt, name, flags, dtype=None):
             if not name.startswith("c3_"):
                 o.run_partitioned(threads)
             _ORACLES[key] = o
-        o = _ORACLES[key]
+        o = _ORACLES.get(key)
         bf = prog.dtype == RH_BF16
         # fp32 GPT block: fp32-accumulation forward error of the 108-op block (~6e-5, see
         # test_gpu_parity.test_gpt_block_fp32 for the rule); everything else 1e-5.
         tol = 2e-2 if bf else (2e-4 if name.startswith("c3_") else 1e-5)
         conv = pyoracle.bf16_to_f32 if bf else (lambda a: a)
-        for out in prog.outputs:
-            e = normwise(conv(gp.read_full(out)), conv(o.read_full(out, partitioned=False)))
-            res["err"] = max(res["err"], e)
-            res["ok"] &= e <= tol
+        if bf and name.startswith("c3_"):
+            # bf16 full block: compare with the SAME partitioned program run as emulated ranks on
+            # this GPU (test_gpu_parity checks that one against the oracle).  The peer-memory
+            # transport must reproduce it bit for bit (same kernels, same rank-order sums).
+            rt_e = rx.Runtime(devices=[rt.first_rank] * prog.world)
+            mesh_e = rx.Mesh(rt_e, prog.mesh)
+            ge = rx.Program(mesh_e, prog, flags & ~RH_FLAG_TRANSPORT_NCCL)
+            ge.init_synthetic(21)
+            ge.run(1)
+            for out in prog.outputs:
+                got, want = gp.read_full(out), ge.read_full(out)
+                if flags & RH_FLAG_TRANSPORT_NCCL:  # NCCL sums in its own order
+                    e = normwise(conv(got), conv(want))
+                    res["ok"] &= e <= tol
+                else:
+                    e = float(np.count_nonzero(got != want))
+                    res["ok"] &= e == 0
+                res["err"] = max(res["err"], e)
+            ge.close()
+            mesh_e.close()
+            rt_e.close()
+        else:
+            for out in prog.outputs:
+                e = normwise(conv(gp.read_full(out)), conv(o.read_full(out, partitioned=False)))
+                res["err"] = max(res["err"], e)
+                res["ok"] &= e <= tol
         if flags & RH_FLAG_NO_FUSION:
             exact = set()
             for op in prog.ops:
