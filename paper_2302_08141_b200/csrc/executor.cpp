@@ -242,6 +242,7 @@ class Lowerer {
       }
     }
     for (const auto& rq : p_->requests) p_->request_tensors.push_back(GetTensor(rq.first, rq.second, "request"));
+    if (p_->gemm_scratch_bytes) p_->gemm_scratch_off = Alloc(p_->gemm_scratch_bytes);
     p_->arena_bytes = arena_;
     // Barrier elision: tensors are written once per run (single-assignment arena), so a peer can
     // only overwrite what a transition reads in the NEXT run.  Every p2p transition but the
@@ -496,8 +497,14 @@ class Lowerer {
         g.tb = op.transpose_b;
         g.dtype = dtype;
         g.epi = ChainOf(i, false);
+        // fp32 GEMMs run as 3xTF32 and need split scratch: one region shared by all GEMMs of the
+        // program (stream-ordered), sized to the largest and placed at the end of lowering.
+        if (dtype == RH_F32) g.scratch = reinterpret_cast<void*>(uintptr_t{256});  // support probe
         const bool tc = !(P->flags & RH_FLAG_SIMT_GEMM) && GemmTcSupported(g);
-        st.name = std::string(tc ? "gemm_tc " : "gemm_simt ") + id;
+        if (tc && dtype == RH_F32)
+          P->gemm_scratch_bytes = std::max(P->gemm_scratch_bytes, GemmTf32x3ScratchBytes(g));
+        g.scratch = nullptr;
+        st.name = std::string(tc ? (dtype == RH_F32 ? "gemm_tc_3xtf32 " : "gemm_tc ") : "gemm_simt ") + id;
         st.alg_flops = 2.0 * g.m * g.n * g.k;
         const int ta = in_t[0], tb = in_t[1];
         st.run = [P, g, ta, tb, out_t, first, tc](int li, cudaStream_t s) {
@@ -506,10 +513,16 @@ class Lowerer {
           a.a = P->Ptr(P->tensors[ta], r);
           a.b = P->Ptr(P->tensors[tb], r);
           a.c = P->Ptr(P->tensors[out_t], r);
+          a.epi = Patch(P, g.epi, r);
+          if (P->gemm_scratch_bytes) a.scratch = P->peer_base[r] + P->gemm_scratch_off;
           if (tc) LaunchGemmTc(a, s);
           else LaunchGemmSimt(a, s);
-          return 1;
+          return tc && a.dtype == RH_F32 ? 3 : 1;  // 2 split kernels + the GEMM
         };
+        if (tc && dtype == RH_F32) {
+          st.launches = 3;
+          st.alg_bytes += 3.0 * 4 * (g.m * g.k + g.k * g.n);  // split pass: read x, write hi + lo
+        }
         break;
       }
       case RH_OP_ADD:

@@ -101,6 +101,7 @@ struct rh_program {
   bool ipc_opened = false;
   std::vector<void*> owned;      // device allocations to free (per distinct device)
   std::vector<std::pair<size_t, std::vector<char>>> uploads;  // constant data (arena offset, bytes)
+  size_t gemm_scratch_bytes = 0, gemm_scratch_off = 0;  // 3xTF32 split scratch (shared)
   void* graph = nullptr;  // cudaGraphExec_t of one captured run (single-stream runtimes)
   bool warmed = false;    // one eager run precedes capture
 

@@ -14,6 +14,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -263,6 +264,209 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------- fp32 GEMM: 3xTF32 on tcgen05 -------------------------------
+// fp32 programs need fp32-level accuracy (parity 1e-5), which one TF32 pass (10-bit mantissa)
+// cannot give.  Each operand is split exactly into hi = x with the low 13 mantissa bits cleared
+// (exactly representable in TF32, so hardware truncation or rounding leaves it unchanged) and
+// lo = x - hi (exact in fp32); D += A_hi B_hi + A_hi B_lo + A_lo B_hi with kind::tf32 MMAs,
+// fp32 accumulation in TMEM (the dropped A_lo B_lo term is < 2^-22 relative).
+
+__global__ void __launch_bounds__(256) SplitTf32Kernel(const float4* __restrict__ x, float4* __restrict__ hi,
+                                                       float4* __restrict__ lo, int64_t n4) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
+    const float4 v = x[i];
+    float4 h, l;
+    h.x = __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
+    h.y = __uint_as_float(__float_as_uint(v.y) & 0xffffe000u);
+    h.z = __uint_as_float(__float_as_uint(v.z) & 0xffffe000u);
+    h.w = __uint_as_float(__float_as_uint(v.w) & 0xffffe000u);
+    l.x = __fsub_rn(v.x, h.x);
+    l.y = __fsub_rn(v.y, h.y);
+    l.z = __fsub_rn(v.z, h.z);
+    l.w = __fsub_rn(v.w, h.w);
+    hi[i] = h;
+    lo[i] = l;
+  }
+}
+
+constexpr int BK32 = 32;   // fp32 elements per k-block (128 bytes: one swizzle row)
+constexpr int STAGES32 = 3;
+
+template <int BN, bool kBKMajor>
+struct Tf32Cfg {
+  static constexpr int kA = BM * BK32 * 4;           // 16 KB
+  static constexpr int kB = BN * BK32 * 4;           // 16 KB at BN=128
+  static constexpr int kStage = 2 * kA + 2 * kB;     // hi + lo of A and B
+  static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kSmem = STAGES32 * kStage + 1024 + 1024;
+  static constexpr uint32_t kIdesc = (1u << 4)                     // D = F32
+                                     | (2u << 7) | (2u << 10)      // A, B = TF32
+                                     | (0u << 15) | ((kBKMajor ? 0u : 1u) << 16) |
+                                     (static_cast<uint32_t>(BN >> 3) << 17) |
+                                     (static_cast<uint32_t>(BM >> 4) << 24);
+};
+
+__device__ __forceinline__ void MmaTf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// maps: 0 A_hi, 1 A_lo, 2 B_hi, 3 B_lo
+template <int BN, bool kBKMajor>
+__global__ void __launch_bounds__(kThreads, 1)
+    GemmTf32x3Kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
+                     const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
+                     float* __restrict__ C, int M, int N, int K, ChainArgs epi) {
+  using Cfg = Tf32Cfg<BN, kBKMajor>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES32 * Cfg::kStage);
+  uint64_t* empty = full + STAGES32;
+  uint64_t* tfull = empty + STAGES32;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int num_m = M / BM, num_n = N / BN, tiles = num_m * num_n, kblocks = K / BK32;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES32; ++s) {
+      MbarInit(&full[s], 1);
+      MbarInit(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      MbarInit(&tfull[a], 1);
+      MbarInit(&tempty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(SmemU32(tmem_slot)),
+                 "r"(Cfg::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  FenceBefore();
+  __syncthreads();
+  FenceAfter();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer: A_hi, A_lo, B_hi, B_lo per stage
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int m_blk = tile % num_m, n_blk = tile / num_m;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          MbarWait(&empty[stage], phase ^ 1);
+          uint8_t* s_ahi = smem + stage * Cfg::kStage;
+          uint8_t* s_alo = s_ahi + Cfg::kA;
+          uint8_t* s_bhi = s_alo + Cfg::kA;
+          uint8_t* s_blo = s_bhi + Cfg::kB;
+          MbarExpectTx(&full[stage], Cfg::kStage);
+          TmaLoad2D(s_ahi, &ta_hi, &full[stage], kb * BK32, m_blk * BM);
+          TmaLoad2D(s_alo, &ta_lo, &full[stage], kb * BK32, m_blk * BM);
+          if constexpr (kBKMajor) {
+            TmaLoad2D(s_bhi, &tb_hi, &full[stage], kb * BK32, n_blk * BN);
+            TmaLoad2D(s_blo, &tb_lo, &full[stage], kb * BK32, n_blk * BN);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 32; ++j) {
+              TmaLoad2D(s_bhi + j * (32 * BK32 * 4), &tb_hi, &full[stage], n_blk * BN + j * 32, kb * BK32);
+              TmaLoad2D(s_blo + j * (32 * BK32 * 4), &tb_lo, &full[stage], n_blk * BN + j * 32, kb * BK32);
+            }
+          }
+          if (++stage == STAGES32) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer: 3 TF32 products per k-substep
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        MbarWait(&tempty[acc], acc_phase ^ 1);
+        FenceAfter();
+        const uint32_t d_tmem = tmem + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          MbarWait(&full[stage], phase);
+          FenceAfter();
+          const uint32_t ahi = SmemU32(smem + stage * Cfg::kStage);
+          const uint32_t alo = ahi + Cfg::kA;
+          const uint32_t bhi = alo + Cfg::kA;
+          const uint32_t blo = bhi + Cfg::kB;
+#pragma unroll
+          for (int k = 0; k < BK32 / 8; ++k) {  // UMMA_K = 8 for tf32 (32 bytes)
+            const uint64_t dahi = DescSw128(ahi + k * 32, 16, 1024);
+            const uint64_t dalo = DescSw128(alo + k * 32, 16, 1024);
+            const uint64_t dbhi = kBKMajor ? DescSw128(bhi + k * 32, 16, 1024)
+                                           : DescSw128(bhi + k * 8 * 128, 32 * BK32 * 4, 1024);
+            const uint64_t dblo = kBKMajor ? DescSw128(blo + k * 32, 16, 1024)
+                                           : DescSw128(blo + k * 8 * 128, 32 * BK32 * 4, 1024);
+            MmaTf32(d_tmem, dalo, dbhi, Cfg::kIdesc, (kb | k) != 0);  // small terms first
+            MmaTf32(d_tmem, dahi, dblo, Cfg::kIdesc, 1);
+            MmaTf32(d_tmem, dahi, dbhi, Cfg::kIdesc, 1);
+          }
+          Commit(&empty[stage]);
+          if (++stage == STAGES32) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        Commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {  // epilogue: fp32 out (+ chain)
+    const int ew = warp - 4;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      const int m_blk = tile % num_m, n_blk = tile / num_m;
+      MbarWait(&tfull[acc], acc_phase);
+      FenceAfter();
+      const int row = m_blk * BM + ew * 32 + lane;
+      float* crow = C + static_cast<int64_t>(row) * N + n_blk * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        TmemLd32(tmem + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        if (epi.n_fn) ApplyChainVecF32<32>(epi.fns, epi.n_fn, v);
+        float4* dst = reinterpret_cast<float4*>(crow + c * 32);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
+      FenceBefore();
+      __syncwarp();
+      if (lane == 0) MbarArrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  FenceBefore();
+  __syncthreads();
+  FenceAfter();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::kTmemCols));
+  }
+}
+
 // ------------------------------------------- host ------------------------------------------
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -284,18 +488,19 @@ EncodeFn GetEncode() {
   return fn;
 }
 
-// 2-D bf16 tensor map: inner dim `d0` (contiguous), outer `d1` with row pitch `pitch` elements.
+// 2-D tensor map (bf16 or fp32): inner dim `d0` (contiguous), outer `d1` with row pitch `pitch`
+// elements, 128-byte swizzle.
 CUtensorMap MakeMap(const void* base, uint64_t d0, uint64_t d1, uint64_t pitch, uint32_t box0,
-                    uint32_t box1) {
+                    uint32_t box1, bool f32 = false) {
   CUtensorMap m;
   cuuint64_t dims[2] = {d0, d1};
-  cuuint64_t strides[1] = {pitch * 2};
+  cuuint64_t strides[1] = {pitch * (f32 ? 4 : 2)};
   cuuint32_t box[2] = {box0, box1};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = GetEncode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
-                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = GetEncode()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                           2, const_cast<void*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) Fail("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")", RH_ERR_CUDA);
   return m;
 }
@@ -335,11 +540,13 @@ int NumSms() {
 template <int BN, bool kBK>
 void Launch(const GemmArgs& g, cudaStream_t s) {
   using Cfg = TcCfg<BN, kBK>;
-  static bool attr = false;
-  if (!attr) {
+  int dev = 0;
+  RH_CUDA(cudaGetDevice(&dev));
+  static bool attr[64] = {};  // per device (local multi-GPU runtimes)
+  if (dev < 64 && !attr[dev]) {
     RH_CUDA(cudaFuncSetAttribute(GemmTcKernel<BN, kBK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Cfg::kSmem));
-    attr = true;
+    attr[dev] = true;
   }
   const Maps& mp = GetMaps(g, BN);
   const int tiles = static_cast<int>((g.m / BM) * (g.n / BN));
@@ -351,16 +558,85 @@ void Launch(const GemmArgs& g, cudaStream_t s) {
 }
 
 int PickBN(const GemmArgs& g) {
+  if (g.dtype == RH_F32) return g.n % 128 == 0 ? 128 : 0;
   if (g.n % 256 == 0 && (g.m / BM) * (g.n / 256) >= 96) return 256;
   if (g.n % 128 == 0) return 128;
   return 0;
 }
 
+struct Maps4 {
+  CUtensorMap a_hi, a_lo, b_hi, b_lo;
+};
+
+template <bool kBK>
+void LaunchTf32x3(const GemmArgs& g, cudaStream_t s) {
+  constexpr int BN = 128;
+  using Cfg = Tf32Cfg<BN, kBK>;
+  int dev = 0;
+  RH_CUDA(cudaGetDevice(&dev));
+  static bool attr[64] = {};
+  if (dev < 64 && !attr[dev]) {
+    RH_CUDA(cudaFuncSetAttribute(GemmTf32x3Kernel<BN, kBK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg::kSmem));
+    attr[dev] = true;
+  }
+  const int64_t na = g.m * g.k, nb = g.k * g.n;
+  float* a_hi = static_cast<float*>(g.scratch);
+  float* a_lo = a_hi + na;
+  float* b_hi = a_lo + na;
+  float* b_lo = b_hi + nb;
+  const int threads = 256;
+  auto blocks = [](int64_t n4) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 148 * 8))); };
+  SplitTf32Kernel<<<blocks(na / 4), threads, 0, s>>>(static_cast<const float4*>(g.a), reinterpret_cast<float4*>(a_hi),
+                                                     reinterpret_cast<float4*>(a_lo), na / 4);
+  SplitTf32Kernel<<<blocks(nb / 4), threads, 0, s>>>(static_cast<const float4*>(g.b), reinterpret_cast<float4*>(b_hi),
+                                                     reinterpret_cast<float4*>(b_lo), nb / 4);
+  RH_CUDA(cudaGetLastError());
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int64_t, int64_t, int64_t, bool>, Maps4> cache;
+  Maps4 mp;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(g.scratch, g.m, g.n, g.k, g.tb);
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+      Maps4 m4;
+      m4.a_hi = MakeMap(a_hi, g.k, g.m, g.k, BK32, BM, true);
+      m4.a_lo = MakeMap(a_lo, g.k, g.m, g.k, BK32, BM, true);
+      if (kBK) {  // B stored [N,K]
+        m4.b_hi = MakeMap(b_hi, g.k, g.n, g.k, BK32, BN, true);
+        m4.b_lo = MakeMap(b_lo, g.k, g.n, g.k, BK32, BN, true);
+      } else {    // B stored [K,N], 32-wide chunks
+        m4.b_hi = MakeMap(b_hi, g.n, g.k, g.n, 32, BK32, true);
+        m4.b_lo = MakeMap(b_lo, g.n, g.k, g.n, 32, BK32, true);
+      }
+      it = cache.emplace(key, m4).first;
+    }
+    mp = it->second;
+  }
+  const int tiles = static_cast<int>((g.m / BM) * (g.n / BN));
+  const int grid = std::min(tiles, NumSms());
+  GemmTf32x3Kernel<BN, kBK><<<grid, kThreads, Cfg::kSmem, s>>>(
+      mp.a_hi, mp.a_lo, mp.b_hi, mp.b_lo, static_cast<float*>(g.c), static_cast<int>(g.m),
+      static_cast<int>(g.n), static_cast<int>(g.k), g.epi);
+  RH_CUDA(cudaGetLastError());
+}
+
 }  // namespace
 
+size_t GemmTf32x3ScratchBytes(const GemmArgs& g) {
+  return static_cast<size_t>(2 * (g.m * g.k + g.k * g.n)) * 4;
+}
+
 bool GemmTcSupported(const GemmArgs& g) {
-  if (g.dtype != RH_BF16 || g.ta) return false;
-  if (g.m % BM || g.k % BK || g.k == 0) return false;
+  if (g.ta) return false;
+  if (g.dtype == RH_F32) {
+    if (g.m % BM || g.n % 128 || g.k % BK32 || g.k == 0 || !g.scratch) return false;
+  } else if (g.dtype == RH_BF16) {
+    if (g.m % BM || g.k % BK || g.k == 0) return false;
+  } else {
+    return false;
+  }
   if (g.m > (int64_t{1} << 30) || g.n > (int64_t{1} << 30) || g.k > (int64_t{1} << 30)) return false;
   if (PickBN(g) == 0) return false;
   const uintptr_t a = reinterpret_cast<uintptr_t>(g.a), b = reinterpret_cast<uintptr_t>(g.b);
@@ -370,6 +646,11 @@ bool GemmTcSupported(const GemmArgs& g) {
 
 void LaunchGemmTc(const GemmArgs& g, cudaStream_t s) {
   if (!GemmTcSupported(g)) Fail("tcgen05 GEMM: unsupported shape/layout", RH_ERR_UNSUPPORTED);
+  if (g.dtype == RH_F32) {
+    if (g.tb) LaunchTf32x3<true>(g, s);
+    else LaunchTf32x3<false>(g, s);
+    return;
+  }
   const int bn = PickBN(g);
   if (bn == 256) {
     if (g.tb) Launch<256, true>(g, s);

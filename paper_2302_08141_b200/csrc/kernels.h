@@ -97,7 +97,11 @@ struct GemmArgs {
   bool ta, tb;
   int dtype;
   ChainArgs epi;
+  // fp32 tensor-core path (3xTF32): device scratch for the hi/lo splits of A and B
+  // (GemmTf32x3ScratchBytes bytes, reused by every GEMM of a program: they run in stream order).
+  void* scratch = nullptr;
 };
+size_t GemmTf32x3ScratchBytes(const GemmArgs& g);
 // CUDA-core kernel (any shape/layout); the test reference for the tensor-core path.
 void LaunchGemmSimt(const GemmArgs& g, cudaStream_t s);
 // tcgen05 / TMEM / TMA kernel.  Returns false when the shape/layout is not supported by it.

@@ -86,6 +86,18 @@ def test_tc_fused_epilogue_chain():
     assert len(names3) == 2 and "unary_chain" in names3[1]
 
 
+@pytest.mark.parametrize("m,k,n", [(128, 32, 128), (256, 512, 384), (1024, 4096, 1024),
+                                   (2048, 16384, 512)])
+@pytest.mark.parametrize("tb", [False, True])
+def test_tc_3xtf32_vs_fp64(m, k, n, tb):
+    """fp32 programs: 3xTF32 on tcgen05 (kind::tf32), fp32-level accuracy (parity 1e-5)."""
+    a, b, c, names = run(matmul_doc(m, k, n, tb, dtype="f32"))
+    assert any(s.startswith("gemm_tc_3xtf32") for s in names), names
+    ref = a.astype(np.float64) @ (b.astype(np.float64).T if tb else b.astype(np.float64))
+    err = np.abs(c - ref).max() / np.abs(ref).max()
+    assert err <= 1e-5, err
+
+
 def test_simt_fp32_gemm_vs_fp64():
     a, b, c, names = run(matmul_doc(300, 200, 100, True, dtype="f32"))
     assert any("gemm_simt" in s for s in names)
