@@ -289,6 +289,22 @@ __global__ void __launch_bounds__(256) SplitTf32Kernel(const float4* __restrict_
   }
 }
 
+// B stored [K,N] (MN-major): split AND transpose to [N,K] in the same pass (32x33 smem tile),
+// so the MMA always reads K-major TF32 operands.
+__global__ void __launch_bounds__(256) SplitTransposeTf32Kernel(const float* __restrict__ b, float* __restrict__ hi_t,
+                                                                float* __restrict__ lo_t, int64_t K, int64_t N) {
+  __shared__ float tile[32][33];
+  const int64_t k0 = int64_t(blockIdx.y) * 32, n0 = int64_t(blockIdx.x) * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) tile[j][threadIdx.x] = b[(k0 + j) * N + n0 + threadIdx.x];
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const float v = tile[threadIdx.x][j];
+    const float h = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
+    hi_t[(n0 + j) * K + k0 + threadIdx.x] = h;
+    lo_t[(n0 + j) * K + k0 + threadIdx.x] = __fsub_rn(v, h);
+  }
+}
+
 constexpr int BK32 = 32;   // fp32 elements per k-block (128 bytes: one swizzle row)
 constexpr int STAGES32 = 3;
 
@@ -571,12 +587,12 @@ struct Maps4 {
 template <bool kBK>
 void LaunchTf32x3(const GemmArgs& g, cudaStream_t s) {
   constexpr int BN = 128;
-  using Cfg = Tf32Cfg<BN, kBK>;
+  using Cfg = Tf32Cfg<BN, true>;
   int dev = 0;
   RH_CUDA(cudaGetDevice(&dev));
   static bool attr[64] = {};
   if (dev < 64 && !attr[dev]) {
-    RH_CUDA(cudaFuncSetAttribute(GemmTf32x3Kernel<BN, kBK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RH_CUDA(cudaFuncSetAttribute(GemmTf32x3Kernel<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Cfg::kSmem));
     attr[dev] = true;
   }
@@ -589,8 +605,14 @@ void LaunchTf32x3(const GemmArgs& g, cudaStream_t s) {
   auto blocks = [](int64_t n4) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 148 * 8))); };
   SplitTf32Kernel<<<blocks(na / 4), threads, 0, s>>>(static_cast<const float4*>(g.a), reinterpret_cast<float4*>(a_hi),
                                                      reinterpret_cast<float4*>(a_lo), na / 4);
-  SplitTf32Kernel<<<blocks(nb / 4), threads, 0, s>>>(static_cast<const float4*>(g.b), reinterpret_cast<float4*>(b_hi),
-                                                     reinterpret_cast<float4*>(b_lo), nb / 4);
+  if (kBK) {
+    SplitTf32Kernel<<<blocks(nb / 4), threads, 0, s>>>(static_cast<const float4*>(g.b),
+                                                       reinterpret_cast<float4*>(b_hi),
+                                                       reinterpret_cast<float4*>(b_lo), nb / 4);
+  } else {  // [K,N] -> hi/lo of [N,K]
+    SplitTransposeTf32Kernel<<<dim3(static_cast<unsigned>(g.n / 32), static_cast<unsigned>(g.k / 32)),
+                               dim3(32, 8), 0, s>>>(static_cast<const float*>(g.b), b_hi, b_lo, g.k, g.n);
+  }
   RH_CUDA(cudaGetLastError());
   static std::mutex mu;
   static std::map<std::tuple<const void*, int64_t, int64_t, int64_t, bool>, Maps4> cache;
@@ -603,20 +625,16 @@ void LaunchTf32x3(const GemmArgs& g, cudaStream_t s) {
       Maps4 m4;
       m4.a_hi = MakeMap(a_hi, g.k, g.m, g.k, BK32, BM, true);
       m4.a_lo = MakeMap(a_lo, g.k, g.m, g.k, BK32, BM, true);
-      if (kBK) {  // B stored [N,K]
-        m4.b_hi = MakeMap(b_hi, g.k, g.n, g.k, BK32, BN, true);
-        m4.b_lo = MakeMap(b_lo, g.k, g.n, g.k, BK32, BN, true);
-      } else {    // B stored [K,N], 32-wide chunks
-        m4.b_hi = MakeMap(b_hi, g.n, g.k, g.n, 32, BK32, true);
-        m4.b_lo = MakeMap(b_lo, g.n, g.k, g.n, 32, BK32, true);
-      }
+      // the split buffers of B are always [N,K] (K-major)
+      m4.b_hi = MakeMap(b_hi, g.k, g.n, g.k, BK32, BN, true);
+      m4.b_lo = MakeMap(b_lo, g.k, g.n, g.k, BK32, BN, true);
       it = cache.emplace(key, m4).first;
     }
     mp = it->second;
   }
   const int tiles = static_cast<int>((g.m / BM) * (g.n / BN));
   const int grid = std::min(tiles, NumSms());
-  GemmTf32x3Kernel<BN, kBK><<<grid, kThreads, Cfg::kSmem, s>>>(
+  GemmTf32x3Kernel<BN, true><<<grid, kThreads, Cfg::kSmem, s>>>(
       mp.a_hi, mp.a_lo, mp.b_hi, mp.b_lo, static_cast<float*>(g.c), static_cast<int>(g.m),
       static_cast<int>(g.n), static_cast<int>(g.k), g.epi);
   RH_CUDA(cudaGetLastError());
