@@ -307,6 +307,7 @@ __global__ void __launch_bounds__(256) SplitTransposeTf32Kernel(const float* __r
 
 constexpr int BK32 = 32;   // fp32 elements per k-block (128 bytes: one swizzle row)
 constexpr int STAGES32 = 3;
+constexpr int kChunkKb = 8;  // k-blocks (8 x 32 = K 256) per TMEM accumulation chunk
 
 template <int BN, bool kBKMajor>
 struct Tf32Cfg {
@@ -408,70 +409,90 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {  // MMA issuer: 3 TF32 products per k-substep
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
+      // The TMEM accumulator adds each MMA's partial sums with truncation (measured: error
+      // growing linearly in K, 3.7e-5 at K=4096).  So TMEM accumulates only a K-chunk of
+      // kChunkKb k-blocks; the epilogue warps add the chunks in fp32 registers with
+      // round-to-nearest (error ~(chunk/8) * 2^-24 + RN noise: ~1e-6).
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        MbarWait(&tempty[acc], acc_phase ^ 1);
-        FenceAfter();
-        const uint32_t d_tmem = tmem + acc * BN;
-        for (int kb = 0; kb < kblocks; ++kb) {
-          MbarWait(&full[stage], phase);
+        for (int kb0 = 0; kb0 < kblocks; kb0 += kChunkKb) {
+          MbarWait(&tempty[acc], acc_phase ^ 1);
           FenceAfter();
-          const uint32_t ahi = SmemU32(smem + stage * Cfg::kStage);
-          const uint32_t alo = ahi + Cfg::kA;
-          const uint32_t bhi = alo + Cfg::kA;
-          const uint32_t blo = bhi + Cfg::kB;
+          const uint32_t d_tmem = tmem + acc * BN;
+          const int kb1 = min(kb0 + kChunkKb, kblocks);
+          for (int kb = kb0; kb < kb1; ++kb) {
+            MbarWait(&full[stage], phase);
+            FenceAfter();
+            const uint32_t ahi = SmemU32(smem + stage * Cfg::kStage);
+            const uint32_t alo = ahi + Cfg::kA;
+            const uint32_t bhi = alo + Cfg::kA;
+            const uint32_t blo = bhi + Cfg::kB;
 #pragma unroll
-          for (int k = 0; k < BK32 / 8; ++k) {  // UMMA_K = 8 for tf32 (32 bytes)
-            const uint64_t dahi = DescSw128(ahi + k * 32, 16, 1024);
-            const uint64_t dalo = DescSw128(alo + k * 32, 16, 1024);
-            const uint64_t dbhi = kBKMajor ? DescSw128(bhi + k * 32, 16, 1024)
-                                           : DescSw128(bhi + k * 8 * 128, 32 * BK32 * 4, 1024);
-            const uint64_t dblo = kBKMajor ? DescSw128(blo + k * 32, 16, 1024)
-                                           : DescSw128(blo + k * 8 * 128, 32 * BK32 * 4, 1024);
-            MmaTf32(d_tmem, dalo, dbhi, Cfg::kIdesc, (kb | k) != 0);  // small terms first
-            MmaTf32(d_tmem, dahi, dblo, Cfg::kIdesc, 1);
-            MmaTf32(d_tmem, dahi, dbhi, Cfg::kIdesc, 1);
+            for (int k = 0; k < BK32 / 8; ++k) {  // UMMA_K = 8 for tf32 (32 bytes)
+              const uint64_t dahi = DescSw128(ahi + k * 32, 16, 1024);
+              const uint64_t dalo = DescSw128(alo + k * 32, 16, 1024);
+              const uint64_t dbhi = DescSw128(bhi + k * 32, 16, 1024);
+              const uint64_t dblo = DescSw128(blo + k * 32, 16, 1024);
+              MmaTf32(d_tmem, dalo, dbhi, Cfg::kIdesc, (kb != kb0) || k != 0);  // small terms first
+              MmaTf32(d_tmem, dahi, dblo, Cfg::kIdesc, 1);
+              MmaTf32(d_tmem, dahi, dbhi, Cfg::kIdesc, 1);
+            }
+            Commit(&empty[stage]);
+            if (++stage == STAGES32) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
-          Commit(&empty[stage]);
-          if (++stage == STAGES32) {
-            stage = 0;
-            phase ^= 1;
+          Commit(&tfull[acc]);
+          if (++acc == 2) {
+            acc = 0;
+            acc_phase ^= 1;
           }
-        }
-        Commit(&tfull[acc]);
-        if (++acc == 2) {
-          acc = 0;
-          acc_phase ^= 1;
         }
       }
     }
-  } else if (warp >= 4) {  // epilogue: fp32 out (+ chain)
+  } else if (warp >= 4) {  // epilogue: RN accumulation of the chunks, fp32 out (+ chain)
     const int ew = warp - 4;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       const int m_blk = tile % num_m, n_blk = tile / num_m;
-      MbarWait(&tfull[acc], acc_phase);
-      FenceAfter();
+      float sum[BN];
+#pragma unroll
+      for (int j = 0; j < BN; ++j) sum[j] = 0.0f;
+      for (int kb0 = 0; kb0 < kblocks; kb0 += kChunkKb) {
+        MbarWait(&tfull[acc], acc_phase);
+        FenceAfter();
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          TmemLd32(tmem + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sum[c * 32 + j] = __fadd_rn(sum[c * 32 + j], __uint_as_float(r[j]));
+        }
+        FenceBefore();
+        __syncwarp();
+        if (lane == 0) MbarArrive(&tempty[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
       const int row = m_blk * BM + ew * 32 + lane;
       float* crow = C + static_cast<int64_t>(row) * N + n_blk * BN;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        TmemLd32(tmem + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
-        float v[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if (epi.n_fn) ApplyChainVecF32<32>(epi.fns, epi.n_fn, v);
+      for (int c = 0; c < BN / 32; ++c) {
+        float* v = sum + c * 32;
+        if (epi.n_fn) {
+          float t[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) t[j] = v[j];
+          ApplyChainVecF32<32>(epi.fns, epi.n_fn, t);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = t[j];
+        }
         float4* dst = reinterpret_cast<float4*>(crow + c * 32);
 #pragma unroll
         for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-      }
-      FenceBefore();
-      __syncwarp();
-      if (lane == 0) MbarArrive(&tempty[acc]);
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
       }
     }
   }
