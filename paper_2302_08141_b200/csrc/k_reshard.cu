@@ -148,6 +148,103 @@ __global__ void __launch_bounds__(256) PullSumKernel(PullDev a, int d) {
   }
 }
 
+// Fine-grained (strided) sources: Shard(dim, s) with runs shorter than 16 bytes interleave the
+// d members element by element, so a per-element pull would issue 2-4-byte gathers.  Instead a
+// block takes L consecutive destination elements whose global range [f0, f0+L) is aligned to a
+// full round-robin cycle Lr = Qs_from * d: each member then owns ONE contiguous L/d slice of it
+// (local offset (f0/Lr)*Qs_from).  The block copies the d slices into shared memory with 16-byte
+// loads (local HBM or NVLink peer), then writes the L destination elements with 16-byte stores,
+// re-interleaving through shared memory.
+struct StagedDev {
+  char* dst;
+  const char* src[kMaxGroup];
+  int to_shard;
+  FastDiv qst;  // destination run (elements)
+  FastDiv qsf;  // source run (elements)
+  FastDiv dd;
+  uint32_t coord;
+  uint32_t L;       // elements per chunk
+  uint32_t per;     // L / d
+  uint32_t chunks;  // destination chunks
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) PullStagedKernel(StagedDev a) {
+  extern __shared__ __align__(16) unsigned char smem_stage[];
+  T* tile = reinterpret_cast<T*>(smem_stage);
+  constexpr int E = 16 / sizeof(T);  // elements per 16-byte vector
+  const uint32_t d = a.dd.d;
+  const uint32_t Lr = a.qsf.d * d;
+  for (uint32_t chunk = blockIdx.x; chunk < a.chunks; chunk += gridDim.x) {
+    const uint32_t i0 = chunk * a.L;
+    uint32_t f0 = i0;
+    if (a.to_shard) {
+      const uint32_t p = Div(a.qst, i0);
+      f0 = (p * d + a.coord) * a.qst.d + (i0 - p * a.qst.d);
+    }
+    const uint32_t base = (f0 / Lr) * a.qsf.d;  // each member's local start
+    const uint32_t vper = a.per / E;
+    for (uint32_t v = threadIdx.x; v < vper * d; v += blockDim.x) {
+      const uint32_t k = v / vper, j = v - k * vper;
+      reinterpret_cast<uint4*>(tile)[v] = reinterpret_cast<const uint4*>(a.src[k] + size_t(base) * sizeof(T))[j];
+    }
+    __syncthreads();
+    for (uint32_t v = threadIdx.x; v < a.L / E; v += blockDim.x) {
+      T out[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const uint32_t i = v * E + e;         // offset in the chunk == offset from f0
+        const uint32_t q = Div(a.qsf, i);     // run index
+        const uint32_t qd = Div(a.dd, q);
+        const uint32_t r = q - qd * d;        // owner
+        out[e] = tile[r * a.per + qd * a.qsf.d + (i - q * a.qsf.d)];
+      }
+      reinterpret_cast<uint4*>(a.dst + size_t(i0) * sizeof(T))[v] = *reinterpret_cast<uint4*>(out);
+    }
+    __syncthreads();
+  }
+}
+
+// Returns true when the staged kernel was launched.
+bool TryLaunchStaged(const PullArgs& a, cudaStream_t s) {
+  if (a.from.kind != RH_SHARD) return false;
+  const int eb = ElemBytes(a.dtype);
+  const int64_t qsf = a.from.Qs, d = a.from.d;
+  if (qsf * eb >= 16) return false;  // runs already vectorize in the plain pull kernel
+  const int64_t Lr = qsf * d;
+  const int64_t run = a.to.kind == RH_SHARD ? a.to.Qs : a.n_dst;
+  if (a.to.kind == RH_SHARD && a.to.Qs % Lr != 0) return false;
+  const int64_t E = 16 / eb;
+  int64_t L = 0;
+  for (int64_t m = 1; Lr * m <= 8192; m *= 2) {
+    const int64_t cand = Lr * m;
+    if (run % cand == 0 && (cand / d) % E == 0) L = cand;
+  }
+  if (L == 0) return false;
+  for (int k = 0; k < d; ++k)
+    if (reinterpret_cast<uintptr_t>(a.src[k]) % 16) return false;
+  if (reinterpret_cast<uintptr_t>(a.dst) % 16) return false;
+  const int64_t total = a.to.kind == RH_SHARD ? a.n_dst * a.to.d : a.n_dst;
+  if (total >= (int64_t{1} << 32)) return false;
+  StagedDev sd{};
+  sd.dst = static_cast<char*>(a.dst);
+  for (int k = 0; k < kMaxGroup; ++k) sd.src[k] = static_cast<const char*>(a.src[k]);
+  sd.to_shard = a.to.kind == RH_SHARD;
+  sd.qst = MakeFastDiv(sd.to_shard ? static_cast<uint32_t>(a.to.Qs) : 1u);
+  sd.qsf = MakeFastDiv(static_cast<uint32_t>(qsf));
+  sd.dd = MakeFastDiv(static_cast<uint32_t>(d));
+  sd.coord = static_cast<uint32_t>(a.coord);
+  sd.L = static_cast<uint32_t>(L);
+  sd.per = static_cast<uint32_t>(L / d);
+  sd.chunks = static_cast<uint32_t>(a.n_dst / L);
+  const int blocks = static_cast<int>(std::min<int64_t>(sd.chunks, 148 * 8));
+  const size_t smem = static_cast<size_t>(L) * eb;
+  if (eb == 2) PullStagedKernel<uint16_t><<<blocks, 256, smem, s>>>(sd);
+  else PullStagedKernel<uint32_t><<<blocks, 256, smem, s>>>(sd);
+  RH_CUDA(cudaGetLastError());
+  return true;
+}
+
 int Gcd(int64_t a, int64_t b) {
   while (b) {
     int64_t t = a % b;
@@ -185,6 +282,7 @@ int LaunchPull(const PullArgs& a, cudaStream_t s) {
     RH_CUDA(cudaMemsetAsync(a.dst, 0, a.n_dst * eb, s));
     return 1;
   }
+  if (TryLaunchStaged(a, s)) return 1;
   // Vector width: the largest power-of-two unit (<= 16 B) that divides every contiguous run and
   // every buffer alignment.
   int64_t g = a.n_dst;
