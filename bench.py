@@ -1,19 +1,20 @@
 #!/usr/bin/env python3
 """Benchmark: partitioned-program step time and tokens/s on 1-8 B200 (BASELINE.json metric).
 
-Workload (config.workload): the GPT-style Transformer block of BASELINE.json configs[2]
-(`gpt_like(1, hidden 4096, batch/seq 2048)` from proj/src/fixtures.cpp:101-137, 108 ops) planned
-by the UNCHANGED reference planner for a mesh of N devices (tests/golden/plans/c3_gpt_block_dN)
-and executed by librhino_exec.so.  One step = one forward execution of the partitioned program
-including the final output materialization; tokens = rows of the program input x (2048).
-Synthetic Philox inputs/parameters (no datasets).  --dtype bf16 (default; tensor-core GEMMs,
-tolerance 2e-2) or f32.
+Default workload (config.workload): the GPT-style Transformer block of BASELINE.json configs[2]
+(`gpt_like(1, hidden 4096, batch/seq 2048)`, proj/src/fixtures.cpp:101-137, 108 ops) planned by
+the UNCHANGED reference planner for a mesh of N devices (tests/golden/plans/c3_gpt_block_dN) and
+executed by librhino_exec.so.  One step = one forward execution of the partitioned program,
+including the final output materialization; tokens = rows of the program input x.  Synthetic
+Philox inputs/parameters (no datasets).  --workload mlp / mlp_strided / mlp_pinned run the C1/C2
+programs (fp32, latency-bound) for the record.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--dtype bf16|f32]
 N > 1 is launched by torchrun (one process per GPU); all ranks time K steps between barriers and
 rank 0 prints the max over ranks as one JSON line.
 """
 import argparse
+import contextlib
 import json
 import math
 import os
@@ -25,8 +26,36 @@ import time
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-HIDDEN, SEQ = 4096, 2048
 NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+
+WORKLOADS = {
+    "gpt_block": dict(plan="c3_gpt_block_d{n}", name="gpt_block_h4096_s2048", dtype="bf16",
+                      metric="partitioned-program tokens/s (GPT block, hidden 4096, seq 2048)"),
+    "mlp": dict(plan="c1_mlp_d{n}", name="mlp2_b64_h1024", dtype="f32",
+                metric="partitioned-program tokens/s (2-layer MLP, batch 64, hidden 1024)"),
+    "mlp_strided": dict(plan="c2_mlp_reshape_d{n}", name="mlp_reshape_strided_b64_h1024", dtype="f32",
+                        metric="partitioned-program tokens/s (strided MLP, batch 64, hidden 1024)"),
+    "mlp_pinned": dict(plan="c2_mlp_pinned_d{n}", name="mlp_pinned_strided_b64_h1024", dtype="f32",
+                       metric="partitioned-program tokens/s (pinned strided MLP, batch 64, hidden 1024)"),
+}
+
+
+def plan_name(workload, n):
+    return WORKLOADS[workload]["plan"].format(n=n)
+
+
+@contextlib.contextmanager
+def stdout_to_stderr():
+    """Native libraries (NCCL's version banner) print to fd 1; keep stdout for the JSON line."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        yield
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
 
 
 def peaks():
@@ -99,10 +128,6 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def plan_name(n):
-    return f"c3_gpt_block_d{n}"
-
-
 def cpu_baseline(prog, threads):
     """The CPU oracle (oracle/ref_cpu_exec.cpp: the reference has no executor) on one
     full unpartitioned step of the same program: test-infrastructure timing, not the product."""
@@ -114,6 +139,10 @@ def cpu_baseline(prog, threads):
     return time.perf_counter() - t0
 
 
+def tokens_of(prog):
+    return prog.ops[prog.op_index("x")].shape[0]
+
+
 def run_reference(args):
     """--impl reference: the oracle port timed on this box's host cores (rank 0 only)."""
     from paper_2302_08141_b200.abi import RH_BF16, RH_F32
@@ -122,22 +151,27 @@ def run_reference(args):
     world, rank, _ = env()
     if rank != 0:
         return
-    prog = LoweredProgram.load(plan_name(1)).with_dtype(RH_BF16 if args.dtype == "bf16" else RH_F32)
+    wl = WORKLOADS[args.workload]
+    name = plan_name(args.workload, 1) if args.workload != "mlp_strided" else plan_name(args.workload, 2)
+    prog = LoweredProgram.load(name).with_dtype(RH_BF16 if args.dtype == "bf16" else RH_F32)
     cores = os.cpu_count() or 1
-    k, w = min(args.steps, 2), min(args.warmup, 1)
+    tok = tokens_of(prog)
+    small = prog.flops() < 1e10
+    k, w = (args.steps, args.warmup) if small else (min(args.steps, 2), min(args.warmup, 1))
     for _ in range(w):
         cpu_baseline(prog, cores)
     ts = [cpu_baseline(prog, cores) for _ in range(k)]
     sec = sum(ts) / len(ts)
-    value = SEQ / sec
+    value = tok / sec
     line = {
-        "impl": "reference", "metric": "partitioned-program tokens/s (GPT block, hidden 4096, seq 2048)",
-        "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": k, "warmup": w,
-        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": args.dtype, "data": "synthetic (Philox)",
-        "config": {"workload": "gpt_block_h4096_s2048", "mesh": [1], "global_batch": SEQ, "seq_len": SEQ},
+        "impl": "reference", "metric": wl["metric"], "value": value, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": k, "warmup": w, "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic (Philox)",
+        "config": {"workload": wl["name"], "mesh": [1], "global_batch": tok, "seq_len": tok},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
-                         "sample": f"{k} full unpartitioned step(s) of the 108-op GPT block on {cores} threads"},
+                         "sample": f"{k} full unpartitioned step(s) of {name} ({len(prog.ops)} ops) "
+                                   f"on {cores} threads (oracle/ref_cpu_exec)"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -149,12 +183,15 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--workload", default="gpt_block", choices=sorted(WORKLOADS))
+    ap.add_argument("--dtype", default=None, choices=["bf16", "f32"])
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--simt", action="store_true", help="force the CUDA-core GEMM (comparison)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.dtype is None:
+        args.dtype = WORKLOADS[args.workload]["dtype"]
     if args.impl == "reference":
         return run_reference(args)
 
@@ -167,102 +204,109 @@ def main():
                                            RH_FLAG_TRANSPORT_NCCL)
     from paper_2302_08141_b200.program import LoweredProgram
 
+    wl = WORKLOADS[args.workload]
     world, rank, local = D.env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dtype = RH_BF16 if args.dtype == "bf16" else RH_F32
-    prog = LoweredProgram.load(plan_name(world)).with_dtype(dtype)
+    pname = plan_name(args.workload, world)
+    prog = LoweredProgram.load(pname).with_dtype(dtype)
+    tok = tokens_of(prog)
     flags = (RH_FLAG_TRANSPORT_NCCL if args.transport == "nccl" else 0) | (RH_FLAG_SIMT_GEMM if args.simt else 0)
-    rt = D.make_runtime()
-    mesh = rx.Mesh(rt, prog.mesh)
-    gp = rx.Program(mesh, prog, flags)
-    gp.init_synthetic(0)
-    gp.run(args.warmup)
-    D.barrier()
-    torch.cuda.synchronize()
-    with Clocks(local) as clk:
-        ms_dev = gp.profile(args.steps)  # CUDA events around every step, no host sync inside
-    D.barrier()
-    ms_step = D.max_over_ranks(ms_dev)
-    steps = gp.steps()
-    launches = gp.launch_count() * args.steps
+    with stdout_to_stderr():
+        rt = D.make_runtime()
+        mesh = rx.Mesh(rt, prog.mesh)
+        gp = rx.Program(mesh, prog, flags)
+        gp.init_synthetic(0)
+        gp.run(args.warmup)
+        D.barrier()
+        torch.cuda.synchronize()
+        with Clocks(local) as clk:
+            ms_dev = gp.profile(args.steps)  # one CUDA graph of K runs, events around every step
+        D.barrier()
+        ms_step = D.max_over_ranks(ms_dev)
+        steps = gp.steps()
+        launches = gp.launch_count() * args.steps
 
-    # End to end through the public API with host buffers: H2D of x, one run, D2H of res2.
-    x = prog.op_index("x")
-    out = prog.outputs[0]
-    np_dt = np.uint16 if dtype == RH_BF16 else np.float32
-    xin = torch.empty(prog.full_bytes(x), dtype=torch.uint8).pin_memory()
-    xin.numpy().view(np_dt)[:] = (np.random.default_rng(0).uniform(-1, 1, prog.ops[x].shape).astype(np.float32)
-                                  .view(np.uint32) >> 16).astype(np.uint16).ravel() if dtype == RH_BF16 else \
-        np.random.default_rng(0).uniform(-1, 1, math.prod(prog.ops[x].shape)).astype(np.float32)
-    yout = torch.empty(prog.full_bytes(out), dtype=torch.uint8).pin_memory()
-    gp.step_host([x], [xin.data_ptr()], [yout.data_ptr()])
-    D.barrier()
-    e2e = []
-    for _ in range(args.steps):
-        e2e.append(gp.step_host([x], [xin.data_ptr()], [yout.data_ptr()]))
-    e2e_ms = D.max_over_ranks(sum(e2e) / len(e2e))
+        # End to end through the public API with host buffers: H2D of x, one run, D2H of the output.
+        x = prog.op_index("x")
+        out = prog.outputs[0]
+        xin = torch.empty(prog.full_bytes(x), dtype=torch.uint8).pin_memory()
+        xf = np.random.default_rng(0).uniform(-1, 1, math.prod(prog.ops[x].shape)).astype(np.float32)
+        if dtype == RH_BF16:
+            xin.numpy().view(np.uint16)[:] = (xf.view(np.uint32) >> 16).astype(np.uint16)
+        else:
+            xin.numpy().view(np.float32)[:] = xf
+        yout = torch.empty(prog.full_bytes(out), dtype=torch.uint8).pin_memory()
+        gp.step_host([x], [xin.data_ptr()], [yout.data_ptr()])
+        D.barrier()
+        e2e = [gp.step_host([x], [xin.data_ptr()], [yout.data_ptr()]) for _ in range(args.steps)]
+        e2e_ms = D.max_over_ranks(sum(e2e) / len(e2e))
 
-    # Roofline of the dominant kernel (largest share of the step).
-    pk = peaks()
-    kern = [s for s in steps if s["kind"] == 0]
-    dom = max(kern, key=lambda s: s["ms"])
-    gemm_ms = sum(s["ms"] for s in kern if s["alg_flops"] > 0 and "gemm" in s["name"])
-    if "gemm" in dom["name"]:
-        achieved = dom["alg_flops"] / (dom["ms"] * 1e-3) / 1e12
-        peak = pk["bf16_tflops_sustained"] if dtype == RH_BF16 else pk["bf16_tflops_sustained"] / 2 / 3
-        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None, "kernel": dom["name"],
-                "peak_note": ("sustained bf16 of MEASURED_PEAKS.json" if dtype == RH_BF16 else
-                              "3xTF32 effective = sustained bf16 / 2 / 3") + f" ({pk['source']})",
-                "share_of_step": dom["ms"] / ms_dev}
-    else:
-        achieved = dom["alg_bytes"] / (dom["ms"] * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / pk["hbm_gbs"], "traffic": None, "kernel": dom["name"],
-                "share_of_step": dom["ms"] / ms_dev}
-    tr_path = os.path.join(REPO, "profiles", "ncu_traffic.json")
-    if os.path.exists(tr_path):
-        with open(tr_path) as f:
-            tr = json.load(f)
-        key = f"{plan_name(world)}:{args.dtype}:{dom['name'].split(' ')[0]}"
-        roof["traffic"] = tr.get(key)
-    trans = [s for s in steps if s["kind"] == 1 and s["wire_bytes"] > 0]
-    reshard = None
-    if trans:
-        wire = sum(s["wire_bytes"] for s in trans)
-        t = sum(s["ms"] for s in trans)
-        reshard = {"transitions": len(trans), "wire_bytes_per_rank": wire, "ms": t,
-                   "busbw_gbs": wire / (t * 1e-3) / 1e9 if t > 0 else None,
-                   "peak_gbs": NVLINK_PEER_GBS, "transport": args.transport,
-                   "per_transition": [{"name": s["name"], "ms": s["ms"],
-                                       "busbw_gbs": s["wire_bytes"] / (s["ms"] * 1e-3) / 1e9 if s["ms"] else None}
-                                      for s in trans]}
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cores = os.cpu_count() or 1
-        sec = cpu_baseline(prog, cores)
-        cpu = {"value": SEQ / sec, "unit": "tokens/s", "cores": cores, "kind": "port",
-               "sample": f"1 full unpartitioned step (2048 tokens) of the same program, oracle/ref_cpu_exec, {cores} threads"}
-    h2d = prog.full_bytes(x) * world
-    d2h = prog.full_bytes(out) * world
+        # Roofline of the dominant kernel (largest share of the step).
+        pk = peaks()
+        kern = [s for s in steps if s["kind"] == 0]
+        dom = max(kern, key=lambda s: s["ms"])
+        gemm_ms = sum(s["ms"] for s in kern if "gemm" in s["name"])
+        if "gemm_tc" in dom["name"]:
+            achieved = dom["alg_flops"] / (dom["ms"] * 1e-3) / 1e12
+            f32 = dtype == RH_F32
+            peak = pk["bf16_tflops_sustained"] / 6 if f32 else pk["bf16_tflops_sustained"]
+            roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": None, "kernel": dom["name"],
+                    "peak_note": ("3xTF32 effective fp32 = sustained bf16 / 2 (tf32 rate) / 3 (products)"
+                                  if f32 else "sustained bf16") + f" of MEASURED_PEAKS.json ({pk['source']})",
+                    "share_of_step": dom["ms"] / ms_dev}
+        else:
+            achieved = dom["alg_bytes"] / (dom["ms"] * 1e-3) / 1e9
+            roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": achieved / pk["hbm_gbs"], "traffic": None, "kernel": dom["name"],
+                    "share_of_step": dom["ms"] / ms_dev}
+        tr_path = os.path.join(REPO, "profiles", "ncu_traffic.json")
+        if os.path.exists(tr_path):
+            with open(tr_path) as f:
+                tr = json.load(f)
+            roof["traffic"] = tr.get(f"{pname}:{args.dtype}:{dom['name'].split(' ')[0]}")
+        trans = [s for s in steps if s["kind"] == 1 and s["wire_bytes"] > 0]
+        reshard = None
+        if trans:
+            wire = sum(s["wire_bytes"] for s in trans)
+            t = sum(s["ms"] for s in trans)
+            reshard = {"transitions": len(trans), "wire_bytes_per_rank": wire, "ms": t,
+                       "busbw_gbs": wire / (t * 1e-3) / 1e9 if t > 0 else None,
+                       "peak_gbs": NVLINK_PEER_GBS, "transport": args.transport,
+                       "per_transition": [{"name": s["name"], "ms": s["ms"],
+                                           "busbw_gbs": s["wire_bytes"] / (s["ms"] * 1e-3) / 1e9 if s["ms"] else None}
+                                          for s in trans]}
+        cpu = None
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            cores = os.cpu_count() or 1
+            sec = cpu_baseline(prog, cores)
+            cpu = {"value": tok / sec, "unit": "tokens/s", "cores": cores, "kind": "port",
+                   "sample": f"1 full unpartitioned step ({tok} tokens) of the same program, "
+                             f"oracle/ref_cpu_exec, {cores} threads"}
+        h2d = prog.full_bytes(x) * world
+        d2h = prog.full_bytes(out) * world
+        gp.close()
+        mesh.close()
+        rt.close()
     if rank == 0:
         line = {
-            "metric": "partitioned-program tokens/s (GPT block, hidden 4096, seq 2048)",
-            "value": SEQ / (ms_step * 1e-3), "unit": "tokens/s", "n_gpus": world,
+            "metric": wl["metric"], "value": tok / (ms_step * 1e-3), "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": args.dtype, "data": "synthetic (Philox4x32-10 inputs/params)",
-            "config": {"workload": "gpt_block_h4096_s2048", "plan": plan_name(world), "mesh": prog.mesh,
-                       "global_batch": SEQ, "seq_len": SEQ, "hidden": HIDDEN,
+            "config": {"workload": wl["name"], "plan": pname, "mesh": prog.mesh,
+                       "global_batch": tok, "seq_len": tok, "ops": len(prog.ops),
                        "parallelism": f"rhino-spmd mesh {prog.mesh}", "transport": args.transport,
                        "gemm": "simt" if args.simt else "tcgen05",
-                       "l2": "no flush: per-step working set (weights 384 MB bf16 + activations) > 126 MB L2"},
+                       "l2": "no flush: per-step working set > 126 MB L2" if prog.flops() > 1e11
+                       else "no flush: small latency-bound program (L2-resident; reported as such)"},
             "gflop_per_step": prog.flops() / 1e9,
             "tflops": prog.flops() / (ms_step * 1e-3) / 1e12,
             "gemm_ms": gemm_ms,
-            "e2e": {"value": SEQ / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
+            "e2e": {"value": tok / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "roofline": roof,
@@ -273,9 +317,6 @@ def main():
                                 key=lambda s: -s["ms"])[:8],
         }
         print(json.dumps(line), flush=True)
-    gp.close()
-    mesh.close()
-    rt.close()
 
 
 if __name__ == "__main__":

@@ -674,6 +674,23 @@ class Lowerer {
     auto it = cache_.find(Key(p_->tensors[src].op, to_specs));
     if (it != cache_.end()) return it->second;
     const Tensor X = p_->tensors[src];
+    {
+      // All-reduce over d > 2 peers as reduce-scatter + all-gather: each rank then moves
+      // 2(d-1)/d of the tensor over NVLink (reshard_cost's bytes) instead of the (d-1)x of a
+      // one-shot pull of every peer's full partial.
+      const int d = mesh_[axis];
+      const bool nccl = (p_->flags & RH_FLAG_TRANSPORT_NCCL) && rt_->dist;
+      if (X.specs[axis].kind == RH_PARTIAL && to_specs[axis].kind == RH_REPLICATED && d > 2 && !nccl) {
+        const Dims D = LocalDims(X.gdims, X.specs, mesh_, axis);
+        for (int dim = 0; dim < static_cast<int>(D.size()); ++dim) {
+          if (D[dim] % d != 0) continue;
+          Specs mid = to_specs;
+          mid[axis] = Sh(dim, D[dim] / d);
+          const int m = Move(src, axis, mid, why);
+          return Move(m, axis, to_specs, why);
+        }
+      }
+    }
     const int dst = NewTensor(X.op, to_specs);
     const Tensor Y = p_->tensors[dst];
     const int d = mesh_[axis];
