@@ -501,8 +501,8 @@ class Lowerer {
         // program (stream-ordered), sized to the largest and placed at the end of lowering.
         if (dtype == RH_F32) g.scratch = reinterpret_cast<void*>(uintptr_t{256});  // support probe
         const bool tc = !(P->flags & RH_FLAG_SIMT_GEMM) && GemmTcSupported(g);
-        if (tc && dtype == RH_F32)
-          P->gemm_scratch_bytes = std::max(P->gemm_scratch_bytes, GemmTf32x3ScratchBytes(g));
+        if (tc) P->gemm_scratch_bytes = std::max(P->gemm_scratch_bytes, GemmTcScratchBytes(g));
+        if (!tc) P->gemm_scratch_bytes = std::max(P->gemm_scratch_bytes, GemmSimtScratchBytes(g));
         g.scratch = nullptr;
         st.name = std::string(tc ? (dtype == RH_F32 ? "gemm_tc_3xtf32 " : "gemm_tc ") : "gemm_simt ") + id;
         st.alg_flops = 2.0 * g.m * g.n * g.k;
@@ -515,10 +515,13 @@ class Lowerer {
           a.c = P->Ptr(P->tensors[out_t], r);
           a.epi = Patch(P, g.epi, r);
           if (P->gemm_scratch_bytes) a.scratch = P->peer_base[r] + P->gemm_scratch_off;
-          if (tc) LaunchGemmTc(a, s);
-          else LaunchGemmSimt(a, s);
-          return tc && a.dtype == RH_F32 ? 3 : 1;  // 2 split kernels + the GEMM
+          if (!tc) return LaunchGemmSimt(a, s);  // (+ split-K reduce for small M)
+          LaunchGemmTc(a, s);
+          // 3xTF32: 2 split kernels + the GEMM; bf16 split-K: the GEMM + the reduce
+          return a.dtype == RH_F32 ? 3 : (GemmTcScratchBytes(a) > 0 ? 2 : 1);
         };
+        if (tc && dtype == RH_BF16 && GemmTcScratchBytes(g) > 0) st.launches = 2;
+        if (!tc && GemmSimtScratchBytes(g) > 0) st.launches = 2;
         if (tc && dtype == RH_F32) {
           st.launches = 3;
           st.alg_bytes += 3.0 * 4 * (g.m * g.k + g.k * g.n);  // split pass: read x, write hi + lo

@@ -22,22 +22,28 @@ __device__ __forceinline__ float Ld<__nv_bfloat16>(const __nv_bfloat16* p, int64
   return __bfloat162float(p[i]);
 }
 
+// Split-K (blockIdx.z = split): small-M GEMMs (the MLP configs' [64,1024] activations) have too
+// few 128x128 tiles to fill 148 SMs; each split writes its fp32 partial tile to `ws` and a reduce
+// kernel sums the splits in order, then rounds and applies the epilogue chain.
 template <typename T, bool TA, bool TB>
 __global__ void __launch_bounds__(256) GemmSimtKernel(T* __restrict__ C, const T* __restrict__ A,
                                                       const T* __restrict__ B, int64_t M,
-                                                      int64_t N, int64_t K, ChainArgs epi) {
+                                                      int64_t N, int64_t K, ChainArgs epi,
+                                                      int64_t kchunk, float* __restrict__ ws) {
   __shared__ __align__(16) float As[BK][BM];
   __shared__ __align__(16) float Bs[BK][BN];
   const int tid = threadIdx.x;
   const int tx = tid % 16, ty = tid / 16;
   const int64_t m0 = int64_t(blockIdx.y) * BM, n0 = int64_t(blockIdx.x) * BN;
+  const int64_t kbeg = int64_t(blockIdx.z) * kchunk;
+  const int64_t kend = min(K, kbeg + kchunk);
   float acc[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
 
-  for (int64_t k0 = 0; k0 < K; k0 += BK) {
+  for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
     // A tile -> As[k][m]
     if (!TA) {  // A [M,K]: 4 consecutive k per thread
       const int r = tid / 2, kc = (tid % 2) * 4;
@@ -45,7 +51,7 @@ __global__ void __launch_bounds__(256) GemmSimtKernel(T* __restrict__ C, const T
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int64_t gk = k0 + kc + j;
-        As[kc + j][r] = (gm < M && gk < K) ? Ld<T>(A, gm * K + gk) : 0.0f;
+        As[kc + j][r] = (gm < M && gk < kend) ? Ld<T>(A, gm * K + gk) : 0.0f;
       }
     } else {  // A stored [K,M]: 4 consecutive m per thread
       const int kr = tid / 32, mc = (tid % 32) * 4;
@@ -53,7 +59,7 @@ __global__ void __launch_bounds__(256) GemmSimtKernel(T* __restrict__ C, const T
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int64_t gm = m0 + mc + j;
-        As[kr][mc + j] = (gm < M && gk < K) ? Ld<T>(A, gk * M + gm) : 0.0f;
+        As[kr][mc + j] = (gm < M && gk < kend) ? Ld<T>(A, gk * M + gm) : 0.0f;
       }
     }
     if (!TB) {  // B [K,N]: 4 consecutive n per thread
@@ -62,7 +68,7 @@ __global__ void __launch_bounds__(256) GemmSimtKernel(T* __restrict__ C, const T
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int64_t gn = n0 + nc + j;
-        Bs[kr][nc + j] = (gn < N && gk < K) ? Ld<T>(B, gk * N + gn) : 0.0f;
+        Bs[kr][nc + j] = (gn < N && gk < kend) ? Ld<T>(B, gk * N + gn) : 0.0f;
       }
     } else {  // B stored [N,K]: 4 consecutive k per thread
       const int r = tid / 2, kc = (tid % 2) * 4;
@@ -70,7 +76,7 @@ __global__ void __launch_bounds__(256) GemmSimtKernel(T* __restrict__ C, const T
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int64_t gk = k0 + kc + j;
-        Bs[kc + j][r] = (gn < N && gk < K) ? Ld<T>(B, gn * K + gk) : 0.0f;
+        Bs[kc + j][r] = (gn < N && gk < kend) ? Ld<T>(B, gn * K + gk) : 0.0f;
       }
     }
     __syncthreads();
@@ -101,6 +107,10 @@ __global__ void __launch_bounds__(256) GemmSimtKernel(T* __restrict__ C, const T
       const int64_t gn = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
       if (gn >= N) continue;
       float v = acc[i][j];
+      if (ws) {  // split-K partial
+        ws[(int64_t(blockIdx.z) * M + gm) * N + gn] = v;
+        continue;
+      }
       if constexpr (sizeof(T) == 2) v = RoundBf16(v);
       v = ApplyChainFns<sizeof(T) == 2>(epi.fns, epi.n_fn, v);
       if constexpr (sizeof(T) == 2) {
@@ -113,29 +123,68 @@ __global__ void __launch_bounds__(256) GemmSimtKernel(T* __restrict__ C, const T
 }
 
 template <typename T>
-void Dispatch(const GemmArgs& g, cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>((g.n + BN - 1) / BN), static_cast<unsigned>((g.m + BM - 1) / BM));
+__global__ void __launch_bounds__(256) SplitReduceKernel(T* __restrict__ C, const float* __restrict__ ws,
+                                                         int64_t n, int splits, ChainArgs epi) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    float v = ws[i];
+    for (int z = 1; z < splits; ++z) v = __fadd_rn(v, ws[int64_t(z) * n + i]);
+    if constexpr (sizeof(T) == 2) v = RoundBf16(v);
+    v = ApplyChainFns<sizeof(T) == 2>(epi.fns, epi.n_fn, v);
+    if constexpr (sizeof(T) == 2) {
+      C[i] = __float2bfloat16_rn(v);
+    } else {
+      C[i] = v;
+    }
+  }
+}
+
+int SplitsFor(const GemmArgs& g) {
+  const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN);
+  if (tiles >= 148 || g.k < 128) return 1;
+  int64_t splits = (296 + tiles - 1) / tiles;
+  splits = std::min<int64_t>(splits, std::min<int64_t>(g.k / 64, 32));
+  return static_cast<int>(std::max<int64_t>(splits, 1));
+}
+
+template <typename T>
+int Dispatch(const GemmArgs& g, cudaStream_t s) {
+  const int splits = g.scratch ? SplitsFor(g) : 1;
+  const int64_t kchunk = ((g.k + splits - 1) / splits + BK - 1) / BK * BK;
+  const int z = static_cast<int>((g.k + kchunk - 1) / kchunk);
+  float* ws = z > 1 ? static_cast<float*>(g.scratch) : nullptr;
+  dim3 grid(static_cast<unsigned>((g.n + BN - 1) / BN), static_cast<unsigned>((g.m + BM - 1) / BM),
+            static_cast<unsigned>(z));
   T* c = static_cast<T*>(g.c);
   const T* a = static_cast<const T*>(g.a);
   const T* b = static_cast<const T*>(g.b);
-  if (!g.ta && !g.tb) GemmSimtKernel<T, false, false><<<grid, 256, 0, s>>>(c, a, b, g.m, g.n, g.k, g.epi);
-  else if (!g.ta && g.tb) GemmSimtKernel<T, false, true><<<grid, 256, 0, s>>>(c, a, b, g.m, g.n, g.k, g.epi);
-  else if (g.ta && !g.tb) GemmSimtKernel<T, true, false><<<grid, 256, 0, s>>>(c, a, b, g.m, g.n, g.k, g.epi);
-  else GemmSimtKernel<T, true, true><<<grid, 256, 0, s>>>(c, a, b, g.m, g.n, g.k, g.epi);
+  if (!g.ta && !g.tb) GemmSimtKernel<T, false, false><<<grid, 256, 0, s>>>(c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws);
+  else if (!g.ta && g.tb) GemmSimtKernel<T, false, true><<<grid, 256, 0, s>>>(c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws);
+  else if (g.ta && !g.tb) GemmSimtKernel<T, true, false><<<grid, 256, 0, s>>>(c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws);
+  else GemmSimtKernel<T, true, true><<<grid, 256, 0, s>>>(c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws);
+  if (!ws) return 1;
+  const int64_t n = g.m * g.n;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)));
+  SplitReduceKernel<T><<<blocks, 256, 0, s>>>(c, ws, n, z, g.epi);
+  return 2;
 }
 
 }  // namespace
 
-void LaunchGemmSimt(const GemmArgs& g, cudaStream_t s) {
-  if (g.m == 0 || g.n == 0) return;
+size_t GemmSimtScratchBytes(const GemmArgs& g) {
+  const int splits = SplitsFor(g);
+  return splits > 1 ? static_cast<size_t>(splits) * g.m * g.n * 4 : 0;
+}
+
+int LaunchGemmSimt(const GemmArgs& g, cudaStream_t s) {
+  if (g.m == 0 || g.n == 0) return 0;
   if (g.k == 0) {
     RH_CUDA(cudaMemsetAsync(g.c, 0, g.m * g.n * ElemBytes(g.dtype), s));
-    return;
+    return 1;
   }
   if (g.m / BM >= 65535) Fail("gemm: M too large for the SIMT grid");
-  if (g.dtype == RH_BF16) Dispatch<__nv_bfloat16>(g, s);
-  else Dispatch<float>(g, s);
+  const int launches = g.dtype == RH_BF16 ? Dispatch<__nv_bfloat16>(g, s) : Dispatch<float>(g, s);
   RH_CUDA(cudaGetLastError());
+  return launches;
 }
 
 }  // namespace rh

@@ -109,6 +109,26 @@ __device__ __forceinline__ void TmemLd32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Split-K finish: sum the fp32 partials in split order, round to bf16, apply the chain.
+__global__ void __launch_bounds__(256) SplitReduceBf16(__nv_bfloat16* __restrict__ C, const float4* __restrict__ ws,
+                                                       int64_t n4, int splits, ChainArgs epi) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
+    float4 v = ws[i];
+    for (int z = 1; z < splits; ++z) {
+      const float4 w = ws[int64_t(z) * n4 + i];
+      v.x = __fadd_rn(v.x, w.x);
+      v.y = __fadd_rn(v.y, w.y);
+      v.z = __fadd_rn(v.z, w.z);
+      v.w = __fadd_rn(v.w, w.w);
+    }
+    float f[4] = {v.x, v.y, v.z, v.w};
+    __nv_bfloat16 o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[e] = __float2bfloat16_rn(ApplyChainFns<true>(epi.fns, epi.n_fn, RoundBf16(f[e])));
+    reinterpret_cast<uint2*>(C)[i] = *reinterpret_cast<uint2*>(o);
+  }
+}
+
 template <int BN, bool kBKMajor>
 struct TcCfg {
   static constexpr int kABytes = BM * BK * 2;
@@ -127,7 +147,10 @@ struct TcCfg {
 template <int BN, bool kBKMajor>
 __global__ void __launch_bounds__(kThreads, 1)
     GemmTcKernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                 __nv_bfloat16* __restrict__ C, int M, int N, int K, ChainArgs epi) {
+                 __nv_bfloat16* __restrict__ C, int M, int N, int K, ChainArgs epi, int ksplit,
+                 float* __restrict__ ws) {
+  // Work unit = (m tile, n tile, k split).  ksplit > 1 (few tiles: the sharded GEMMs at N >= 4)
+  // writes fp32 partial tiles to ws[split][M][N]; SplitReduceBf16 finishes them.
   using Cfg = TcCfg<BN, kBKMajor>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -138,7 +161,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int num_m = M / BM, num_n = N / BN, tiles = num_m * num_n, kblocks = K / BK;
+  const int num_m = M / BM, num_n = N / BN, mn = num_m * num_n, tiles = mn * ksplit;
+  const int kblocks = K / BK / ksplit;  // per split
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
@@ -168,8 +192,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int m_blk = tile % num_m, n_blk = tile / num_m;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        const int t = tile % mn, ks = tile / mn;
+        const int m_blk = t % num_m, n_blk = t / num_m;
+        for (int kb = ks * kblocks; kb < (ks + 1) * kblocks; ++kb) {
           MbarWait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::kStage;
           uint8_t* sb = sa + Cfg::kABytes;
@@ -227,15 +252,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      const int m_blk = tile % num_m, n_blk = tile / num_m;
+      const int t = tile % mn, ks = tile / mn;
+      const int m_blk = t % num_m, n_blk = t / num_m;
       MbarWait(&tfull[acc], acc_phase);
       FenceAfter();
       const int row = m_blk * BM + ew * 32 + lane;
       __nv_bfloat16* crow = C + static_cast<int64_t>(row) * N + n_blk * BN;
+      float* wrow = ws ? ws + (static_cast<int64_t>(ks) * M + row) * N + n_blk * BN : nullptr;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
         TmemLd32(tmem + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
+        if (wrow) {  // split-K partial (fp32, unrounded)
+          float4* dst = reinterpret_cast<float4*>(wrow + c * 32);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                 __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+          continue;
+        }
         uint4 out[4];
         __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out);
 #pragma unroll
@@ -574,6 +609,27 @@ int NumSms() {
   return n;
 }
 
+int PickBN(const GemmArgs& g) {
+  if (g.dtype == RH_F32) return g.n % 128 == 0 ? 128 : 0;
+  if (g.n % 256 == 0 && (g.m / BM) * (g.n / 256) >= 120) return 256;
+  if (g.n % 128 == 0) return 128;
+  return 0;
+}
+
+// bf16 split-K factor: when the output tiles cannot fill the SMs (< 120 tiles), split K so that
+// work units reach ~2 waves while every split keeps >= 8 k-blocks (K >= 512).
+int KSplit(const GemmArgs& g, int bn) {
+  if (g.dtype != RH_BF16) return 1;
+  const int64_t tiles = (g.m / BM) * (g.n / bn), kb = g.k / BK;
+  if (tiles >= 120) return 1;
+  int best = 1;
+  for (int ks = 2; ks <= 8; ks *= 2) {
+    if (kb % ks || kb / ks < 8 || tiles * (ks / 2) > 148) break;
+    best = ks;
+  }
+  return best;
+}
+
 template <int BN, bool kBK>
 void Launch(const GemmArgs& g, cudaStream_t s) {
   using Cfg = TcCfg<BN, kBK>;
@@ -586,19 +642,21 @@ void Launch(const GemmArgs& g, cudaStream_t s) {
     attr[dev] = true;
   }
   const Maps& mp = GetMaps(g, BN);
-  const int tiles = static_cast<int>((g.m / BM) * (g.n / BN));
+  const int ks = g.scratch ? KSplit(g, BN) : 1;
+  const int tiles = static_cast<int>((g.m / BM) * (g.n / BN)) * ks;
   const int grid = std::min(tiles, NumSms());
+  float* ws = ks > 1 ? static_cast<float*>(g.scratch) : nullptr;
   GemmTcKernel<BN, kBK><<<grid, kThreads, Cfg::kSmem, s>>>(
       mp.a, mp.b, static_cast<__nv_bfloat16*>(g.c), static_cast<int>(g.m), static_cast<int>(g.n),
-      static_cast<int>(g.k), g.epi);
+      static_cast<int>(g.k), g.epi, ks, ws);
   RH_CUDA(cudaGetLastError());
-}
-
-int PickBN(const GemmArgs& g) {
-  if (g.dtype == RH_F32) return g.n % 128 == 0 ? 128 : 0;
-  if (g.n % 256 == 0 && (g.m / BM) * (g.n / 256) >= 96) return 256;
-  if (g.n % 128 == 0) return 128;
-  return 0;
+  if (ws) {
+    const int64_t n4 = g.m * g.n / 4;
+    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 148 * 8)));
+    SplitReduceBf16<<<blocks, 256, 0, s>>>(static_cast<__nv_bfloat16*>(g.c), reinterpret_cast<const float4*>(ws),
+                                           n4, ks, g.epi);
+    RH_CUDA(cudaGetLastError());
+  }
 }
 
 struct Maps4 {
@@ -665,6 +723,13 @@ void LaunchTf32x3(const GemmArgs& g, cudaStream_t s) {
 
 size_t GemmTf32x3ScratchBytes(const GemmArgs& g) {
   return static_cast<size_t>(2 * (g.m * g.k + g.k * g.n)) * 4;
+}
+
+size_t GemmTcScratchBytes(const GemmArgs& g) {
+  if (g.dtype == RH_F32) return GemmTf32x3ScratchBytes(g);
+  const int bn = PickBN(g);
+  const int ks = bn ? KSplit(g, bn) : 1;
+  return ks > 1 ? static_cast<size_t>(ks) * g.m * g.n * 4 : 0;
 }
 
 bool GemmTcSupported(const GemmArgs& g) {

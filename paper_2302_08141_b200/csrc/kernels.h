@@ -102,8 +102,12 @@ struct GemmArgs {
   void* scratch = nullptr;
 };
 size_t GemmTf32x3ScratchBytes(const GemmArgs& g);
-// CUDA-core kernel (any shape/layout); the test reference for the tensor-core path.
-void LaunchGemmSimt(const GemmArgs& g, cudaStream_t s);
+// Scratch the tensor-core path wants for this GEMM (3xTF32 splits, or bf16 split-K partials).
+size_t GemmTcScratchBytes(const GemmArgs& g);
+// CUDA-core kernel (any shape/layout); the test reference for the tensor-core path.  With
+// g.scratch (>= GemmSimtScratchBytes) small-M shapes run split-K.  Returns the launches issued.
+int LaunchGemmSimt(const GemmArgs& g, cudaStream_t s);
+size_t GemmSimtScratchBytes(const GemmArgs& g);
 // tcgen05 / TMEM / TMA kernel.  Returns false when the shape/layout is not supported by it.
 bool GemmTcSupported(const GemmArgs& g);
 void LaunchGemmTc(const GemmArgs& g, cudaStream_t s);
