@@ -609,13 +609,6 @@ int NumSms() {
   return n;
 }
 
-int PickBN(const GemmArgs& g) {
-  if (g.dtype == RH_F32) return g.n % 128 == 0 ? 128 : 0;
-  if (g.n % 256 == 0 && (g.m / BM) * (g.n / 256) >= 120) return 256;
-  if (g.n % 128 == 0) return 128;
-  return 0;
-}
-
 // bf16 split-K factor: when the output tiles cannot fill the SMs (< 120 tiles), split K so that
 // work units reach ~2 waves while every split keeps >= 8 k-blocks (K >= 512).
 int KSplit(const GemmArgs& g, int bn) {
@@ -628,6 +621,15 @@ int KSplit(const GemmArgs& g, int bn) {
     best = ks;
   }
   return best;
+}
+
+int PickBN(const GemmArgs& g) {
+  if (g.dtype == RH_F32) return g.n % 128 == 0 ? 128 : 0;
+  // BN = 256 halves the A-operand shared-memory traffic per flop (128 x 128 tiles are
+  // smem-bandwidth-bound at ~50% of peak); too few tiles are filled by split-K instead.
+  if (g.n % 256 == 0 && (g.m / BM) * (g.n / 256) * KSplit(g, 256) >= 96) return 256;
+  if (g.n % 128 == 0) return 128;
+  return 0;
 }
 
 template <int BN, bool kBK>
