@@ -124,10 +124,14 @@ int64_t RunOnce(rh_program* p, std::vector<cudaEvent_t>* prof) {
   rh_runtime* rt = p->mesh->rt;
   int64_t launches = 0;
   const bool multi_dev = rt->devs.size() > 1;
+  if (p->n_sync_slots) {  // new run epoch for the barriers fused into the pull kernels
+    rh::LaunchEpochTick(reinterpret_cast<uint32_t*>(p->base[0] + p->epoch_off), rt->streams[0]);
+    ++launches;
+  }
   for (size_t si = 0; si < p->steps.size(); ++si) {
     rh::Step& st = p->steps[si];
     if (prof) RH_CUDA(cudaEventRecordWithFlags((*prof)[si], rt->streams[0], cudaEventRecordExternal));
-    if (st.p2p) GroupSync(p, st.axis);
+    if (st.p2p && st.sync_slot < 0) GroupSync(p, st.axis);
     for (int li = 0; li < rt->n_local(); ++li) {
       if (multi_dev) RH_CUDA(cudaSetDevice(rt->device_of(li)));
       launches += st.run(li, rt->stream_of(li));
@@ -787,7 +791,9 @@ int rh_program_launch_count(const rh_program* p, int64_t* launches) {
     int64_t n = 0;
     for (const auto& s : p->steps) n += static_cast<int64_t>(s.launches) * p->mesh->rt->n_local();
     for (const auto& s : p->steps)
-      if (s.p2p && p->mesh->rt->dist && p->mesh->rt->world > 1) n += s.post_sync ? 2 : 1;  // barriers
+      if (s.p2p && p->mesh->rt->dist && p->mesh->rt->world > 1)
+        n += (s.sync_slot < 0 ? 1 : 0) + (s.post_sync ? 1 : 0);  // separate barrier kernels
+    if (p->n_sync_slots) n += 1;                                 // epoch tick
     *launches = n;
   });
 }

@@ -243,6 +243,10 @@ class Lowerer {
     }
     for (const auto& rq : p_->requests) p_->request_tensors.push_back(GetTensor(rq.first, rq.second, "request"));
     if (p_->gemm_scratch_bytes) p_->gemm_scratch_off = Alloc(p_->gemm_scratch_bytes);
+    if (p_->n_sync_slots) {
+      p_->sync_off = Alloc(static_cast<size_t>(p_->n_sync_slots) * rt_->world * 4);
+      p_->epoch_off = Alloc(4);
+    }
     p_->arena_bytes = arena_;
     // Barrier elision: tensors are written once per run (single-assignment arena), so a peer can
     // only overwrite what a transition reads in the NEXT run.  Every p2p transition but the
@@ -720,8 +724,12 @@ class Lowerer {
     const bool remote = from.kind != RH_REPLICATED && d > 1;
     const bool nccl = (P->flags & RH_FLAG_TRANSPORT_NCCL) && rt_->dist && remote;
     st.p2p = remote && !nccl;
+    // One process per GPU: the pre-transition group barrier rides inside the pull kernel
+    // (not for zero-fill targets, whose non-zero-coordinate ranks launch no kernel).
+    if (st.p2p && rt_->dist && rt_->world > 1 && to.kind != RH_PARTIAL) st.sync_slot = p_->n_sync_slots++;
     if (!nccl) {
-      st.run = [P, src, dst, axis, fv, tv, dtype](int li, cudaStream_t s) {
+      const int slot = st.sync_slot;
+      st.run = [P, src, dst, axis, fv, tv, dtype, slot](int li, cudaStream_t s) {
         const int g = P->mesh->rt->first_rank + li;
         const std::vector<int> members = P->mesh->Group(axis, g);
         const int coord = P->mesh->Coords(g)[axis];
@@ -733,6 +741,17 @@ class Lowerer {
         a.coord = coord;
         a.n_dst = P->tensors[dst].elems();
         a.dtype = dtype;
+        if (slot >= 0) {
+          const size_t row = P->sync_off + static_cast<size_t>(slot) * P->mesh->rt->world * 4;
+          a.sync.d = static_cast<int>(members.size());
+          a.sync.me = g;
+          for (size_t k = 0; k < members.size(); ++k) {
+            a.sync.members[k] = members[k];
+            a.sync.peer_slot[k] = reinterpret_cast<uint32_t*>(P->peer_base[members[k]] + row);
+          }
+          a.sync.my_slot = reinterpret_cast<uint32_t*>(P->peer_base[g] + row);
+          a.sync.epoch = reinterpret_cast<const uint32_t*>(P->peer_base[g] + P->epoch_off);
+        }
         return LaunchPull(a, s);
       };
     } else {

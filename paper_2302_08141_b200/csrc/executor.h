@@ -64,6 +64,7 @@ struct Step {
   bool p2p = false;          // transition reads peer buffers (needs pre/post group sync)
   bool post_sync = true;     // p2p only: false when a later p2p step on the same axis (same
                              // iteration) already orders the peers' next writes after our reads
+  int sync_slot = -1;        // dist p2p: flag row of the barrier fused into the pull kernel
   double alg_bytes = 0, alg_flops = 0, wire_bytes = 0;
   int launches = 0;          // per rank per run
   double ms = 0;             // from the last profile
@@ -96,6 +97,8 @@ struct rh_program {
   // memory
   size_t arena_bytes = 0;
   size_t flags_off = 0, counter_off = 0;
+  size_t sync_off = 0, epoch_off = 0;  // fused-barrier flag rows [slots][world] + run counter
+  int n_sync_slots = 0;
   std::vector<char*> base;       // per local rank
   std::vector<char*> peer_base;  // per global rank (dist: IPC-mapped; local: = base)
   bool ipc_opened = false;

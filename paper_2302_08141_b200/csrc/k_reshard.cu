@@ -62,7 +62,35 @@ struct PullDev {
   FastDiv dd;   // group size
   uint32_t coord;
   uint32_t n;   // destination units
+  PeerSync sync;
 };
+
+__device__ __forceinline__ void StRelaxedSys(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t LdRelaxedSys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Fused pre-transition barrier (see PeerSync): arrive (every CTA, idempotent), then wait.
+__device__ __forceinline__ void ArriveAndWait(const PeerSync& s) {
+  if (s.d == 0) return;
+  const int t = threadIdx.x;
+  if (t < s.d) {
+    const uint32_t e = *reinterpret_cast<const volatile uint32_t*>(s.epoch);
+    __threadfence_system();  // this rank's producer writes precede the signal
+    StRelaxedSys(s.peer_slot[t] + s.me, e);
+    const uint32_t* f = s.my_slot + s.members[t];
+    while (static_cast<int32_t>(LdRelaxedSys(f) - e) < 0) {
+    }
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+__global__ void EpochTickKernel(uint32_t* epoch) { *epoch += 1; }
 
 __device__ __forceinline__ uint32_t DstToGlobal(const PullDev& a, uint32_t i) {
   if (!a.to_shard) return i;
@@ -76,6 +104,7 @@ template <int VB, bool kFromShard>
 __global__ void __launch_bounds__(256) PullCopyKernel(PullDev a) {
   using V = typename VecT<VB>::T;
   constexpr int U = 4;
+  ArriveAndWait(a.sync);
   const uint32_t stride = gridDim.x * blockDim.x;
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   for (; i < a.n; i += U * stride) {
@@ -130,6 +159,7 @@ template <typename T, int VB>
 __global__ void __launch_bounds__(256) PullSumKernel(PullDev a, int d) {
   using V = typename VecT<VB>::T;
   constexpr int E = VB / sizeof(T);
+  ArriveAndWait(a.sync);
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
     const uint32_t f = DstToGlobal(a, i);
@@ -166,12 +196,14 @@ struct StagedDev {
   uint32_t L;       // elements per chunk
   uint32_t per;     // L / d
   uint32_t chunks;  // destination chunks
+  PeerSync sync;
 };
 
 template <typename T>
 __global__ void __launch_bounds__(256) PullStagedKernel(StagedDev a) {
   extern __shared__ __align__(16) unsigned char smem_stage[];
   T* tile = reinterpret_cast<T*>(smem_stage);
+  ArriveAndWait(a.sync);
   constexpr int E = 16 / sizeof(T);  // elements per 16-byte vector
   const uint32_t d = a.dd.d;
   const uint32_t Lr = a.qsf.d * d;
@@ -234,6 +266,7 @@ bool TryLaunchStaged(const PullArgs& a, cudaStream_t s) {
   sd.qsf = MakeFastDiv(static_cast<uint32_t>(qsf));
   sd.dd = MakeFastDiv(static_cast<uint32_t>(d));
   sd.coord = static_cast<uint32_t>(a.coord);
+  sd.sync = a.sync;
   sd.L = static_cast<uint32_t>(L);
   sd.per = static_cast<uint32_t>(L / d);
   sd.chunks = static_cast<uint32_t>(a.n_dst / L);
@@ -279,6 +312,7 @@ int LaunchPull(const PullArgs& a, cudaStream_t s) {
   const int eb = ElemBytes(a.dtype);
   if (a.n_dst == 0) return 0;
   if (a.to.kind == RH_PARTIAL && a.coord != 0) {  // zero-fill (sharding.cpp:132-135)
+    if (a.sync.d) Fail("internal: fused barrier on a zero-fill transition");
     RH_CUDA(cudaMemsetAsync(a.dst, 0, a.n_dst * eb, s));
     return 1;
   }
@@ -312,6 +346,7 @@ int LaunchPull(const PullArgs& a, cudaStream_t s) {
   const int d = a.to.kind == RH_SHARD ? a.to.d : a.from.d;
   dv.dd = MakeFastDiv(static_cast<uint32_t>(std::max(d, 1)));
   dv.coord = static_cast<uint32_t>(a.coord);
+  dv.sync = a.sync;
   switch (vb) {
     case 16: LaunchPullVB<16>(a, dv, s); break;
     case 8: LaunchPullVB<8>(a, dv, s); break;
@@ -425,6 +460,11 @@ void LaunchSynthetic(void* dst, const ComposedMap& m, int64_t n, uint64_t seed, 
 
 void LaunchBarrier(const BarrierArgs& b, cudaStream_t s) {
   BarrierKernel<<<1, 32, 0, s>>>(b);
+  RH_CUDA(cudaGetLastError());
+}
+
+void LaunchEpochTick(uint32_t* epoch, cudaStream_t s) {
+  EpochTickKernel<<<1, 1, 0, s>>>(epoch);
   RH_CUDA(cudaGetLastError());
 }
 

@@ -31,6 +31,20 @@ __host__ __device__ inline uint32_t Div(const FastDiv& f, uint32_t n) {
 // (layout `from`) directly — device-local, peer (NVLink P2P / CUDA IPC) or, for the NCCL
 // baseline, sub-buffers of a staging buffer.  Partial sources are summed in rank order
 // 0..d-1 in fp32 (bf16 rounded once), matching the oracle bit for bit.
+// Fused pre-transition group barrier (one process per GPU): every CTA of the pull kernel
+// first publishes this run's epoch into each member's flag slot for this transition (idempotent
+// 4-byte peer stores, so no CTA depends on another CTA of its own grid being resident), then
+// waits until every member's epoch has arrived in its own slot.  Replaces a separate barrier
+// kernel launch per transition.
+struct PeerSync {
+  uint32_t* peer_slot[kMaxGroup];  // member k's flag row for this transition (mapped): [world]
+  uint32_t* my_slot;               // this rank's flag row for this transition
+  const uint32_t* epoch;           // this rank's run counter (device)
+  int members[kMaxGroup];
+  int d;                           // 0: no fused barrier
+  int me;
+};
+
 struct PullArgs {
   void* dst;
   const void* src[kMaxGroup];
@@ -38,7 +52,10 @@ struct PullArgs {
   int coord;
   int64_t n_dst;  // destination elements
   int dtype;
+  PeerSync sync;  // sync.d == 0 unless fused
 };
+// Increments the device run counter (start of every run with fused barriers).
+void LaunchEpochTick(uint32_t* epoch, cudaStream_t s);
 // Returns the number of kernel launches (0 or 1).
 int LaunchPull(const PullArgs& a, cudaStream_t s);
 
