@@ -75,17 +75,26 @@ __device__ __forceinline__ uint32_t LdRelaxedSys(const uint32_t* p) {
 }
 
 // Fused pre-transition barrier (see PeerSync): arrive (every CTA, idempotent), then wait.
+__device__ __forceinline__ uint32_t LdAcquireSysU32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Block 0 publishes the arrival (it is dispatched first; every other CTA only polls its own,
+// local flag row, so no CTA waits on a CTA of its own grid that might not be resident).
 __device__ __forceinline__ void ArriveAndWait(const PeerSync& s) {
   if (s.d == 0) return;
   const int t = threadIdx.x;
   if (t < s.d) {
     const uint32_t e = *reinterpret_cast<const volatile uint32_t*>(s.epoch);
-    __threadfence_system();  // this rank's producer writes precede the signal
-    StRelaxedSys(s.peer_slot[t] + s.me, e);
-    const uint32_t* f = s.my_slot + s.members[t];
-    while (static_cast<int32_t>(LdRelaxedSys(f) - e) < 0) {
+    if (blockIdx.x == 0) {
+      __threadfence_system();  // this rank's producer writes precede the signal
+      StRelaxedSys(s.peer_slot[t] + s.me, e);
     }
-    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    const uint32_t* f = s.my_slot + s.members[t];
+    while (static_cast<int32_t>(LdAcquireSysU32(f) - e) < 0) {
+    }
   }
   __syncthreads();
 }
