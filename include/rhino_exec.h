@@ -110,6 +110,8 @@ typedef struct {
 #define RH_FLAG_NO_MATERIALIZE 0x8u     /* leave program outputs in their planned spec */
 #define RH_FLAG_SIMT_GEMM 0x10u         /* force the CUDA-core GEMM (test/reference kernel) */
 #define RH_FLAG_NO_GRAPH 0x20u          /* launch eagerly instead of replaying a CUDA graph */
+#define RH_FLAG_KEEP_ALL 0x40u          /* give every intermediate its own buffer (no arena reuse)
+                                           so rh_program_read_* can read any op after a run */
 
 typedef struct rh_runtime rh_runtime;
 typedef struct rh_mesh rh_mesh;
@@ -163,6 +165,10 @@ int rh_program_read_local(rh_program* prog, int op, int rank, void* dst, size_t 
  * from the local shards (every rank must be local). */
 int rh_program_read_full(rh_program* prog, int op, void* dst, size_t bytes);
 int rh_program_local_bytes(const rh_program* prog, int op, int rank, size_t* bytes);
+/* Device memory of the program per rank: the whole symmetric arena, and the part of it that is
+ * persistent (sources, outputs, peer-read transition sources, tables, scratch); the rest is the
+ * liveness-planned pool that intermediates share (none with RH_FLAG_KEEP_ALL). */
+int rh_program_memory(const rh_program* prog, size_t* arena_bytes, size_t* pool_bytes);
 /* Verification: the full value of the tensor `op` consumed at input `slot` (its producer in the
  * layout the op's strategy demanded, after resharding), assembled from every rank (all local). */
 int rh_program_read_input_full(rh_program* prog, int op, int slot, void* dst, size_t bytes);

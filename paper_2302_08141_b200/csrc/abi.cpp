@@ -712,6 +712,21 @@ int rh_program_step_host(rh_program* p, int n_in, const int* in_ops, const void*
   });
 }
 
+int rh_program_memory(const rh_program* p, size_t* arena_bytes, size_t* pool_bytes) {
+  return Guard([&] {
+    if (arena_bytes) *arena_bytes = p->arena_bytes;
+    if (pool_bytes) *pool_bytes = p->pool_bytes;
+  });
+}
+
+namespace {
+void RequireLive(const rh::Tensor& t) {
+  if (t.recycled)
+    Fail("intermediate buffer is reused by the arena planner after its last use; load the program "
+         "with RH_FLAG_KEEP_ALL to read intermediates");
+}
+}  // namespace
+
 int rh_program_local_bytes(const rh_program* p, int op, int rank, size_t* bytes) {
   return Guard([&] {
     (void)rank;
@@ -727,6 +742,7 @@ int rh_program_read_local(rh_program* p, int op, int rank, void* dst, size_t byt
     if (p->out_tensor[op] < 0) Fail("op was fused into its consumer's kernel (use RH_FLAG_NO_FUSION)");
     const rh::Tensor& t = p->tensors[p->out_tensor[op]];
     if (bytes != t.bytes) Fail("rh_program_read_local: size mismatch");
+    RequireLive(t);
     const int li = p->LocalIndex(rank);
     SyncAll(p->mesh->rt);
     DeviceGuard dg(p->mesh->rt->device_of(li));
@@ -751,6 +767,7 @@ int rh_program_read_full(rh_program* p, int op, void* dst, size_t bytes) {
       return;
     }
     if (p->out_tensor[op] < 0) Fail("op was fused into its consumer's kernel (use RH_FLAG_NO_FUSION)");
+    RequireLive(p->tensors[p->out_tensor[op]]);
     AssembleFull(p, p->tensors[p->out_tensor[op]], dst);
   });
 }
@@ -763,6 +780,7 @@ int rh_program_read_input_full(rh_program* p, int op, int slot, void* dst, size_
     SyncAll(p->mesh->rt);
     const rh::Tensor& t = p->tensors[p->in_tensor[op][slot]];
     if (bytes != static_cast<size_t>(Prod(t.gdims)) * rh::ElemBytes(t.dtype)) Fail("size mismatch");
+    RequireLive(t);
     AssembleFull(p, t, dst);
   });
 }

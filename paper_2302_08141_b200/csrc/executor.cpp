@@ -247,6 +247,7 @@ class Lowerer {
       p_->sync_off = Alloc(static_cast<size_t>(p_->n_sync_slots) * rt_->world * 4);
       p_->epoch_off = Alloc(4);
     }
+    PlanArena();
     p_->arena_bytes = arena_;
     // Barrier elision: tensors are written once per run (single-assignment arena), so a peer can
     // only overwrite what a transition reads in the NEXT run.  Every p2p transition but the
@@ -262,8 +263,112 @@ class Lowerer {
  private:
   size_t Alloc(size_t bytes) {
     const size_t off = arena_;
-    arena_ += (bytes + 255) / 256 * 256;
+    arena_ += Align(bytes);
     return off;
+  }
+  static size_t Align(size_t bytes) { return (bytes + 255) / 256 * 256; }
+
+  int Root(int t) const {
+    while (p_->tensors[t].alias >= 0) t = p_->tensors[t].alias;
+    return t;
+  }
+
+  // Arena planner: tensor storage is placed after lowering, from the schedule's liveness.
+  // Persistent (own storage for the program's lifetime): parameters and inputs, outputs and
+  // their materialized copies, request targets, and every tensor a transition reads from a
+  // PEER (a peer may still be reading it while this rank runs ahead; the transition barriers
+  // only order the next write of that same buffer).  Every other buffer lives from the step
+  // that writes it to the last step that reads it, and buffers with disjoint lifetimes share
+  // storage (best-fit over a coalescing free list).  The schedule is one stream per rank, so
+  // stream order is the only ordering reuse needs.  RH_FLAG_KEEP_ALL disables reuse.
+  void PlanArena() {
+    auto& T = p_->tensors;
+    const int nt = static_cast<int>(T.size());
+    const int ns = static_cast<int>(p_->steps.size());
+    std::vector<bool> persist(nt, (p_->flags & RH_FLAG_KEEP_ALL) != 0);
+    for (size_t i = 0; i < p_->ops.size(); ++i)
+      if ((p_->ops[i].kind == RH_OP_PARAMETER || p_->ops[i].kind == RH_OP_INPUT) && p_->out_tensor[i] >= 0)
+        persist[Root(p_->out_tensor[i])] = true;
+    for (int o : p_->outputs) {
+      if (p_->out_tensor[o] >= 0) persist[Root(p_->out_tensor[o])] = true;
+      if (p_->mat_tensor[o] >= 0) persist[Root(p_->mat_tensor[o])] = true;
+    }
+    for (int t : p_->request_tensors) persist[Root(t)] = true;
+    for (int t : remote_read_) persist[Root(t)] = true;
+    std::vector<int> def(nt, -1), last(nt, -1);
+    for (int s = 0; s < ns; ++s) {
+      for (int w : p_->steps[s].writes) {
+        const int r = Root(w);
+        if (def[r] < 0) def[r] = s;
+        last[r] = std::max(last[r], s);
+      }
+      for (int x : p_->steps[s].reads) {
+        const int r = Root(x);
+        if (def[r] < 0) persist[r] = true;  // read before any step writes it: host-written
+        last[r] = std::max(last[r], s);
+      }
+    }
+    std::vector<std::vector<int>> born(ns), dies(ns);
+    for (int t = 0; t < nt; ++t) {
+      if (!T[t].storage || T[t].alias >= 0) continue;
+      if (persist[t] || def[t] < 0) {
+        persist[t] = true;
+        T[t].offset = Alloc(T[t].bytes);
+        continue;
+      }
+      born[def[t]].push_back(t);
+      dies[last[t]].push_back(t);
+    }
+    const size_t base = arena_;
+    size_t top = 0;
+    std::map<size_t, size_t> free_blocks;  // offset -> size (coalesced)
+    for (int s = 0; s < ns; ++s) {
+      for (int t : born[s]) {  // outputs of step s never overlap its inputs (freed after)
+        const size_t need = Align(T[t].bytes);
+        auto best = free_blocks.end();
+        for (auto it = free_blocks.begin(); it != free_blocks.end(); ++it)
+          if (it->second >= need && (best == free_blocks.end() || it->second < best->second)) best = it;
+        if (best != free_blocks.end()) {
+          T[t].offset = base + best->first;
+          if (best->second > need) free_blocks[best->first + need] = best->second - need;
+          free_blocks.erase(best);
+        } else if (!free_blocks.empty() && std::prev(free_blocks.end())->first + std::prev(free_blocks.end())->second == top) {
+          auto tail = std::prev(free_blocks.end());  // grow the block at the top
+          T[t].offset = base + tail->first;
+          top = tail->first + need;
+          free_blocks.erase(tail);
+        } else {
+          T[t].offset = base + top;
+          top += need;
+        }
+        T[t].recycled = true;
+      }
+      for (int t : dies[s]) {
+        size_t off = T[t].offset - base, len = Align(T[t].bytes);
+        auto next = free_blocks.lower_bound(off);
+        if (next != free_blocks.end() && off + len == next->first) {
+          len += next->second;
+          next = free_blocks.erase(next);
+        }
+        if (next != free_blocks.begin()) {
+          auto prev = std::prev(next);
+          if (prev->first + prev->second == off) {
+            off = prev->first;
+            len += prev->second;
+            free_blocks.erase(prev);
+          }
+        }
+        free_blocks[off] = len;
+      }
+    }
+    arena_ = base + top;
+    p_->pool_bytes = top;
+    for (int t = 0; t < nt; ++t) {
+      if (T[t].alias < 0) continue;
+      const int r = Root(t);
+      T[t].offset = T[r].offset;
+      T[t].recycled = T[r].recycled;
+    }
   }
 
   Dims GDims(int i) const { return Dims(p_->ops[i].dims, p_->ops[i].dims + p_->ops[i].rank); }
@@ -276,7 +381,7 @@ class Lowerer {
     t.ldims = LocalDims(t.gdims, specs, mesh_, specs.size());
     t.dtype = p_->ops[op].dtype;
     t.bytes = static_cast<size_t>(t.elems()) * ElemBytes(t.dtype);
-    if (alloc) t.offset = Alloc(t.bytes);
+    t.storage = alloc;  // placed by PlanArena
     p_->tensors.push_back(t);
     const int idx = static_cast<int>(p_->tensors.size()) - 1;
     cache_[Key(op, specs)] = idx;
@@ -456,7 +561,7 @@ class Lowerer {
     // Reshape: pass-through layouts keep the local buffer byte-identical -> alias, no kernel.
     if (op.kind == RH_OP_RESHAPE) {
       int t = NewTensor(i, nat, /*alloc=*/false);
-      p_->tensors[t].offset = p_->tensors[in_t[0]].offset;
+      p_->tensors[t].alias = in_t[0];
       p_->out_tensor[i] = t;
       if (!direct) p_->out_tensor[i] = GetTensor(i, p_->out_specs[i], "pin");
       return;
@@ -645,6 +750,8 @@ class Lowerer {
         Fail(std::string("cannot execute op kind ") + KindName(op.kind));
     }
     (void)eb;
+    st.reads = in_t;
+    st.writes = {out_t};
     AddStep(std::move(st));
   }
 
@@ -802,6 +909,9 @@ class Lowerer {
         return 1 + LaunchPull(a, s);
       };
     }
+    if (remote) remote_read_.push_back(src);
+    st.reads = {src};
+    st.writes = {dst};
     AddStep(std::move(st));
     return dst;
   }
@@ -814,6 +924,7 @@ class Lowerer {
   std::vector<bool> absorbed_;
   std::vector<std::vector<int>> chain_;
   std::map<int, size_t> tanh_tables_;
+  std::vector<int> remote_read_;  // tensors read by peers (transition sources)
 };
 
 }  // namespace

@@ -49,6 +49,9 @@ struct Tensor {
   int dtype = RH_F32;
   size_t bytes = 0;   // local bytes per rank
   size_t offset = 0;  // arena offset (identical on every rank: the arena is symmetric)
+  int alias = -1;      // reshape pass-through: shares the storage of this tensor
+  bool storage = true; // owns arena storage (false: alias or bufferless chain member)
+  bool recycled = false;  // storage is reused by later tensors within a run (arena planner)
   int64_t elems() const {
     int64_t n = 1;
     for (auto x : ldims) n *= x;
@@ -68,6 +71,7 @@ struct Step {
   double alg_bytes = 0, alg_flops = 0, wire_bytes = 0;
   int launches = 0;          // per rank per run
   double ms = 0;             // from the last profile
+  std::vector<int> reads, writes;  // tensors (for the arena planner's liveness)
   // Enqueue this step for local rank `li` on stream `s`; returns the launches issued.
   std::function<int(int li, cudaStream_t s)> run;
 };
@@ -96,6 +100,7 @@ struct rh_program {
 
   // memory
   size_t arena_bytes = 0;
+  size_t pool_bytes = 0;  // liveness-planned part of the arena (recycled intermediates)
   size_t flags_off = 0, counter_off = 0;
   size_t sync_off = 0, epoch_off = 0;  // fused-barrier flag rows [slots][world] + run counter
   int n_sync_slots = 0;

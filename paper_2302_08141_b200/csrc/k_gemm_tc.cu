@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(256) SplitReduceBf16(__nv_bfloat16* __restrict
   }
 }
 
-template <int BN, bool kBKMajor>
+template <int BN, bool kBKMajor, bool kAKMajor>
 struct TcCfg {
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = BN * BK * 2;
@@ -138,20 +138,23 @@ struct TcCfg {
   static constexpr int kSmem = STAGES * kStage + 1024 /*barriers*/ + 1024 /*align*/;
   static constexpr uint32_t kIdesc = (1u << 4)                     // D = F32
                                      | (1u << 7) | (1u << 10)      // A, B = BF16
-                                     | (0u << 15)                  // A K-major
+                                     | ((kAKMajor ? 0u : 1u) << 15)  // A major
                                      | ((kBKMajor ? 0u : 1u) << 16)  // B major
                                      | (static_cast<uint32_t>(BN >> 3) << 17) |
                                      (static_cast<uint32_t>(BM >> 4) << 24);
 };
 
-template <int BN, bool kBKMajor>
+// A and B each either K-major ([M,K] / [N,K] row-major: one 128 x 64 box per stage) or MN-major
+// ([K,M] / [K,N]: 64-wide column chunks, the transpose_a / non-transposed-B layouts) — the MMA
+// reads both straight from the swizzled tiles, no transpose pass.
+template <int BN, bool kBKMajor, bool kAKMajor>
 __global__ void __launch_bounds__(kThreads, 1)
     GemmTcKernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                  __nv_bfloat16* __restrict__ C, int M, int N, int K, ChainArgs epi, int ksplit,
                  float* __restrict__ ws) {
   // Work unit = (m tile, n tile, k split).  ksplit > 1 (few tiles: the sharded GEMMs at N >= 4)
   // writes fp32 partial tiles to ws[split][M][N]; SplitReduceBf16 finishes them.
-  using Cfg = TcCfg<BN, kBKMajor>;
+  using Cfg = TcCfg<BN, kBKMajor, kAKMajor>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStage);
@@ -199,7 +202,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* sa = smem + stage * Cfg::kStage;
           uint8_t* sb = sa + Cfg::kABytes;
           MbarExpectTx(&full[stage], Cfg::kStage);
-          TmaLoad2D(sa, &tma_a, &full[stage], kb * BK, m_blk * BM);
+          if constexpr (kAKMajor) {
+            TmaLoad2D(sa, &tma_a, &full[stage], kb * BK, m_blk * BM);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              TmaLoad2D(sa + j * (64 * BK * 2), &tma_a, &full[stage], m_blk * BM + j * 64, kb * BK);
+          }
           if constexpr (kBKMajor) {
             TmaLoad2D(sb, &tma_b, &full[stage], kb * BK, n_blk * BN);
           } else {
@@ -229,7 +238,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sb = sa + Cfg::kABytes;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = DescSw128(sa + k * 32, 16, 1024);
+            const uint64_t ad = kAKMajor ? DescSw128(sa + k * 32, 16, 1024)
+                                         : DescSw128(sa + k * 16 * 128, 64 * BK * 2, 1024);
             const uint64_t bd = kBKMajor ? DescSw128(sb + k * 32, 16, 1024)
                                          : DescSw128(sb + k * 16 * 128, 64 * BK * 2, 1024);
             MmaF16(d_tmem, ad, bd, Cfg::kIdesc, (kb | k) != 0);
@@ -584,13 +594,17 @@ struct Maps {
 // Tensor maps depend only on (pointer, shape); arena pointers are static, so cache them.
 const Maps& GetMaps(const GemmArgs& g, int bn) {
   static std::mutex mu;
-  static std::map<std::tuple<const void*, const void*, int64_t, int64_t, int64_t, bool, int>, Maps> cache;
+  static std::map<std::tuple<const void*, const void*, int64_t, int64_t, int64_t, bool, bool, int>, Maps> cache;
   std::lock_guard<std::mutex> lk(mu);
-  auto key = std::make_tuple(g.a, g.b, g.m, g.n, g.k, g.tb, bn);
+  auto key = std::make_tuple(g.a, g.b, g.m, g.n, g.k, g.ta, g.tb, bn);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   Maps m;
-  m.a = MakeMap(g.a, g.k, g.m, g.k, BK, BM);
+  if (g.ta) {
+    m.a = MakeMap(g.a, g.m, g.k, g.m, 64, BK);  // A stored [K,M]: MN-major, 64-wide chunks
+  } else {
+    m.a = MakeMap(g.a, g.k, g.m, g.k, BK, BM);  // A stored [M,K]: K-major
+  }
   if (g.tb) {
     m.b = MakeMap(g.b, g.k, g.n, g.k, BK, bn);  // B stored [N,K]: K-major
   } else {
@@ -632,14 +646,14 @@ int PickBN(const GemmArgs& g) {
   return 0;
 }
 
-template <int BN, bool kBK>
+template <int BN, bool kBK, bool kAK>
 void Launch(const GemmArgs& g, cudaStream_t s) {
-  using Cfg = TcCfg<BN, kBK>;
+  using Cfg = TcCfg<BN, kBK, kAK>;
   int dev = 0;
   RH_CUDA(cudaGetDevice(&dev));
   static bool attr[64] = {};  // per device (local multi-GPU runtimes)
   if (dev < 64 && !attr[dev]) {
-    RH_CUDA(cudaFuncSetAttribute(GemmTcKernel<BN, kBK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RH_CUDA(cudaFuncSetAttribute(GemmTcKernel<BN, kBK, kAK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Cfg::kSmem));
     attr[dev] = true;
   }
@@ -648,7 +662,7 @@ void Launch(const GemmArgs& g, cudaStream_t s) {
   const int tiles = static_cast<int>((g.m / BM) * (g.n / BN)) * ks;
   const int grid = std::min(tiles, NumSms());
   float* ws = ks > 1 ? static_cast<float*>(g.scratch) : nullptr;
-  GemmTcKernel<BN, kBK><<<grid, kThreads, Cfg::kSmem, s>>>(
+  GemmTcKernel<BN, kBK, kAK><<<grid, kThreads, Cfg::kSmem, s>>>(
       mp.a, mp.b, static_cast<__nv_bfloat16*>(g.c), static_cast<int>(g.m), static_cast<int>(g.n),
       static_cast<int>(g.k), g.epi, ks, ws);
   RH_CUDA(cudaGetLastError());
@@ -684,8 +698,13 @@ void LaunchTf32x3(const GemmArgs& g, cudaStream_t s) {
   float* b_lo = b_hi + nb;
   const int threads = 256;
   auto blocks = [](int64_t n4) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 148 * 8))); };
-  SplitTf32Kernel<<<blocks(na / 4), threads, 0, s>>>(static_cast<const float4*>(g.a), reinterpret_cast<float4*>(a_hi),
-                                                     reinterpret_cast<float4*>(a_lo), na / 4);
+  if (!g.ta) {
+    SplitTf32Kernel<<<blocks(na / 4), threads, 0, s>>>(static_cast<const float4*>(g.a), reinterpret_cast<float4*>(a_hi),
+                                                       reinterpret_cast<float4*>(a_lo), na / 4);
+  } else {  // [K,M] -> hi/lo of [M,K]
+    SplitTransposeTf32Kernel<<<dim3(static_cast<unsigned>(g.m / 32), static_cast<unsigned>(g.k / 32)),
+                               dim3(32, 8), 0, s>>>(static_cast<const float*>(g.a), a_hi, a_lo, g.k, g.m);
+  }
   if (kBK) {
     SplitTf32Kernel<<<blocks(nb / 4), threads, 0, s>>>(static_cast<const float4*>(g.b),
                                                        reinterpret_cast<float4*>(b_hi),
@@ -735,7 +754,6 @@ size_t GemmTcScratchBytes(const GemmArgs& g) {
 }
 
 bool GemmTcSupported(const GemmArgs& g) {
-  if (g.ta) return false;
   if (g.dtype == RH_F32) {
     if (g.m % BM || g.n % 128 || g.k % BK32 || g.k == 0 || !g.scratch) return false;
   } else if (g.dtype == RH_BF16) {
@@ -758,12 +776,16 @@ void LaunchGemmTc(const GemmArgs& g, cudaStream_t s) {
     return;
   }
   const int bn = PickBN(g);
-  if (bn == 256) {
-    if (g.tb) Launch<256, true>(g, s);
-    else Launch<256, false>(g, s);
-  } else {
-    if (g.tb) Launch<128, true>(g, s);
-    else Launch<128, false>(g, s);
+  const int v = (bn == 256 ? 4 : 0) | (g.tb ? 2 : 0) | (g.ta ? 0 : 1);
+  switch (v) {
+    case 0: Launch<128, false, false>(g, s); break;
+    case 1: Launch<128, false, true>(g, s); break;
+    case 2: Launch<128, true, false>(g, s); break;
+    case 3: Launch<128, true, true>(g, s); break;
+    case 4: Launch<256, false, false>(g, s); break;
+    case 5: Launch<256, false, true>(g, s); break;
+    case 6: Launch<256, true, false>(g, s); break;
+    default: Launch<256, true, true>(g, s); break;
   }
 }
 

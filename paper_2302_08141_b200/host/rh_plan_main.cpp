@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <fstream>
 #include <iostream>
+#include <limits>
 #include <random>
 #include <sstream>
 #include <string>
@@ -84,6 +85,78 @@ rhino::LoweredProgram RandomChoice(const TensorProgram& g, const std::vector<int
   return rhino::StrategiesFromChoice(g, mesh, chosen, strat);
 }
 
+// Forward + backward programs: the reference search (cone tables + ILP) does not
+// scale to the backward graph (every backward op is multi-input; measured >17 GB and minutes on
+// a 298-op block), so the first `k_fwd` ops (the forward program) are planned by the UNCHANGED
+// planner, and every later op takes, in order, the candidate of the reference's own
+// generate_candidates that minimises the reference's objective terms (comp_flops/device_flops +
+// reshard_cost from its producers' chosen specs) — a greedy solver over the planner's candidates
+// and cost model.
+rhino::LoweredProgram PlanFwdGreedyBwd(const TensorProgram& g, int k_fwd, const ClusterConfig& cluster,
+                                       const PlanOptions& opts, json* extra) {
+  TensorProgram gf;
+  for (int i = 0; i < k_fwd; ++i) gf.Add(g.op(i));
+  gf.SetOutputs({g.op(k_fwd - 1).id});
+  gf.Validate();
+  ExecutionPlan pf = plan(gf, cluster, opts);
+  rhino::LoweredProgram lf = rhino::RecoverStrategies(gf, pf, opts);
+  const std::vector<int>& mesh = pf.mesh.dims;
+  std::vector<std::vector<AxisSpec>> chosen;
+  std::vector<int> chosen_d;
+  std::vector<std::vector<OpStrategy>> strat(mesh.size(), std::vector<OpStrategy>(g.size()));
+  for (size_t axis = 0; axis < mesh.size(); ++axis) {
+    const int d = mesh[axis];
+    std::vector<AxisSpec> specs(g.size(), AxisSpec::Replicated());
+    if (d < 2) {
+      for (int i = 0; i < g.size(); ++i) {
+        strat[axis][i].input_specs.assign(g.input_indices(i).size(), AxisSpec::Replicated());
+        strat[axis][i].output_spec = AxisSpec::Replicated();
+      }
+      chosen.push_back(specs);
+      chosen_d.push_back(d);
+      continue;
+    }
+    auto shapes = EffectiveShapes(g, chosen, chosen_d);
+    CandidateMap cand = generate_candidates(g, shapes, d, opts.flops_threshold, static_cast<int>(axis));
+    for (int i = 0; i < g.size(); ++i) {
+      if (i < k_fwd) {
+        strat[axis][i] = lf.strat[axis][i];
+        specs[i] = strat[axis][i].output_spec;
+        continue;
+      }
+      const auto& in_idx = g.input_indices(i);
+      double best_cost = std::numeric_limits<double>::infinity();
+      int best = -1;
+      for (size_t c = 0; c < cand[i].size(); ++c) {
+        bool valid = true;
+        double cost = cand[i][c].comp_flops / cluster.device_flops;
+        for (size_t slot = 0; slot < in_idx.size() && valid; ++slot) {
+          TensorShape s = g.op(in_idx[slot]).output_shape;
+          for (size_t a = 0; a < axis; ++a) s = LocalShape(s, strat[a][i].input_specs[slot], mesh[a]);
+          valid = SpecValidForShape(cand[i][c].input_specs[slot], s, d);
+          if (valid)
+            cost += reshard_cost(specs[in_idx[slot]], cand[i][c].input_specs[slot], shapes[in_idx[slot]],
+                                 pf.mesh, static_cast<int>(axis)).seconds;
+        }
+        if (valid && cost < best_cost) {
+          best_cost = cost;
+          best = static_cast<int>(c);
+        }
+      }
+      if (best < 0) throw std::runtime_error("no consistent candidate for op " + g.op(i).id);
+      strat[axis][i] = cand[i][best];
+      specs[i] = strat[axis][i].output_spec;
+    }
+    chosen.push_back(specs);
+    chosen_d.push_back(d);
+  }
+  (*extra)["forward_plan"] = {{"descriptor", pf.descriptor}, {"ops", k_fwd},
+                              {"recovery_matched", lf.recovery.empty() || lf.recovery[0].replay_matched}};
+  rhino::LoweredProgram lp = rhino::StrategiesFromChoice(g, mesh, chosen, strat);
+  lp.descriptor = pf.descriptor + "+greedy-bwd";
+  return lp;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -92,6 +165,8 @@ int main(int argc, char** argv) {
   bool equal_bw = false;
   long long random_seed = -1;
   double ilp_limit = 60.0;
+  int opt_level = 0;  // PlanOptions.opt_level: 0 auto (O3 below 5000 ops), 2 = O2, 3 = O3
+  int greedy_after = 0;  // > 0: plan the first N ops (forward) with the planner, rest greedy
   for (int i = 1; i < argc; ++i) {
     std::string a = argv[i];
     auto next = [&]() -> std::string {
@@ -106,6 +181,8 @@ int main(int argc, char** argv) {
     else if (a == "--gpus") gpus = std::stoi(next());
     else if (a == "--equal-bw") equal_bw = true;
     else if (a == "--ilp-time-limit") ilp_limit = std::stod(next());
+    else if (a == "--opt-level") opt_level = std::stoi(next());
+    else if (a == "--greedy-after") greedy_after = std::stoi(next());
     else if (a == "--random-choice") random_seed = std::stoll(next());
     else if (a == "--mesh") mesh_s = next();
     else if (a == "--dtype") dtype = next();
@@ -161,6 +238,18 @@ int main(int argc, char** argv) {
       PlanOptions opts;
       opts.pipeline_stages = -1;  // SPMD plans (pipeline execution is SURVEY §8f-1)
       opts.ilp_time_limit = ilp_limit;
+      opts.opt_level = opt_level;
+      if (greedy_after > 0) {
+        lp = PlanFwdGreedyBwd(g, greedy_after, cluster, opts, &extra);
+        extra["plan_seconds"] =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        json jj = json::parse(rhino::LoweredToJson(g, lp, name, dtype));
+        for (auto it = extra.begin(); it != extra.end(); ++it) jj[it.key()] = it.value();
+        std::ofstream(out_path) << jj.dump(1) << "\n";
+        std::cerr << "rh_plan: " << name << " fwd+greedy-bwd mesh=" << json(lp.mesh).dump()
+                  << " ops=" << g.size() << "\n";
+        return 0;
+      }
       ExecutionPlan p = plan(g, cluster, opts);
       auto t1 = std::chrono::steady_clock::now();
       lp = rhino::RecoverStrategies(g, p, opts);

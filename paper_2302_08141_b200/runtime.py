@@ -18,7 +18,7 @@ EXPORTS = [
     "rh_runtime_create_dist", "rh_runtime_world", "rh_runtime_destroy", "rh_mesh_create",
     "rh_mesh_destroy", "rh_program_load", "rh_program_destroy", "rh_program_init_synthetic",
     "rh_program_write_full", "rh_program_run", "rh_program_step_host", "rh_program_read_local",
-    "rh_program_read_full", "rh_program_read_input_full", "rh_program_local_bytes", "rh_program_num_steps",
+    "rh_program_read_full", "rh_program_read_input_full", "rh_program_local_bytes", "rh_program_memory", "rh_program_num_steps",
     "rh_program_step_info", "rh_program_profile", "rh_program_launch_count", "rh_reshard",
 ]
 
@@ -60,6 +60,7 @@ def lib():
     L.rh_program_read_full.argtypes = [vp, i, vp, sz]
     L.rh_program_read_input_full.argtypes = [vp, i, i, vp, sz]
     L.rh_program_local_bytes.argtypes = [vp, i, i, P(sz)]
+    L.rh_program_memory.argtypes = [vp, P(sz), P(sz)]
     L.rh_program_num_steps.argtypes = [vp, P(i)]
     L.rh_program_step_info.argtypes = [vp, i, P(RhStepInfo)]
     L.rh_program_profile.argtypes = [vp, i, P(ctypes.c_double)]
@@ -210,6 +211,12 @@ class Program:
                         "alg_bytes": s.alg_bytes, "alg_flops": s.alg_flops,
                         "wire_bytes": s.wire_bytes, "ms": s.ms})
         return out
+
+    def memory(self):
+        """(arena bytes, liveness-planned pool bytes) per rank."""
+        a, p = ctypes.c_size_t(), ctypes.c_size_t()
+        check(lib().rh_program_memory(self.h, ctypes.byref(a), ctypes.byref(p)))
+        return a.value, p.value
 
     def launch_count(self):
         n = ctypes.c_int64()

@@ -15,7 +15,7 @@ sys.path.insert(0, REPO)
 from oracle import pyoracle  # noqa: E402
 from paper_2302_08141_b200 import dist as D  # noqa: E402
 from paper_2302_08141_b200 import runtime as rx  # noqa: E402
-from paper_2302_08141_b200.abi import (RH_BF16, RH_FLAG_NO_FUSION, RH_FLAG_SIMT_GEMM,  # noqa: E402
+from paper_2302_08141_b200.abi import (RH_BF16, RH_FLAG_KEEP_ALL, RH_FLAG_NO_FUSION, RH_FLAG_SIMT_GEMM,  # noqa: E402
                                        RH_FLAG_TRANSPORT_NCCL)
 from paper_2302_08141_b200.program import LoweredProgram  # noqa: E402
 
@@ -34,7 +34,8 @@ def check(rt, name, flags, dtype=None):
     if dtype is not None:
         prog = prog.with_dtype(dtype)
     mesh = rx.Mesh(rt, prog.mesh)
-    gp = rx.Program(mesh, prog, flags)
+    # NO_FUSION runs read every op's local buffer afterwards: keep all intermediates
+    gp = rx.Program(mesh, prog, flags | (RH_FLAG_KEEP_ALL if flags & RH_FLAG_NO_FUSION else 0))
     res = {"name": name, "flags": flags, "ok": True, "err": 0.0}
     try:
         gp.init_synthetic(21)

@@ -1,6 +1,6 @@
 """K1: the tcgen05/TMEM/TMA GEMM (bf16 in, fp32 accumulate) and the CUDA-core GEMM against an
 fp64 reference on the same bf16 inputs, through the C-ABI (single-op programs), including the
-fused unary-chain epilogue and both B layouts (transpose_b)."""
+fused unary-chain epilogue and all four operand layouts (transpose_a x transpose_b)."""
 import numpy as np
 import pytest
 
@@ -10,13 +10,14 @@ from paper_2302_08141_b200.program import LoweredProgram
 pytestmark = pytest.mark.gpu
 
 
-def matmul_doc(m, k, n, tb=False, chain=(), dtype="bf16"):
+def matmul_doc(m, k, n, tb=False, chain=(), dtype="bf16", ta=False):
     R = ["replicated"]
     ops = [
-        {"id": "a", "kind": "input", "inputs": [], "shape": [m, k], "out_spec": R, "in_specs": [[]]},
+        {"id": "a", "kind": "input", "inputs": [], "shape": [k, m] if ta else [m, k], "out_spec": R,
+         "in_specs": [[]]},
         {"id": "b", "kind": "param", "inputs": [], "shape": [n, k] if tb else [k, n], "out_spec": R,
          "in_specs": [[]]},
-        {"id": "c", "kind": "matmul", "inputs": [0, 1], "shape": [m, n], "transpose_a": False,
+        {"id": "c", "kind": "matmul", "inputs": [0, 1], "shape": [m, n], "transpose_a": ta,
          "transpose_b": tb, "out_spec": R, "in_specs": [R * 2]},
     ]
     for i, fn in enumerate(chain):
@@ -53,20 +54,22 @@ def run(doc, flags=0):
 @pytest.mark.parametrize("m,k,n", [(128, 64, 128), (128, 128, 256), (256, 512, 384), (512, 1024, 1024),
                                    (2048, 4096, 4096), (2048, 16384, 512)])
 @pytest.mark.parametrize("tb", [False, True])
-def test_tc_gemm_vs_fp64(m, k, n, tb):
-    a, b, c, names = run(matmul_doc(m, k, n, tb))
+@pytest.mark.parametrize("ta", [False, True])
+def test_tc_gemm_vs_fp64(m, k, n, tb, ta):
+    a, b, c, names = run(matmul_doc(m, k, n, tb, ta=ta))
     assert any(s.startswith("gemm_tc") for s in names), names
     A, B = bf16_to_f64(a), bf16_to_f64(b)
-    ref = A @ (B.T if tb else B)
+    ref = (A.T if ta else A) @ (B.T if tb else B)
     got = bf16_to_f64(c)
     err = np.abs(got - ref).max() / np.abs(ref).max()
     assert err <= 1e-2, err  # bf16 output rounding (2^-9) + fp32 accumulation
 
 
 @pytest.mark.parametrize("tb", [False, True])
-def test_tc_matches_simt(tb):
-    _, _, c_tc, n1 = run(matmul_doc(256, 1024, 512, tb))
-    _, _, c_simt, n2 = run(matmul_doc(256, 1024, 512, tb), RH_FLAG_SIMT_GEMM)
+@pytest.mark.parametrize("ta", [False, True])
+def test_tc_matches_simt(tb, ta):
+    _, _, c_tc, n1 = run(matmul_doc(256, 1024, 512, tb, ta=ta))
+    _, _, c_simt, n2 = run(matmul_doc(256, 1024, 512, tb, ta=ta), RH_FLAG_SIMT_GEMM)
     assert any("gemm_tc" in s for s in n1) and any("gemm_simt" in s for s in n2)
     x, y = bf16_to_f64(c_tc), bf16_to_f64(c_simt)
     # same inputs, both fp32-accumulated (different orders), both rounded to bf16: the results
@@ -89,11 +92,13 @@ def test_tc_fused_epilogue_chain():
 @pytest.mark.parametrize("m,k,n", [(128, 32, 128), (256, 512, 384), (1024, 4096, 1024),
                                    (2048, 16384, 512)])
 @pytest.mark.parametrize("tb", [False, True])
-def test_tc_3xtf32_vs_fp64(m, k, n, tb):
+@pytest.mark.parametrize("ta", [False, True])
+def test_tc_3xtf32_vs_fp64(m, k, n, tb, ta):
     """fp32 programs: 3xTF32 on tcgen05 (kind::tf32), fp32-level accuracy (parity 1e-5)."""
-    a, b, c, names = run(matmul_doc(m, k, n, tb, dtype="f32"))
+    a, b, c, names = run(matmul_doc(m, k, n, tb, dtype="f32", ta=ta))
     assert any(s.startswith("gemm_tc_3xtf32") for s in names), names
-    ref = a.astype(np.float64) @ (b.astype(np.float64).T if tb else b.astype(np.float64))
+    A = a.astype(np.float64)
+    ref = (A.T if ta else A) @ (b.astype(np.float64).T if tb else b.astype(np.float64))
     err = np.abs(c - ref).max() / np.abs(ref).max()
     assert err <= 1e-5, err
 

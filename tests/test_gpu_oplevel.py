@@ -15,7 +15,7 @@ placement of every intermediate.
 import numpy as np
 import pytest
 
-from paper_2302_08141_b200.abi import OP_KINDS, RH_BF16, RH_F32, RH_FLAG_NO_FUSION
+from paper_2302_08141_b200.abi import OP_KINDS, RH_BF16, RH_F32, RH_FLAG_KEEP_ALL, RH_FLAG_NO_FUSION
 from paper_2302_08141_b200.program import LoweredProgram
 
 pytestmark = pytest.mark.gpu
@@ -45,14 +45,15 @@ def as_f64(a):
     return a.astype(np.float64)
 
 
-@pytest.mark.parametrize("name", ["c3_gpt_block_d1", "c3_gpt_block_d8", "c3_gpt_block_2x4"])
+@pytest.mark.parametrize("name", ["c3_gpt_block_d1", "c3_gpt_block_d8", "c3_gpt_block_2x4",
+                                  "c5_gpt_small_d2", "c5_gpt_small_d4"])
 @pytest.mark.parametrize("dtype", [RH_BF16, RH_F32])
 def test_gpt_block_op_level(oracle_lib, name, dtype):
     from paper_2302_08141_b200 import runtime as rx
     prog = LoweredProgram.load(name).with_dtype(dtype)
     rt = rx.Runtime(devices=[0] * prog.world)
     mesh = rx.Mesh(rt, prog.mesh)
-    gp = rx.Program(mesh, prog, RH_FLAG_NO_FUSION)
+    gp = rx.Program(mesh, prog, RH_FLAG_NO_FUSION | RH_FLAG_KEEP_ALL)
     try:
         gp.init_synthetic(17)
         gp.run(1)

@@ -13,7 +13,7 @@ import os
 import numpy as np
 import pytest
 
-from paper_2302_08141_b200.abi import (RH_BF16, RH_FLAG_NO_FUSION, RH_FLAG_SIMT_GEMM,
+from paper_2302_08141_b200.abi import (RH_BF16, RH_FLAG_KEEP_ALL, RH_FLAG_NO_FUSION, RH_FLAG_SIMT_GEMM,
                                        RH_FLAG_UNLABELED_IDENTITY)
 from paper_2302_08141_b200.program import PLANS_DIR, LoweredProgram
 
@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 
 TOL_F32, TOL_BF16 = 1e-5, 2e-2
 SMALL = sorted(os.path.basename(p)[:-5] for p in glob.glob(os.path.join(PLANS_DIR, "*.json"))
-               if not os.path.basename(p).startswith("c3_"))
+               if not os.path.basename(p).startswith(("c3_", "c5_big")))
 DATA_MOVEMENT_KINDS = {0, 1, 6, 7, 9, 10}  # param, input, reshape, transpose, broadcast, concat
 
 
@@ -76,7 +76,7 @@ def test_local_buffers(rx, oracle_lib, name):
     """Every op's per-rank local buffer vs the oracle's partitioned execution: bit-exact for
     data-movement ops (sources: synthetic init keyed by global index), tolerance otherwise."""
     prog = LoweredProgram.load(name)
-    rt, mesh, gp = load(rx, prog, RH_FLAG_NO_FUSION | RH_FLAG_SIMT_GEMM)
+    rt, mesh, gp = load(rx, prog, RH_FLAG_NO_FUSION | RH_FLAG_SIMT_GEMM | RH_FLAG_KEEP_ALL)
     try:
         gp.init_synthetic(5)
         gp.run(1)
@@ -100,8 +100,36 @@ def test_local_buffers(rx, oracle_lib, name):
         close(rt, mesh, gp)
 
 
+@pytest.mark.parametrize("name", ["c5_gpt_small_d2", "c3_gpt_block_d8"])
+def test_arena_reuse(rx, oracle_lib, name):
+    """The arena planner shares storage between intermediates with disjoint lifetimes: outputs
+    are unchanged (bit-exact vs KEEP_ALL), the arena shrinks, and reading a recycled
+    intermediate fails loudly instead of returning another tensor's bytes."""
+    prog = LoweredProgram.load(name).with_dtype(RH_BF16)
+    outs, mem = {}, {}
+    for flags in (0, RH_FLAG_KEEP_ALL):
+        rt, mesh, gp = load(rx, prog, flags)
+        try:
+            gp.init_synthetic(4)
+            gp.run(2)
+            outs[flags] = [gp.read_full(o) for o in prog.outputs]
+            mem[flags] = gp.memory()
+            if flags == 0:
+                inter = [op.index for op in prog.ops if op.kind not in (0, 1)
+                         and op.index not in prog.outputs]
+                with pytest.raises(rx.RhinoError, match="KEEP_ALL|fused"):
+                    for i in inter:
+                        gp.read_full(i)
+        finally:
+            close(rt, mesh, gp)
+    for a, b in zip(outs[0], outs[RH_FLAG_KEEP_ALL]):
+        np.testing.assert_array_equal(a, b)
+    assert mem[RH_FLAG_KEEP_ALL][1] == 0 and mem[0][1] > 0
+    assert mem[0][0] < mem[RH_FLAG_KEEP_ALL][0], mem
+
+
 @pytest.mark.parametrize("name", ["c1_mlp_d4", "c2_mlp_reshape_d8", "c2_mlp_pinned_d4",
-                                  "rand_gpt_like_2x2_s2", "moe_small_d2"])
+                                  "rand_gpt_like_2x2_s2", "moe_small_d2", "c5_gpt_small_d4"])
 def test_bf16_programs(rx, oracle_lib, name):
     prog = LoweredProgram.load(name).with_dtype(RH_BF16)
     rt, mesh, gp = load(rx, prog)
