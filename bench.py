@@ -31,6 +31,11 @@ NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
 WORKLOADS = {
     "gpt_block": dict(plan="c3_gpt_block_d{n}", name="gpt_block_h4096_s2048", dtype="bf16",
                       metric="partitioned-program tokens/s (GPT block, hidden 4096, seq 2048)"),
+    # C5: 24-layer GPT forward + backward (tests/golden/make_fwd_bwd.py); the CPU sample is one
+    # layer of the same shapes (the full 24-layer step is minutes of CPU), scaled by 1/24
+    "gpt24_train": dict(plan="c5_big_gpt24_d{n}", name="gpt24_fwd_bwd_h2048_t2048", dtype="bf16",
+                        metric="partitioned-program tokens/s (24-layer GPT fwd+bwd, hidden 2048, 2048 tokens)",
+                        cpu_plan="c5_big_gpt1_d1", cpu_scale=24),
     "mlp": dict(plan="c1_mlp_d{n}", name="mlp2_b64_h1024", dtype="f32",
                 metric="partitioned-program tokens/s (2-layer MLP, batch 64, hidden 1024)"),
     "mlp_strided": dict(plan="c2_mlp_reshape_d{n}", name="mlp_reshape_strided_b64_h1024", dtype="f32",
@@ -153,6 +158,8 @@ def run_reference(args):
         return
     wl = WORKLOADS[args.workload]
     name = plan_name(args.workload, 1) if args.workload != "mlp_strided" else plan_name(args.workload, 2)
+    name = wl.get("cpu_plan", name)
+    scale = wl.get("cpu_scale", 1)
     prog = LoweredProgram.load(name).with_dtype(RH_BF16 if args.dtype == "bf16" else RH_F32)
     cores = os.cpu_count() or 1
     tok = tokens_of(prog)
@@ -161,7 +168,7 @@ def run_reference(args):
     for _ in range(w):
         cpu_baseline(prog, cores)
     ts = [cpu_baseline(prog, cores) for _ in range(k)]
-    sec = sum(ts) / len(ts)
+    sec = sum(ts) / len(ts) * scale
     value = tok / sec
     line = {
         "impl": "reference", "metric": wl["metric"], "value": value, "unit": "tokens/s",
@@ -171,7 +178,8 @@ def run_reference(args):
         "config": {"workload": wl["name"], "mesh": [1], "global_batch": tok, "seq_len": tok},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
                          "sample": f"{k} full unpartitioned step(s) of {name} ({len(prog.ops)} ops) "
-                                   f"on {cores} threads (oracle/ref_cpu_exec)"},
+                                   f"on {cores} threads (oracle/ref_cpu_exec)"
+                                   + (f", time x{scale} (one of {scale} identical layers)" if scale > 1 else "")},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -223,31 +231,49 @@ def main():
         D.barrier()
         torch.cuda.synchronize()
         with Clocks(local) as clk:
-            ms_dev = gp.profile(args.steps)  # one CUDA graph of K runs, events around every step
+            ms_dev = gp.run(args.steps)  # K graph replays, CUDA events on the rank's stream
         D.barrier()
         ms_step = D.max_over_ranks(ms_dev)
+        # per-step breakdown from a separate profiled pass (an event node around every step,
+        # which inflates programs of thousands of steps: used for shares only, never the value)
+        ms_prof = gp.profile(min(args.steps, 3))
+        D.barrier()
         steps = gp.steps()
         launches = gp.launch_count() * args.steps
 
-        # End to end through the public API with host buffers: H2D of x, one run, D2H of the output.
-        x = prog.op_index("x")
+        # End to end through the public API with host buffers: H2D of every program input (x, and
+        # dy for fwd+bwd programs), one run, D2H of the first output.
+        xs = [op.index for op in prog.ops if op.kind == 1]
         out = prog.outputs[0]
-        xin = torch.empty(prog.full_bytes(x), dtype=torch.uint8).pin_memory()
-        xf = np.random.default_rng(0).uniform(-1, 1, math.prod(prog.ops[x].shape)).astype(np.float32)
-        if dtype == RH_BF16:
-            xin.numpy().view(np.uint16)[:] = (xf.view(np.uint32) >> 16).astype(np.uint16)
-        else:
-            xin.numpy().view(np.float32)[:] = xf
+        hin = []
+        for j, x in enumerate(xs):
+            xin = torch.empty(prog.full_bytes(x), dtype=torch.uint8).pin_memory()
+            xf = np.random.default_rng(j).uniform(-1, 1, math.prod(prog.ops[x].shape)).astype(np.float32)
+            if dtype == RH_BF16:
+                xin.numpy().view(np.uint16)[:] = (xf.view(np.uint32) >> 16).astype(np.uint16)
+            else:
+                xin.numpy().view(np.float32)[:] = xf
+            hin.append(xin)
         yout = torch.empty(prog.full_bytes(out), dtype=torch.uint8).pin_memory()
-        gp.step_host([x], [xin.data_ptr()], [yout.data_ptr()])
+        ptrs = [h.data_ptr() for h in hin]
+        gp.step_host(xs, ptrs, [yout.data_ptr()])
         D.barrier()
-        e2e = [gp.step_host([x], [xin.data_ptr()], [yout.data_ptr()]) for _ in range(args.steps)]
+        e2e = [gp.step_host(xs, ptrs, [yout.data_ptr()]) for _ in range(args.steps)]
         e2e_ms = D.max_over_ranks(sum(e2e) / len(e2e))
 
-        # Roofline of the dominant kernel (largest share of the step).
+        # Roofline of the dominant kernel (the kernel class with the largest share of the step:
+        # achieved = algorithmic flops or bytes summed over its launches / their summed time).
         pk = peaks()
         kern = [s for s in steps if s["kind"] == 0]
-        dom = max(kern, key=lambda s: s["ms"])
+        classes = {}
+        for s in kern:
+            c = classes.setdefault(s["name"].split(" ")[0], {"ms": 0.0, "alg_flops": 0.0, "alg_bytes": 0.0, "n": 0})
+            c["ms"] += s["ms"]
+            c["alg_flops"] += s["alg_flops"]
+            c["alg_bytes"] += s["alg_bytes"]
+            c["n"] += 1
+        cname, c = max(classes.items(), key=lambda kv: kv[1]["ms"])
+        dom = dict(c, name=cname)
         gemm_ms = sum(s["ms"] for s in kern if "gemm" in s["name"])
         if "gemm_tc" in dom["name"]:
             achieved = dom["alg_flops"] / (dom["ms"] * 1e-3) / 1e12
@@ -257,12 +283,12 @@ def main():
                     "frac": achieved / peak, "traffic": None, "kernel": dom["name"],
                     "peak_note": ("3xTF32 effective fp32 = sustained bf16 / 2 (tf32 rate) / 3 (products)"
                                   if f32 else "sustained bf16") + f" of MEASURED_PEAKS.json ({pk['source']})",
-                    "share_of_step": dom["ms"] / ms_dev}
+                    "launches": dom["n"], "share_of_step": dom["ms"] / ms_prof}
         else:
             achieved = dom["alg_bytes"] / (dom["ms"] * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                     "frac": achieved / pk["hbm_gbs"], "traffic": None, "kernel": dom["name"],
-                    "share_of_step": dom["ms"] / ms_dev}
+                    "launches": dom["n"], "share_of_step": dom["ms"] / ms_prof}
         tr_path = os.path.join(REPO, "profiles", "ncu_traffic.json")
         if os.path.exists(tr_path):
             with open(tr_path) as f:
@@ -282,11 +308,15 @@ def main():
         cpu = None
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1
-            sec = cpu_baseline(prog, cores)
+            scale = wl.get("cpu_scale", 1)
+            cprog = LoweredProgram.load(wl["cpu_plan"]).with_dtype(dtype) if "cpu_plan" in wl else prog
+            sec = cpu_baseline(cprog, cores) * scale
             cpu = {"value": tok / sec, "unit": "tokens/s", "cores": cores, "kind": "port",
-                   "sample": f"1 full unpartitioned step ({tok} tokens) of the same program, "
-                             f"oracle/ref_cpu_exec, {cores} threads"}
-        h2d = prog.full_bytes(x) * world
+                   "sample": f"1 full unpartitioned step ({tok} tokens) of "
+                             + (f"{wl['cpu_plan']} (1 of {scale} identical layers, time x{scale})"
+                                if scale > 1 else "the same program")
+                             + f", oracle/ref_cpu_exec, {cores} threads"}
+        h2d = sum(prog.full_bytes(x) for x in xs) * world
         d2h = prog.full_bytes(out) * world
         gp.close()
         mesh.close()
@@ -313,6 +343,9 @@ def main():
             "reshard": reshard,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
+            "kernel_classes": {k: {"ms": round(v["ms"], 4), "launches": v["n"]} for k, v in
+                               sorted(classes.items(), key=lambda kv: -kv[1]["ms"])[:8]},
+            "profiled_ms_per_step": ms_prof,
             "top_steps": sorted(({"name": s["name"], "ms": round(s["ms"], 4)} for s in steps),
                                 key=lambda s: -s["ms"])[:8],
         }

@@ -212,6 +212,14 @@ ncclDataType_t NcclType(int dtype) { return dtype == RH_BF16 ? ncclBfloat16 : nc
       ::rh::Fail(std::string("NCCL: ") + ncclGetErrorString(r_) + " (" #x ")", RH_ERR_NCCL); \
   } while (0)
 
+struct EwPlan {
+  std::vector<int> members;                   // chain ops in order (members[0] = head)
+  std::vector<std::vector<int>> src;          // per member, per operand: -1 acc, kEwSrcKeep,
+                                              // kEwSrcAcc (second use of acc), k = inputs[k]
+  std::vector<std::pair<int, Specs>> inputs;  // external operands (producer, demanded specs)
+  std::vector<bool> keep_after, stored;
+};
+
 class Lowerer {
  public:
   explicit Lowerer(rh_program* p) : p_(p), mesh_(p->mesh->dims), rt_(p->mesh->rt) {}
@@ -233,6 +241,10 @@ class Lowerer {
         continue;
       }
       if (absorbed_[i]) continue;  // computed by its chain head's kernel
+      if (!ew_of_.empty() && ew_of_[i] >= 0) {  // elementwise chain: one kernel at its tail
+        if (ew_[ew_of_[i]].members.back() == i) EmitEwChain(ew_[ew_of_[i]]);
+        continue;
+      }
       EmitOp(i);
     }
     if (!(p_->flags & RH_FLAG_NO_MATERIALIZE)) {
@@ -457,9 +469,7 @@ class Lowerer {
     };
     for (int h : p_->order) {
       const rh_op& op = p_->ops[h];
-      const bool head_kind = IsElementwiseUnary(h) || op.kind == RH_OP_MATMUL ||
-                             op.kind == RH_OP_ADD || op.kind == RH_OP_MUL;
-      if (!head_kind || absorbed_[h]) continue;
+      if (op.kind != RH_OP_MATMUL || absorbed_[h]) continue;  // elementwise heads: PlanEwChains
       int cur = h;
       while (true) {
         if (uses[cur] != 1 || is_out[cur]) break;
@@ -487,6 +497,158 @@ class Lowerer {
         for (int v : chain_[h]) absorbed_[v] = false;
         chain_[h].clear();
       }
+    }
+    PlanEwChains(is_out, natural_ok, no_partial);
+  }
+
+  bool IsEw(int i) const {
+    const int k = p_->ops[i].kind;
+    return IsElementwiseUnary(i) || k == RH_OP_ADD || k == RH_OP_MUL;
+  }
+
+  // Elementwise chains (kernels.h EwArgs).  Greedy over the schedule order: a chain starts at an
+  // elementwise op and follows the accumulator to the EARLIEST elementwise consumer whose edge
+  // needs no resharding; the consumer's other operand is an external input, the kept register
+  // (an earlier chain value) or the accumulator itself.  Chain values with consumers outside the
+  // chain are stored.  The kernel runs at the tail's position, so a chain may only grow while
+  // every outside consumer of its values comes after the new tail (which also guarantees that
+  // no external input depends on a chain value).  A chain that is a plain single-use unary run
+  // behind one op is handed to the classic head + chain kernels (chain_).
+  template <typename NatOk, typename NoPartial>
+  void PlanEwChains(const std::vector<bool>& is_out, NatOk natural_ok, NoPartial no_partial) {
+    const int n = static_cast<int>(p_->ops.size());
+    std::vector<std::vector<int>> cons(n);
+    for (int i = 0; i < n; ++i)
+      for (int s : p_->inputs[i])
+        if (cons[s].empty() || cons[s].back() != i) cons[s].push_back(i);
+    std::vector<int> pos(n, 0);
+    for (size_t k = 0; k < p_->order.size(); ++k) pos[p_->order[k]] = static_cast<int>(k);
+    ew_of_.assign(n, -1);
+    const bool bf16_prog = !p_->ops.empty() && p_->ops[0].dtype == RH_BF16;
+    (void)bf16_prog;
+    for (int h : p_->order) {
+      if (!IsEw(h) || absorbed_[h] || ew_of_[h] >= 0 || !natural_ok(h)) continue;
+      EwPlan c;
+      c.members = {h};
+      auto add_input = [&](int prod, const Specs& sp) {
+        for (size_t k = 0; k < c.inputs.size(); ++k)
+          if (c.inputs[k].first == prod && SpecsEq(c.inputs[k].second, sp)) return static_cast<int>(k);
+        c.inputs.emplace_back(prod, sp);
+        return static_cast<int>(c.inputs.size()) - 1;
+      };
+      {
+        std::vector<int> src;
+        for (size_t sl = 0; sl < p_->inputs[h].size(); ++sl) src.push_back(add_input(p_->inputs[h][sl], p_->in_specs[h][sl]));
+        if (src.size() == 2 && src[1] == src[0]) src[1] = kEwSrcAcc;
+        c.src.push_back(src);
+      }
+      c.keep_after.push_back(false);
+      int cur = h, kept = -1, last_keep_use = -1;
+      auto member_index = [&](int op) {
+        for (size_t j = 0; j < c.members.size(); ++j)
+          if (c.members[j] == op) return static_cast<int>(j);
+        return -1;
+      };
+      while (static_cast<int>(c.members.size()) < kMaxChain) {
+        if (!no_partial(p_->out_specs[cur])) break;
+        // successor: the earliest qualifying elementwise consumer of the accumulator
+        int v = -1;
+        for (int cand : cons[cur]) {
+          if (!IsEw(cand) || absorbed_[cand] || ew_of_[cand] >= 0 || member_index(cand) >= 0) continue;
+          if (p_->ops[cand].dtype != p_->ops[h].dtype || GDims(cand) != GDims(cur) || !natural_ok(cand)) continue;
+          bool edge_ok = false;
+          for (size_t sl = 0; sl < p_->inputs[cand].size(); ++sl)
+            if (p_->inputs[cand][sl] == cur && SpecsEq(p_->in_specs[cand][sl], p_->out_specs[cur])) edge_ok = true;
+          if (!edge_ok) continue;
+          if (v < 0 || pos[cand] < pos[v]) v = cand;
+        }
+        if (v < 0) break;
+        // operands of v
+        EwPlan t = c;
+        int t_kept = kept, t_last = last_keep_use;
+        const int vi = static_cast<int>(t.members.size());
+        std::vector<int> src;
+        bool acc_used = false, ok = true;
+        for (size_t sl = 0; sl < p_->inputs[v].size() && ok; ++sl) {
+          const int pr = p_->inputs[v][sl];
+          const int j = member_index(pr);
+          if (pr == cur && SpecsEq(p_->in_specs[v][sl], p_->out_specs[cur])) {
+            src.push_back(acc_used ? kEwSrcAcc : -1);
+            acc_used = true;
+          } else if (j >= 0) {
+            if (!SpecsEq(p_->in_specs[v][sl], p_->out_specs[pr])) { ok = false; break; }
+            if (t_kept != j) {
+              if (t_last > j) { ok = false; break; }
+              t.keep_after[j] = true;
+              t_kept = j;
+            }
+            t_last = vi;
+            src.push_back(kEwSrcKeep);
+          } else {
+            EwPlan* tp = &t;
+            int k = -1;
+            for (size_t q = 0; q < tp->inputs.size(); ++q)
+              if (tp->inputs[q].first == pr && SpecsEq(tp->inputs[q].second, p_->in_specs[v][sl])) k = static_cast<int>(q);
+            if (k < 0) {
+              tp->inputs.emplace_back(pr, p_->in_specs[v][sl]);
+              k = static_cast<int>(tp->inputs.size()) - 1;
+            }
+            src.push_back(k);
+          }
+        }
+        if (!ok || !acc_used || static_cast<int>(t.inputs.size()) > kMaxEwIn) break;
+        // the accumulator operand goes first (ops are commutative; bf16/fp32 results identical)
+        if (src.size() == 2 && src[0] != -1) std::swap(src[0], src[1]);
+        t.members.push_back(v);
+        t.src.push_back(src);
+        t.keep_after.push_back(false);
+        // schedule check + output / code budget
+        std::vector<bool> in_chain(n, false);
+        for (int m : t.members) in_chain[m] = true;
+        int stores = 0, code = 1;
+        bool order_ok = true;
+        for (size_t j = 0; j < t.members.size(); ++j) {
+          const int m = t.members[j];
+          bool outside = is_out[m] || j + 1 == t.members.size();
+          for (int cns : cons[m])
+            if (!in_chain[cns]) {
+              outside = true;
+              if (pos[cns] < pos[v]) order_ok = false;
+            }
+          stores += outside;
+          code += 2 + (outside ? 1 : 0) + (t.keep_after[j] ? 1 : 0);
+        }
+        if (!order_ok || stores > kMaxEwOut || code > kMaxEwCode) break;
+        c = std::move(t);
+        kept = t_kept;
+        last_keep_use = t_last;
+        cur = v;
+      }
+      if (c.members.size() < 2) continue;
+      // stored values
+      std::vector<bool> in_chain(n, false);
+      for (int m : c.members) in_chain[m] = true;
+      c.stored.assign(c.members.size(), false);
+      for (size_t j = 0; j < c.members.size(); ++j) {
+        const int m = c.members[j];
+        bool st = is_out[m] || j + 1 == c.members.size();
+        for (int cns : cons[m]) st = st || !in_chain[cns];
+        c.stored[j] = st;
+      }
+      // classic form: one op then single-use unary ops, only the tail stored
+      bool classic = true;
+      for (size_t j = 1; j < c.members.size(); ++j)
+        classic = classic && IsElementwiseUnary(c.members[j]) && !c.stored[j - 1] && !c.keep_after[j - 1];
+      if (classic) {
+        for (size_t j = 1; j < c.members.size(); ++j) {
+          chain_[h].push_back(c.members[j]);
+          absorbed_[c.members[j]] = true;
+        }
+        continue;
+      }
+      const int id = static_cast<int>(ew_.size());
+      for (int m : c.members) ew_of_[m] = id;
+      ew_.push_back(std::move(c));
     }
   }
   static constexpr size_t kMaxGemmEpilogue = 2;
@@ -576,6 +738,129 @@ class Lowerer {
       p_->out_tensor[i] = out_t;
       p_->out_tensor[i] = GetTensor(i, p_->out_specs[i], "pin");
     }
+  }
+
+  void EmitEwChain(const EwPlan& c) {
+    rh_program* P = p_;
+    const int h = c.members.front();
+    const int dtype = P->ops[h].dtype;
+    const bool bf16 = dtype == RH_BF16;
+    std::vector<int> in_t;
+    for (const auto& in : c.inputs) in_t.push_back(GetTensor(in.first, in.second, "edge"));
+    // tensors of the stored values
+    std::vector<int> out_t;
+    std::vector<int> out_slot(c.members.size(), -1);
+    for (size_t j = 0; j < c.members.size(); ++j) {
+      if (!c.stored[j]) continue;
+      const int m = c.members[j];
+      const int t = NewTensor(m, p_->out_specs[m]);
+      p_->out_tensor[m] = t;
+      out_slot[j] = static_cast<int>(out_t.size());
+      out_t.push_back(t);
+    }
+    for (int m : c.members) {
+      std::vector<int> ins;
+      for (size_t sl = 0; sl < p_->inputs[m].size(); ++sl) {
+        auto it = cache_.find(Key(p_->inputs[m][sl], p_->in_specs[m][sl]));
+        ins.push_back(it != cache_.end() ? it->second : -1);
+      }
+      p_->in_tensor[m] = ins;
+    }
+    // tanh runs (bf16): maximal runs of tanh members whose intermediate values are neither
+    // stored nor kept become one T^k lookup; at most kMaxTanhRuns distinct k per kernel (other
+    // lengths decompose into T^1 lookups)
+    std::vector<int> run_len(c.members.size(), 0);  // at a run's first member
+    std::vector<bool> in_run(c.members.size(), false);
+    std::map<int, int> len_count;
+    if (bf16) {
+      for (size_t j = 0; j < c.members.size();) {
+        if (!(IsElementwiseUnary(c.members[j]) && UnaryFn(c.members[j]) == RH_FN_TANH)) {
+          ++j;
+          continue;
+        }
+        size_t k = j;
+        while (k + 1 < c.members.size() && !c.stored[k] && !c.keep_after[k] &&
+               IsElementwiseUnary(c.members[k + 1]) && UnaryFn(c.members[k + 1]) == RH_FN_TANH)
+          ++k;
+        run_len[j] = static_cast<int>(k - j + 1);
+        for (size_t q = j; q <= k; ++q) in_run[q] = true;
+        ++len_count[run_len[j]];
+        j = k + 1;
+      }
+    }
+    EwArgs a{};
+    std::map<int, int> table_of;  // run length -> table slot
+    auto table = [&](int k) {
+      auto it = table_of.find(k);
+      if (it != table_of.end()) return it->second;
+      const int slot = a.n_tab++;
+      a.tab_off[slot] = TanhTable(k);
+      table_of[k] = slot;
+      return slot;
+    };
+    if (bf16 && !len_count.empty()) {
+      std::vector<std::pair<int, int>> by_count;
+      for (auto& kv : len_count) by_count.emplace_back(-kv.second, kv.first);
+      std::sort(by_count.begin(), by_count.end());
+      if (static_cast<int>(by_count.size()) > kMaxTanhRuns) table(1);
+      for (auto& bc : by_count)
+        if (a.n_tab < kMaxTanhRuns) table(bc.second);
+    }
+    std::vector<int32_t> code;
+    auto emit_after = [&](size_t j) {
+      if (out_slot[j] >= 0) code.push_back(EwIns(kEwStore, out_slot[j]));
+      if (c.keep_after[j]) code.push_back(EwIns(kEwKeep, 0));
+    };
+    for (size_t j = 0; j < c.members.size(); ++j) {
+      const int m = c.members[j];
+      const auto& src = c.src[j];
+      if (j == 0) code.push_back(EwIns(kEwLoad, src[0]));
+      if (IsElementwiseUnary(m)) {
+        if (bf16 && in_run[j]) {
+          if (run_len[j] == 0) continue;  // inside a run: covered by its first member
+          const int k = run_len[j];
+          if (table_of.count(k)) {
+            code.push_back(EwIns(kEwUnary, kFnTanhRun + table_of[k]));
+          } else {
+            for (int q = 0; q < k; ++q) code.push_back(EwIns(kEwUnary, kFnTanhRun + table_of.at(1)));
+          }
+          emit_after(j + k - 1);
+          continue;
+        }
+        code.push_back(EwIns(kEwUnary, UnaryFn(m)));
+      } else {
+        const int other = j == 0 ? src[1] : (src[0] == -1 ? src[1] : src[0]);
+        code.push_back(EwIns(p_->ops[m].kind == RH_OP_MUL ? kEwMul : kEwAdd, other));
+      }
+      emit_after(j);
+    }
+    if (static_cast<int>(code.size()) > kMaxEwCode) Fail("internal: elementwise chain code too long");
+    a.n_code = static_cast<int32_t>(code.size());
+    a.n_in = static_cast<int32_t>(in_t.size());
+    std::copy(code.begin(), code.end(), a.code);
+    a.n = P->tensors[out_t[0]].elems();
+    Step st;
+    st.kind = Step::kKernel;
+    st.launches = 1;
+    st.name = "ew_chain " + OpName(h) + ".." + OpName(c.members.back()) + " (" +
+              std::to_string(c.members.size()) + " ops, " + std::to_string(in_t.size()) + " in, " +
+              std::to_string(out_t.size()) + " out)";
+    for (int t : in_t) st.alg_bytes += static_cast<double>(P->tensors[t].bytes);
+    for (int t : out_t) st.alg_bytes += static_cast<double>(P->tensors[t].bytes);
+    const int first = rt_->first_rank;
+    st.run = [P, a, in_t, out_t, first, dtype](int li, cudaStream_t s) {
+      const int r = first + li;
+      EwArgs x = a;
+      for (size_t k = 0; k < in_t.size(); ++k) x.in[k] = P->Ptr(P->tensors[in_t[k]], r);
+      for (size_t k = 0; k < out_t.size(); ++k) x.out[k] = P->Ptr(P->tensors[out_t[k]], r);
+      for (int t = 0; t < x.n_tab; ++t)
+        x.tab[t] = reinterpret_cast<const uint16_t*>(P->peer_base[r] + x.tab_off[t]);
+      LaunchEwProg(x, dtype, s);
+      return 1;
+    };
+    st.reads = in_t;
+    st.writes = out_t;
+    AddStep(std::move(st));
   }
 
   void EmitKernel(int i, const std::vector<int>& in_t, int out_t) {
@@ -925,6 +1210,8 @@ class Lowerer {
   std::vector<std::vector<int>> chain_;
   std::map<int, size_t> tanh_tables_;
   std::vector<int> remote_read_;  // tensors read by peers (transition sources)
+  std::vector<EwPlan> ew_;
+  std::vector<int> ew_of_;  // op -> elementwise chain id (-1: none)
 };
 
 }  // namespace

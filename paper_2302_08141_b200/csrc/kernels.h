@@ -88,6 +88,31 @@ void LaunchUnaryChain(void* out, const void* in, int64_t n, const ChainArgs& c, 
                       cudaStream_t s);
 void LaunchSoftmaxRows(void* out, const void* in, int64_t rows, int64_t cols, int dtype,
                        cudaStream_t s);
+// Elementwise chain program (one kernel for a chain of add / mul / unary ops that crosses
+// multi-use values: the forward tanh chains whose outputs the backward keeps, the backward's
+// dy * (1 - y^2) accumulations).  An accumulator walks the chain; every instruction is
+// warp-uniform, so the interpreter costs one switch per 8 elements:
+//   LOAD k          acc = in[k]
+//   UNARY fn        acc = fn(acc)        (fn >= kFnTanhRun: T^k table lookup, bf16)
+//   ADD src/MUL src acc = acc op src     (src: input k, kEwSrcKeep, kEwSrcAcc)
+//   KEEP            keep = acc
+//   STORE j         out[j] = acc
+// Every op result is rounded to the program dtype, as in the one-op-per-kernel path.
+constexpr int kMaxEwIn = 8, kMaxEwOut = 16, kMaxEwCode = 96;
+enum EwOpcode : int32_t { kEwLoad = 0, kEwUnary = 1, kEwAdd = 2, kEwMul = 3, kEwKeep = 4, kEwStore = 5 };
+constexpr int kEwSrcKeep = 30, kEwSrcAcc = 31;
+inline int32_t EwIns(int op, int arg) { return op | (arg << 8); }
+struct EwArgs {
+  int32_t n_code, n_in;
+  int32_t code[kMaxEwCode];
+  const void* in[kMaxEwIn];
+  void* out[kMaxEwOut];
+  int32_t n_tab;
+  uint64_t tab_off[kMaxTanhRuns];     // arena offsets (host side)
+  const uint16_t* tab[kMaxTanhRuns];  // device pointers, patched per rank at launch
+  int64_t n;
+};
+void LaunchEwProg(const EwArgs& a, int dtype, cudaStream_t s);
 // out = a (+|*) b, then an optional unary chain (epilogue fusion).
 void LaunchBinary(void* out, const void* a, const void* b, int64_t n, bool mul, const ChainArgs& c,
                   int dtype, cudaStream_t s);

@@ -13,7 +13,7 @@ import os
 import numpy as np
 import pytest
 
-from paper_2302_08141_b200.abi import (RH_BF16, RH_FLAG_KEEP_ALL, RH_FLAG_NO_FUSION, RH_FLAG_SIMT_GEMM,
+from paper_2302_08141_b200.abi import (RH_BF16, RH_F32, RH_FLAG_KEEP_ALL, RH_FLAG_NO_FUSION, RH_FLAG_SIMT_GEMM,
                                        RH_FLAG_UNLABELED_IDENTITY)
 from paper_2302_08141_b200.program import PLANS_DIR, LoweredProgram
 
@@ -98,6 +98,29 @@ def test_local_buffers(rx, oracle_lib, name):
                     assert normwise(got, want) <= TOL_F32 or np.abs(want).max() == 0, (name, op.id, r)
     finally:
         close(rt, mesh, gp)
+
+
+@pytest.mark.parametrize("name,dtype", [("c5_gpt_small_d2", RH_BF16), ("c5_gpt_small_d2", RH_F32),
+                                        ("c5_gpt_small_d4", RH_BF16), ("c3_gpt_block_d1", RH_BF16)])
+def test_fusion_bit_exact(rx, name, dtype):
+    """Fused kernels (elementwise chain programs, unary chains, GEMM epilogues) round every op
+    exactly like the one-op-per-kernel schedule: outputs are bit-identical with NO_FUSION."""
+    prog = LoweredProgram.load(name).with_dtype(dtype)
+    outs, names = {}, {}
+    for flags in (0, RH_FLAG_NO_FUSION):
+        rt, mesh, gp = load(rx, prog, flags)
+        try:
+            gp.init_synthetic(6)
+            gp.run(1)
+            outs[flags] = [gp.read_full(o) for o in prog.outputs]
+            names[flags] = [s["name"] for s in gp.steps()]
+        finally:
+            close(rt, mesh, gp)
+    for o, a, b in zip(prog.outputs, outs[0], outs[RH_FLAG_NO_FUSION]):
+        np.testing.assert_array_equal(a, b, err_msg=f"{name}:{prog.ops[o].id}")
+    assert len(names[0]) < len(names[RH_FLAG_NO_FUSION])
+    if name.startswith("c5_"):
+        assert any(n.startswith("ew_chain") for n in names[0]), names[0][:20]
 
 
 @pytest.mark.parametrize("name", ["c5_gpt_small_d2", "c3_gpt_block_d8"])
