@@ -35,7 +35,7 @@ WORKLOADS = {
     # layer of the same shapes (the full 24-layer step is minutes of CPU), scaled by 1/24
     "gpt24_train": dict(plan="c5_big_gpt24_d{n}", name="gpt24_fwd_bwd_h2048_t2048", dtype="bf16",
                         metric="partitioned-program tokens/s (24-layer GPT fwd+bwd, hidden 2048, 2048 tokens)",
-                        cpu_plan="c5_big_gpt1_d1", cpu_scale=24),
+                        cpu_plan="c5_big_gpt1_d1", cpu_scale=24, reduce_outputs=True),
     "mlp": dict(plan="c1_mlp_d{n}", name="mlp2_b64_h1024", dtype="f32",
                 metric="partitioned-program tokens/s (2-layer MLP, batch 64, hidden 1024)"),
     "mlp_strided": dict(plan="c2_mlp_reshape_d{n}", name="mlp_reshape_strided_b64_h1024", dtype="f32",
@@ -208,7 +208,7 @@ def main():
 
     from paper_2302_08141_b200 import dist as D
     from paper_2302_08141_b200 import runtime as rx
-    from paper_2302_08141_b200.abi import (RH_BF16, RH_F32, RH_FLAG_SIMT_GEMM,
+    from paper_2302_08141_b200.abi import (RH_BF16, RH_F32, RH_FLAG_REDUCE_OUTPUTS, RH_FLAG_SIMT_GEMM,
                                            RH_FLAG_TRANSPORT_NCCL)
     from paper_2302_08141_b200.program import LoweredProgram
 
@@ -222,6 +222,11 @@ def main():
     prog = LoweredProgram.load(pname).with_dtype(dtype)
     tok = tokens_of(prog)
     flags = (RH_FLAG_TRANSPORT_NCCL if args.transport == "nccl" else 0) | (RH_FLAG_SIMT_GEMM if args.simt else 0)
+    # training step (fwd+bwd): gradients end reduced (Partial -> all-reduced), sharded ones stay
+    # sharded; the forward-only workloads materialize their output replicated
+    reduce_outputs = bool(wl.get("reduce_outputs"))
+    if reduce_outputs:
+        flags |= RH_FLAG_REDUCE_OUTPUTS
     with stdout_to_stderr():
         rt = D.make_runtime()
         mesh = rx.Mesh(rt, prog.mesh)
@@ -317,7 +322,7 @@ def main():
                                 if scale > 1 else "the same program")
                              + f", oracle/ref_cpu_exec, {cores} threads"}
         h2d = sum(prog.full_bytes(x) for x in xs) * world
-        d2h = prog.full_bytes(out) * world
+        d2h = (gp.local_bytes(out, rank) if reduce_outputs else prog.full_bytes(out)) * world
         gp.close()
         mesh.close()
         rt.close()
@@ -331,6 +336,8 @@ def main():
                        "global_batch": tok, "seq_len": tok, "ops": len(prog.ops),
                        "parallelism": f"rhino-spmd mesh {prog.mesh}", "transport": args.transport,
                        "gemm": "simt" if args.simt else "tcgen05",
+                       "outputs": "partial axes reduced, sharded axes kept" if reduce_outputs
+                       else "materialized replicated",
                        "l2": "no flush: per-step working set > 126 MB L2" if prog.flops() > 1e11
                        else "no flush: small latency-bound program (L2-resident; reported as such)"},
             "gflop_per_step": prog.flops() / 1e9,

@@ -14,6 +14,7 @@ S1~s for s in {1, 8, 64}, and P as a source.  One JSON line per case:
 import argparse
 import json
 import os
+import re
 import sys
 
 REPO = os.path.dirname(os.path.abspath(__file__))
@@ -54,6 +55,7 @@ def main():
     ap.add_argument("--emulate", type=int, default=0)
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--pairs", default="all", help="all | quick | FROM:TO[,FROM:TO]")
+    ap.add_argument("--flags", type=lambda x: int(x, 0), default=0, help="extra rh_program flags")
     a = ap.parse_args()
 
     import torch
@@ -73,7 +75,7 @@ def main():
     mesh = rx.Mesh(rt, [d])
     dtype = RH_BF16 if a.dtype == "bf16" else RH_F32
     eb = 2 if dtype == RH_BF16 else 4
-    flags = RH_FLAG_TRANSPORT_NCCL if a.transport == "nccl" else 0
+    flags = (RH_FLAG_TRANSPORT_NCCL if a.transport == "nccl" else 0) | a.flags
     mult = {"K": 1 << 10, "M": 1 << 20, "G": 1 << 30}
     sizes = [int(x[:-1]) * mult[x[-1]] for x in a.sizes.split(",")]
     names = specs_for(d)
@@ -83,7 +85,8 @@ def main():
         pairs = [("partial", "replicated"), ("partial", "shard(0,max)"), ("shard(0,max)", "replicated"),
                  ("shard(1,max)", "shard(0,max)"), ("replicated", "shard(0,max)"), ("shard(1,1)", "shard(0,max)")]
     else:
-        pairs = [tuple(p.split(":")) for p in a.pairs.split(",")]
+        spec = r"(?:[a-z]+\([^)]*\)|[a-z]+)"  # commas inside shard(dim,stride) are not separators
+        pairs = re.findall(rf"({spec}):({spec})", a.pairs)
     n_local = rt.n_local
     results = []
     for S in sizes:

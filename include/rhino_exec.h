@@ -110,6 +110,8 @@ typedef struct {
 #define RH_FLAG_NO_MATERIALIZE 0x8u     /* leave program outputs in their planned spec */
 #define RH_FLAG_SIMT_GEMM 0x10u         /* force the CUDA-core GEMM (test/reference kernel) */
 #define RH_FLAG_NO_GRAPH 0x20u          /* launch eagerly instead of replaying a CUDA graph */
+#define RH_FLAG_REDUCE_OUTPUTS 0x80u    /* outputs: reduce Partial axes only (P -> R), leave
+                                           sharded axes sharded (a training step's gradients) */
 #define RH_FLAG_KEEP_ALL 0x40u          /* give every intermediate its own buffer (no arena reuse)
                                            so rh_program_read_* can read any op after a run */
 
@@ -154,7 +156,8 @@ int rh_program_write_full(rh_program* prog, int op, const void* src, size_t byte
 /* Run the program `iters` times; *ms_per_iter = device time per run (max over local ranks). */
 int rh_program_run(rh_program* prog, int iters, double* ms_per_iter);
 /* End-to-end step through host buffers: H2D of every `n_in` (op, host ptr) input, one run,
- * D2H of every program output into out_ptrs (full, materialized).  Timed inside. */
+ * D2H of the first n_outs program outputs into out_ptrs: the full tensor when materialized,
+ * else this process's first local rank's shard (rh_program_local_bytes).  Timed inside. */
 int rh_program_step_host(rh_program* prog, int n_in, const int* in_ops, const void* const* in_ptrs,
                          int n_outs, void* const* out_ptrs, double* ms);
 

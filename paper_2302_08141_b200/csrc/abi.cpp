@@ -118,6 +118,24 @@ void GroupSync(rh_program* p, int axis) {
   for (auto e : ev) cudaEventDestroy(e);
 }
 
+// Dist mode: a device-side barrier over the whole world on rank 0's stream, enqueued right
+// before a timed region so every rank's timeline starts together (host launch skew between
+// processes would otherwise be charged to the first transition's fused barrier).
+void WorldSync(rh_program* p) {
+  rh_runtime* rt = p->mesh->rt;
+  if (!rt->dist || rt->world == 1) return;
+  rh::BarrierArgs b{};
+  b.d = rt->world;
+  for (int k = 0; k < b.d; ++k) {
+    b.members[k] = k;
+    b.peer_flags[k] = reinterpret_cast<uint32_t*>(p->peer_base[k] + p->flags_off);
+  }
+  b.my_flags = reinterpret_cast<uint32_t*>(p->base[0] + p->flags_off);
+  b.counter = reinterpret_cast<uint32_t*>(p->base[0] + p->counter_off);
+  b.me = rt->first_rank;
+  rh::LaunchBarrier(b, rt->streams[0]);
+}
+
 // One run of the schedule.  `prof` (optional): n_steps + 1 boundary events recorded on local
 // rank 0's stream before every step and after the last.
 int64_t RunOnce(rh_program* p, std::vector<cudaEvent_t>* prof) {
@@ -613,7 +631,14 @@ int rh_program_write_full(rh_program* p, int op, const void* src, size_t bytes) 
 int rh_program_run(rh_program* p, int iters, double* ms_per_iter) {
   return Guard([&] {
     rh_runtime* rt = p->mesh->rt;
+    // graph capture / instantiation is host work: do it before the timed region (the eager
+    // first run it needs is one extra, identical run of the program)
+    if (UseGraph(p) && !p->graph && iters > 0) {
+      if (!p->warmed) RunStep(p);
+      p->graph = CaptureRuns(p, 1, nullptr);
+    }
     SyncAll(rt);
+    WorldSync(p);
     std::vector<cudaEvent_t> ev0(rt->streams.size()), ev1(rt->streams.size());
     for (size_t i = 0; i < rt->streams.size(); ++i) {
       DeviceGuard dg(rt->devs[i]);
@@ -650,6 +675,7 @@ int rh_program_profile(rh_program* p, int iters, double* ms_per_iter) {
     if (UseGraph(p) && iters > 0) {
       // the whole timed region is one graph: K runs back to back with external event nodes
       cudaGraphExec_t g = CaptureRuns(p, iters, &ev);
+      WorldSync(p);
       RH_CUDA(cudaGraphLaunch(g, rt->streams[0]));
       SyncAll(rt);
       cudaGraphExecDestroy(g);
@@ -682,6 +708,7 @@ int rh_program_step_host(rh_program* p, int n_in, const int* in_ops, const void*
     cudaEvent_t e0, e1;
     RH_CUDA(cudaEventCreate(&e0));
     RH_CUDA(cudaEventCreate(&e1));
+    WorldSync(p);
     RH_CUDA(cudaEventRecord(e0, rt->streams[0]));
     auto h0 = std::chrono::steady_clock::now();
     for (int k = 0; k < n_in; ++k) {
@@ -693,8 +720,9 @@ int rh_program_step_host(rh_program* p, int n_in, const int* in_ops, const void*
     if (n_outs > static_cast<int>(p->outputs.size())) Fail("too many output buffers");
     for (int k = 0; k < n_outs; ++k) {
       const int op = p->outputs[k];
-      const int ti = p->mat_tensor[op] >= 0 ? p->mat_tensor[op] : -1;
-      if (ti < 0) Fail("output not materialized (RH_FLAG_NO_MATERIALIZE)");
+      // materialized: the full tensor; otherwise this process's first local rank's shard
+      const int ti = p->mat_tensor[op] >= 0 ? p->mat_tensor[op] : p->out_tensor[op];
+      if (ti < 0) Fail("output has no buffer");
       const rh::Tensor& t = p->tensors[ti];
       RH_CUDA(cudaMemcpyAsync(out_ptrs[k], p->base[0] + t.offset, t.bytes, cudaMemcpyDeviceToHost,
                               rt->streams[0]));
@@ -849,7 +877,8 @@ int rh_reshard(rh_mesh* mesh, int axis, rh_spec from, rh_spec to, int ndim, cons
       RH_CUDA(cudaMemcpy(p->base[li] + x.offset, src[li], x.bytes, cudaMemcpyDeviceToDevice));
     }
     HostBarrier(rt);
-    RunOnce(p, nullptr);  // warm-up
+    RunStep(p);  // warm-up (eager), then capture + first replay: both outside the timed runs
+    RunStep(p);
     SyncAll(rt);
     HostBarrier(rt);
     double t = 0;

@@ -247,7 +247,20 @@ class Lowerer {
       }
       EmitOp(i);
     }
-    if (!(p_->flags & RH_FLAG_NO_MATERIALIZE)) {
+    if ((p_->flags & RH_FLAG_REDUCE_OUTPUTS) && !(p_->flags & RH_FLAG_NO_MATERIALIZE)) {
+      // training-step outputs: reduce Partial axes (the gradient all-reduce / reduce of a
+      // data-parallel step), keep sharded axes sharded (the optimizer updates shards in place)
+      for (int o : p_->outputs) {
+        Specs fin = p_->tensors[p_->out_tensor[o]].specs;
+        bool rep = true;
+        for (auto& x : fin) {
+          if (x.kind == RH_PARTIAL) x = Rep();
+          rep = rep && x.kind == RH_REPLICATED;
+        }
+        p_->out_tensor[o] = GetTensor(o, fin, "reduce");
+        if (rep) p_->mat_tensor[o] = p_->out_tensor[o];
+      }
+    } else if (!(p_->flags & RH_FLAG_NO_MATERIALIZE)) {
       for (int o : p_->outputs) {
         Specs rep(p_->n_axes, Rep());
         p_->mat_tensor[o] = GetTensor(o, rep, "materialize");

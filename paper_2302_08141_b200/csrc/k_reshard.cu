@@ -62,8 +62,15 @@ struct PullDev {
   FastDiv dd;   // group size
   uint32_t coord;
   uint32_t n;   // destination units
+  uint32_t rot; // traversal start (units): coord * n / d, so that at any moment the d ranks of a
+                // group read from d different sources instead of all hammering the same peer
   PeerSync sync;
 };
+
+__device__ __forceinline__ uint32_t Rotate(uint32_t i, uint32_t rot, uint32_t n) {
+  const uint32_t j = i + rot;
+  return j >= n ? j - n : j;
+}
 
 __device__ __forceinline__ void StRelaxedSys(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -120,8 +127,8 @@ __global__ void __launch_bounds__(256) PullCopyKernel(PullDev a) {
     V v[U];
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      const uint32_t ii = i + j * stride;
-      if (ii < a.n) {
+      const uint32_t ii = Rotate(i + j * stride, a.rot, a.n);
+      if (i + j * stride < a.n) {
         const uint32_t f = DstToGlobal(a, ii);
         if (kFromShard) {
           const uint32_t q = Div(a.qsf, f);
@@ -136,8 +143,7 @@ __global__ void __launch_bounds__(256) PullCopyKernel(PullDev a) {
     }
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      const uint32_t ii = i + j * stride;
-      if (ii < a.n) reinterpret_cast<V*>(a.dst)[ii] = v[j];
+      if (i + j * stride < a.n) reinterpret_cast<V*>(a.dst)[Rotate(i + j * stride, a.rot, a.n)] = v[j];
     }
   }
 }
@@ -170,7 +176,8 @@ __global__ void __launch_bounds__(256) PullSumKernel(PullDev a, int d) {
   constexpr int E = VB / sizeof(T);
   ArriveAndWait(a.sync);
   const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
+  for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < a.n; i0 += stride) {
+    const uint32_t i = Rotate(i0, a.rot, a.n);
     const uint32_t f = DstToGlobal(a, i);
     float acc[E];
     for (int k = 0; k < d; ++k) {
@@ -216,7 +223,8 @@ __global__ void __launch_bounds__(256) PullStagedKernel(StagedDev a) {
   constexpr int E = 16 / sizeof(T);  // elements per 16-byte vector
   const uint32_t d = a.dd.d;
   const uint32_t Lr = a.qsf.d * d;
-  for (uint32_t chunk = blockIdx.x; chunk < a.chunks; chunk += gridDim.x) {
+  for (uint32_t c0 = blockIdx.x; c0 < a.chunks; c0 += gridDim.x) {
+    const uint32_t chunk = Rotate(c0, a.coord * (a.chunks / d), a.chunks);
     const uint32_t i0 = chunk * a.L;
     uint32_t f0 = i0;
     if (a.to_shard) {
@@ -355,6 +363,7 @@ int LaunchPull(const PullArgs& a, cudaStream_t s) {
   const int d = a.to.kind == RH_SHARD ? a.to.d : a.from.d;
   dv.dd = MakeFastDiv(static_cast<uint32_t>(std::max(d, 1)));
   dv.coord = static_cast<uint32_t>(a.coord);
+  dv.rot = static_cast<uint32_t>((static_cast<uint64_t>(dv.n) / std::max(d, 1)) * a.coord % std::max<uint32_t>(dv.n, 1));
   dv.sync = a.sync;
   switch (vb) {
     case 16: LaunchPullVB<16>(a, dv, s); break;

@@ -113,7 +113,7 @@ def main():
         for flags in ((0, RH_FLAG_NO_FUSION | RH_FLAG_SIMT_GEMM, RH_FLAG_TRANSPORT_NCCL) if full
                       else (0, RH_FLAG_TRANSPORT_NCCL)):
             out.append(check(rt, name, flags))
-        if name.startswith("c3_") or name.startswith("c1_"):
+        if name.startswith(("c3_", "c1_", "c5_")):
             out.append(check(rt, name, 0, RH_BF16))
     rt.close()
     if rt.first_rank == 0:

@@ -13,7 +13,7 @@ import os
 import numpy as np
 import pytest
 
-from paper_2302_08141_b200.abi import (RH_BF16, RH_F32, RH_FLAG_KEEP_ALL, RH_FLAG_NO_FUSION, RH_FLAG_SIMT_GEMM,
+from paper_2302_08141_b200.abi import (RH_BF16, RH_F32, RH_FLAG_KEEP_ALL, RH_FLAG_REDUCE_OUTPUTS, RH_FLAG_NO_FUSION, RH_FLAG_SIMT_GEMM,
                                        RH_FLAG_UNLABELED_IDENTITY)
 from paper_2302_08141_b200.program import PLANS_DIR, LoweredProgram
 
@@ -121,6 +121,27 @@ def test_fusion_bit_exact(rx, name, dtype):
     assert len(names[0]) < len(names[RH_FLAG_NO_FUSION])
     if name.startswith("c5_"):
         assert any(n.startswith("ew_chain") for n in names[0]), names[0][:20]
+
+
+@pytest.mark.parametrize("name", ["c5_gpt_small_d2", "c5_gpt_small_d4"])
+def test_reduce_outputs(rx, name):
+    """RH_FLAG_REDUCE_OUTPUTS: a training step's outputs end with Partial axes reduced and sharded
+    axes kept — same values as the replicated materialization, without the output all-gathers."""
+    prog = LoweredProgram.load(name).with_dtype(RH_BF16)
+    outs, names = {}, {}
+    for flags in (0, RH_FLAG_REDUCE_OUTPUTS):
+        rt, mesh, gp = load(rx, prog, flags)
+        try:
+            gp.init_synthetic(8)
+            gp.run(1)
+            outs[flags] = [gp.read_full(o) for o in prog.outputs]
+            names[flags] = [s["name"] for s in gp.steps()]
+        finally:
+            close(rt, mesh, gp)
+    for a, b in zip(outs[0], outs[RH_FLAG_REDUCE_OUTPUTS]):
+        np.testing.assert_array_equal(a, b)
+    assert not any("materialize" in n for n in names[RH_FLAG_REDUCE_OUTPUTS])
+    assert not any(n.startswith("all_gather") and "(reduce)" in n for n in names[RH_FLAG_REDUCE_OUTPUTS])
 
 
 @pytest.mark.parametrize("name", ["c5_gpt_small_d2", "c3_gpt_block_d8"])
