@@ -195,6 +195,7 @@ def main():
     ap.add_argument("--dtype", default=None, choices=["bf16", "f32"])
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true", help="keep every transition on the main stream")
     ap.add_argument("--simt", action="store_true", help="force the CUDA-core GEMM (comparison)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -208,8 +209,8 @@ def main():
 
     from paper_2302_08141_b200 import dist as D
     from paper_2302_08141_b200 import runtime as rx
-    from paper_2302_08141_b200.abi import (RH_BF16, RH_F32, RH_FLAG_REDUCE_OUTPUTS, RH_FLAG_SIMT_GEMM,
-                                           RH_FLAG_TRANSPORT_NCCL)
+    from paper_2302_08141_b200.abi import (RH_BF16, RH_F32, RH_FLAG_NO_OVERLAP, RH_FLAG_REDUCE_OUTPUTS,
+                                           RH_FLAG_SIMT_GEMM, RH_FLAG_TRANSPORT_NCCL)
     from paper_2302_08141_b200.program import LoweredProgram
 
     wl = WORKLOADS[args.workload]
@@ -227,6 +228,8 @@ def main():
     reduce_outputs = bool(wl.get("reduce_outputs"))
     if reduce_outputs:
         flags |= RH_FLAG_REDUCE_OUTPUTS
+    if args.no_overlap:
+        flags |= RH_FLAG_NO_OVERLAP
     with stdout_to_stderr():
         rt = D.make_runtime()
         mesh = rx.Mesh(rt, prog.mesh)
@@ -304,7 +307,10 @@ def main():
         if trans:
             wire = sum(s["wire_bytes"] for s in trans)
             t = sum(s["ms"] for s in trans)
+            ov = [s for s in trans if "[overlap]" in s["name"]]
             reshard = {"transitions": len(trans), "wire_bytes_per_rank": wire, "ms": t,
+                       "overlapped": len(ov), "overlapped_ms": sum(s["ms"] for s in ov),
+                       "exposed_ms": t - sum(s["ms"] for s in ov),
                        "busbw_gbs": wire / (t * 1e-3) / 1e9 if t > 0 else None,
                        "peak_gbs": NVLINK_PEER_GBS, "transport": args.transport,
                        "per_transition": [{"name": s["name"], "ms": s["ms"],
@@ -335,6 +341,7 @@ def main():
             "config": {"workload": wl["name"], "plan": pname, "mesh": prog.mesh,
                        "global_batch": tok, "seq_len": tok, "ops": len(prog.ops),
                        "parallelism": f"rhino-spmd mesh {prog.mesh}", "transport": args.transport,
+                       "overlap": not args.no_overlap,
                        "gemm": "simt" if args.simt else "tcgen05",
                        "outputs": "partial axes reduced, sharded axes kept" if reduce_outputs
                        else "materialized replicated",

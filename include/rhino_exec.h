@@ -112,6 +112,8 @@ typedef struct {
 #define RH_FLAG_NO_GRAPH 0x20u          /* launch eagerly instead of replaying a CUDA graph */
 #define RH_FLAG_REDUCE_OUTPUTS 0x80u    /* outputs: reduce Partial axes only (P -> R), leave
                                            sharded axes sharded (a training step's gradients) */
+#define RH_FLAG_NO_OVERLAP 0x100u       /* dist: keep every transition on the main stream (no
+                                           side-stream overlap of off-critical-path transitions) */
 #define RH_FLAG_KEEP_ALL 0x40u          /* give every intermediate its own buffer (no arena reuse)
                                            so rh_program_read_* can read any op after a run */
 

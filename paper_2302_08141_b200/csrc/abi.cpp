@@ -84,22 +84,27 @@ rh::ComposedMap MakeComposed(const rh_program* p, const rh::Tensor& t, int globa
 bool SameStream(const rh_runtime* rt) { return rt->streams.size() == 1; }
 
 // Cross-rank ordering around a transition that reads peer buffers.
-void GroupSync(rh_program* p, int axis) {
+// `side`: the barrier of an async transition, on the side stream with its own flag/counter
+// state (the main and side streams' barriers interleave differently on every rank, but each
+// stream's sequence is the same on all ranks).
+void GroupSync(rh_program* p, int axis, bool side = false) {
   rh_runtime* rt = p->mesh->rt;
   if (rt->dist) {
     if (rt->world == 1) return;
     const int g = rt->first_rank;
     const std::vector<int> members = p->mesh->Group(axis, g);
+    const size_t flags_off = side ? p->side_flags_off : p->flags_off;
+    const size_t counter_off = side ? p->side_counter_off : p->counter_off;
     rh::BarrierArgs b{};
     b.d = static_cast<int>(members.size());
     for (int k = 0; k < b.d; ++k) {
       b.members[k] = members[k];
-      b.peer_flags[k] = reinterpret_cast<uint32_t*>(p->peer_base[members[k]] + p->flags_off);
+      b.peer_flags[k] = reinterpret_cast<uint32_t*>(p->peer_base[members[k]] + flags_off);
     }
-    b.my_flags = reinterpret_cast<uint32_t*>(p->base[0] + p->flags_off);
-    b.counter = reinterpret_cast<uint32_t*>(p->base[0] + p->counter_off);
+    b.my_flags = reinterpret_cast<uint32_t*>(p->base[0] + flags_off);
+    b.counter = reinterpret_cast<uint32_t*>(p->base[0] + counter_off);
     b.me = g;
-    rh::LaunchBarrier(b, rt->streams[0]);
+    rh::LaunchBarrier(b, side ? p->side : rt->streams[0]);
     return;
   }
   if (SameStream(rt)) return;  // emulated ranks on one GPU share one in-order stream
@@ -137,18 +142,35 @@ void WorldSync(rh_program* p) {
 }
 
 // One run of the schedule.  `prof` (optional): n_steps + 1 boundary events recorded on local
-// rank 0's stream before every step and after the last.
+// rank 0's stream before every step and after the last, then 2 per async step (begin / end on
+// the side stream).
 int64_t RunOnce(rh_program* p, std::vector<cudaEvent_t>* prof) {
   rh_runtime* rt = p->mesh->rt;
   int64_t launches = 0;
   const bool multi_dev = rt->devs.size() > 1;
+  cudaStream_t main = rt->streams[0];
   if (p->n_sync_slots) {  // new run epoch for the barriers fused into the pull kernels
-    rh::LaunchEpochTick(reinterpret_cast<uint32_t*>(p->base[0] + p->epoch_off), rt->streams[0]);
+    rh::LaunchEpochTick(reinterpret_cast<uint32_t*>(p->base[0] + p->epoch_off), main);
     ++launches;
   }
-  for (size_t si = 0; si < p->steps.size(); ++si) {
+  const size_t n = p->steps.size();
+  for (size_t si = 0; si < n; ++si) {
     rh::Step& st = p->steps[si];
-    if (prof) RH_CUDA(cudaEventRecordWithFlags((*prof)[si], rt->streams[0], cudaEventRecordExternal));
+    if (prof) RH_CUDA(cudaEventRecordWithFlags((*prof)[si], main, cudaEventRecordExternal));
+    for (int k : p->joins_at[si]) RH_CUDA(cudaStreamWaitEvent(main, p->done_ev[k], 0));
+    if (st.async) {  // fork onto the side stream (dist: one local rank)
+      const int k = st.async_id;
+      RH_CUDA(cudaEventRecord(p->fork_ev[k], main));
+      RH_CUDA(cudaStreamWaitEvent(p->side, p->fork_ev[k], 0));
+      if (prof) RH_CUDA(cudaEventRecordWithFlags((*prof)[n + 1 + 2 * k], p->side, cudaEventRecordExternal));
+      GroupSync(p, st.axis, /*side=*/true);
+      launches += st.run(0, p->side);
+      GroupSync(p, st.axis, /*side=*/true);
+      launches += 2;
+      if (prof) RH_CUDA(cudaEventRecordWithFlags((*prof)[n + 2 + 2 * k], p->side, cudaEventRecordExternal));
+      RH_CUDA(cudaEventRecord(p->done_ev[k], p->side));
+      continue;
+    }
     if (st.p2p && st.sync_slot < 0) GroupSync(p, st.axis);
     for (int li = 0; li < rt->n_local(); ++li) {
       if (multi_dev) RH_CUDA(cudaSetDevice(rt->device_of(li)));
@@ -156,7 +178,9 @@ int64_t RunOnce(rh_program* p, std::vector<cudaEvent_t>* prof) {
     }
     if (st.p2p && st.post_sync) GroupSync(p, st.axis);
   }
-  if (prof) RH_CUDA(cudaEventRecordWithFlags(prof->back(), rt->streams[0], cudaEventRecordExternal));
+  for (const auto& st : p->steps)  // join what no later step waited for
+    if (st.async && st.join < 0) RH_CUDA(cudaStreamWaitEvent(main, p->done_ev[st.async_id], 0));
+  if (prof) RH_CUDA(cudaEventRecordWithFlags((*prof)[n], main, cudaEventRecordExternal));
   if (multi_dev) RH_CUDA(cudaSetDevice(rt->devs[0]));
   return launches;
 }
@@ -268,6 +292,16 @@ void Allocate(rh_program* p) {
     p->peer_base[r] = static_cast<char*>(ptr);
   }
   p->ipc_opened = true;
+  if (p->n_async) {  // side stream + fork/done events of the async transitions
+    DeviceGuard dg(rt->devs[0]);
+    RH_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+    p->fork_ev.assign(p->n_async, nullptr);
+    p->done_ev.assign(p->n_async, nullptr);
+    for (int k = 0; k < p->n_async; ++k) {
+      RH_CUDA(cudaEventCreateWithFlags(&p->fork_ev[k], cudaEventDisableTiming));
+      RH_CUDA(cudaEventCreateWithFlags(&p->done_ev[k], cudaEventDisableTiming));
+    }
+  }
   HostBarrier(rt);  // every arena zeroed (flags included) before any barrier kernel runs
 }
 
@@ -287,6 +321,9 @@ void DestroyProgram(rh_program* p) {
       if (r != rt->first_rank && p->peer_base[r]) cudaIpcCloseMemHandle(p->peer_base[r]);
   }
   if (p->graph) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(p->graph));
+  for (auto e : p->fork_ev) cudaEventDestroy(e);
+  for (auto e : p->done_ev) cudaEventDestroy(e);
+  if (p->side) cudaStreamDestroy(p->side);
   for (int li = 0; li < rt->n_local() && li < static_cast<int>(p->owned.size()); ++li) {
     DeviceGuard dg(rt->device_of(li));
     cudaFree(p->owned[li]);
@@ -669,7 +706,7 @@ int rh_program_profile(rh_program* p, int iters, double* ms_per_iter) {
     DeviceGuard dg(rt->devs[0]);
     const size_t n = p->steps.size();
     // Boundary events for every (iteration, step); no host sync inside the timed region.
-    std::vector<std::vector<cudaEvent_t>> ev(std::max(iters, 0), std::vector<cudaEvent_t>(n + 1));
+    std::vector<std::vector<cudaEvent_t>> ev(std::max(iters, 0), std::vector<cudaEvent_t>(n + 1 + 2 * p->n_async));
     for (auto& row : ev)
       for (auto& e : row) RH_CUDA(cudaEventCreate(&e));
     if (UseGraph(p) && iters > 0) {
@@ -687,7 +724,13 @@ int rh_program_profile(rh_program* p, int iters, double* ms_per_iter) {
     for (int it = 0; it < iters; ++it)
       for (size_t i = 0; i < n; ++i) {
         float ms = 0;
-        RH_CUDA(cudaEventElapsedTime(&ms, ev[it][i], ev[it][i + 1]));
+        const rh::Step& st = p->steps[i];
+        if (st.async) {  // side-stream duration (fork to done, including its barriers)
+          const size_t k = static_cast<size_t>(st.async_id);
+          RH_CUDA(cudaEventElapsedTime(&ms, ev[it][n + 1 + 2 * k], ev[it][n + 2 + 2 * k]));
+        } else {
+          RH_CUDA(cudaEventElapsedTime(&ms, ev[it][i], ev[it][i + 1]));
+        }
         acc[i] += ms;
       }
     float total = 0;
@@ -838,7 +881,7 @@ int rh_program_launch_count(const rh_program* p, int64_t* launches) {
     for (const auto& s : p->steps) n += static_cast<int64_t>(s.launches) * p->mesh->rt->n_local();
     for (const auto& s : p->steps)
       if (s.p2p && p->mesh->rt->dist && p->mesh->rt->world > 1)
-        n += (s.sync_slot < 0 ? 1 : 0) + (s.post_sync ? 1 : 0);  // separate barrier kernels
+        n += (s.sync_slot < 0 || s.async ? 1 : 0) + (s.post_sync ? 1 : 0);  // separate barrier kernels
     if (p->n_sync_slots) n += 1;                                 // epoch tick
     *launches = n;
   });

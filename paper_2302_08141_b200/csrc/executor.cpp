@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <sstream>
@@ -186,6 +187,15 @@ rh_spec Natural(const rh_op& op, const std::vector<rh_spec>& in, const std::vect
   }
 }
 
+// Grid cap of side-stream (overlapped) pull kernels; RH_SIDE_BLOCKS overrides (tuning).
+int SideBlocks() {
+  static const int n = [] {
+    const char* e = std::getenv("RH_SIDE_BLOCKS");
+    return e ? std::max(1, std::atoi(e)) : 148 * 2;
+  }();
+  return n;
+}
+
 // Reshard wire bytes of one single-axis transition (sharding.cpp:113-135).
 double WireBytes(const rh_spec& from, const rh_spec& to, double S, int d) {
   const double frac = static_cast<double>(d - 1) / d;
@@ -272,17 +282,21 @@ class Lowerer {
       p_->sync_off = Alloc(static_cast<size_t>(p_->n_sync_slots) * rt_->world * 4);
       p_->epoch_off = Alloc(4);
     }
+    PlanAsync();
     PlanArena();
     p_->arena_bytes = arena_;
-    // Barrier elision: tensors are written once per run (single-assignment arena), so a peer can
-    // only overwrite what a transition reads in the NEXT run.  Every p2p transition but the
-    // last one on its axis can drop its post-barrier: the next p2p transition on that axis
-    // begins with a barrier of the same group, which peers cannot pass before we finished.
+    // Barrier elision: transition sources are persistent (never recycled by the arena planner)
+    // and written once per run, so a peer can only overwrite what a transition reads in the
+    // NEXT run.  Every main-stream p2p transition but the last one on its axis can drop its
+    // post-barrier: the next p2p transition on that axis begins with a barrier of the same
+    // group, which peers cannot pass before we finished.  Async (side-stream) transitions keep
+    // their post-barrier (on the side stream's own barrier state).
     std::vector<int> last(p_->n_axes, -1);
     for (size_t i = 0; i < p_->steps.size(); ++i)
-      if (p_->steps[i].p2p) last[p_->steps[i].axis] = static_cast<int>(i);
+      if (p_->steps[i].p2p && !p_->steps[i].async) last[p_->steps[i].axis] = static_cast<int>(i);
     for (size_t i = 0; i < p_->steps.size(); ++i)
-      if (p_->steps[i].p2p) p_->steps[i].post_sync = static_cast<int>(i) == last[p_->steps[i].axis];
+      if (p_->steps[i].p2p)
+        p_->steps[i].post_sync = p_->steps[i].async || static_cast<int>(i) == last[p_->steps[i].axis];
   }
 
  private:
@@ -292,6 +306,49 @@ class Lowerer {
     return off;
   }
   static size_t Align(size_t bytes) { return (bytes + 255) / 256 * 256; }
+
+  // Overlap (dist mode): a p2p transition whose result is first needed well after it can start
+  // runs on a side stream, concurrently with the main stream's kernels — the gradient
+  // reductions of a backward pass, activations resharded for a much later consumer.  The main
+  // stream waits for it right before its first reader (or at the end of the run).  Estimated
+  // times: kernels max(flops / 1.2 PF/s, bytes / 5 TB/s) + 2 us, transitions wire / 500 GB/s +
+  // 15 us; a transition goes async when the main-stream work it can hide behind is at least
+  // half its own estimate.
+  void PlanAsync() {
+    auto& S = p_->steps;
+    const int ns = static_cast<int>(S.size());
+    p_->joins_at.assign(ns, {});
+    if (!rt_->dist || rt_->world < 2 || (p_->flags & RH_FLAG_NO_OVERLAP)) return;
+    auto est = [&](const Step& s) {
+      if (s.kind == Step::kTransition) return s.wire_bytes / 5e11 + 15e-6;
+      return std::max(s.alg_flops / 1.2e15, s.alg_bytes / 5e12) + 2e-6;
+    };
+    for (int i = 0; i < ns; ++i) {
+      Step& st = S[i];
+      if (st.kind != Step::kTransition || !st.p2p || st.sync_slot < 0 || st.writes.size() != 1) continue;
+      const int y = Root(st.writes[0]);
+      int j = -1;
+      for (int k = i + 1; k < ns && j < 0; ++k)
+        for (int r : S[k].reads)
+          if (Root(r) == y) {
+            j = k;
+            break;
+          }
+      double hide = 0;
+      for (int k = i + 1; k < (j < 0 ? ns : j); ++k)
+        if (!S[k].async) hide += est(S[k]);
+      if (hide < 0.5 * est(st)) continue;
+      st.async = true;
+      st.name += " [overlap]";
+      st.join = j;
+      st.async_id = p_->n_async++;
+      if (j >= 0) p_->joins_at[j].push_back(st.async_id);
+    }
+    if (p_->n_async) {
+      p_->side_flags_off = Alloc(static_cast<size_t>(rt_->world) * 4);
+      p_->side_counter_off = Alloc(4);
+    }
+  }
 
   int Root(int t) const {
     while (p_->tensors[t].alias >= 0) t = p_->tensors[t].alias;
@@ -1134,7 +1191,8 @@ class Lowerer {
     if (st.p2p && rt_->dist && rt_->world > 1 && to.kind != RH_PARTIAL) st.sync_slot = p_->n_sync_slots++;
     if (!nccl) {
       const int slot = st.sync_slot;
-      st.run = [P, src, dst, axis, fv, tv, dtype, slot](int li, cudaStream_t s) {
+      const size_t si = p_->steps.size();  // this step's index
+      st.run = [P, src, dst, axis, fv, tv, dtype, slot, si](int li, cudaStream_t s) {
         const int g = P->mesh->rt->first_rank + li;
         const std::vector<int> members = P->mesh->Group(axis, g);
         const int coord = P->mesh->Coords(g)[axis];
@@ -1146,7 +1204,11 @@ class Lowerer {
         a.coord = coord;
         a.n_dst = P->tensors[dst].elems();
         a.dtype = dtype;
-        if (slot >= 0) {
+        const bool async = P->steps[si].async;
+        if (async) a.max_blocks = SideBlocks();  // side stream: leave SMs to compute
+        // async: the pre-barrier is a 1-CTA kernel before the pull (no grid-wide spinning next
+        // to the main stream's kernels)
+        if (slot >= 0 && !async) {
           const size_t row = P->sync_off + static_cast<size_t>(slot) * P->mesh->rt->world * 4;
           a.sync.d = static_cast<int>(members.size());
           a.sync.me = g;

@@ -72,6 +72,9 @@ struct Step {
   int launches = 0;          // per rank per run
   double ms = 0;             // from the last profile
   std::vector<int> reads, writes;  // tensors (for the arena planner's liveness)
+  bool async = false;  // dist p2p transition on the side stream, overlapping the compute
+  int join = -1;       // async: main-stream step that first needs the result (-1: end of run)
+  int async_id = -1;   // index into the program's fork/done events
   // Enqueue this step for local rank `li` on stream `s`; returns the launches issued.
   std::function<int(int li, cudaStream_t s)> run;
 };
@@ -111,6 +114,12 @@ struct rh_program {
   std::vector<std::pair<size_t, std::vector<char>>> uploads;  // constant data (arena offset, bytes)
   size_t gemm_scratch_bytes = 0, gemm_scratch_off = 0;  // 3xTF32 split scratch (shared)
   void* graph = nullptr;  // cudaGraphExec_t of one captured run (single-stream runtimes)
+  // overlap (dist): side stream for async transitions + its own barrier state
+  int n_async = 0;
+  size_t side_flags_off = 0, side_counter_off = 0;
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> fork_ev, done_ev;
+  std::vector<std::vector<int>> joins_at;  // main step -> async ids to wait for before it
   bool warmed = false;    // one eager run precedes capture
 
   char* Ptr(const rh::Tensor& t, int global_rank) const { return peer_base[global_rank] + t.offset; }

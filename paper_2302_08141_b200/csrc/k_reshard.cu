@@ -287,7 +287,7 @@ bool TryLaunchStaged(const PullArgs& a, cudaStream_t s) {
   sd.L = static_cast<uint32_t>(L);
   sd.per = static_cast<uint32_t>(L / d);
   sd.chunks = static_cast<uint32_t>(a.n_dst / L);
-  const int blocks = static_cast<int>(std::min<int64_t>(sd.chunks, 148 * 8));
+  const int blocks = static_cast<int>(std::min<int64_t>(sd.chunks, a.max_blocks > 0 ? a.max_blocks : 148 * 6));
   const size_t smem = static_cast<size_t>(L) * eb;
   if (eb == 2) PullStagedKernel<uint16_t><<<blocks, 256, smem, s>>>(sd);
   else PullStagedKernel<uint32_t><<<blocks, 256, smem, s>>>(sd);
@@ -307,13 +307,15 @@ int Gcd(int64_t a, int64_t b) {
 template <int VB>
 void LaunchPullVB(const PullArgs& a, PullDev& dv, cudaStream_t s) {
   const uint32_t n = dv.n;
-  int blocks = static_cast<int>(std::min<int64_t>((n + 1023) / 1024, 148 * 8));
+  const int cap = a.max_blocks > 0 ? a.max_blocks : 148 * 6;
+  int blocks = static_cast<int>(std::min<int64_t>((n + 1023) / 1024, cap));
   blocks = std::max(blocks, 1);
   if (a.from.kind == RH_PARTIAL) {
+    const int sb = static_cast<int>(std::min<int64_t>((n + 255) / 256, cap));
     if (a.dtype == RH_BF16) {
-      if constexpr (VB >= 2) PullSumKernel<__nv_bfloat16, VB><<<blocks * 4, 256, 0, s>>>(dv, a.from.d);
+      if constexpr (VB >= 2) PullSumKernel<__nv_bfloat16, VB><<<sb, 256, 0, s>>>(dv, a.from.d);
     } else {
-      if constexpr (VB >= 4) PullSumKernel<float, VB><<<blocks * 4, 256, 0, s>>>(dv, a.from.d);
+      if constexpr (VB >= 4) PullSumKernel<float, VB><<<sb, 256, 0, s>>>(dv, a.from.d);
     }
   } else if (a.from.kind == RH_SHARD) {
     PullCopyKernel<VB, true><<<blocks, 256, 0, s>>>(dv);

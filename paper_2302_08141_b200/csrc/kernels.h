@@ -53,6 +53,9 @@ struct PullArgs {
   int64_t n_dst;  // destination elements
   int dtype;
   PeerSync sync;  // sync.d == 0 unless fused
+  int max_blocks = 0;  // grid cap (0: default).  Spinning pull grids never fill the GPU (at most
+                       // 6 of 8 CTA slots per SM), so a pull on the side stream can always be
+                       // scheduled next to a main-stream pull that waits for a peer.
 };
 // Increments the device run counter (start of every run with fused barriers).
 void LaunchEpochTick(uint32_t* epoch, cudaStream_t s);
