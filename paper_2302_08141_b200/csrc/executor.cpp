@@ -981,10 +981,12 @@ class Lowerer {
           if (P->gemm_scratch_bytes) a.scratch = P->peer_base[r] + P->gemm_scratch_off;
           if (!tc) return LaunchGemmSimt(a, s);  // (+ split-K reduce for small M)
           LaunchGemmTc(a, s);
-          // 3xTF32: 2 split kernels + the GEMM; bf16 split-K: the GEMM + the reduce
-          return a.dtype == RH_F32 ? 3 : (GemmTcScratchBytes(a) > 0 ? 2 : 1);
+          return GemmTcLaunches(a);
         };
-        if (tc && dtype == RH_BF16 && GemmTcScratchBytes(g) > 0) st.launches = 2;
+        if (tc) {
+          st.launches = GemmTcLaunches(g);
+          st.name += GemmTcSchedule(g);
+        }
         if (!tc && GemmSimtScratchBytes(g) > 0) st.launches = 2;
         if (tc && dtype == RH_F32) {
           st.launches = 3;

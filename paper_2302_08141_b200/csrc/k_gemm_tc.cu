@@ -768,6 +768,18 @@ bool GemmTcSupported(const GemmArgs& g) {
   return true;
 }
 
+const char* GemmTcSchedule(const GemmArgs& g) {
+  if (g.dtype == RH_F32) return "";
+  const int bn = PickBN(g);
+  return bn && KSplit(g, bn) > 1 ? " [split-k]" : "";
+}
+
+int GemmTcLaunches(const GemmArgs& g) {
+  if (g.dtype == RH_F32) return 3;
+  const int bn = PickBN(g);
+  return bn && KSplit(g, bn) > 1 ? 2 : 1;
+}
+
 void LaunchGemmTc(const GemmArgs& g, cudaStream_t s) {
   if (!GemmTcSupported(g)) Fail("tcgen05 GEMM: unsupported shape/layout", RH_ERR_UNSUPPORTED);
   if (g.dtype == RH_F32) {

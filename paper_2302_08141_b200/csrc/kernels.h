@@ -156,6 +156,9 @@ size_t GemmSimtScratchBytes(const GemmArgs& g);
 // tcgen05 / TMEM / TMA kernel.  Returns false when the shape/layout is not supported by it.
 bool GemmTcSupported(const GemmArgs& g);
 void LaunchGemmTc(const GemmArgs& g, cudaStream_t s);
+// Launches LaunchGemmTc issues: 3xTF32 3 (two splits + GEMM), bf16 split-K 2 (+ reduce), else 1.
+int GemmTcLaunches(const GemmArgs& g);
+const char* GemmTcSchedule(const GemmArgs& g);  // " [split-k]" or ""
 
 // --------------------------------------- cross-GPU sync --------------------------------------
 // Group barrier over CUDA-IPC-mapped flag arrays (one process per GPU only: every member runs on

@@ -51,8 +51,11 @@ def run(doc, flags=0):
     return a, b, c, names
 
 
+# (512, 1024, 1024) and (2048, 16384, 512): split-K; 128 / 256 / 384-tile shapes: one and a half
+# to three waves on 148 SMs
 @pytest.mark.parametrize("m,k,n", [(128, 64, 128), (128, 128, 256), (256, 512, 384), (512, 1024, 1024),
-                                   (2048, 4096, 4096), (2048, 16384, 512)])
+                                   (2048, 4096, 4096), (2048, 16384, 512), (2048, 2048, 2048),
+                                   (4096, 3072, 1024)])
 @pytest.mark.parametrize("tb", [False, True])
 @pytest.mark.parametrize("ta", [False, True])
 def test_tc_gemm_vs_fp64(m, k, n, tb, ta):
