@@ -904,6 +904,33 @@ class Lowerer {
       }
       emit_after(j);
     }
+    // peephole for the tanh backward (dy - (dy*y)*y), same roundings in one instruction:
+    //   KEEP, MUL k, MUL k, UNARY neg, ADD keep      ->  TBWD k
+    //   LOAD b, MUL k, MUL k, UNARY neg, ADD b       ->  LOAD b, TBWD k   (TBWD also sets keep:
+    //                                                    only when no later instruction reads the
+    //                                                    old keep before the next KEEP)
+    auto keep_read_later = [&](size_t from) {
+      for (size_t q = from; q < code.size(); ++q) {
+        if (code[q] == EwIns(kEwKeep, 0)) return false;
+        const int op = code[q] & 0xff;
+        if ((op == kEwAdd || op == kEwMul) && (code[q] >> 8) == kEwSrcKeep) return true;
+      }
+      return false;
+    };
+    for (size_t q = 0; q + 4 < code.size(); ++q) {
+      const int32_t m = code[q + 1];
+      const bool mm = (m & 0xff) == kEwMul && (m >> 8) < kMaxEwIn && code[q + 2] == m &&
+                      code[q + 3] == EwIns(kEwUnary, RH_FN_NEG);
+      if (!mm) continue;
+      if (code[q] == EwIns(kEwKeep, 0) && code[q + 4] == EwIns(kEwAdd, kEwSrcKeep)) {
+        code[q] = EwIns(kEwTanhBwd, m >> 8);
+        code.erase(code.begin() + q + 1, code.begin() + q + 5);
+      } else if ((code[q] & 0xff) == kEwLoad && code[q + 4] == EwIns(kEwAdd, code[q] >> 8) &&
+                 !keep_read_later(q + 5)) {
+        code[q + 1] = EwIns(kEwTanhBwd, m >> 8);
+        code.erase(code.begin() + q + 2, code.begin() + q + 5);
+      }
+    }
     if (static_cast<int>(code.size()) > kMaxEwCode) Fail("internal: elementwise chain code too long");
     a.n_code = static_cast<int32_t>(code.size());
     a.n_in = static_cast<int32_t>(in_t.size());

@@ -269,6 +269,23 @@ __device__ __forceinline__ void EwRunVec(const EwArgs& a, int64_t i, const uint1
       case kEwStore:
         reinterpret_cast<uint4*>(a.out[arg])[i] = make_uint4(acc[0], acc[1], acc[2], acc[3]);
         break;
+      case kEwTanhBwd: {
+        const uint4 v = EwPick(raw, arg);
+        const uint32_t y[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          keep[e] = acc[e];
+          if constexpr (kBf16) {
+            const uint32_t t = MulBf16x2(MulBf16x2(acc[e], y[e]), y[e]);
+            acc[e] = AddBf16x2(keep[e], t ^ 0x80008000u);
+          } else {
+            const float yy = __uint_as_float(y[e]);
+            const float t = __fmul_rn(__fmul_rn(__uint_as_float(acc[e]), yy), yy);
+            acc[e] = __float_as_uint(__fadd_rn(__uint_as_float(keep[e]), -t));
+          }
+        }
+        break;
+      }
       case kEwAdd:
       case kEwMul: {
         uint32_t w[4];
@@ -327,6 +344,17 @@ __device__ __forceinline__ void EwRunScalar(const EwArgs& a, int64_t i, const ui
       case kEwLoad: acc = LoadScalar<kBf16>(a.in[arg], i); break;
       case kEwKeep: keep = acc; break;
       case kEwStore: StoreScalar<kBf16>(a.out[arg], i, acc); break;
+      case kEwTanhBwd: {
+        const float y = LoadScalar<kBf16>(a.in[arg], i);
+        keep = acc;
+        float t = __fmul_rn(acc, y);
+        if (kBf16) t = RoundBf16(t);
+        t = __fmul_rn(t, y);
+        if (kBf16) t = RoundBf16(t);
+        acc = __fadd_rn(keep, -t);
+        if (kBf16) acc = RoundBf16(acc);
+        break;
+      }
       case kEwAdd:
       case kEwMul: {
         const float w = arg == kEwSrcKeep ? keep : arg == kEwSrcAcc ? acc : LoadScalar<kBf16>(a.in[arg], i);

@@ -1,17 +1,38 @@
-import sys, os
-sys.path.insert(0, "/root/repo")
-from paper_2302_08141_b200 import runtime as rx
-from paper_2302_08141_b200.abi import RH_BF16
-from paper_2302_08141_b200.program import LoweredProgram
-prog = LoweredProgram.load("c5_big_gpt24_d1").with_dtype(RH_BF16)
-rt = rx.Runtime(devices=[0]); mesh = rx.Mesh(rt, [1]); gp = rx.Program(mesh, prog, 0)
-gp.init_synthetic(0); gp.run(2); gp.profile(2)
+"""Elementwise-chain breakdown of the C5 fwd+bwd step: time and achieved GB/s grouped by chain
+signature (ops, inputs, outputs, elements)."""
+import collections
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2302_08141_b200 import runtime as rx  # noqa: E402
+from paper_2302_08141_b200.abi import RH_BF16  # noqa: E402
+from paper_2302_08141_b200.program import LoweredProgram  # noqa: E402
+
+plan = sys.argv[1] if len(sys.argv) > 1 else "c5_big_gpt24_d1"
+prog = LoweredProgram.load(plan).with_dtype(RH_BF16)
+rt = rx.Runtime(devices=[0] * prog.world)
+mesh = rx.Mesh(rt, prog.mesh)
+gp = rx.Program(mesh, prog, 0)
+gp.init_synthetic(0)
+gp.run(2)
+gp.profile(3)
 st = gp.steps()
-ew = [s for s in st if s["name"].startswith("ew_chain")]
 print("arena/pool GB", [x / 1e9 for x in gp.memory()])
-print("n ew", len(ew), "total ms", sum(s["ms"] for s in ew))
-for s in sorted(ew, key=lambda s: -s["ms"])[:25]:
-    print(f'{s["ms"]*1e3:8.1f} us {s["alg_bytes"]/1e6:8.1f} MB {s["alg_bytes"]/(s["ms"]*1e-3)/1e9:7.0f} GB/s  {s["name"]}')
-# one layer's worth in order
-for s in st[:80]:
-    print(f'{s["ms"]*1e3:8.1f} us {s["alg_bytes"]/1e6:8.1f} MB  {s["name"]}')
+g = collections.defaultdict(lambda: [0, 0.0, 0.0])
+for s in st:
+    if s["kind"] != 0:
+        continue
+    name = s["name"]
+    if name.startswith("ew_chain"):
+        sig = "ew " + name[name.index("("):]
+    else:
+        sig = name.split(" ")[0]
+    k = (sig, round(s["alg_bytes"] / 1e6, 1))
+    g[k][0] += 1
+    g[k][1] += s["ms"]
+    g[k][2] += s["alg_bytes"]
+tot = sum(v[1] for v in g.values())
+print(f"kernel steps total {tot:.2f} ms (profiled)")
+for (sig, mb), (n, ms, b) in sorted(g.items(), key=lambda kv: -kv[1][1])[:40]:
+    print(f"{ms:8.3f} ms  x{n:4d}  {mb:8.1f} MB/launch  {b / (ms * 1e-3) / 1e9:6.0f} GB/s  {sig}")
