@@ -239,11 +239,12 @@ __device__ __forceinline__ uint32_t MulBf16x2(uint32_t a, uint32_t b) {
 
 // TanhRunLookup on both halves of a bf16x2 register.
 __device__ __forceinline__ uint32_t TanhRunLookup2(uint32_t p, const uint16_t* tab) {
+  constexpr uint32_t kLo = 122u << 7, kSpan = 0x7f80u - (122u << 7), kLast = kTanhRunEntries - 1;
   const uint32_t lo = p & 0x7fffu, hi = (p >> 16) & 0x7fffu;
-  const uint32_t tlo = tab[min(max(static_cast<int>(lo) - (122 << 7), 0), kTanhRunEntries - 1)];
-  const uint32_t thi = tab[min(max(static_cast<int>(hi) - (122 << 7), 0), kTanhRunEntries - 1)];
-  uint32_t rlo = lo < (122u << 7) || lo > 0x7f80u ? lo : tlo;
-  uint32_t rhi = hi < (122u << 7) || hi > 0x7f80u ? hi : thi;
+  const uint32_t ulo = lo - kLo, uhi = hi - kLo;
+  const uint32_t tlo = tab[min(ulo, kLast)], thi = tab[min(uhi, kLast)];
+  const uint32_t rlo = ulo > kSpan ? lo : tlo;
+  const uint32_t rhi = uhi > kSpan ? hi : thi;
   return (p & 0x80008000u) | rlo | (rhi << 16);
 }
 

@@ -101,13 +101,13 @@ __device__ __forceinline__ uint32_t PackBf16x2(float lo, float hi) {
 // bf16 tanh): |x| < 2^-5 is a fixed point of T (tanh(x)/x > 1 - 2^-11.6 never crosses half an
 // ulp), |x| >= 4 maps like 4 (T(x) = +-1), NaN stays NaN, and the 7 binades [2^-5, 4) (896
 // entries) are tabulated; T is odd.  Branch-free: the clamped slot is always read.
+// One unsigned compare covers both pass-through cases: u = a - 2^-5's pattern wraps around for
+// a < 2^-5 and exceeds 0x7f80 - (122 << 7) only for NaN.
 __device__ __forceinline__ uint32_t TanhRunLookup(uint32_t h, const uint16_t* tab) {
-  const uint32_t a = h & 0x7fffu, s = h & 0x8000u;
-  const int idx = min(max(static_cast<int>(a) - (122 << 7), 0), kTanhRunEntries - 1);
-  const uint32_t t = tab[idx];
-  uint32_t r = a < (122u << 7) ? a : t;
-  r = a > 0x7f80u ? a : r;  // NaN stays NaN
-  return s | r;
+  const uint32_t a = h & 0x7fffu;
+  const uint32_t u = a - (122u << 7);
+  const uint32_t t = tab[min(u, static_cast<uint32_t>(kTanhRunEntries - 1))];
+  return (h & 0x8000u) | (u > 0x7f80u - (122u << 7) ? a : t);
 }
 
 // bf16 chain over P packed bf16x2 registers (2P elements).  tanh runs (tables in shared memory,

@@ -73,6 +73,9 @@ def main():
     ap.add_argument("--launches", default=None)
     ap.add_argument("--traffic-key", action="append", default=[],
                     help="KEY=REPNAME[:INDEX]: write DRAM bytes of that launch into ncu_traffic.json")
+    ap.add_argument("--traffic-avg", action="append", default=[],
+                    help="KEY=REPNAME:SUBSTRING: mean DRAM bytes per launch over that report's "
+                         "launches whose kernel name contains SUBSTRING")
     a = ap.parse_args()
     lines = [f"# ncu summary ({a.round})", "",
              "Captured with `ncu --set full --clock-control none --import-source on` on one B200 "
@@ -109,6 +112,11 @@ def main():
         rep, _, idx = rest.partition(":")
         d = tables[rep][int(idx or 0)]
         traffic[key] = d.get("dram_read", 0) + d.get("dram_write", 0)
+    for spec in a.traffic_avg:
+        key, rest = spec.split("=")
+        rep, _, sub = rest.partition(":")
+        rows = [d for d in tables[rep] if sub in d["kernel"]]
+        traffic[key] = sum(d.get("dram_read", 0) + d.get("dram_write", 0) for d in rows) / max(len(rows), 1)
     with open(tpath, "w") as f:
         json.dump(traffic, f, indent=1, sort_keys=True)
     print("\n".join(lines))
