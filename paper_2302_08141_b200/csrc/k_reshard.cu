@@ -212,9 +212,12 @@ struct StagedDev {
   uint32_t L;       // elements per chunk
   uint32_t per;     // L / d
   uint32_t chunks;  // destination chunks
+  uint32_t cpb;     // chunks per block iteration
   PeerSync sync;
 };
 
+// A block iteration handles `cpb` consecutive chunks (cpb x L ~ 4096 elements), so short chunks
+// (L = 32..64 elements for stride-1 sources) still give every thread 16-byte work.
 template <typename T>
 __global__ void __launch_bounds__(256) PullStagedKernel(StagedDev a) {
   extern __shared__ __align__(16) unsigned char smem_stage[];
@@ -223,32 +226,42 @@ __global__ void __launch_bounds__(256) PullStagedKernel(StagedDev a) {
   constexpr int E = 16 / sizeof(T);  // elements per 16-byte vector
   const uint32_t d = a.dd.d;
   const uint32_t Lr = a.qsf.d * d;
-  for (uint32_t c0 = blockIdx.x; c0 < a.chunks; c0 += gridDim.x) {
-    const uint32_t chunk = Rotate(c0, a.coord * (a.chunks / d), a.chunks);
-    const uint32_t i0 = chunk * a.L;
-    uint32_t f0 = i0;
+  const uint32_t vper = a.per / E, vchunk_in = vper * d, vchunk_out = a.L / E;
+  const uint32_t rot = a.coord * (a.chunks / d);
+  auto chunk_base = [&](uint32_t chunk, uint32_t* i0) {  // dst offset, each member's local start
+    *i0 = chunk * a.L;
+    uint32_t f0 = *i0;
     if (a.to_shard) {
-      const uint32_t p = Div(a.qst, i0);
-      f0 = (p * d + a.coord) * a.qst.d + (i0 - p * a.qst.d);
+      const uint32_t p = Div(a.qst, *i0);
+      f0 = (p * d + a.coord) * a.qst.d + (*i0 - p * a.qst.d);
     }
-    const uint32_t base = (f0 / Lr) * a.qsf.d;  // each member's local start
-    const uint32_t vper = a.per / E;
-    for (uint32_t v = threadIdx.x; v < vper * d; v += blockDim.x) {
-      const uint32_t k = v / vper, j = v - k * vper;
-      reinterpret_cast<uint4*>(tile)[v] = reinterpret_cast<const uint4*>(a.src[k] + size_t(base) * sizeof(T))[j];
+    return (f0 / Lr) * a.qsf.d;
+  };
+  for (uint32_t g0 = blockIdx.x * a.cpb; g0 < a.chunks; g0 += gridDim.x * a.cpb) {
+    const uint32_t ng = min(a.cpb, a.chunks - g0);
+    for (uint32_t v = threadIdx.x; v < ng * vchunk_in; v += blockDim.x) {
+      const uint32_t cg = v / vchunk_in, rem = v - cg * vchunk_in;
+      const uint32_t k = rem / vper, j = rem - k * vper;
+      uint32_t i0;
+      const uint32_t base = chunk_base(Rotate(g0 + cg, rot, a.chunks), &i0);
+      reinterpret_cast<uint4*>(tile + cg * a.L)[k * vper + j] =
+          reinterpret_cast<const uint4*>(a.src[k] + size_t(base) * sizeof(T))[j];
     }
     __syncthreads();
-    for (uint32_t v = threadIdx.x; v < a.L / E; v += blockDim.x) {
+    for (uint32_t v = threadIdx.x; v < ng * vchunk_out; v += blockDim.x) {
+      const uint32_t cg = v / vchunk_out, vv = v - cg * vchunk_out;
+      const uint32_t chunk = Rotate(g0 + cg, rot, a.chunks);
+      const T* t = tile + cg * a.L;
       T out[E];
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const uint32_t i = v * E + e;         // offset in the chunk == offset from f0
+        const uint32_t i = vv * E + e;        // offset in the chunk == offset from f0
         const uint32_t q = Div(a.qsf, i);     // run index
         const uint32_t qd = Div(a.dd, q);
         const uint32_t r = q - qd * d;        // owner
-        out[e] = tile[r * a.per + qd * a.qsf.d + (i - q * a.qsf.d)];
+        out[e] = t[r * a.per + qd * a.qsf.d + (i - q * a.qsf.d)];
       }
-      reinterpret_cast<uint4*>(a.dst + size_t(i0) * sizeof(T))[v] = *reinterpret_cast<uint4*>(out);
+      reinterpret_cast<uint4*>(a.dst + size_t(chunk) * a.L * sizeof(T))[vv] = *reinterpret_cast<uint4*>(out);
     }
     __syncthreads();
   }
@@ -287,8 +300,10 @@ bool TryLaunchStaged(const PullArgs& a, cudaStream_t s) {
   sd.L = static_cast<uint32_t>(L);
   sd.per = static_cast<uint32_t>(L / d);
   sd.chunks = static_cast<uint32_t>(a.n_dst / L);
-  const int blocks = static_cast<int>(std::min<int64_t>(sd.chunks, a.max_blocks > 0 ? a.max_blocks : 148 * 6));
-  const size_t smem = static_cast<size_t>(L) * eb;
+  sd.cpb = static_cast<uint32_t>(std::max<int64_t>(1, 4096 / L));
+  const int64_t groups = (sd.chunks + sd.cpb - 1) / sd.cpb;
+  const int blocks = static_cast<int>(std::min<int64_t>(groups, a.max_blocks > 0 ? a.max_blocks : 148 * 6));
+  const size_t smem = static_cast<size_t>(sd.cpb) * L * eb;
   if (eb == 2) PullStagedKernel<uint16_t><<<blocks, 256, smem, s>>>(sd);
   else PullStagedKernel<uint32_t><<<blocks, 256, smem, s>>>(sd);
   RH_CUDA(cudaGetLastError());
