@@ -129,6 +129,22 @@ __global__ void __launch_bounds__(256) SplitReduceBf16(__nv_bfloat16* __restrict
   }
 }
 
+// The exact packed bf16 ops the lowering lets into a bf16 GEMM epilogue (executor.cpp: relu /
+// neg / identity; LaunchGemmTc rejects anything else).  Warp-uniform fn loop outside the
+// element loop: small code.
+__device__ __forceinline__ void EpiPackedBf16(const ChainArgs& epi, uint32_t (&p)[16]) {
+  for (int i = 0; i < epi.n_fn; ++i) {
+    const int fn = epi.fns[i];
+    if (fn == RH_FN_RELU) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) p[j] = ReluBf16x2(p[j]);
+    } else if (fn == RH_FN_NEG) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) p[j] ^= 0x80008000u;
+    }
+  }
+}
+
 template <int BN, bool kBKMajor, bool kAKMajor>
 struct TcCfg {
   static constexpr int kABytes = BM * BK * 2;
@@ -281,16 +297,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                                  __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
           continue;
         }
-        uint4 out[4];
-        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out);
+        // fp32 -> bf16 pairs (one cvt.rn.bf16x2 each), then the exact packed ops: the epilogue
+        // stays a few hundred instructions (a generic per-element chain inlined 32x made the
+        // kernel ~10k instructions and its first tile instruction-fetch-bound)
+        uint32_t p[16];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          float v = ApplyChainFns<true>(epi.fns, epi.n_fn, RoundBf16(__uint_as_float(r[j])));
-          o[j] = __float2bfloat16_rn(v);
-        }
+        for (int j = 0; j < 16; ++j) p[j] = PackBf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+        EpiPackedBf16(epi, p);
         uint4* dst = reinterpret_cast<uint4*>(crow + c * 32);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) dst[q] = out[q];
+        for (int q = 0; q < 4; ++q) dst[q] = make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
       }
       FenceBefore();
       __syncwarp();
@@ -786,6 +802,11 @@ void LaunchGemmTc(const GemmArgs& g, cudaStream_t s) {
     if (g.tb) LaunchTf32x3<true>(g, s);
     else LaunchTf32x3<false>(g, s);
     return;
+  }
+  for (int i = 0; i < g.epi.n_fn; ++i) {
+    const int fn = g.epi.fns[i];
+    if (fn != RH_FN_RELU && fn != RH_FN_NEG && fn != RH_FN_IDENTITY)
+      Fail("tcgen05 bf16 GEMM epilogue takes only relu / neg / identity", RH_ERR_UNSUPPORTED);
   }
   const int bn = PickBN(g);
   const int v = (bn == 256 ? 4 : 0) | (g.tb ? 2 : 0) | (g.ta ? 0 : 1);
