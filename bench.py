@@ -197,6 +197,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="keep every transition on the main stream")
     ap.add_argument("--simt", action="store_true", help="force the CUDA-core GEMM (comparison)")
+    ap.add_argument("--no-pdl", action="store_true", help="no programmatic dependent launch (A/B)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.dtype is None:
@@ -209,7 +210,7 @@ def main():
 
     from paper_2302_08141_b200 import dist as D
     from paper_2302_08141_b200 import runtime as rx
-    from paper_2302_08141_b200.abi import (RH_BF16, RH_F32, RH_FLAG_NO_OVERLAP, RH_FLAG_REDUCE_OUTPUTS,
+    from paper_2302_08141_b200.abi import (RH_BF16, RH_F32, RH_FLAG_NO_OVERLAP, RH_FLAG_NO_PDL, RH_FLAG_REDUCE_OUTPUTS,
                                            RH_FLAG_SIMT_GEMM, RH_FLAG_TRANSPORT_NCCL)
     from paper_2302_08141_b200.program import LoweredProgram
 
@@ -230,6 +231,8 @@ def main():
         flags |= RH_FLAG_REDUCE_OUTPUTS
     if args.no_overlap:
         flags |= RH_FLAG_NO_OVERLAP
+    if args.no_pdl:
+        flags |= RH_FLAG_NO_PDL
     with stdout_to_stderr():
         rt = D.make_runtime()
         mesh = rx.Mesh(rt, prog.mesh)
@@ -341,7 +344,7 @@ def main():
             "config": {"workload": wl["name"], "plan": pname, "mesh": prog.mesh,
                        "global_batch": tok, "seq_len": tok, "ops": len(prog.ops),
                        "parallelism": f"rhino-spmd mesh {prog.mesh}", "transport": args.transport,
-                       "overlap": not args.no_overlap,
+                       "overlap": not args.no_overlap, "pdl": not args.no_pdl,
                        "gemm": "simt" if args.simt else "tcgen05",
                        "outputs": "partial axes reduced, sharded axes kept" if reduce_outputs
                        else "materialized replicated",

@@ -114,6 +114,7 @@ typedef struct {
                                            sharded axes sharded (a training step's gradients) */
 #define RH_FLAG_NO_OVERLAP 0x100u       /* dist: keep every transition on the main stream (no
                                            side-stream overlap of off-critical-path transitions) */
+#define RH_FLAG_NO_PDL 0x200u          /* no programmatic dependent launch between compute kernels */
 #define RH_FLAG_KEEP_ALL 0x40u          /* give every intermediate its own buffer (no arena reuse)
                                            so rh_program_read_* can read any op after a run */
 

@@ -30,6 +30,7 @@ RH_FLAG_NO_GRAPH = 0x20
 RH_FLAG_KEEP_ALL = 0x40
 RH_FLAG_REDUCE_OUTPUTS = 0x80
 RH_FLAG_NO_OVERLAP = 0x100
+RH_FLAG_NO_PDL = 0x200
 
 
 class RhSpec(ctypes.Structure):

@@ -20,6 +20,14 @@ void LowerProgram(rh_program* p);
 
 using rh::Fail;
 
+namespace rh {
+namespace {
+thread_local bool g_pdl = false;
+}
+void SetPdl(bool on) { g_pdl = on; }
+bool PdlEnabled() { return g_pdl; }
+}  // namespace rh
+
 namespace {
 
 thread_local std::string g_err;
@@ -154,6 +162,7 @@ int64_t RunOnce(rh_program* p, std::vector<cudaEvent_t>* prof) {
     ++launches;
   }
   const size_t n = p->steps.size();
+  bool prev_kernel = false;  // the previous main-stream step was a compute kernel step
   for (size_t si = 0; si < n; ++si) {
     rh::Step& st = p->steps[si];
     if (prof) RH_CUDA(cudaEventRecordWithFlags((*prof)[si], main, cudaEventRecordExternal));
@@ -172,10 +181,22 @@ int64_t RunOnce(rh_program* p, std::vector<cudaEvent_t>* prof) {
       continue;
     }
     if (st.p2p && st.sync_slot < 0) GroupSync(p, st.axis);
-    for (int li = 0; li < rt->n_local(); ++li) {
-      if (multi_dev) RH_CUDA(cudaSetDevice(rt->device_of(li)));
-      launches += st.run(li, rt->stream_of(li));
+    // PDL (launch.cuh) only between compute kernels: never after a transition (pull kernels
+    // spin on peers) nor after a cross-stream join or a profiling event
+    const bool pdl = !(p->flags & RH_FLAG_NO_PDL) && !prof && prev_kernel && p->joins_at[si].empty() &&
+                     st.kind == rh::Step::kKernel;
+    rh::SetPdl(pdl);
+    try {
+      for (int li = 0; li < rt->n_local(); ++li) {
+        if (multi_dev) RH_CUDA(cudaSetDevice(rt->device_of(li)));
+        launches += st.run(li, rt->stream_of(li));
+      }
+    } catch (...) {
+      rh::SetPdl(false);
+      throw;
     }
+    rh::SetPdl(false);
+    prev_kernel = st.kind == rh::Step::kKernel;
     if (st.p2p && st.post_sync) GroupSync(p, st.axis);
   }
   for (const auto& st : p->steps)  // join what no later step waited for

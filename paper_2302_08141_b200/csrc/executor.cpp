@@ -751,6 +751,19 @@ class Lowerer {
     return c;
   }
 
+  // Arena offset of the tanh ladder table for these cumulative powers (TanhLadderTable).
+  size_t LadderTable(const std::vector<int>& powers) {
+    auto it = ladder_tables_.find(powers);
+    if (it != ladder_tables_.end()) return it->second;
+    std::vector<uint16_t> tab(static_cast<size_t>(kTanhRunEntries) * kLadderWidth);
+    TanhLadderTable(powers.data(), static_cast<int>(powers.size()), tab.data());
+    const size_t off = Alloc(tab.size() * 2);
+    p_->uploads.emplace_back(off, std::vector<char>(reinterpret_cast<char*>(tab.data()),
+                                                    reinterpret_cast<char*>(tab.data()) + tab.size() * 2));
+    ladder_tables_[powers] = off;
+    return off;
+  }
+
   // Arena offset of the T^k table (uploaded to every rank's arena after allocation).
   size_t TanhTable(int k) {
     auto it = tanh_tables_.find(k);
@@ -932,6 +945,38 @@ class Lowerer {
       }
     }
     if (static_cast<int>(code.size()) > kMaxEwCode) Fail("internal: elementwise chain code too long");
+    // tanh ladder (bf16): the maximal suffix of tanh runs and stores, from its first tanh run
+    // on (stores before it belong to the prefix), with >= 3 stores -> one ladder-table row per
+    // element (EwArgs::lad_*).  The full code stays for the scalar tail.
+    a.lad_pc = static_cast<int32_t>(code.size());
+    static const bool no_ladder = getenv("RH_NO_LADDER") != nullptr;  // A/B knob (profiles/)
+    if (bf16 && !no_ladder) {
+      std::map<int, int> k_of_slot;
+      for (auto& kv : table_of) k_of_slot[kv.second] = kv.first;
+      size_t q = code.size();
+      while (q > 0) {
+        const int op = code[q - 1] & 0xff, arg = code[q - 1] >> 8;
+        if (op == kEwStore || op == kEwKeep || (op == kEwUnary && arg >= kFnTanhRun)) --q;
+        else break;
+      }
+      while (q < code.size() && (code[q] & 0xff) != kEwUnary) ++q;
+      std::vector<int> powers, outs;
+      int cum = 0;
+      for (size_t z = q; z < code.size(); ++z) {
+        const int op = code[z] & 0xff, arg = code[z] >> 8;
+        if (op == kEwUnary) cum += k_of_slot.at(arg - kFnTanhRun);
+        else if (op == kEwStore) {
+          powers.push_back(cum);
+          outs.push_back(arg);
+        }
+      }
+      if (q > 0 && powers.size() >= 3 && powers.size() <= static_cast<size_t>(kLadderWidth)) {
+        a.lad_pc = static_cast<int32_t>(q);
+        a.lad_n = static_cast<int32_t>(powers.size());
+        std::copy(outs.begin(), outs.end(), a.lad_out);
+        a.lad_off = LadderTable(powers);
+      }
+    }
     a.n_code = static_cast<int32_t>(code.size());
     a.n_in = static_cast<int32_t>(in_t.size());
     std::copy(code.begin(), code.end(), a.code);
@@ -941,7 +986,7 @@ class Lowerer {
     st.launches = 1;
     st.name = "ew_chain " + OpName(h) + ".." + OpName(c.members.back()) + " (" +
               std::to_string(c.members.size()) + " ops, " + std::to_string(in_t.size()) + " in, " +
-              std::to_string(out_t.size()) + " out)";
+              std::to_string(out_t.size()) + " out)" + (a.lad_n ? " [ladder]" : "");
     for (int t : in_t) st.alg_bytes += static_cast<double>(P->tensors[t].bytes);
     for (int t : out_t) st.alg_bytes += static_cast<double>(P->tensors[t].bytes);
     const int first = rt_->first_rank;
@@ -952,6 +997,7 @@ class Lowerer {
       for (size_t k = 0; k < out_t.size(); ++k) x.out[k] = P->Ptr(P->tensors[out_t[k]], r);
       for (int t = 0; t < x.n_tab; ++t)
         x.tab[t] = reinterpret_cast<const uint16_t*>(P->peer_base[r] + x.tab_off[t]);
+      if (x.lad_n) x.lad = reinterpret_cast<const uint4*>(P->peer_base[r] + x.lad_off);
       LaunchEwProg(x, dtype, s);
       return 1;
     };
@@ -1313,6 +1359,7 @@ class Lowerer {
   std::vector<bool> absorbed_;
   std::vector<std::vector<int>> chain_;
   std::map<int, size_t> tanh_tables_;
+  std::map<std::vector<int>, size_t> ladder_tables_;
   std::vector<int> remote_read_;  // tensors read by peers (transition sources)
   std::vector<EwPlan> ew_;
   std::vector<int> ew_of_;  // op -> elementwise chain id (-1: none)

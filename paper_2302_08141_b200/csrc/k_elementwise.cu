@@ -12,6 +12,7 @@
 #include <cstring>
 
 #include "kernels.h"
+#include "launch.cuh"
 #include "unary.cuh"
 
 namespace rh {
@@ -77,6 +78,21 @@ void TanhRunTable(int k, uint16_t* out) {
   }
 }
 
+void TanhLadderTable(const int* powers, int n, uint16_t* out) {
+  for (int i = 0; i < kTanhRunEntries; ++i) {
+    uint16_t h = i < 896 ? static_cast<uint16_t>((122u << 7) + i) : static_cast<uint16_t>(129u << 7);
+    int done = 0;
+    for (int s = 0; s < kLadderWidth; ++s) {
+      if (s < n) {
+        for (; done < powers[s]; ++done) h = TanhBf16(h);
+        out[i * kLadderWidth + s] = h;
+      } else {
+        out[i * kLadderWidth + s] = 0;
+      }
+    }
+  }
+}
+
 namespace {
 
 // 16-byte packets: 4 fp32 or 8 bf16.
@@ -130,6 +146,7 @@ __device__ __forceinline__ void StoreScalar(void* p, int64_t i, float x) {
 template <bool kBf16>
 __global__ void __launch_bounds__(256) UnaryChainKernel(void* out, const void* in, int64_t n,
                                                         ChainArgs c) {
+  PdlTrigger();
   constexpr int E = Pack<kBf16>::E;
   __shared__ uint16_t tab_s[kBf16 ? kMaxTanhRuns * kTanhRunEntries : 1];
   const uint16_t* tab = nullptr;
@@ -137,6 +154,7 @@ __global__ void __launch_bounds__(256) UnaryChainKernel(void* out, const void* i
     LoadRunTables(c, tab_s);
     tab = tab_s;
   }
+  PdlWait();  // the tables are program constants; inputs come from the previous kernel
   const int64_t nv = n / E;
   const int64_t npair = nv / 2;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -173,6 +191,7 @@ __global__ void __launch_bounds__(256) UnaryChainKernel(void* out, const void* i
 template <bool kBf16>
 __global__ void __launch_bounds__(256) BinaryKernel(void* out, const void* a, const void* b,
                                                     int64_t n, bool mul, ChainArgs c) {
+  PdlTrigger();
   constexpr int E = Pack<kBf16>::E;
   __shared__ uint16_t tab_s[kBf16 ? kMaxTanhRuns * kTanhRunEntries : 1];
   const uint16_t* tab = nullptr;
@@ -180,6 +199,7 @@ __global__ void __launch_bounds__(256) BinaryKernel(void* out, const void* a, co
     LoadRunTables(c, tab_s);
     tab = tab_s;
   }
+  PdlWait();  // the tables are program constants; inputs come from the previous kernel
   const int64_t nv = n / E;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nv; i += stride) {
@@ -249,13 +269,16 @@ __device__ __forceinline__ uint32_t TanhRunLookup2(uint32_t p, const uint16_t* t
 }
 
 template <bool kBf16>
-__device__ __forceinline__ void EwRunVec(const EwArgs& a, int64_t i, const uint16_t* tabs) {
+__device__ __forceinline__ void EwRunVec(const EwArgs& a, int64_t i, const uint16_t* tabs, int pc_end,
+                                         uint32_t (&acc)[4]) {
   uint4 raw[kMaxEwIn];
 #pragma unroll
   for (int k = 0; k < kMaxEwIn; ++k)
     if (k < a.n_in) raw[k] = reinterpret_cast<const uint4*>(a.in[k])[i];
-  uint32_t acc[4] = {0, 0, 0, 0}, keep[4] = {0, 0, 0, 0};
-  for (int pc = 0; pc < a.n_code; ++pc) {
+  uint32_t keep[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) acc[e] = 0;
+  for (int pc = 0; pc < pc_end; ++pc) {
     const int ins = a.code[pc], op = ins & 0xff, arg = ins >> 8;
     switch (op) {
       case kEwLoad: {
@@ -376,23 +399,86 @@ __device__ __forceinline__ void EwRunScalar(const EwArgs& a, int64_t i, const ui
 
 template <bool kBf16>
 __global__ void __launch_bounds__(256) EwProgKernel(const __grid_constant__ EwArgs a) {
+  PdlTrigger();
   __shared__ uint16_t tab_s[kBf16 ? kMaxTanhRuns * kTanhRunEntries : 1];
   if constexpr (kBf16) {
     for (int t = 0; t < a.n_tab; ++t)
       for (int i = threadIdx.x; i < kTanhRunEntries; i += blockDim.x) tab_s[t * kTanhRunEntries + i] = a.tab[t][i];
     __syncthreads();
   }
+  PdlWait();
   constexpr int E = kBf16 ? 8 : 4;
   const int64_t nv = a.n / E;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nv; i += stride)
-    EwRunVec<kBf16>(a, i, tab_s);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nv; i += stride) {
+    uint32_t acc[4];
+    EwRunVec<kBf16>(a, i, tab_s, a.n_code, acc);
+  }
   for (int64_t i = nv * E + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.n; i += stride)
     EwRunScalar<kBf16>(a, i, tab_s);
 }
 
+// bf16 chain program with a tanh ladder suffix (EwArgs::lad_*): the interpreter runs the
+// prefix, then every element's lad_n outputs come from its ladder row (2 x 16-byte shared
+// loads) and are re-packed per output with byte permutes: ~30 instructions per element for a
+// 12-store chain instead of ~20 per op and element.  |x| < 2^-5 and NaN pass through every
+// T^c unchanged; T is odd, so the sign is OR-ed back.
+__device__ __forceinline__ uint32_t U32Of(const uint4 (&r)[2], int w) {
+  const uint4 q = r[w >> 2];
+  return (w & 3) == 0 ? q.x : (w & 3) == 1 ? q.y : (w & 3) == 2 ? q.z : q.w;
+}
+
+__global__ void __launch_bounds__(256, 2) EwLadderKernel(const __grid_constant__ EwArgs a) {
+  PdlTrigger();
+  extern __shared__ uint4 lad_s[];  // kTanhRunEntries rows x 2 uint4
+  __shared__ uint16_t tab_s[kMaxTanhRuns * kTanhRunEntries];
+  for (int t = 0; t < a.n_tab; ++t)
+    for (int i = threadIdx.x; i < kTanhRunEntries; i += blockDim.x) tab_s[t * kTanhRunEntries + i] = a.tab[t][i];
+  for (int i = threadIdx.x; i < kTanhRunEntries * 2; i += blockDim.x) lad_s[i] = a.lad[i];
+  __syncthreads();
+  PdlWait();
+  constexpr uint32_t kLo = 122u << 7, kSpan = 0x7f80u - (122u << 7), kLast = kTanhRunEntries - 1;
+  const int64_t nv = a.n / 8;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nv; i += stride) {
+    uint32_t acc[4];
+    EwRunVec<true>(a, i, tab_s, a.lad_pc, acc);
+    uint4 r[8][2];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t pr = acc[e >> 1];
+      const uint32_t ab = ((e & 1) ? (pr >> 16) : pr) & 0x7fffu;
+      const uint32_t u = ab - kLo;
+      const uint32_t row = min(u, kLast);
+      r[e][0] = lad_s[2 * row];
+      r[e][1] = lad_s[2 * row + 1];
+      if (u > kSpan) {
+        const uint32_t rep = ab | (ab << 16);
+        r[e][0] = r[e][1] = make_uint4(rep, rep, rep, rep);
+      }
+    }
+    uint32_t sg[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sg[q] = acc[q] & 0x80008000u;
+#pragma unroll
+    for (int s = 0; s < kLadderWidth; ++s) {
+      if (s >= a.lad_n) break;
+      const uint32_t sel = (s & 1) ? 0x7632u : 0x5410u;
+      uint32_t p[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        p[q] = __byte_perm(U32Of(r[2 * q], s >> 1), U32Of(r[2 * q + 1], s >> 1), sel) | sg[q];
+      reinterpret_cast<uint4*>(a.out[a.lad_out[s]])[i] = make_uint4(p[0], p[1], p[2], p[3]);
+    }
+  }
+  for (int64_t i = nv * 8 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.n; i += stride)
+    EwRunScalar<true>(a, i, tab_s);
+}
+
 template <bool kBf16>
 __global__ void __launch_bounds__(256) SoftmaxRowsKernel(void* out, const void* in, int64_t cols) {
+  PdlTrigger();
+  PdlWait();
   const int64_t row = blockIdx.x;
   const int64_t base = row * cols;
   __shared__ float red[32];
@@ -430,6 +516,8 @@ __global__ void __launch_bounds__(256) SoftmaxRowsKernel(void* out, const void* 
 template <bool kBf16>
 __global__ void __launch_bounds__(256) ReduceColsKernel(void* out, const void* in, int64_t outer,
                                                         int64_t e, int64_t inner) {
+  PdlTrigger();
+  PdlWait();
   const int64_t n = outer * inner;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n;
        t += int64_t(gridDim.x) * blockDim.x) {
@@ -445,6 +533,8 @@ __global__ void __launch_bounds__(256) ReduceColsKernel(void* out, const void* i
 template <bool kBf16>
 __global__ void __launch_bounds__(256) ReduceRowsKernel(void* out, const void* in, int64_t rows,
                                                         int64_t e) {
+  PdlTrigger();
+  PdlWait();
   const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows) return;
@@ -457,6 +547,8 @@ __global__ void __launch_bounds__(256) ReduceRowsKernel(void* out, const void* i
 // 2-D transpose [R,C] -> [C,R] through a padded shared-memory tile (coalesced both sides).
 template <typename T>
 __global__ void __launch_bounds__(256) Transpose2DKernel(T* out, const T* in, int64_t R, int64_t C) {
+  PdlTrigger();
+  PdlWait();
   __shared__ T tile[32][33];
   const int64_t r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
   for (int j = threadIdx.y; j < 32; j += 8) {
@@ -478,6 +570,8 @@ struct PermDev {
 
 template <typename T>
 __global__ void TransposeNDKernel(T* out, const T* in, PermDev p, int64_t n) {
+  PdlTrigger();
+  PdlWait();
   for (int64_t f = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; f < n;
        f += int64_t(gridDim.x) * blockDim.x) {
     int64_t t = f, src = 0;
@@ -492,6 +586,8 @@ __global__ void TransposeNDKernel(T* out, const T* in, PermDev p, int64_t n) {
 
 template <typename T>
 __global__ void BroadcastKernel(T* out, const T* in, int64_t n_out, int64_t n_in) {
+  PdlTrigger();
+  PdlWait();
   for (int64_t f = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; f < n_out;
        f += int64_t(gridDim.x) * blockDim.x)
     out[f] = in[f % n_in];
@@ -500,6 +596,8 @@ __global__ void BroadcastKernel(T* out, const T* in, int64_t n_out, int64_t n_in
 template <typename T>
 __global__ void ConcatPieceKernel(T* out, const T* in, int64_t outer, int64_t row, int64_t orow,
                                   int64_t off) {
+  PdlTrigger();
+  PdlWait();
   const int64_t n = outer * row;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n;
        t += int64_t(gridDim.x) * blockDim.x) {
@@ -519,9 +617,9 @@ void LaunchUnaryChain(void* out, const void* in, int64_t n, const ChainArgs& c, 
                       cudaStream_t s) {
   if (n == 0) return;
   if (dtype == RH_BF16) {
-    UnaryChainKernel<true><<<Blocks(n, 8), 256, 0, s>>>(out, in, n, c);
+    LaunchPdl(UnaryChainKernel<true>, Blocks(n, 8), 256, 0, s, out, in, n, c);
   } else {
-    UnaryChainKernel<false><<<Blocks(n, 4), 256, 0, s>>>(out, in, n, c);
+    LaunchPdl(UnaryChainKernel<false>, Blocks(n, 4), 256, 0, s, out, in, n, c);
   }
   RH_CUDA(cudaGetLastError());
 }
@@ -531,19 +629,31 @@ void LaunchSoftmaxRows(void* out, const void* in, int64_t rows, int64_t cols, in
   if (rows == 0) return;
   if (rows > 0x7fffffff) Fail("softmax: too many rows");
   if (dtype == RH_BF16) {
-    SoftmaxRowsKernel<true><<<static_cast<unsigned>(rows), 256, 0, s>>>(out, in, cols);
+    LaunchPdl(SoftmaxRowsKernel<true>, static_cast<unsigned>(rows), 256, 0, s, out, in, cols);
   } else {
-    SoftmaxRowsKernel<false><<<static_cast<unsigned>(rows), 256, 0, s>>>(out, in, cols);
+    LaunchPdl(SoftmaxRowsKernel<false>, static_cast<unsigned>(rows), 256, 0, s, out, in, cols);
   }
   RH_CUDA(cudaGetLastError());
 }
 
 void LaunchEwProg(const EwArgs& a, int dtype, cudaStream_t s) {
   if (a.n == 0) return;
-  if (dtype == RH_BF16) {
-    EwProgKernel<true><<<Blocks(a.n, 8), 256, 0, s>>>(a);
+  if (dtype == RH_BF16 && a.lad_n > 0) {
+    constexpr int kLadSmem = kTanhRunEntries * kLadderWidth * 2;
+    static bool attr[64] = {};
+    int dev = 0;
+    RH_CUDA(cudaGetDevice(&dev));
+    if (dev < 64 && !attr[dev]) {
+      RH_CUDA(cudaFuncSetAttribute(EwLadderKernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLadSmem));
+      attr[dev] = true;
+    }
+    // persistent-ish grid: each block stages the 28 KB ladder table once
+    const int blocks = std::min(Blocks(a.n, 8), 148 * 4);
+    LaunchPdl(EwLadderKernel, blocks, 256, kLadSmem, s, a);
+  } else if (dtype == RH_BF16) {
+    LaunchPdl(EwProgKernel<true>, Blocks(a.n, 8), 256, 0, s, a);
   } else {
-    EwProgKernel<false><<<Blocks(a.n, 4), 256, 0, s>>>(a);
+    LaunchPdl(EwProgKernel<false>, Blocks(a.n, 4), 256, 0, s, a);
   }
   RH_CUDA(cudaGetLastError());
 }
@@ -552,9 +662,9 @@ void LaunchBinary(void* out, const void* a, const void* b, int64_t n, bool mul, 
                   int dtype, cudaStream_t s) {
   if (n == 0) return;
   if (dtype == RH_BF16) {
-    BinaryKernel<true><<<Blocks(n, 8), 256, 0, s>>>(out, a, b, n, mul, c);
+    LaunchPdl(BinaryKernel<true>, Blocks(n, 8), 256, 0, s, out, a, b, n, mul, c);
   } else {
-    BinaryKernel<false><<<Blocks(n, 4), 256, 0, s>>>(out, a, b, n, mul, c);
+    LaunchPdl(BinaryKernel<false>, Blocks(n, 4), 256, 0, s, out, a, b, n, mul, c);
   }
   RH_CUDA(cudaGetLastError());
 }
@@ -566,11 +676,11 @@ void LaunchReduceSum(void* out, const void* in, int64_t outer, int64_t e, int64_
   if (inner == 1) {
     const int64_t threads = outer * 32;
     const int blocks = static_cast<int>((threads + 255) / 256);
-    if (bf) ReduceRowsKernel<true><<<blocks, 256, 0, s>>>(out, in, outer, e);
-    else ReduceRowsKernel<false><<<blocks, 256, 0, s>>>(out, in, outer, e);
+    if (bf) LaunchPdl(ReduceRowsKernel<true>, blocks, 256, 0, s, out, in, outer, e);
+    else LaunchPdl(ReduceRowsKernel<false>, blocks, 256, 0, s, out, in, outer, e);
   } else {
-    if (bf) ReduceColsKernel<true><<<Blocks(outer * inner), 256, 0, s>>>(out, in, outer, e, inner);
-    else ReduceColsKernel<false><<<Blocks(outer * inner), 256, 0, s>>>(out, in, outer, e, inner);
+    if (bf) LaunchPdl(ReduceColsKernel<true>, Blocks(outer * inner), 256, 0, s, out, in, outer, e, inner);
+    else LaunchPdl(ReduceColsKernel<false>, Blocks(outer * inner), 256, 0, s, out, in, outer, e, inner);
   }
   RH_CUDA(cudaGetLastError());
 }
@@ -585,8 +695,8 @@ void LaunchTranspose(void* out, const void* in, int nd, const int64_t* in_dims, 
     const int64_t R = in_dims[0], C = in_dims[1];
     dim3 grid(static_cast<unsigned>((C + 31) / 32), static_cast<unsigned>((R + 31) / 32));
     dim3 block(32, 8);
-    if (bf) Transpose2DKernel<<<grid, block, 0, s>>>(static_cast<uint16_t*>(out), static_cast<const uint16_t*>(in), R, C);
-    else Transpose2DKernel<<<grid, block, 0, s>>>(static_cast<uint32_t*>(out), static_cast<const uint32_t*>(in), R, C);
+    if (bf) LaunchPdl(Transpose2DKernel<uint16_t>, grid, block, 0, s, static_cast<uint16_t*>(out), static_cast<const uint16_t*>(in), R, C);
+    else LaunchPdl(Transpose2DKernel<uint32_t>, grid, block, 0, s, static_cast<uint32_t*>(out), static_cast<const uint32_t*>(in), R, C);
   } else {
     PermDev p{};
     p.nd = nd;
@@ -600,8 +710,8 @@ void LaunchTranspose(void* out, const void* in, int nd, const int64_t* in_dims, 
       p.odims[i] = in_dims[perm[i]];
       p.istride_of_out[i] = istride[perm[i]];
     }
-    if (bf) TransposeNDKernel<<<Blocks(n), 256, 0, s>>>(static_cast<uint16_t*>(out), static_cast<const uint16_t*>(in), p, n);
-    else TransposeNDKernel<<<Blocks(n), 256, 0, s>>>(static_cast<uint32_t*>(out), static_cast<const uint32_t*>(in), p, n);
+    if (bf) LaunchPdl(TransposeNDKernel<uint16_t>, Blocks(n), 256, 0, s, static_cast<uint16_t*>(out), static_cast<const uint16_t*>(in), p, n);
+    else LaunchPdl(TransposeNDKernel<uint32_t>, Blocks(n), 256, 0, s, static_cast<uint32_t*>(out), static_cast<const uint32_t*>(in), p, n);
   }
   RH_CUDA(cudaGetLastError());
 }
@@ -609,16 +719,16 @@ void LaunchTranspose(void* out, const void* in, int nd, const int64_t* in_dims, 
 void LaunchBroadcast(void* out, const void* in, int64_t n_out, int64_t n_in, int dtype,
                      cudaStream_t s) {
   if (n_out == 0) return;
-  if (dtype == RH_BF16) BroadcastKernel<<<Blocks(n_out), 256, 0, s>>>(static_cast<uint16_t*>(out), static_cast<const uint16_t*>(in), n_out, n_in);
-  else BroadcastKernel<<<Blocks(n_out), 256, 0, s>>>(static_cast<uint32_t*>(out), static_cast<const uint32_t*>(in), n_out, n_in);
+  if (dtype == RH_BF16) LaunchPdl(BroadcastKernel<uint16_t>, Blocks(n_out), 256, 0, s, static_cast<uint16_t*>(out), static_cast<const uint16_t*>(in), n_out, n_in);
+  else LaunchPdl(BroadcastKernel<uint32_t>, Blocks(n_out), 256, 0, s, static_cast<uint32_t*>(out), static_cast<const uint32_t*>(in), n_out, n_in);
   RH_CUDA(cudaGetLastError());
 }
 
 void LaunchConcatPiece(void* out, const void* in, int64_t outer, int64_t row, int64_t orow,
                        int64_t off, int dtype, cudaStream_t s) {
   if (outer * row == 0) return;
-  if (dtype == RH_BF16) ConcatPieceKernel<<<Blocks(outer * row), 256, 0, s>>>(static_cast<uint16_t*>(out), static_cast<const uint16_t*>(in), outer, row, orow, off);
-  else ConcatPieceKernel<<<Blocks(outer * row), 256, 0, s>>>(static_cast<uint32_t*>(out), static_cast<const uint32_t*>(in), outer, row, orow, off);
+  if (dtype == RH_BF16) LaunchPdl(ConcatPieceKernel<uint16_t>, Blocks(outer * row), 256, 0, s, static_cast<uint16_t*>(out), static_cast<const uint16_t*>(in), outer, row, orow, off);
+  else LaunchPdl(ConcatPieceKernel<uint32_t>, Blocks(outer * row), 256, 0, s, static_cast<uint32_t*>(out), static_cast<const uint32_t*>(in), outer, row, orow, off);
   RH_CUDA(cudaGetLastError());
 }
 

@@ -3,7 +3,10 @@
 // tcgen05 path is tested against and the path for shapes the tensor-core kernel does not tile.
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "kernels.h"
+#include "launch.cuh"
 #include "unary.cuh"
 
 namespace rh {
@@ -30,6 +33,8 @@ __global__ void __launch_bounds__(256) GemmSimtKernel(T* __restrict__ C, const T
                                                       const T* __restrict__ B, int64_t M,
                                                       int64_t N, int64_t K, ChainArgs epi,
                                                       int64_t kchunk, float* __restrict__ ws) {
+  PdlTrigger();
+  PdlWait();
   __shared__ __align__(16) float As[BK][BM];
   __shared__ __align__(16) float Bs[BK][BN];
   const int tid = threadIdx.x;
@@ -125,6 +130,8 @@ __global__ void __launch_bounds__(256) GemmSimtKernel(T* __restrict__ C, const T
 template <typename T>
 __global__ void __launch_bounds__(256) SplitReduceKernel(T* __restrict__ C, const float* __restrict__ ws,
                                                          int64_t n, int splits, ChainArgs epi) {
+  PdlTrigger();
+  PdlWait();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     float v = ws[i];
     for (int z = 1; z < splits; ++z) v = __fadd_rn(v, ws[int64_t(z) * n + i]);
@@ -157,15 +164,22 @@ int Dispatch(const GemmArgs& g, cudaStream_t s) {
   T* c = static_cast<T*>(g.c);
   const T* a = static_cast<const T*>(g.a);
   const T* b = static_cast<const T*>(g.b);
-  if (!g.ta && !g.tb) GemmSimtKernel<T, false, false><<<grid, 256, 0, s>>>(c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws);
-  else if (!g.ta && g.tb) GemmSimtKernel<T, false, true><<<grid, 256, 0, s>>>(c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws);
-  else if (g.ta && !g.tb) GemmSimtKernel<T, true, false><<<grid, 256, 0, s>>>(c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws);
-  else GemmSimtKernel<T, true, true><<<grid, 256, 0, s>>>(c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws);
+  if (!g.ta && !g.tb) LaunchPdl(GemmSimtKernel<T, false, false>, grid, 256, 0, s, c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws);
+  else if (!g.ta && g.tb) LaunchPdl(GemmSimtKernel<T, false, true>, grid, 256, 0, s, c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws);
+  else if (g.ta && !g.tb) LaunchPdl(GemmSimtKernel<T, true, false>, grid, 256, 0, s, c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws);
+  else LaunchPdl(GemmSimtKernel<T, true, true>, grid, 256, 0, s, c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws);
   if (!ws) return 1;
   const int64_t n = g.m * g.n;
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)));
-  SplitReduceKernel<T><<<blocks, 256, 0, s>>>(c, ws, n, z, g.epi);
+  LaunchPdl(SplitReduceKernel<T>, blocks, 256, 0, s, c, ws, n, z, g.epi);
   return 2;
+}
+
+__global__ void __launch_bounds__(256) ZeroWordsKernel(uint32_t* p, int64_t n) {
+  PdlTrigger();
+  PdlWait();
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = 0;
 }
 
 }  // namespace
@@ -177,8 +191,10 @@ size_t GemmSimtScratchBytes(const GemmArgs& g) {
 
 int LaunchGemmSimt(const GemmArgs& g, cudaStream_t s) {
   if (g.m == 0 || g.n == 0) return 0;
-  if (g.k == 0) {
-    RH_CUDA(cudaMemsetAsync(g.c, 0, g.m * g.n * ElemBytes(g.dtype), s));
+  if (g.k == 0) {  // empty contraction: C = 0 (a kernel, not a memset node: PDL edges link kernels)
+    const int64_t words = g.m * g.n * ElemBytes(g.dtype) / 4;
+    LaunchPdl(ZeroWordsKernel, static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((words + 255) / 256, 148 * 8))),
+              256, 0, s, static_cast<uint32_t*>(g.c), words);
     return 1;
   }
   if (g.m / BM >= 65535) Fail("gemm: M too large for the SIMT grid");

@@ -15,12 +15,14 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
 #include <tuple>
 
 #include "kernels.h"
+#include "launch.cuh"
 #include "unary.cuh"
 
 namespace rh {
@@ -112,6 +114,8 @@ __device__ __forceinline__ void TmemLd32(uint32_t taddr, uint32_t (&r)[32]) {
 // Split-K finish: sum the fp32 partials in split order, round to bf16, apply the chain.
 __global__ void __launch_bounds__(256) SplitReduceBf16(__nv_bfloat16* __restrict__ C, const float4* __restrict__ ws,
                                                        int64_t n4, int splits, ChainArgs epi) {
+  PdlTrigger();
+  PdlWait();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
     float4 v = ws[i];
     for (int z = 1; z < splits; ++z) {
@@ -168,6 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     GemmTcKernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                  __nv_bfloat16* __restrict__ C, int M, int N, int K, ChainArgs epi, int ksplit,
                  float* __restrict__ ws) {
+  PdlTrigger();
   // Work unit = (m tile, n tile, k split).  ksplit > 1 (few tiles: the sharded GEMMs at N >= 4)
   // writes fp32 partial tiles to ws[split][M][N]; SplitReduceBf16 finishes them.
   using Cfg = TcCfg<BN, kBKMajor, kAKMajor>;
@@ -205,6 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   FenceAfter();
   const uint32_t tmem = *tmem_slot;
+  PdlWait();  // prologue above overlaps the previous kernel's tail (launch.cuh)
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer ----------------
@@ -334,6 +340,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 __global__ void __launch_bounds__(256) SplitTf32Kernel(const float4* __restrict__ x, float4* __restrict__ hi,
                                                        float4* __restrict__ lo, int64_t n4) {
+  PdlTrigger();
+  PdlWait();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
     const float4 v = x[i];
     float4 h, l;
@@ -354,6 +362,8 @@ __global__ void __launch_bounds__(256) SplitTf32Kernel(const float4* __restrict_
 // so the MMA always reads K-major TF32 operands.
 __global__ void __launch_bounds__(256) SplitTransposeTf32Kernel(const float* __restrict__ b, float* __restrict__ hi_t,
                                                                 float* __restrict__ lo_t, int64_t K, int64_t N) {
+  PdlTrigger();
+  PdlWait();
   __shared__ float tile[32][33];
   const int64_t k0 = int64_t(blockIdx.y) * 32, n0 = int64_t(blockIdx.x) * 32;
   for (int j = threadIdx.y; j < 32; j += 8) tile[j][threadIdx.x] = b[(k0 + j) * N + n0 + threadIdx.x];
@@ -401,6 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     GemmTf32x3Kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                      const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
                      float* __restrict__ C, int M, int N, int K, ChainArgs epi) {
+  PdlTrigger();
   using Cfg = Tf32Cfg<BN, kBKMajor>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -433,6 +444,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   FenceAfter();
   const uint32_t tmem = *tmem_slot;
+  PdlWait();  // prologue above overlaps the previous kernel's tail (launch.cuh)
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer: A_hi, A_lo, B_hi, B_lo per stage
@@ -639,27 +651,41 @@ int NumSms() {
   return n;
 }
 
-// bf16 split-K factor: when the output tiles cannot fill the SMs (< 120 tiles), split K so that
-// work units reach ~2 waves while every split keeps >= 8 k-blocks (K >= 512).
+// Experiment knobs (profiles/gemm_shapes.py A/B runs): RH_GEMM_BN forces the tile width,
+// RH_GEMM_MAX_SPLIT caps split-K.  Unset in production.
+int EnvInt(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+// Tile width: BN = 256 halves the A-operand shared-memory traffic per flop, so it is used
+// whenever it yields >= 96 tiles; else BN = 128 (twice the tiles); split-K only when even
+// 128-wide tiles cannot fill the SMs.  Measured (profiles/gemm_shapes.py, B200): 2048x1024
+// output, K = 4096: BN=256 + split-K 2 28.3 us, BN=128 21.0 us; 2048x2048 output, K = 1024:
+// 24.3 vs 12.3 us; the fp32 partials' round trip costs more than the idle SMs it fills.
+int PickBN(const GemmArgs& g) {
+  if (g.dtype == RH_F32) return g.n % 128 == 0 ? 128 : 0;
+  static const int force = EnvInt("RH_GEMM_BN", 0);
+  if (force && g.n % force == 0) return force;
+  const int64_t mt = g.m / BM;
+  if (g.n % 256 == 0 && mt * (g.n / 256) >= 96) return 256;
+  if (g.n % 128 == 0) return 128;
+  return 0;
+}
+
+// bf16 split-K factor: when the output tiles cannot fill the SMs (< 96 tiles), split K so that
+// work units reach ~1-2 waves while every split keeps >= 8 k-blocks (K >= 512).
 int KSplit(const GemmArgs& g, int bn) {
   if (g.dtype != RH_BF16) return 1;
+  static const int max_split = EnvInt("RH_GEMM_MAX_SPLIT", 8);
   const int64_t tiles = (g.m / BM) * (g.n / bn), kb = g.k / BK;
-  if (tiles >= 120) return 1;
+  if (tiles >= 96) return 1;
   int best = 1;
-  for (int ks = 2; ks <= 8; ks *= 2) {
+  for (int ks = 2; ks <= max_split; ks *= 2) {
     if (kb % ks || kb / ks < 8 || tiles * (ks / 2) > 148) break;
     best = ks;
   }
   return best;
-}
-
-int PickBN(const GemmArgs& g) {
-  if (g.dtype == RH_F32) return g.n % 128 == 0 ? 128 : 0;
-  // BN = 256 halves the A-operand shared-memory traffic per flop (128 x 128 tiles are
-  // smem-bandwidth-bound at ~50% of peak); too few tiles are filled by split-K instead.
-  if (g.n % 256 == 0 && (g.m / BM) * (g.n / 256) * KSplit(g, 256) >= 96) return 256;
-  if (g.n % 128 == 0) return 128;
-  return 0;
 }
 
 template <int BN, bool kBK, bool kAK>
@@ -678,14 +704,14 @@ void Launch(const GemmArgs& g, cudaStream_t s) {
   const int tiles = static_cast<int>((g.m / BM) * (g.n / BN)) * ks;
   const int grid = std::min(tiles, NumSms());
   float* ws = ks > 1 ? static_cast<float*>(g.scratch) : nullptr;
-  GemmTcKernel<BN, kBK, kAK><<<grid, kThreads, Cfg::kSmem, s>>>(
+  LaunchPdl(GemmTcKernel<BN, kBK, kAK>, grid, kThreads, Cfg::kSmem, s, 
       mp.a, mp.b, static_cast<__nv_bfloat16*>(g.c), static_cast<int>(g.m), static_cast<int>(g.n),
       static_cast<int>(g.k), g.epi, ks, ws);
   RH_CUDA(cudaGetLastError());
   if (ws) {
     const int64_t n4 = g.m * g.n / 4;
     const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 148 * 8)));
-    SplitReduceBf16<<<blocks, 256, 0, s>>>(static_cast<__nv_bfloat16*>(g.c), reinterpret_cast<const float4*>(ws),
+    LaunchPdl(SplitReduceBf16, blocks, 256, 0, s, static_cast<__nv_bfloat16*>(g.c), reinterpret_cast<const float4*>(ws),
                                            n4, ks, g.epi);
     RH_CUDA(cudaGetLastError());
   }
@@ -715,19 +741,19 @@ void LaunchTf32x3(const GemmArgs& g, cudaStream_t s) {
   const int threads = 256;
   auto blocks = [](int64_t n4) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 148 * 8))); };
   if (!g.ta) {
-    SplitTf32Kernel<<<blocks(na / 4), threads, 0, s>>>(static_cast<const float4*>(g.a), reinterpret_cast<float4*>(a_hi),
+    LaunchPdl(SplitTf32Kernel, blocks(na / 4), threads, 0, s, static_cast<const float4*>(g.a), reinterpret_cast<float4*>(a_hi),
                                                        reinterpret_cast<float4*>(a_lo), na / 4);
   } else {  // [K,M] -> hi/lo of [M,K]
-    SplitTransposeTf32Kernel<<<dim3(static_cast<unsigned>(g.m / 32), static_cast<unsigned>(g.k / 32)),
-                               dim3(32, 8), 0, s>>>(static_cast<const float*>(g.a), a_hi, a_lo, g.k, g.m);
+    LaunchPdl(SplitTransposeTf32Kernel, dim3(static_cast<unsigned>(g.m / 32), static_cast<unsigned>(g.k / 32)),
+                               dim3(32, 8), 0, s, static_cast<const float*>(g.a), a_hi, a_lo, g.k, g.m);
   }
   if (kBK) {
-    SplitTf32Kernel<<<blocks(nb / 4), threads, 0, s>>>(static_cast<const float4*>(g.b),
+    LaunchPdl(SplitTf32Kernel, blocks(nb / 4), threads, 0, s, static_cast<const float4*>(g.b),
                                                        reinterpret_cast<float4*>(b_hi),
                                                        reinterpret_cast<float4*>(b_lo), nb / 4);
   } else {  // [K,N] -> hi/lo of [N,K]
-    SplitTransposeTf32Kernel<<<dim3(static_cast<unsigned>(g.n / 32), static_cast<unsigned>(g.k / 32)),
-                               dim3(32, 8), 0, s>>>(static_cast<const float*>(g.b), b_hi, b_lo, g.k, g.n);
+    LaunchPdl(SplitTransposeTf32Kernel, dim3(static_cast<unsigned>(g.n / 32), static_cast<unsigned>(g.k / 32)),
+                               dim3(32, 8), 0, s, static_cast<const float*>(g.b), b_hi, b_lo, g.k, g.n);
   }
   RH_CUDA(cudaGetLastError());
   static std::mutex mu;
@@ -750,7 +776,7 @@ void LaunchTf32x3(const GemmArgs& g, cudaStream_t s) {
   }
   const int tiles = static_cast<int>((g.m / BM) * (g.n / BN));
   const int grid = std::min(tiles, NumSms());
-  GemmTf32x3Kernel<BN, true><<<grid, kThreads, Cfg::kSmem, s>>>(
+  LaunchPdl(GemmTf32x3Kernel<BN, true>, grid, kThreads, Cfg::kSmem, s, 
       mp.a_hi, mp.a_lo, mp.b_hi, mp.b_lo, static_cast<float*>(g.c), static_cast<int>(g.m),
       static_cast<int>(g.n), static_cast<int>(g.k), g.epi);
   RH_CUDA(cudaGetLastError());

@@ -10,6 +10,11 @@ namespace rh {
 
 constexpr int kMaxGroup = 8;  // ranks per mesh-axis group (one B200 box)
 
+// Programmatic dependent launch for the next compute-kernel launches of this host thread
+// (launch.cuh; set per step by the executor's run loop).
+void SetPdl(bool on);
+bool PdlEnabled();
+
 // Unsigned 32-bit division by an invariant (Granlund & Montgomery 1994, Fig. 4.1): exact for
 // every 32-bit dividend.  Used for the block-cyclic index maps inside the resharding kernels.
 struct FastDiv {
@@ -117,7 +122,19 @@ struct EwArgs {
   uint64_t tab_off[kMaxTanhRuns];     // arena offsets (host side)
   const uint16_t* tab[kMaxTanhRuns];  // device pointers, patched per rank at launch
   int64_t n;
+  // tanh ladder (bf16): code[lad_pc..] is only tanh runs and stores.  Store s of the suffix
+  // holds T^{c_s}(x0) with x0 = acc at lad_pc, so the vector path reads all lad_n outputs of an
+  // element from one 32-byte row of the ladder table (TanhLadderTable) instead of walking the
+  // chain one lookup per op.  lad_n = 0: no ladder.
+  int32_t lad_pc, lad_n;
+  int32_t lad_out[kMaxEwOut];
+  uint64_t lad_off;  // arena offset (host side)
+  const uint4* lad;  // device pointer, patched per rank at launch
 };
+// Ladder rows: kTanhRunEntries rows x kLadderWidth u16; row r, column s = T^{powers[s]} of the
+// row's representative |x| (the TanhRunTable indexing).
+constexpr int kLadderWidth = 16;
+void TanhLadderTable(const int* powers, int n, uint16_t* out);
 void LaunchEwProg(const EwArgs& a, int dtype, cudaStream_t s);
 // out = a (+|*) b, then an optional unary chain (epilogue fusion).
 void LaunchBinary(void* out, const void* a, const void* b, int64_t n, bool mul, const ChainArgs& c,

@@ -124,6 +124,36 @@ def test_fusion_bit_exact(rx, name, dtype):
 
 
 @pytest.mark.parametrize("name", ["c5_gpt_small_d2", "c5_gpt_small_d4"])
+def test_ladder_values_bit_exact(rx, name):
+    """Every value a tanh-ladder chain stores (one table row per element instead of one lookup
+    per op) is bit-identical, on every rank, to the one-op-per-kernel schedule's."""
+    prog = LoweredProgram.load(name).with_dtype(RH_BF16)
+    bufs, names = {}, {}
+    for flags in (RH_FLAG_KEEP_ALL, RH_FLAG_KEEP_ALL | RH_FLAG_NO_FUSION):
+        rt, mesh, gp = load(rx, prog, flags)
+        try:
+            gp.init_synthetic(3)
+            gp.run(1)
+            names[flags] = [s["name"] for s in gp.steps()]
+            got = {}
+            for i in range(len(prog.ops)):
+                for r in range(prog.world):
+                    try:
+                        got[(i, r)] = gp.read_local(i, r)
+                    except Exception:  # not materialized in this schedule (fused away)
+                        pass
+            bufs[flags] = got
+        finally:
+            close(rt, mesh, gp)
+    assert any("[ladder]" in n for n in names[RH_FLAG_KEEP_ALL]), names[RH_FLAG_KEEP_ALL][:30]
+    fused, ref = bufs[RH_FLAG_KEEP_ALL], bufs[RH_FLAG_KEEP_ALL | RH_FLAG_NO_FUSION]
+    common = [k for k in fused if k in ref]
+    assert len(common) > len(prog.ops) // 2
+    for k in common:
+        np.testing.assert_array_equal(fused[k], ref[k], err_msg=f"{name}:{prog.ops[k[0]].id}@{k[1]}")
+
+
+@pytest.mark.parametrize("name", ["c5_gpt_small_d2", "c5_gpt_small_d4"])
 def test_reduce_outputs(rx, name):
     """RH_FLAG_REDUCE_OUTPUTS: a training step's outputs end with Partial axes reduced and sharded
     axes kept — same values as the replicated materialization, without the output all-gathers."""
