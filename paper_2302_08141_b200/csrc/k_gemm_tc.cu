@@ -331,6 +331,252 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------- bf16 GEMM on a CTA pair (tcgen05 cta_group::2) -------------------------
+// Two CTAs of a cluster (the two SMs of a TPC) compute one 256 x BN tile: each CTA stages its
+// own 128 rows of A and HALF of the BN columns of B, and the leader's single thread issues
+// tcgen05.mma.cta_group::2 (M = 256), which reads A from each CTA and B from both; each CTA's
+// TMEM receives its 128 rows.  Per SM and k-block the shared-memory operand traffic drops from
+// (128 + BN) x 64 to (128 + BN/2) x 64 elements for the same 128 x BN x 64 MMA work, which is what
+// lets 128-wide pair tiles (the small sharded GEMMs at N >= 4) run near the MMA rate.
+//   both CTAs, warp 0: TMA of own A half / B half into own smem; completion is counted on the
+//                      LEADER's full barrier (cp.async.bulk.tensor .cta_group::2);
+//   leader, warp 1:    MMA issuer; tcgen05.commit .multicast::cluster frees the stage in both
+//                      CTAs and signals both epilogues;
+//   both, warps 4-7:   epilogue of own TMEM rows; release the accumulator on the leader's
+//                      tempty barrier (8 arrivals: 4 warps x 2 CTAs).
+__device__ __forceinline__ uint32_t ClusterRank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t MapaShared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void ClusterSync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void MbarWaitCluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(SmemU32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void MbarArriveRemote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void TmaLoad2D2Sm(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                             int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          SmemU32(dst)),
+      "l"(map), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void MmaF16Pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void CommitPair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          SmemU32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+template <int BN, bool kBKMajor, bool kAKMajor>
+struct Tc2Cfg {
+  static constexpr int kABytes = BM * BK * 2;        // own 128 rows
+  static constexpr int kBBytes = (BN / 2) * BK * 2;  // own half of the columns
+  static constexpr int kStage = kABytes + kBBytes;
+  static constexpr int kStages = (192 * 1024) / kStage;  // 6 (BN 256) / 8 (BN 128)
+  static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kSmem = kStages * kStage + 1024 + 1024;
+  static constexpr uint32_t kIdesc = (1u << 4)                     // D = F32
+                                     | (1u << 7) | (1u << 10)      // A, B = BF16
+                                     | ((kAKMajor ? 0u : 1u) << 15) | ((kBKMajor ? 0u : 1u) << 16) |
+                                     (static_cast<uint32_t>(BN >> 3) << 17) |
+                                     (static_cast<uint32_t>((2 * BM) >> 4) << 24);  // M = 256
+};
+
+template <int BN, bool kBKMajor, bool kAKMajor>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    GemmTcPairKernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                     __nv_bfloat16* __restrict__ C, int M, int N, int K, ChainArgs epi, int ksplit,
+                     float* __restrict__ ws) {
+  PdlTrigger();
+  using Cfg = Tc2Cfg<BN, kBKMajor, kAKMajor>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStage);
+  uint64_t* empty = full + Cfg::kStages;
+  uint64_t* tfull = empty + Cfg::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = ClusterRank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int num_m = M / (2 * BM), num_n = N / BN, mn = num_m * num_n, tiles = mn * ksplit;
+  const int kblocks = K / BK / ksplit;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
+    for (int st = 0; st < Cfg::kStages; ++st) {
+      MbarInit(&full[st], 1);
+      MbarInit(&empty[st], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      MbarInit(&tfull[a], 1);
+      MbarInit(&tempty[a], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(SmemU32(tmem_slot)),
+                 "r"(Cfg::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  FenceBefore();
+  ClusterSync();  // barrier inits and TMEM allocation visible to both CTAs of the pair
+  FenceAfter();
+  const uint32_t tmem = *tmem_slot;
+  PdlWait();
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs) ----------------
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = pair; tile < tiles; tile += n_pairs) {
+        const int t = tile % mn, ks = tile / mn;
+        const int m_blk = t % num_m, n_blk = t / num_m;
+        const int m0 = m_blk * 2 * BM + static_cast<int>(rank) * BM;
+        const int n0 = n_blk * BN + static_cast<int>(rank) * (BN / 2);
+        for (int kb = ks * kblocks; kb < (ks + 1) * kblocks; ++kb) {
+          MbarWait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * Cfg::kStage;
+          uint8_t* sb = sa + Cfg::kABytes;
+          const uint32_t fb = MapaShared(SmemU32(&full[stage]), 0);
+          if (leader) MbarExpectTx(&full[stage], 2 * Cfg::kStage);
+          if constexpr (kAKMajor) {
+            TmaLoad2D2Sm(sa, &tma_a, fb, kb * BK, m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) TmaLoad2D2Sm(sa + j * (64 * BK * 2), &tma_a, fb, m0 + j * 64, kb * BK);
+          }
+          if constexpr (kBKMajor) {
+            TmaLoad2D2Sm(sb, &tma_b, fb, kb * BK, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 128; ++j) TmaLoad2D2Sm(sb + j * (64 * BK * 2), &tma_b, fb, n0 + j * 64, kb * BK);
+          }
+          if (++stage == Cfg::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // ---------------- MMA issuer (leader) ----------------
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int tile = pair; tile < tiles; tile += n_pairs) {
+        MbarWaitCluster(&tempty[acc], acc_phase ^ 1);
+        FenceAfter();
+        const uint32_t d_tmem = tmem + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          MbarWait(&full[stage], phase);
+          FenceAfter();
+          const uint32_t sa = SmemU32(smem + stage * Cfg::kStage);
+          const uint32_t sb = sa + Cfg::kABytes;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = kAKMajor ? DescSw128(sa + k * 32, 16, 1024)
+                                         : DescSw128(sa + k * 16 * 128, 64 * BK * 2, 1024);
+            const uint64_t bd = kBKMajor ? DescSw128(sb + k * 32, 16, 1024)
+                                         : DescSw128(sb + k * 16 * 128, 64 * BK * 2, 1024);
+            MmaF16Pair(d_tmem, ad, bd, Cfg::kIdesc, (kb | k) != 0);
+          }
+          CommitPair(&empty[stage]);
+          if (++stage == Cfg::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        CommitPair(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue (both CTAs) ----------------
+    const int ew = warp - 4;
+    const uint32_t tempty_leader[2] = {MapaShared(SmemU32(&tempty[0]), 0), MapaShared(SmemU32(&tempty[1]), 0)};
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = pair; tile < tiles; tile += n_pairs) {
+      const int t = tile % mn, ks = tile / mn;
+      const int m_blk = t % num_m, n_blk = t / num_m;
+      MbarWait(&tfull[acc], acc_phase);
+      FenceAfter();
+      const int row = m_blk * 2 * BM + static_cast<int>(rank) * BM + ew * 32 + lane;
+      __nv_bfloat16* crow = C + static_cast<int64_t>(row) * N + n_blk * BN;
+      float* wrow = ws ? ws + (static_cast<int64_t>(ks) * M + row) * N + n_blk * BN : nullptr;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        TmemLd32(tmem + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
+        if (wrow) {
+          float4* dst = reinterpret_cast<float4*>(wrow + c * 32);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                 __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+          continue;
+        }
+        uint32_t p[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) p[j] = PackBf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+        EpiPackedBf16(epi, p);
+        uint4* dst = reinterpret_cast<uint4*>(crow + c * 32);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[q] = make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
+      }
+      FenceBefore();
+      __syncwarp();
+      if (lane == 0) MbarArriveRemote(tempty_leader[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  FenceBefore();
+  __syncthreads();
+  ClusterSync();  // the peer's last remote arrivals / MMAs done before TMEM is released
+  FenceAfter();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::kTmemCols));
+  }
+}
+
 // ------------------------------- fp32 GEMM: 3xTF32 on tcgen05 -------------------------------
 // fp32 programs need fp32-level accuracy (parity 1e-5), which one TF32 pass (10-bit mantissa)
 // cannot give.  Each operand is split exactly into hi = x with the low 13 mantissa bits cleared
@@ -688,6 +934,24 @@ int KSplit(const GemmArgs& g, int bn) {
   return best;
 }
 
+// CTA-pair kernel: bf16 with M a multiple of 256 (RH_GEMM_PAIR=0 disables it, for A/B).
+bool UsePair(const GemmArgs& g) {
+  static const int on = EnvInt("RH_GEMM_PAIR", 1);
+  return on && g.dtype == RH_BF16 && g.m % (2 * BM) == 0;
+}
+
+int KSplitPair(const GemmArgs& g, int bn) {
+  static const int max_split = EnvInt("RH_GEMM_MAX_SPLIT", 8);
+  const int64_t ctas = 2 * (g.m / (2 * BM)) * (g.n / bn), kb = g.k / BK;
+  if (ctas >= 96) return 1;
+  int best = 1;
+  for (int ks = 2; ks <= max_split; ks *= 2) {
+    if (kb % ks || kb / ks < 8 || ctas * (ks / 2) > 148) break;
+    best = ks;
+  }
+  return best;
+}
+
 template <int BN, bool kBK, bool kAK>
 void Launch(const GemmArgs& g, cudaStream_t s) {
   using Cfg = TcCfg<BN, kBK, kAK>;
@@ -713,6 +977,48 @@ void Launch(const GemmArgs& g, cudaStream_t s) {
     const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 148 * 8)));
     LaunchPdl(SplitReduceBf16, blocks, 256, 0, s, static_cast<__nv_bfloat16*>(g.c), reinterpret_cast<const float4*>(ws),
                                            n4, ks, g.epi);
+    RH_CUDA(cudaGetLastError());
+  }
+}
+
+// Pair-tile (256 x BN) launch: clusters of 2 CTAs, one pair per TPC, persistent over the tiles.
+template <int BN, bool kBK, bool kAK>
+void LaunchPair(const GemmArgs& g, cudaStream_t s) {
+  using Cfg = Tc2Cfg<BN, kBK, kAK>;
+  int dev = 0;
+  RH_CUDA(cudaGetDevice(&dev));
+  static bool attr[64] = {};
+  if (dev < 64 && !attr[dev]) {
+    RH_CUDA(cudaFuncSetAttribute(GemmTcPairKernel<BN, kBK, kAK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg::kSmem));
+    attr[dev] = true;
+  }
+  const Maps& mp = GetMaps(g, BN / 2);  // B box: half of the pair's columns per CTA
+  const int ks = g.scratch ? KSplitPair(g, BN) : 1;
+  const int tiles = static_cast<int>((g.m / (2 * BM)) * (g.n / BN)) * ks;
+  const int pairs = std::min(tiles, NumSms() / 2);
+  float* ws = ks > 1 ? static_cast<float*>(g.scratch) : nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = PdlEnabled() ? 2 : 1;
+  RH_CUDA(cudaLaunchKernelEx(&cfg, GemmTcPairKernel<BN, kBK, kAK>, mp.a, mp.b, static_cast<__nv_bfloat16*>(g.c),
+                             static_cast<int>(g.m), static_cast<int>(g.n), static_cast<int>(g.k), g.epi, ks, ws));
+  if (ws) {
+    const int64_t n4 = g.m * g.n / 4;
+    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 148 * 8)));
+    LaunchPdl(SplitReduceBf16, blocks, 256, 0, s, static_cast<__nv_bfloat16*>(g.c), reinterpret_cast<const float4*>(ws),
+              n4, ks, g.epi);
     RH_CUDA(cudaGetLastError());
   }
 }
@@ -788,11 +1094,32 @@ size_t GemmTf32x3ScratchBytes(const GemmArgs& g) {
   return static_cast<size_t>(2 * (g.m * g.k + g.k * g.n)) * 4;
 }
 
+namespace {
+struct Sched {
+  bool pair;
+  int bn, ks;
+};
+// Measured (profiles/gemm_shapes.py, B200, bf16): the CTA-pair kernel with 256 x 256 pair
+// tiles wins once they fill a wave (2048x4096 output, K 4096: 46.8 vs 49.4 us; K 16384: 174 vs
+// 200 us) and, with split-K, for long-K GEMMs with few tiles (512x4096 output, K 16384: 61 vs
+// 77 us); below a wave, and with 256 x 128 pair tiles, the single-CTA kernel is faster (2048^3:
+// 14.7 vs 15.6 us; 512x4096 output, K 4096: 19.3 vs 23.4 us).
+Sched ScheduleOf(const GemmArgs& g) {
+  if (UsePair(g) && g.n % 256 == 0) {
+    static const int force = EnvInt("RH_GEMM_BN", 0);
+    const int64_t ctas = (g.m / BM) * (g.n / 256);
+    if (force == 256 || ctas >= 148) return {true, 256, 1};
+    if (ctas < 96 && g.k / BK >= 128) return {true, 256, KSplitPair(g, 256)};
+  }
+  const int bn = PickBN(g);
+  return {false, bn, bn ? KSplit(g, bn) : 1};
+}
+}  // namespace
+
 size_t GemmTcScratchBytes(const GemmArgs& g) {
   if (g.dtype == RH_F32) return GemmTf32x3ScratchBytes(g);
-  const int bn = PickBN(g);
-  const int ks = bn ? KSplit(g, bn) : 1;
-  return ks > 1 ? static_cast<size_t>(ks) * g.m * g.n * 4 : 0;
+  const Sched sc = ScheduleOf(g);
+  return sc.ks > 1 ? static_cast<size_t>(sc.ks) * g.m * g.n * 4 : 0;
 }
 
 bool GemmTcSupported(const GemmArgs& g) {
@@ -804,7 +1131,7 @@ bool GemmTcSupported(const GemmArgs& g) {
     return false;
   }
   if (g.m > (int64_t{1} << 30) || g.n > (int64_t{1} << 30) || g.k > (int64_t{1} << 30)) return false;
-  if (PickBN(g) == 0) return false;
+  if (g.dtype == RH_F32 ? PickBN(g) == 0 : ScheduleOf(g).bn == 0) return false;
   const uintptr_t a = reinterpret_cast<uintptr_t>(g.a), b = reinterpret_cast<uintptr_t>(g.b);
   if ((a | b) % 16) return false;
   return true;
@@ -812,14 +1139,14 @@ bool GemmTcSupported(const GemmArgs& g) {
 
 const char* GemmTcSchedule(const GemmArgs& g) {
   if (g.dtype == RH_F32) return "";
-  const int bn = PickBN(g);
-  return bn && KSplit(g, bn) > 1 ? " [split-k]" : "";
+  const Sched sc = ScheduleOf(g);
+  if (sc.pair) return sc.ks > 1 ? " [pair, split-k]" : " [pair]";
+  return sc.ks > 1 ? " [split-k]" : "";
 }
 
 int GemmTcLaunches(const GemmArgs& g) {
   if (g.dtype == RH_F32) return 3;
-  const int bn = PickBN(g);
-  return bn && KSplit(g, bn) > 1 ? 2 : 1;
+  return ScheduleOf(g).ks > 1 ? 2 : 1;
 }
 
 void LaunchGemmTc(const GemmArgs& g, cudaStream_t s) {
@@ -834,8 +1161,21 @@ void LaunchGemmTc(const GemmArgs& g, cudaStream_t s) {
     if (fn != RH_FN_RELU && fn != RH_FN_NEG && fn != RH_FN_IDENTITY)
       Fail("tcgen05 bf16 GEMM epilogue takes only relu / neg / identity", RH_ERR_UNSUPPORTED);
   }
-  const int bn = PickBN(g);
-  const int v = (bn == 256 ? 4 : 0) | (g.tb ? 2 : 0) | (g.ta ? 0 : 1);
+  const Sched sc = ScheduleOf(g);
+  const int v = (sc.bn == 256 ? 4 : 0) | (g.tb ? 2 : 0) | (g.ta ? 0 : 1);
+  if (sc.pair) {
+    switch (v) {
+      case 0: LaunchPair<128, false, false>(g, s); break;
+      case 1: LaunchPair<128, false, true>(g, s); break;
+      case 2: LaunchPair<128, true, false>(g, s); break;
+      case 3: LaunchPair<128, true, true>(g, s); break;
+      case 4: LaunchPair<256, false, false>(g, s); break;
+      case 5: LaunchPair<256, false, true>(g, s); break;
+      case 6: LaunchPair<256, true, false>(g, s); break;
+      default: LaunchPair<256, true, true>(g, s); break;
+    }
+    return;
+  }
   switch (v) {
     case 0: Launch<128, false, false>(g, s); break;
     case 1: Launch<128, false, true>(g, s); break;
