@@ -28,7 +28,7 @@
 namespace rh {
 namespace {
 
-constexpr int BM = 128, BK = 64, STAGES = 4;
+constexpr int BM = 128, BK = 64;
 constexpr int kThreads = 256;
 
 __device__ __forceinline__ uint32_t SmemU32(const void* p) {
@@ -149,13 +149,14 @@ __device__ __forceinline__ void EpiPackedBf16(const ChainArgs& epi, uint32_t (&p
   }
 }
 
-template <int BN, bool kBKMajor, bool kAKMajor>
+template <int BN, bool kBKMajor, bool kAKMajor, int KB = BK>
 struct TcCfg {
-  static constexpr int kABytes = BM * BK * 2;
-  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kABytes = BM * KB * 2;
+  static constexpr int kBBytes = BN * KB * 2;
   static constexpr int kStage = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered fp32 accumulator
-  static constexpr int kSmem = STAGES * kStage + 1024 /*barriers*/ + 1024 /*align*/;
+  static constexpr int kStages = (192 * 1024) / kStage;  // 4 (BN 256, KB 64) / 3 (BN 128, KB 128)
+  static constexpr int kSmem = kStages * kStage + 1024 /*barriers*/ + 1024 /*align*/;
   static constexpr uint32_t kIdesc = (1u << 4)                     // D = F32
                                      | (1u << 7) | (1u << 10)      // A, B = BF16
                                      | ((kAKMajor ? 0u : 1u) << 15)  // A major
@@ -164,10 +165,12 @@ struct TcCfg {
                                      (static_cast<uint32_t>(BM >> 4) << 24);
 };
 
-// A and B each either K-major ([M,K] / [N,K] row-major: one 128 x 64 box per stage) or MN-major
-// ([K,M] / [K,N]: 64-wide column chunks, the transpose_a / non-transposed-B layouts) — the MMA
-// reads both straight from the swizzled tiles, no transpose pass.
-template <int BN, bool kBKMajor, bool kAKMajor>
+// A and B each either K-major ([M,K] / [N,K] row-major: one rows x 64 box per 64-wide K chunk)
+// or MN-major ([K,M] / [K,N]: 64-wide column chunks of KB rows, the transpose_a /
+// non-transposed-B layouts) — the MMA reads both straight from the swizzled tiles, no
+// transpose pass.  KB = K elements per pipeline stage: 64, or 128 for the 128-wide tiles (twice
+// the MMA work per barrier round trip: their 128 x 128 x 64 k-blocks were issue-latency-bound).
+template <int BN, bool kBKMajor, bool kAKMajor, int KB>
 __global__ void __launch_bounds__(kThreads, 1)
     GemmTcKernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                  __nv_bfloat16* __restrict__ C, int M, int N, int K, ChainArgs epi, int ksplit,
@@ -175,23 +178,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   PdlTrigger();
   // Work unit = (m tile, n tile, k split).  ksplit > 1 (few tiles: the sharded GEMMs at N >= 4)
   // writes fp32 partial tiles to ws[split][M][N]; SplitReduceBf16 finishes them.
-  using Cfg = TcCfg<BN, kBKMajor, kAKMajor>;
+  using Cfg = TcCfg<BN, kBKMajor, kAKMajor, KB>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStage);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStage);
+  uint64_t* empty = full + Cfg::kStages;
+  uint64_t* tfull = empty + Cfg::kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int num_m = M / BM, num_n = N / BN, mn = num_m * num_n, tiles = mn * ksplit;
-  const int kblocks = K / BK / ksplit;  // per split
+  const int kblocks = K / KB / ksplit;  // per split
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < Cfg::kStages; ++s) {
       MbarInit(&full[s], 1);
       MbarInit(&empty[s], 1);
     }
@@ -225,20 +228,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* sb = sa + Cfg::kABytes;
           MbarExpectTx(&full[stage], Cfg::kStage);
           if constexpr (kAKMajor) {
-            TmaLoad2D(sa, &tma_a, &full[stage], kb * BK, m_blk * BM);
+#pragma unroll
+            for (int q = 0; q < KB / 64; ++q)
+              TmaLoad2D(sa + q * (BM * 128), &tma_a, &full[stage], kb * KB + q * 64, m_blk * BM);
           } else {
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j)
-              TmaLoad2D(sa + j * (64 * BK * 2), &tma_a, &full[stage], m_blk * BM + j * 64, kb * BK);
+              TmaLoad2D(sa + j * (64 * KB * 2), &tma_a, &full[stage], m_blk * BM + j * 64, kb * KB);
           }
           if constexpr (kBKMajor) {
-            TmaLoad2D(sb, &tma_b, &full[stage], kb * BK, n_blk * BN);
+#pragma unroll
+            for (int q = 0; q < KB / 64; ++q)
+              TmaLoad2D(sb + q * (BN * 128), &tma_b, &full[stage], kb * KB + q * 64, n_blk * BN);
           } else {
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
-              TmaLoad2D(sb + j * (64 * BK * 2), &tma_b, &full[stage], n_blk * BN + j * 64, kb * BK);
+              TmaLoad2D(sb + j * (64 * KB * 2), &tma_b, &full[stage], n_blk * BN + j * 64, kb * KB);
           }
-          if (++stage == STAGES) {
+          if (++stage == Cfg::kStages) {
             stage = 0;
             phase ^= 1;
           }
@@ -259,15 +266,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sa = SmemU32(smem + stage * Cfg::kStage);
           const uint32_t sb = sa + Cfg::kABytes;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = kAKMajor ? DescSw128(sa + k * 32, 16, 1024)
-                                         : DescSw128(sa + k * 16 * 128, 64 * BK * 2, 1024);
-            const uint64_t bd = kBKMajor ? DescSw128(sb + k * 32, 16, 1024)
-                                         : DescSw128(sb + k * 16 * 128, 64 * BK * 2, 1024);
+          for (int k = 0; k < KB / 16; ++k) {
+            const uint64_t ad = kAKMajor ? DescSw128(sa + (k / 4) * (BM * 128) + (k % 4) * 32, 16, 1024)
+                                         : DescSw128(sa + k * 16 * 128, 64 * KB * 2, 1024);
+            const uint64_t bd = kBKMajor ? DescSw128(sb + (k / 4) * (BN * 128) + (k % 4) * 32, 16, 1024)
+                                         : DescSw128(sb + k * 16 * 128, 64 * KB * 2, 1024);
             MmaF16(d_tmem, ad, bd, Cfg::kIdesc, (kb | k) != 0);
           }
           Commit(&empty[stage]);
-          if (++stage == STAGES) {
+          if (++stage == Cfg::kStages) {
             stage = 0;
             phase ^= 1;
           }
@@ -866,23 +873,24 @@ struct Maps {
 };
 
 // Tensor maps depend only on (pointer, shape); arena pointers are static, so cache them.
-const Maps& GetMaps(const GemmArgs& g, int bn) {
+// bn = B rows per CTA tile (K-major box), kb = K rows per stage (MN-major box).
+const Maps& GetMaps(const GemmArgs& g, int bn, int kb = BK) {
   static std::mutex mu;
-  static std::map<std::tuple<const void*, const void*, int64_t, int64_t, int64_t, bool, bool, int>, Maps> cache;
+  static std::map<std::tuple<const void*, const void*, int64_t, int64_t, int64_t, bool, bool, int, int>, Maps> cache;
   std::lock_guard<std::mutex> lk(mu);
-  auto key = std::make_tuple(g.a, g.b, g.m, g.n, g.k, g.ta, g.tb, bn);
+  auto key = std::make_tuple(g.a, g.b, g.m, g.n, g.k, g.ta, g.tb, bn, kb);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   Maps m;
   if (g.ta) {
-    m.a = MakeMap(g.a, g.m, g.k, g.m, 64, BK);  // A stored [K,M]: MN-major, 64-wide chunks
+    m.a = MakeMap(g.a, g.m, g.k, g.m, 64, kb);  // A stored [K,M]: MN-major, 64-wide chunks
   } else {
-    m.a = MakeMap(g.a, g.k, g.m, g.k, BK, BM);  // A stored [M,K]: K-major
+    m.a = MakeMap(g.a, g.k, g.m, g.k, BK, BM);  // A stored [M,K]: K-major, one 64-wide K chunk
   }
   if (g.tb) {
     m.b = MakeMap(g.b, g.k, g.n, g.k, BK, bn);  // B stored [N,K]: K-major
   } else {
-    m.b = MakeMap(g.b, g.n, g.k, g.n, 64, BK);  // B stored [K,N]: MN-major, 64-wide chunks
+    m.b = MakeMap(g.b, g.n, g.k, g.n, 64, kb);  // B stored [K,N]: MN-major, 64-wide chunks
   }
   return cache.emplace(key, m).first->second;
 }
@@ -952,23 +960,23 @@ int KSplitPair(const GemmArgs& g, int bn) {
   return best;
 }
 
-template <int BN, bool kBK, bool kAK>
-void Launch(const GemmArgs& g, cudaStream_t s) {
-  using Cfg = TcCfg<BN, kBK, kAK>;
+template <int BN, bool kBK, bool kAK, int KB>
+void LaunchKB(const GemmArgs& g, cudaStream_t s) {
+  using Cfg = TcCfg<BN, kBK, kAK, KB>;
   int dev = 0;
   RH_CUDA(cudaGetDevice(&dev));
   static bool attr[64] = {};  // per device (local multi-GPU runtimes)
   if (dev < 64 && !attr[dev]) {
-    RH_CUDA(cudaFuncSetAttribute(GemmTcKernel<BN, kBK, kAK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RH_CUDA(cudaFuncSetAttribute(GemmTcKernel<BN, kBK, kAK, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Cfg::kSmem));
     attr[dev] = true;
   }
-  const Maps& mp = GetMaps(g, BN);
+  const Maps& mp = GetMaps(g, BN, KB);
   const int ks = g.scratch ? KSplit(g, BN) : 1;
   const int tiles = static_cast<int>((g.m / BM) * (g.n / BN)) * ks;
   const int grid = std::min(tiles, NumSms());
   float* ws = ks > 1 ? static_cast<float*>(g.scratch) : nullptr;
-  LaunchPdl(GemmTcKernel<BN, kBK, kAK>, grid, kThreads, Cfg::kSmem, s, 
+  LaunchPdl(GemmTcKernel<BN, kBK, kAK, KB>, grid, kThreads, Cfg::kSmem, s, 
       mp.a, mp.b, static_cast<__nv_bfloat16*>(g.c), static_cast<int>(g.m), static_cast<int>(g.n),
       static_cast<int>(g.k), g.epi, ks, ws);
   RH_CUDA(cudaGetLastError());
@@ -979,6 +987,14 @@ void Launch(const GemmArgs& g, cudaStream_t s) {
                                            n4, ks, g.epi);
     RH_CUDA(cudaGetLastError());
   }
+}
+
+// KB = 128 K elements per stage for 128-wide tiles when every split holds whole 128-chunks.
+template <int BN, bool kBK, bool kAK>
+void Launch(const GemmArgs& g, cudaStream_t s) {
+  const int ks = g.scratch ? KSplit(g, BN) : 1;
+  if (BN == 128 && g.k % (128 * ks) == 0) LaunchKB<BN, kBK, kAK, 128>(g, s);
+  else LaunchKB<BN, kBK, kAK, 64>(g, s);
 }
 
 // Pair-tile (256 x BN) launch: clusters of 2 CTAs, one pair per TPC, persistent over the tiles.
@@ -1109,6 +1125,7 @@ Sched ScheduleOf(const GemmArgs& g) {
     static const int force = EnvInt("RH_GEMM_BN", 0);
     const int64_t ctas = (g.m / BM) * (g.n / 256);
     if (force == 256 || ctas >= 148) return {true, 256, 1};
+    if (force == 128 && EnvInt("RH_GEMM_PAIR128", 0)) return {true, 128, 1};
     if (ctas < 96 && g.k / BK >= 128) return {true, 256, KSplitPair(g, 256)};
   }
   const int bn = PickBN(g);
