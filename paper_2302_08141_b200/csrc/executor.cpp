@@ -558,11 +558,27 @@ class Lowerer {
       // bf16 GEMM epilogues take only the exact packed ops (relu / neg / identity); tanh runs
       // use the T^k tables of the elementwise kernels.
       bool epi_ok = chain_[h].size() <= kMaxGemmEpilogue;
-      if (op.dtype == RH_BF16)
+      if (op.dtype == RH_BF16) {
+        // bf16: exact packed ops and tanh runs (a run of k tanh = one lookup in the T^k table,
+        // staged in the GEMM's shared memory), at most kMaxGemmEpilogue of them after run
+        // compression (ChainOf)
+        int n_fn = 0;
+        bool ok = true, in_run = false, has_tanh = false;
         for (int v : chain_[h]) {
           const int fn = UnaryFn(v);
-          epi_ok = epi_ok && (fn == RH_FN_RELU || fn == RH_FN_NEG || fn == RH_FN_IDENTITY);
+          if (fn == RH_FN_TANH) {
+            has_tanh = true;
+            if (!in_run) ++n_fn;
+            in_run = true;
+            continue;
+          }
+          in_run = false;
+          ++n_fn;
+          ok = ok && (fn == RH_FN_RELU || fn == RH_FN_NEG || fn == RH_FN_IDENTITY);
         }
+        static const bool no_tanh = getenv("RH_NO_EPI_TANH") != nullptr;  // A/B knob (profiles/)
+        epi_ok = ok && n_fn <= static_cast<int>(kMaxGemmEpilogue) && !(no_tanh && has_tanh);
+      }
       if (op.kind == RH_OP_MATMUL && !epi_ok) {
         for (int v : chain_[h]) absorbed_[v] = false;
         chain_[h].clear();

@@ -28,6 +28,26 @@ __device__ __forceinline__ float Ld<__nv_bfloat16>(const __nv_bfloat16* p, int64
 // Split-K (blockIdx.z = split): small-M GEMMs (the MLP configs' [64,1024] activations) have too
 // few 128x128 tiles to fill 148 SMs; each split writes its fp32 partial tile to `ws` and a reduce
 // kernel sums the splits in order, then rounds and applies the epilogue chain.
+// Epilogue chain on one value; bf16 tanh runs are T^k table lookups (global tables, the
+// executor's run compression, kernels.h kFnTanhRun), every other op as in ApplyChainFns.
+template <typename T>
+__device__ __forceinline__ float EpiChain(const ChainArgs& epi, float v) {
+  if constexpr (sizeof(T) == 2) {
+    for (int i = 0; i < epi.n_fn; ++i) {
+      const int fn = epi.fns[i];
+      if (fn >= kFnTanhRun) {
+        const uint32_t h = TanhRunLookup(__float_as_uint(v) >> 16, epi.tab[fn - kFnTanhRun]);
+        v = __uint_as_float(h << 16);
+      } else {
+        v = RoundBf16(ApplyFn<true>(fn, v));
+      }
+    }
+    return v;
+  } else {
+    return ApplyChainFns<false>(epi.fns, epi.n_fn, v);
+  }
+}
+
 template <typename T, bool TA, bool TB>
 __global__ void __launch_bounds__(256) GemmSimtKernel(T* __restrict__ C, const T* __restrict__ A,
                                                       const T* __restrict__ B, int64_t M,
@@ -117,7 +137,7 @@ __global__ void __launch_bounds__(256) GemmSimtKernel(T* __restrict__ C, const T
         continue;
       }
       if constexpr (sizeof(T) == 2) v = RoundBf16(v);
-      v = ApplyChainFns<sizeof(T) == 2>(epi.fns, epi.n_fn, v);
+      v = EpiChain<T>(epi, v);
       if constexpr (sizeof(T) == 2) {
         C[gm * N + gn] = __float2bfloat16_rn(v);
       } else {
@@ -136,7 +156,7 @@ __global__ void __launch_bounds__(256) SplitReduceKernel(T* __restrict__ C, cons
     float v = ws[i];
     for (int z = 1; z < splits; ++z) v = __fadd_rn(v, ws[int64_t(z) * n + i]);
     if constexpr (sizeof(T) == 2) v = RoundBf16(v);
-    v = ApplyChainFns<sizeof(T) == 2>(epi.fns, epi.n_fn, v);
+    v = EpiChain<T>(epi, v);
     if constexpr (sizeof(T) == 2) {
       C[i] = __float2bfloat16_rn(v);
     } else {

@@ -113,9 +113,49 @@ __device__ __forceinline__ void TmemLd32(uint32_t taddr, uint32_t (&r)[32]) {
 
 // Split-K finish: sum the fp32 partials in split order, round to bf16, apply the chain.
 __global__ void __launch_bounds__(256) SplitReduceBf16(__nv_bfloat16* __restrict__ C, const float4* __restrict__ ws,
+                                                       int64_t n4, int splits, ChainArgs epi);
+
+// The packed bf16 ops the lowering lets into a bf16 GEMM epilogue (executor.cpp: relu / neg /
+// identity, and tanh runs = one T^k table lookup; LaunchGemmTc rejects anything else).
+// Warp-uniform fn loop outside the element loop: small code.  tabs[t] = table of run slot t
+// (shared memory in the GEMM kernels, global in the split-K reduce).
+template <int P>
+__device__ __forceinline__ void EpiPackedBf16(const ChainArgs& epi, uint32_t (&p)[P], const uint16_t* const* tabs) {
+  for (int i = 0; i < epi.n_fn; ++i) {
+    const int fn = epi.fns[i];
+    if (fn >= kFnTanhRun) {
+      const uint16_t* tab = tabs[fn - kFnTanhRun];
+#pragma unroll
+      for (int j = 0; j < P; ++j)
+        p[j] = TanhRunLookup(p[j] & 0xffffu, tab) | (TanhRunLookup(p[j] >> 16, tab) << 16);
+    } else if (fn == RH_FN_RELU) {
+#pragma unroll
+      for (int j = 0; j < P; ++j) p[j] = ReluBf16x2(p[j]);
+    } else if (fn == RH_FN_NEG) {
+#pragma unroll
+      for (int j = 0; j < P; ++j) p[j] ^= 0x80008000u;
+    }
+  }
+}
+
+// Epilogue warps (128 threads, named barrier 1) stage the chain's T^k tables in shared memory.
+__device__ __forceinline__ void StageEpiTables(const ChainArgs& epi, uint16_t* tab_s, int t,
+                                               const uint16_t* (&tp)[kMaxTanhRuns]) {
+  for (int i = t; i < epi.n_tab * kTanhRunEntries; i += 128)
+    tab_s[i] = epi.tab[i / kTanhRunEntries][i % kTanhRunEntries];
+#pragma unroll
+  for (int k = 0; k < kMaxTanhRuns; ++k) tp[k] = tab_s + k * kTanhRunEntries;
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+constexpr int kEpiTabBytes = 8192;  // >= kMaxTanhRuns * kTanhRunEntries * 2
+
+__global__ void __launch_bounds__(256) SplitReduceBf16(__nv_bfloat16* __restrict__ C, const float4* __restrict__ ws,
                                                        int64_t n4, int splits, ChainArgs epi) {
   PdlTrigger();
   PdlWait();
+  const uint16_t* tabs[kMaxTanhRuns];
+#pragma unroll
+  for (int k = 0; k < kMaxTanhRuns; ++k) tabs[k] = epi.tab[k];
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
     float4 v = ws[i];
     for (int z = 1; z < splits; ++z) {
@@ -125,27 +165,9 @@ __global__ void __launch_bounds__(256) SplitReduceBf16(__nv_bfloat16* __restrict
       v.z = __fadd_rn(v.z, w.z);
       v.w = __fadd_rn(v.w, w.w);
     }
-    float f[4] = {v.x, v.y, v.z, v.w};
-    __nv_bfloat16 o[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) o[e] = __float2bfloat16_rn(ApplyChainFns<true>(epi.fns, epi.n_fn, RoundBf16(f[e])));
-    reinterpret_cast<uint2*>(C)[i] = *reinterpret_cast<uint2*>(o);
-  }
-}
-
-// The exact packed bf16 ops the lowering lets into a bf16 GEMM epilogue (executor.cpp: relu /
-// neg / identity; LaunchGemmTc rejects anything else).  Warp-uniform fn loop outside the
-// element loop: small code.
-__device__ __forceinline__ void EpiPackedBf16(const ChainArgs& epi, uint32_t (&p)[16]) {
-  for (int i = 0; i < epi.n_fn; ++i) {
-    const int fn = epi.fns[i];
-    if (fn == RH_FN_RELU) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) p[j] = ReluBf16x2(p[j]);
-    } else if (fn == RH_FN_NEG) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) p[j] ^= 0x80008000u;
-    }
+    uint32_t p[2] = {PackBf16x2(v.x, v.y), PackBf16x2(v.z, v.w)};
+    EpiPackedBf16(epi, p, tabs);
+    reinterpret_cast<uint2*>(C)[i] = make_uint2(p[0], p[1]);
   }
 }
 
@@ -156,7 +178,7 @@ struct TcCfg {
   static constexpr int kStage = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered fp32 accumulator
   static constexpr int kStages = (192 * 1024) / kStage;  // 4 (BN 256, KB 64) / 3 (BN 128, KB 128)
-  static constexpr int kSmem = kStages * kStage + 1024 /*barriers*/ + 1024 /*align*/;
+  static constexpr int kSmem = kStages * kStage + 1024 /*barriers*/ + kEpiTabBytes + 1024 /*align*/;
   static constexpr uint32_t kIdesc = (1u << 4)                     // D = F32
                                      | (1u << 7) | (1u << 10)      // A, B = BF16
                                      | ((kAKMajor ? 0u : 1u) << 15)  // A major
@@ -288,6 +310,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {  // ---------------- epilogue ----------------
     const int ew = warp - 4;  // TMEM lanes [32*ew, 32*ew+32)
+    const uint16_t* tp[kMaxTanhRuns];
+    StageEpiTables(epi, reinterpret_cast<uint16_t*>(smem + Cfg::kStages * Cfg::kStage + 1024), threadIdx.x - 128, tp);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
@@ -316,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t p[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) p[j] = PackBf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-        EpiPackedBf16(epi, p);
+        EpiPackedBf16(epi, p, tp);
         uint4* dst = reinterpret_cast<uint4*>(crow + c * 32);
 #pragma unroll
         for (int q = 0; q < 4; ++q) dst[q] = make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
@@ -411,7 +435,7 @@ struct Tc2Cfg {
   static constexpr int kStage = kABytes + kBBytes;
   static constexpr int kStages = (192 * 1024) / kStage;  // 6 (BN 256) / 8 (BN 128)
   static constexpr int kTmemCols = 2 * BN;
-  static constexpr int kSmem = kStages * kStage + 1024 + 1024;
+  static constexpr int kSmem = kStages * kStage + 1024 + kEpiTabBytes + 1024;
   static constexpr uint32_t kIdesc = (1u << 4)                     // D = F32
                                      | (1u << 7) | (1u << 10)      // A, B = BF16
                                      | ((kAKMajor ? 0u : 1u) << 15) | ((kBKMajor ? 0u : 1u) << 16) |
@@ -535,6 +559,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {  // ---------------- epilogue (both CTAs) ----------------
     const int ew = warp - 4;
+    const uint16_t* tp[kMaxTanhRuns];
+    StageEpiTables(epi, reinterpret_cast<uint16_t*>(smem + Cfg::kStages * Cfg::kStage + 1024), threadIdx.x - 128, tp);
     const uint32_t tempty_leader[2] = {MapaShared(SmemU32(&tempty[0]), 0), MapaShared(SmemU32(&tempty[1]), 0)};
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -561,7 +587,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t p[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) p[j] = PackBf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-        EpiPackedBf16(epi, p);
+        EpiPackedBf16(epi, p, tp);
         uint4* dst = reinterpret_cast<uint4*>(crow + c * 32);
 #pragma unroll
         for (int q = 0; q < 4; ++q) dst[q] = make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
@@ -1175,8 +1201,8 @@ void LaunchGemmTc(const GemmArgs& g, cudaStream_t s) {
   }
   for (int i = 0; i < g.epi.n_fn; ++i) {
     const int fn = g.epi.fns[i];
-    if (fn != RH_FN_RELU && fn != RH_FN_NEG && fn != RH_FN_IDENTITY)
-      Fail("tcgen05 bf16 GEMM epilogue takes only relu / neg / identity", RH_ERR_UNSUPPORTED);
+    if (fn != RH_FN_RELU && fn != RH_FN_NEG && fn != RH_FN_IDENTITY && !(fn >= kFnTanhRun && fn - kFnTanhRun < g.epi.n_tab))
+      Fail("tcgen05 bf16 GEMM epilogue takes only relu / neg / identity / tanh runs", RH_ERR_UNSUPPORTED);
   }
   const Sched sc = ScheduleOf(g);
   const int v = (sc.bn == 256 ? 4 : 0) | (g.tb ? 2 : 0) | (g.ta ? 0 : 1);

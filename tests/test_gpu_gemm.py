@@ -87,9 +87,23 @@ def test_tc_fused_epilogue_chain():
     _, _, c2, names2 = run(matmul_doc(256, 256, 256, False, ("relu", "neg")), RH_FLAG_SIMT_GEMM)
     x, y = bf16_to_f64(c), bf16_to_f64(c2)
     assert np.abs(x - y).max() <= 2.0 ** -6
-    # tanh runs and long chains get their own (T^k table) kernel
-    _, _, _, names3 = run(matmul_doc(256, 256, 256, False, ("relu", "tanh", "")))
+    # chains of more than two ops after run compression get their own kernel
+    _, _, _, names3 = run(matmul_doc(256, 256, 256, False, ("relu", "tanh", "neg", "relu")))
     assert len(names3) == 2 and "unary_chain" in names3[1]
+
+
+@pytest.mark.parametrize("m,k,n", [(256, 256, 256), (2048, 4096, 4096), (256, 16384, 512), (64, 128, 64)])
+def test_tc_epilogue_tanh_runs_bit_exact(m, k, n):
+    """A tanh run (one T^k table lookup staged in shared memory) and an exact op in the GEMM
+    epilogue — single-CTA, CTA-pair, split-K reduce and CUDA-core GEMMs — are bit-identical to
+    the unfused one-op-per-kernel schedule."""
+    from paper_2302_08141_b200.abi import RH_FLAG_NO_FUSION
+    chain = ("tanh", "", "tanh", "relu")
+    _, _, c, names = run(matmul_doc(m, k, n, False, chain))
+    _, _, c0, names0 = run(matmul_doc(m, k, n, False, chain), RH_FLAG_NO_FUSION)
+    assert len(names) == 1, names
+    assert len(names0) == 1 + len(chain), names0
+    np.testing.assert_array_equal(c, c0)
 
 
 @pytest.mark.parametrize("m,k,n", [(128, 32, 128), (256, 512, 384), (1024, 4096, 1024),
