@@ -11,6 +11,7 @@
 #include "executor.h"
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -584,7 +585,50 @@ class Lowerer {
         chain_[h].clear();
       }
     }
+    PlanTransposeFold(uses, consumer, is_out);
     PlanEwChains(is_out, natural_ok, no_partial);
+  }
+
+  // A 2-D transpose whose only consumer is a MatMul folds into the GEMM's operand layout (the
+  // tcgen05 / SIMT kernels read K-major and MN-major operands straight from the buffer): the
+  // MatMul fetches the transpose's input in the permuted spec — the local buffer of a
+  // block-cyclic layout transposes with the tensor, Shard(p, s) of the output <-> Shard(perm[p],
+  // s) of the input — and flips its transpose flag.  No transpose kernel, no extra buffer.
+  void PlanTransposeFold(const std::vector<int>& uses, const std::vector<int>& consumer,
+                         const std::vector<bool>& is_out) {
+    const int n = static_cast<int>(p_->ops.size());
+    fold_t_.assign(n, {false, false});
+    static const bool off = getenv("RH_NO_TRANSPOSE_FOLD") != nullptr;  // A/B knob (profiles/)
+    if (off) return;
+    (void)uses;
+    (void)consumer;
+    std::vector<std::vector<int>> users(n);
+    for (int i = 0; i < n; ++i)
+      for (int s : p_->inputs[i]) users[s].push_back(i);
+    for (int t = 0; t < n; ++t) {
+      const rh_op& op = p_->ops[t];
+      if (op.kind != RH_OP_TRANSPOSE || op.rank != 2 || users[t].empty() || is_out[t] || absorbed_[t]) continue;
+      if (EffPerm(op, 2) != std::vector<int>{1, 0}) continue;
+      // every consumer must be a MatMul reading it in exactly one slot (the forward score GEMM
+      // and the backward's gradient GEMMs all read k^T)
+      bool ok = true;
+      for (int c : users[t]) {
+        const auto& ins = p_->inputs[c];
+        ok = ok && p_->ops[c].kind == RH_OP_MATMUL && !absorbed_[c] && p_->ops[c].dtype == op.dtype &&
+             ins.size() == 2 && ins[0] != ins[1];
+      }
+      if (!ok) continue;
+      for (int c : users[t]) fold_t_[c][p_->inputs[c][0] == t ? 0 : 1] = true;
+      absorbed_[t] = true;
+    }
+  }
+
+  // Spec of the transpose's input that matches spec `s` of its (2-D, perm [1,0]) output.
+  static Specs Transposed(const Specs& s) {
+    Specs o = s;
+    for (auto& x : o)
+      if (x.kind == RH_SHARD) x.dim = 1 - x.dim;
+    return o;
   }
 
   bool IsEw(int i) const {
@@ -812,9 +856,17 @@ class Lowerer {
     const rh_op& op = p_->ops[i];
     const int nin = static_cast<int>(p_->inputs[i].size());
     std::vector<int> in_t(nin);
-    for (int s = 0; s < nin; ++s)
-      in_t[s] = GetTensor(p_->inputs[i][s], p_->in_specs[i][s], "edge");
+    for (int s = 0; s < nin; ++s) {
+      if (s < 2 && !fold_t_.empty() && fold_t_[i][s]) {  // folded transpose: its input, permuted spec
+        const int t = p_->inputs[i][s];
+        in_t[s] = GetTensor(p_->inputs[t][0], Transposed(p_->in_specs[i][s]), "edge");
+      } else {
+        in_t[s] = GetTensor(p_->inputs[i][s], p_->in_specs[i][s], "edge");
+      }
+    }
     p_->in_tensor[i] = in_t;
+    for (int s = 0; s < nin && s < 2; ++s)
+      if (!fold_t_.empty() && fold_t_[i][s]) p_->in_tensor[i][s] = -1;  // not materialized
     const Specs nat = NaturalSpecs(i, p_->in_specs[i]);
     const int tail = chain_[i].empty() ? i : chain_[i].back();
     const bool direct = SpecsEq(nat, p_->out_specs[i]);
@@ -1040,14 +1092,16 @@ class Lowerer {
     switch (op.kind) {
       case RH_OP_MATMUL: {
         const Dims ad = P->tensors[in_t[0]].ldims, bd = P->tensors[in_t[1]].ldims;
+        const bool fa = !fold_t_.empty() && fold_t_[i][0], fb = !fold_t_.empty() && fold_t_[i][1];
+        const bool eta = op.transpose_a != fa, etb = op.transpose_b != fb;
         GemmArgs g{};
-        g.m = op.transpose_a ? ad[1] : ad[0];
-        g.k = op.transpose_a ? ad[0] : ad[1];
-        g.n = op.transpose_b ? bd[0] : bd[1];
-        if ((op.transpose_b ? bd[1] : bd[0]) != g.k) Fail("matmul " + id + ": local k mismatch");
+        g.m = eta ? ad[1] : ad[0];
+        g.k = eta ? ad[0] : ad[1];
+        g.n = etb ? bd[0] : bd[1];
+        if ((etb ? bd[1] : bd[0]) != g.k) Fail("matmul " + id + ": local k mismatch");
         if (T.ldims[0] != g.m || T.ldims[1] != g.n) Fail("matmul " + id + ": local output shape mismatch");
-        g.ta = op.transpose_a;
-        g.tb = op.transpose_b;
+        g.ta = eta;
+        g.tb = etb;
         g.dtype = dtype;
         g.epi = ChainOf(i, false);
         // fp32 GEMMs run as 3xTF32 and need split scratch: one region shared by all GEMMs of the
@@ -1057,7 +1111,8 @@ class Lowerer {
         if (tc) P->gemm_scratch_bytes = std::max(P->gemm_scratch_bytes, GemmTcScratchBytes(g));
         if (!tc) P->gemm_scratch_bytes = std::max(P->gemm_scratch_bytes, GemmSimtScratchBytes(g));
         g.scratch = nullptr;
-        st.name = std::string(tc ? (dtype == RH_F32 ? "gemm_tc_3xtf32 " : "gemm_tc ") : "gemm_simt ") + id;
+        st.name = std::string(tc ? (dtype == RH_F32 ? "gemm_tc_3xtf32 " : "gemm_tc ") : "gemm_simt ") + id +
+                  (fa || fb ? " [T-folded]" : "");
         st.alg_flops = 2.0 * g.m * g.n * g.k;
         const int ta = in_t[0], tb = in_t[1];
         st.run = [P, g, ta, tb, out_t, first, tc](int li, cudaStream_t s) {
@@ -1373,6 +1428,7 @@ class Lowerer {
   size_t arena_ = 0;
   std::map<std::string, int> cache_;
   std::vector<bool> absorbed_;
+  std::vector<std::array<bool, 2>> fold_t_;  // matmul slot reads a folded 2-D transpose
   std::vector<std::vector<int>> chain_;
   std::map<int, size_t> tanh_tables_;
   std::map<std::vector<int>, size_t> ladder_tables_;
