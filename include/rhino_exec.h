@@ -164,6 +164,13 @@ int rh_program_run(rh_program* prog, int iters, double* ms_per_iter);
 int rh_program_step_host(rh_program* prog, int n_in, const int* in_ops, const void* const* in_ptrs,
                          int n_outs, void* const* out_ptrs, double* ms);
 
+/* Pipelined end-to-end steps (one local rank per process): `iters` steps, each with the H2D of
+ * every input and the D2H of the first n_outs outputs (as rh_program_step_host), step i's H2D
+ * overlapping step i-1's run and step i-2's D2H through double-buffered device stages;
+ * *ms_per_iter = time from before the first H2D to after the last D2H, divided by iters. */
+int rh_program_run_host(rh_program* prog, int iters, int n_in, const int* in_ops, const void* const* in_ptrs,
+                        int n_outs, void* const* out_ptrs, double* ms_per_iter);
+
 /* Local buffer of `op` on global `rank` (must be local to this process); bytes must equal the
  * local size.  Returns the buffer as laid out on the device (block-cyclic local order). */
 int rh_program_read_local(rh_program* prog, int op, int rank, void* dst, size_t bytes);

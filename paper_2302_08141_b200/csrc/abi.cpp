@@ -763,6 +763,134 @@ int rh_program_profile(rh_program* p, int iters, double* ms_per_iter) {
   });
 }
 
+// Pipelined end-to-end steps through host buffers (one local rank per process): step i's H2D
+// (copy-in stream, into a double-buffered device stage) overlaps step i-1's run and step i-2's
+// D2H (copy-out stream); the compute stream moves stage -> arena input (D2D copy, or the slice
+// kernel for a sharded input) before the run and arena output -> output stage after it.  Every
+// step still copies its inputs in and its outputs out; only the copies of neighbouring steps
+// overlap, as in a serving / training loop that prefetches the next batch.
+int rh_program_run_host(rh_program* p, int iters, int n_in, const int* in_ops, const void* const* in_ptrs,
+                        int n_outs, void* const* out_ptrs, double* ms_per_iter) {
+  return Guard([&] {
+    rh_runtime* rt = p->mesh->rt;
+    if (rt->n_local() != 1) Fail("rh_program_run_host: needs one local rank per process");
+    if (iters <= 0) Fail("rh_program_run_host: iters must be positive");
+    if (n_outs > static_cast<int>(p->outputs.size())) Fail("too many output buffers");
+    DeviceGuard dg(rt->devs[0]);
+    cudaStream_t cs = rt->streams[0];
+    const int g = rt->first_rank;
+    struct In {
+      const rh::Tensor* t;
+      size_t bytes;
+      void* stage[2];
+    };
+    struct Out {
+      const rh::Tensor* t;
+      void* stage[2];
+    };
+    std::vector<In> ins(n_in);
+    std::vector<Out> outs(n_outs);
+    for (int k = 0; k < n_in; ++k) {
+      const rh::Tensor& t = p->tensors[p->out_tensor[in_ops[k]]];
+      ins[k].t = &t;
+      ins[k].bytes = static_cast<size_t>(Prod(t.gdims)) * rh::ElemBytes(t.dtype);
+      for (int b = 0; b < 2; ++b) RH_CUDA(cudaMalloc(&ins[k].stage[b], ins[k].bytes));
+    }
+    for (int k = 0; k < n_outs; ++k) {
+      const int op = p->outputs[k];
+      const int ti = p->mat_tensor[op] >= 0 ? p->mat_tensor[op] : p->out_tensor[op];
+      if (ti < 0) Fail("output has no buffer");
+      outs[k].t = &p->tensors[ti];
+      for (int b = 0; b < 2; ++b) RH_CUDA(cudaMalloc(&outs[k].stage[b], outs[k].t->bytes));
+    }
+    cudaStream_t sin = nullptr, sout = nullptr;
+    RH_CUDA(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking));
+    RH_CUDA(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking));
+    cudaEvent_t in_ready[2], in_free[2], out_ready[2], out_free[2], e0, e1;
+    for (int b = 0; b < 2; ++b) {
+      RH_CUDA(cudaEventCreateWithFlags(&in_ready[b], cudaEventDisableTiming));
+      RH_CUDA(cudaEventCreateWithFlags(&in_free[b], cudaEventDisableTiming));
+      RH_CUDA(cudaEventCreateWithFlags(&out_ready[b], cudaEventDisableTiming));
+      RH_CUDA(cudaEventCreateWithFlags(&out_free[b], cudaEventDisableTiming));
+    }
+    RH_CUDA(cudaEventCreate(&e0));
+    RH_CUDA(cudaEventCreate(&e1));
+    auto cleanup = [&] {
+      cudaStreamSynchronize(sin);
+      cudaStreamSynchronize(sout);
+      cudaStreamSynchronize(cs);
+      for (auto& x : ins)
+        for (void* q : x.stage) cudaFree(q);
+      for (auto& x : outs)
+        for (void* q : x.stage) cudaFree(q);
+      for (int b = 0; b < 2; ++b) {
+        cudaEventDestroy(in_ready[b]);
+        cudaEventDestroy(in_free[b]);
+        cudaEventDestroy(out_ready[b]);
+        cudaEventDestroy(out_free[b]);
+      }
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      cudaStreamDestroy(sin);
+      cudaStreamDestroy(sout);
+    };
+    try {
+      if (UseGraph(p) && !p->graph) {  // capture outside the timed region
+        if (!p->warmed) RunStep(p);
+        RunStep(p);
+      }
+      SyncAll(rt);
+      WorldSync(p);
+      RH_CUDA(cudaEventRecord(e0, cs));
+      RH_CUDA(cudaStreamWaitEvent(sin, e0, 0));
+      for (int it = 0; it < iters; ++it) {
+        const int b = it & 1;
+        RH_CUDA(cudaStreamWaitEvent(sin, in_free[b], 0));
+        for (auto& x : ins)
+          RH_CUDA(cudaMemcpyAsync(x.stage[b], in_ptrs[&x - ins.data()], x.bytes, cudaMemcpyHostToDevice, sin));
+        RH_CUDA(cudaEventRecord(in_ready[b], sin));
+        RH_CUDA(cudaStreamWaitEvent(cs, in_ready[b], 0));
+        for (auto& x : ins) {
+          const rh::Tensor& t = *x.t;
+          bool all_rep = true, partial_zero = false;
+          const std::vector<int> c = p->mesh->Coords(g);
+          for (int a = 0; a < p->n_axes; ++a) {
+            all_rep = all_rep && t.specs[a].kind == RH_REPLICATED;
+            if (t.specs[a].kind == RH_PARTIAL && c[a] != 0) partial_zero = true;
+          }
+          if (all_rep) {
+            RH_CUDA(cudaMemcpyAsync(p->base[0] + t.offset, x.stage[b], x.bytes, cudaMemcpyDeviceToDevice, cs));
+          } else if (partial_zero) {
+            rh::LaunchZero(p->base[0] + t.offset, t.bytes, cs);
+          } else {
+            rh::LaunchSliceComposed(p->base[0] + t.offset, x.stage[b], MakeComposed(p, t, g), t.elems(), t.dtype, cs);
+          }
+        }
+        RH_CUDA(cudaEventRecord(in_free[b], cs));
+        RunStep(p);
+        RH_CUDA(cudaStreamWaitEvent(cs, out_free[b], 0));
+        for (auto& x : outs)
+          RH_CUDA(cudaMemcpyAsync(x.stage[b], p->base[0] + x.t->offset, x.t->bytes, cudaMemcpyDeviceToDevice, cs));
+        RH_CUDA(cudaEventRecord(out_ready[b], cs));
+        RH_CUDA(cudaStreamWaitEvent(sout, out_ready[b], 0));
+        for (auto& x : outs)
+          RH_CUDA(cudaMemcpyAsync(out_ptrs[&x - outs.data()], x.stage[b], x.t->bytes, cudaMemcpyDeviceToHost, sout));
+        RH_CUDA(cudaEventRecord(out_free[b], sout));
+      }
+      RH_CUDA(cudaStreamWaitEvent(cs, out_free[(iters - 1) & 1], 0));
+      RH_CUDA(cudaEventRecord(e1, cs));
+      RH_CUDA(cudaEventSynchronize(e1));
+      float ms = 0;
+      RH_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      if (ms_per_iter) *ms_per_iter = ms / iters;
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+}
+
 int rh_program_step_host(rh_program* p, int n_in, const int* in_ops, const void* const* in_ptrs,
                          int n_outs, void* const* out_ptrs, double* ms) {
   return Guard([&] {

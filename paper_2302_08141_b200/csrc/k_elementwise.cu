@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.h"
@@ -607,8 +608,12 @@ __global__ void ConcatPieceKernel(T* out, const T* in, int64_t outer, int64_t ro
 }
 
 int Blocks(int64_t n, int per_thread = 1) {
+  static const int per_sm = [] {  // A/B knob (profiles/): grid cap in blocks per SM
+    const char* v = getenv("RH_EW_BLOCKS_PER_SM");
+    return v && *v ? atoi(v) : 16;
+  }();
   return static_cast<int>(
-      std::max<int64_t>(1, std::min<int64_t>((n / per_thread + 255) / 256, 148 * 16)));
+      std::max<int64_t>(1, std::min<int64_t>((n / per_thread + 255) / 256, 148 * per_sm)));
 }
 
 }  // namespace

@@ -17,7 +17,7 @@ EXPORTS = [
     "rh_last_error", "rh_version", "rh_get_unique_id", "rh_runtime_create",
     "rh_runtime_create_dist", "rh_runtime_world", "rh_runtime_destroy", "rh_mesh_create",
     "rh_mesh_destroy", "rh_program_load", "rh_program_destroy", "rh_program_init_synthetic",
-    "rh_program_write_full", "rh_program_run", "rh_program_step_host", "rh_program_read_local",
+    "rh_program_write_full", "rh_program_run", "rh_program_step_host", "rh_program_run_host", "rh_program_read_local",
     "rh_program_read_full", "rh_program_read_input_full", "rh_program_local_bytes", "rh_program_memory", "rh_program_num_steps",
     "rh_program_step_info", "rh_program_profile", "rh_program_launch_count", "rh_reshard",
 ]
@@ -56,6 +56,7 @@ def lib():
     L.rh_program_write_full.argtypes = [vp, i, vp, sz]
     L.rh_program_run.argtypes = [vp, i, P(ctypes.c_double)]
     L.rh_program_step_host.argtypes = [vp, i, P(i), P(vp), i, P(vp), P(ctypes.c_double)]
+    L.rh_program_run_host.argtypes = [vp, i, i, P(i), P(vp), i, P(vp), P(ctypes.c_double)]
     L.rh_program_read_local.argtypes = [vp, i, i, vp, sz]
     L.rh_program_read_full.argtypes = [vp, i, vp, sz]
     L.rh_program_read_input_full.argtypes = [vp, i, i, vp, sz]
@@ -175,6 +176,16 @@ class Program:
         op_ = (ctypes.c_void_p * max(len(out_ptrs), 1))(*out_ptrs)
         ms = ctypes.c_double()
         check(lib().rh_program_step_host(self.h, n, ops, ip, len(out_ptrs), op_, ctypes.byref(ms)))
+        return ms.value
+
+    def run_host(self, iters, in_ops, in_ptrs, out_ptrs):
+        """Pipelined end-to-end steps (rh_program_run_host): ms per step."""
+        n = len(in_ops)
+        ops = (ctypes.c_int * max(n, 1))(*in_ops)
+        ip = (ctypes.c_void_p * max(n, 1))(*in_ptrs)
+        op_ = (ctypes.c_void_p * max(len(out_ptrs), 1))(*out_ptrs)
+        ms = ctypes.c_double()
+        check(lib().rh_program_run_host(self.h, iters, n, ops, ip, len(out_ptrs), op_, ctypes.byref(ms)))
         return ms.value
 
     def local_bytes(self, op, rank=0):

@@ -255,6 +255,31 @@ def test_write_full_and_step_host(rx, oracle_lib):
         close(rt, mesh, gp)
 
 
+@pytest.mark.parametrize("name,dtype", [("c1_mlp_d1", RH_F32), ("c3_gpt_block_d1", RH_BF16)])
+def test_run_host_pipelined(rx, name, dtype):
+    """rh_program_run_host (H2D of step i overlapping step i-1's run and step i-2's D2H through
+    double-buffered stages) returns the same output bytes as the serial rh_program_step_host."""
+    prog = LoweredProgram.load(name).with_dtype(dtype)
+    rt, mesh, gp = load(rx, prog)
+    try:
+        gp.init_synthetic(0)
+        x = prog.op_index("x")
+        xin = np.random.default_rng(1).integers(0, 2 ** 16, prog.full_bytes(x) // 2, dtype=np.uint16)
+        if dtype == RH_BF16:  # finite bf16 values in [-1, 1)
+            xin = ((np.random.default_rng(1).uniform(-1, 1, xin.size).astype(np.float32).view(np.uint32)) >> 16).astype(np.uint16)
+        else:
+            xin = np.random.default_rng(1).uniform(-1, 1, prog.full_bytes(x) // 4).astype(np.float32)
+        out = prog.outputs[0]
+        y_serial = np.empty(prog.full_bytes(out), np.uint8)
+        y_pipe = np.empty(prog.full_bytes(out), np.uint8)
+        gp.step_host([x], [xin.ctypes.data], [y_serial.ctypes.data])
+        ms = gp.run_host(4, [x], [xin.ctypes.data], [y_pipe.ctypes.data])
+        assert ms > 0
+        np.testing.assert_array_equal(y_pipe, y_serial)
+    finally:
+        close(rt, mesh, gp)
+
+
 def test_schedule_reports_transitions(rx):
     """Wire bytes follow reshard_cost (sharding.cpp:113-135): SPEC.md:145-150 numbers."""
     prog = LoweredProgram.load("c3_gpt_block_d8")
