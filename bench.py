@@ -344,7 +344,8 @@ def main():
                                 if scale > 1 else "the same program")
                              + f", oracle/ref_cpu_exec, {cores} threads"}
         h2d = sum(prog.full_bytes(x) for x in xs) * world
-        d2h = (gp.local_bytes(out, rank) if reduce_outputs else prog.full_bytes(out)) * world
+        # materialized outputs: each process reads its 1/world slice (rh_program_step_host)
+        d2h = gp.local_bytes(out, rank) * world if reduce_outputs else prog.full_bytes(out)
         gp.close()
         mesh.close()
         rt.close()

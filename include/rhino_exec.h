@@ -159,8 +159,10 @@ int rh_program_write_full(rh_program* prog, int op, const void* src, size_t byte
 /* Run the program `iters` times; *ms_per_iter = device time per run (max over local ranks). */
 int rh_program_run(rh_program* prog, int iters, double* ms_per_iter);
 /* End-to-end step through host buffers: H2D of every `n_in` (op, host ptr) input, one run,
- * D2H of the first n_outs program outputs into out_ptrs: the full tensor when materialized,
- * else this process's first local rank's shard (rh_program_local_bytes).  Timed inside. */
+ * D2H of the first n_outs program outputs into out_ptrs: the full tensor when materialized
+ * (in a multi-process run: this process's 1/world contiguous slice of it, at its offset in
+ * out_ptrs, so the processes' slices together are the full tensor), else this process's
+ * first local rank's shard (rh_program_local_bytes).  Timed inside. */
 int rh_program_step_host(rh_program* prog, int n_in, const int* in_ops, const void* const* in_ptrs,
                          int n_outs, void* const* out_ptrs, double* ms);
 

@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <tuple>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -763,6 +764,18 @@ int rh_program_profile(rh_program* p, int iters, double* ms_per_iter) {
   });
 }
 
+// Host read of output k: a materialized (replicated) output in a multi-process run is read as
+// this process's 1/world contiguous slice (the processes' slices together are the full tensor;
+// every rank copying the whole replicated tensor would multiply the PCIe traffic by world).
+std::pair<size_t, size_t> OutSlice(const rh_program* p, int op, const rh::Tensor& t) {
+  const rh_runtime* rt = p->mesh->rt;
+  if (rt->dist && rt->world > 1 && p->mat_tensor[op] >= 0 && t.bytes % (static_cast<size_t>(rt->world) * 16) == 0) {
+    const size_t part = t.bytes / rt->world;
+    return {part * rt->first_rank, part};
+  }
+  return {0, t.bytes};
+}
+
 // Pipelined end-to-end steps through host buffers (one local rank per process): step i's H2D
 // (copy-in stream, into a double-buffered device stage) overlaps step i-1's run and step i-2's
 // D2H (copy-out stream); the compute stream moves stage -> arena input (D2D copy, or the slice
@@ -786,6 +799,7 @@ int rh_program_run_host(rh_program* p, int iters, int n_in, const int* in_ops, c
     };
     struct Out {
       const rh::Tensor* t;
+      size_t off, bytes;  // OutSlice
       void* stage[2];
     };
     std::vector<In> ins(n_in);
@@ -801,7 +815,8 @@ int rh_program_run_host(rh_program* p, int iters, int n_in, const int* in_ops, c
       const int ti = p->mat_tensor[op] >= 0 ? p->mat_tensor[op] : p->out_tensor[op];
       if (ti < 0) Fail("output has no buffer");
       outs[k].t = &p->tensors[ti];
-      for (int b = 0; b < 2; ++b) RH_CUDA(cudaMalloc(&outs[k].stage[b], outs[k].t->bytes));
+      std::tie(outs[k].off, outs[k].bytes) = OutSlice(p, op, *outs[k].t);
+      for (int b = 0; b < 2; ++b) RH_CUDA(cudaMalloc(&outs[k].stage[b], outs[k].bytes));
     }
     cudaStream_t sin = nullptr, sout = nullptr;
     RH_CUDA(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking));
@@ -870,11 +885,12 @@ int rh_program_run_host(rh_program* p, int iters, int n_in, const int* in_ops, c
         RunStep(p);
         RH_CUDA(cudaStreamWaitEvent(cs, out_free[b], 0));
         for (auto& x : outs)
-          RH_CUDA(cudaMemcpyAsync(x.stage[b], p->base[0] + x.t->offset, x.t->bytes, cudaMemcpyDeviceToDevice, cs));
+          RH_CUDA(cudaMemcpyAsync(x.stage[b], p->base[0] + x.t->offset + x.off, x.bytes, cudaMemcpyDeviceToDevice, cs));
         RH_CUDA(cudaEventRecord(out_ready[b], cs));
         RH_CUDA(cudaStreamWaitEvent(sout, out_ready[b], 0));
         for (auto& x : outs)
-          RH_CUDA(cudaMemcpyAsync(out_ptrs[&x - outs.data()], x.stage[b], x.t->bytes, cudaMemcpyDeviceToHost, sout));
+          RH_CUDA(cudaMemcpyAsync(static_cast<char*>(out_ptrs[&x - outs.data()]) + x.off, x.stage[b], x.bytes,
+                                  cudaMemcpyDeviceToHost, sout));
         RH_CUDA(cudaEventRecord(out_free[b], sout));
       }
       RH_CUDA(cudaStreamWaitEvent(cs, out_free[(iters - 1) & 1], 0));
@@ -916,8 +932,9 @@ int rh_program_step_host(rh_program* p, int n_in, const int* in_ops, const void*
       const int ti = p->mat_tensor[op] >= 0 ? p->mat_tensor[op] : p->out_tensor[op];
       if (ti < 0) Fail("output has no buffer");
       const rh::Tensor& t = p->tensors[ti];
-      RH_CUDA(cudaMemcpyAsync(out_ptrs[k], p->base[0] + t.offset, t.bytes, cudaMemcpyDeviceToHost,
-                              rt->streams[0]));
+      const auto sl = OutSlice(p, op, t);
+      RH_CUDA(cudaMemcpyAsync(static_cast<char*>(out_ptrs[k]) + sl.first, p->base[0] + t.offset + sl.first,
+                              sl.second, cudaMemcpyDeviceToHost, rt->streams[0]));
     }
     RH_CUDA(cudaEventRecord(e1, rt->streams[0]));
     SyncAll(rt);

@@ -81,6 +81,20 @@ def check(rt, name, flags, dtype=None):
                 e = normwise(conv(gp.read_full(out)), conv(o.read_full(out, partitioned=False)))
                 res["err"] = max(res["err"], e)
                 res["ok"] &= e <= tol
+        if flags == 0 and any(op.id == "x" for op in prog.ops):
+            # pipelined host path vs the serial one on the same host x: outputs[0] read back as
+            # this process's 1/world slice of the materialized tensor, bit-identical
+            x = prog.op_index("x")
+            out0 = prog.outputs[0]
+            xf = np.random.default_rng(5).uniform(-1, 1, prog.full_bytes(x) // prog.elem_bytes()).astype(np.float32)
+            xin = (xf.view(np.uint32) >> 16).astype(np.uint16) if bf else xf
+            want = np.zeros(prog.full_bytes(out0), np.uint8)
+            got = np.zeros(prog.full_bytes(out0), np.uint8)
+            gp.step_host([x], [xin.ctypes.data], [want.ctypes.data])
+            gp.run_host(2, [x], [xin.ctypes.data], [got.ctypes.data])
+            part = want.size // rt.world
+            sl = slice(part * rt.first_rank, part * (rt.first_rank + 1))
+            res["ok"] &= bool(np.array_equal(got[sl], want[sl])) and bool(want[sl].any())
         if flags & RH_FLAG_NO_FUSION:
             exact = set()
             for op in prog.ops:
