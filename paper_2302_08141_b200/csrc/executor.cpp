@@ -298,6 +298,35 @@ class Lowerer {
     for (size_t i = 0; i < p_->steps.size(); ++i)
       if (p_->steps[i].p2p)
         p_->steps[i].post_sync = p_->steps[i].async || static_cast<int>(i) == last[p_->steps[i].axis];
+    // The last one on an axis: the NEXT run's first main-stream p2p transition on that axis
+    // begins with the same group's barrier.  If it comes before the step that (re)writes every
+    // tensor the last transition reads (kernel-written, own storage: not a source op, which the
+    // host may overwrite between runs, nor an alias), peers cannot overwrite what we read before
+    // we passed that barrier, and the post-barrier kernel can go too.
+    std::vector<int> first(p_->n_axes, -1);
+    for (size_t i = 0; i < p_->steps.size(); ++i) {
+      const Step& st = p_->steps[i];
+      if (st.p2p && !st.async && first[st.axis] < 0) first[st.axis] = static_cast<int>(i);
+    }
+    for (int a = 0; a < p_->n_axes; ++a) {
+      const int l = last[a];
+      if (l < 0 || getenv("RH_KEEP_LAST_POST_SYNC")) continue;
+      bool ok = true;
+      for (int t : p_->steps[l].reads) {
+        const Tensor& T = p_->tensors[t];
+        const int kind = p_->ops[T.op].kind;
+        if (T.alias >= 0 || !T.storage || kind == RH_OP_INPUT || kind == RH_OP_PARAMETER) {
+          ok = false;
+          break;
+        }
+        int writer = -1;
+        for (size_t i = 0; i < p_->steps.size() && writer < 0; ++i)
+          for (int w : p_->steps[i].writes)
+            if (w == t) writer = static_cast<int>(i);
+        ok = ok && writer > first[a];
+      }
+      if (ok) p_->steps[l].post_sync = false;
+    }
   }
 
  private:
