@@ -349,6 +349,7 @@ void DestroyProgram(rh_program* p) {
   for (int li = 0; li < rt->n_local() && li < static_cast<int>(p->owned.size()); ++li) {
     DeviceGuard dg(rt->device_of(li));
     cudaFree(p->owned[li]);
+    if (li < static_cast<int>(p->in_stage.size()) && p->in_stage[li]) cudaFree(p->in_stage[li]);
   }
   delete p;
 }
@@ -919,10 +920,26 @@ int rh_program_step_host(rh_program* p, int n_in, const int* in_ops, const void*
     WorldSync(p);
     RH_CUDA(cudaEventRecord(e0, rt->streams[0]));
     auto h0 = std::chrono::steady_clock::now();
+    // persistent staging (one buffer per local rank, grown to the largest input): no per-step
+    // cudaMallocAsync / cudaFreeAsync inside the timed region
+    size_t need = 0;
+    for (int k = 0; k < n_in; ++k) {
+      const rh::Tensor& t = p->tensors[p->out_tensor[in_ops[k]]];
+      need = std::max(need, static_cast<size_t>(Prod(t.gdims)) * rh::ElemBytes(t.dtype));
+    }
+    p->in_stage.resize(rt->n_local(), nullptr);
+    p->in_stage_bytes.resize(rt->n_local(), 0);
+    for (int li = 0; li < rt->n_local(); ++li)
+      if (p->in_stage_bytes[li] < need) {
+        DeviceGuard dgl(rt->device_of(li));
+        if (p->in_stage[li]) RH_CUDA(cudaFree(p->in_stage[li]));
+        RH_CUDA(cudaMalloc(&p->in_stage[li], need));
+        p->in_stage_bytes[li] = need;
+      }
     for (int k = 0; k < n_in; ++k) {
       const int op = in_ops[k];
       const rh::Tensor& t = p->tensors[p->out_tensor[op]];
-      WriteFull(p, t, in_ptrs[k], static_cast<size_t>(Prod(t.gdims)) * rh::ElemBytes(t.dtype), nullptr);
+      WriteFull(p, t, in_ptrs[k], static_cast<size_t>(Prod(t.gdims)) * rh::ElemBytes(t.dtype), &p->in_stage);
     }
     RunStep(p);
     if (n_outs > static_cast<int>(p->outputs.size())) Fail("too many output buffers");

@@ -121,6 +121,9 @@ struct rh_program {
   std::vector<cudaEvent_t> fork_ev, done_ev;
   std::vector<std::vector<int>> joins_at;  // main step -> async ids to wait for before it
   bool warmed = false;    // one eager run precedes capture
+  // rh_program_step_host staging for sharded inputs: [local rank] -> device buffer (grown, reused)
+  std::vector<void*> in_stage;
+  std::vector<size_t> in_stage_bytes;
 
   char* Ptr(const rh::Tensor& t, int global_rank) const { return peer_base[global_rank] + t.offset; }
   int LocalIndex(int global_rank) const;
