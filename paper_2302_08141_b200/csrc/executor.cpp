@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
 #include <sstream>
 
 using rh::Fail;
@@ -244,6 +245,9 @@ class Lowerer {
     p_->flags_off = Alloc(static_cast<size_t>(rt_->world) * 4);
     p_->counter_off = Alloc(4);
     ValidateSpecs();
+    const bool eager = rt_->dist && rt_->world > 1 && !(p_->flags & RH_FLAG_NO_OVERLAP) &&
+                       !getenv("RH_NO_EAGER_TRANSITIONS");
+    if (eager) TransitionFirstOrder();
     PlanFusion();
     for (int i : p_->order) {
       const rh_op& op = p_->ops[i];
@@ -253,10 +257,17 @@ class Lowerer {
       }
       if (absorbed_[i]) continue;  // computed by its chain head's kernel
       if (!ew_of_.empty() && ew_of_[i] >= 0) {  // elementwise chain: one kernel at its tail
-        if (ew_[ew_of_[i]].members.back() == i) EmitEwChain(ew_[ew_of_[i]]);
+        const auto& c = ew_[ew_of_[i]];
+        if (c.members.back() == i) {
+          EmitEwChain(c);
+          if (eager)
+            for (size_t j = 0; j < c.members.size(); ++j)
+              if (c.stored[j]) EagerTransitions(c.members[j]);
+        }
         continue;
       }
       EmitOp(i);
+      if (eager) EagerTransitions(chain_[i].empty() ? i : chain_[i].back());
     }
     if ((p_->flags & RH_FLAG_REDUCE_OUTPUTS) && !(p_->flags & RH_FLAG_NO_MATERIALIZE)) {
       // training-step outputs: reduce Partial axes (the gradient all-reduce / reduce of a
@@ -617,6 +628,58 @@ class Lowerer {
     PlanTransposeFold(uses, consumer, is_out);
     PlanEwChains(is_out, natural_ok, no_partial);
   }
+
+  // Dist runs: a topological order that computes the producers of resharded values as soon as
+  // they are ready (ties: the load order), and emits their transitions right after them
+  // (EagerTransitions), so that independent compute lands between a transition and its first
+  // consumer — PlanAsync then moves the transition to the side stream (at N=2 the all-gather of
+  // v runs under the q / k / score GEMMs).  Any topological order computes the same values.
+  void TransitionFirstOrder() {
+    const int n = static_cast<int>(p_->ops.size());
+    std::vector<int> pos(n), indeg(n, 0);
+    for (int k = 0; k < n; ++k) pos[p_->order[k]] = k;
+    std::vector<std::vector<int>> cons(n);
+    std::vector<char> tprod(n, 0);
+    for (int c = 0; c < n; ++c)
+      for (size_t sl = 0; sl < p_->inputs[c].size(); ++sl) {
+        const int i = p_->inputs[c][sl];
+        ++indeg[c];
+        cons[i].push_back(c);
+        if (!SpecsEq(p_->in_specs[c][sl], p_->out_specs[i])) tprod[i] = 1;
+      }
+    std::set<std::pair<int, int>> ready;  // (!tprod, load position)
+    for (int i = 0; i < n; ++i)
+      if (!indeg[i]) ready.insert({tprod[i] ? 0 : 1, pos[i]});
+    std::vector<int> order;
+    order.reserve(n);
+    while (!ready.empty()) {
+      const int i = p_->order[ready.begin()->second];
+      ready.erase(ready.begin());
+      order.push_back(i);
+      for (int c : cons[i])
+        if (--indeg[c] == 0) ready.insert({tprod[c] ? 0 : 1, pos[c]});
+    }
+    if (static_cast<int>(order.size()) == n) p_->order = order;
+  }
+
+  // Emit now every transition a consumer of `prod` will fetch (GetTensor caches it for the
+  // consumer).  Folded transposes fetch their input in the permuted spec and are left alone.
+  void EagerTransitions(int prod) {
+    if (p_->out_tensor[prod] < 0) return;
+    if (users_.empty()) {
+      users_.resize(p_->ops.size());
+      for (size_t c = 0; c < p_->ops.size(); ++c)
+        for (int i : p_->inputs[c]) users_[i].push_back(static_cast<int>(c));
+    }
+    for (int c : users_[prod]) {
+      if (absorbed_[c]) continue;  // fused consumers read inside their kernel; folded transposes
+      for (size_t sl = 0; sl < p_->inputs[c].size(); ++sl)
+        if (p_->inputs[c][sl] == prod && !SpecsEq(p_->in_specs[c][sl], p_->out_specs[prod]) &&
+            !(sl < 2 && !fold_t_.empty() && fold_t_[c][sl]))
+          GetTensor(prod, p_->in_specs[c][sl], "edge");
+    }
+  }
+  std::vector<std::vector<int>> users_;
 
   // A 2-D transpose whose only consumer is a MatMul folds into the GEMM's operand layout (the
   // tcgen05 / SIMT kernels read K-major and MN-major operands straight from the buffer): the
