@@ -647,9 +647,20 @@ class Lowerer {
         cons[i].push_back(c);
         if (!SpecsEq(p_->in_specs[c][sl], p_->out_specs[i])) tprod[i] = 1;
       }
-    std::set<std::pair<int, int>> ready;  // (!tprod, load position)
+    // lead: load position of the earliest resharded value an op leads to (itself included): the
+    // producers of resharded values first, then the ops feeding the next transition, so that
+    // independent ones fill its wait
+    std::vector<int> lead(n, n);
+    for (int k = n - 1; k >= 0; --k) {
+      const int i = p_->order[k];
+      if (tprod[i]) lead[i] = pos[i];
+      for (int c : cons[i]) lead[i] = std::min(lead[i], lead[c]);
+    }
+    // ready set ordered by (not a resharded producer, lead, load position)
+    auto key = [&](int i) { return std::make_pair((tprod[i] ? 0 : n + 1) + lead[i], pos[i]); };
+    std::set<std::pair<int, int>> ready;
     for (int i = 0; i < n; ++i)
-      if (!indeg[i]) ready.insert({tprod[i] ? 0 : 1, pos[i]});
+      if (!indeg[i]) ready.insert(key(i));
     std::vector<int> order;
     order.reserve(n);
     while (!ready.empty()) {
@@ -657,7 +668,7 @@ class Lowerer {
       ready.erase(ready.begin());
       order.push_back(i);
       for (int c : cons[i])
-        if (--indeg[c] == 0) ready.insert({tprod[c] ? 0 : 1, pos[c]});
+        if (--indeg[c] == 0) ready.insert(key(c));
     }
     if (static_cast<int>(order.size()) == n) p_->order = order;
   }
