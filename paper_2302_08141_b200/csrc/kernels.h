@@ -108,7 +108,7 @@ void LaunchSoftmaxRows(void* out, const void* in, int64_t rows, int64_t cols, in
 //   TBWD k          keep = acc; acc = keep + -((acc * in[k]) * in[k])  — the backward of tanh
 //                   (peephole of KEEP, MUL k, MUL k, UNARY neg, ADD keep; same roundings)
 // Every op result is rounded to the program dtype, as in the one-op-per-kernel path.
-constexpr int kMaxEwIn = 8, kMaxEwOut = 16, kMaxEwCode = 96;
+constexpr int kMaxEwIn = 8, kMaxEwOut = 16, kMaxEwCode = 192;
 enum EwOpcode : int32_t { kEwLoad = 0, kEwUnary = 1, kEwAdd = 2, kEwMul = 3, kEwKeep = 4, kEwStore = 5,
                           kEwTanhBwd = 6 };
 constexpr int kEwSrcKeep = 30, kEwSrcAcc = 31;
