@@ -211,7 +211,7 @@ def main():
     from paper_2302_08141_b200 import dist as D
     from paper_2302_08141_b200 import runtime as rx
     from paper_2302_08141_b200.abi import (RH_BF16, RH_F32, RH_FLAG_NO_OVERLAP, RH_FLAG_NO_PDL, RH_FLAG_REDUCE_OUTPUTS,
-                                           RH_FLAG_SIMT_GEMM, RH_FLAG_TRANSPORT_NCCL)
+                                           RH_FLAG_SIMT_GEMM, RH_FLAG_TRANSPORT_NCCL, RH_REPLICATED)
     from paper_2302_08141_b200.program import LoweredProgram
 
     wl = WORKLOADS[args.workload]
@@ -343,7 +343,13 @@ def main():
                              + (f"{wl['cpu_plan']} (1 of {scale} identical layers, time x{scale})"
                                 if scale > 1 else "the same program")
                              + f", oracle/ref_cpu_exec, {cores} threads"}
-        h2d = sum(prog.full_bytes(x) for x in xs) * world
+        # pipelined path: a fully replicated input in a multi-process run is scattered over PCIe
+        # (1/world per process) and all-gathered over NVLink (ScatterPart, abi.cpp)
+        def scattered(x):
+            return (world > 1 and os.environ.get("RH_E2E_SCATTER", "1") != "0"
+                    and all(sp.kind == RH_REPLICATED for sp in prog.ops[x].out_spec)
+                    and prog.full_bytes(x) % (world * 16) == 0)
+        h2d = sum(prog.full_bytes(x) * (1 if scattered(x) else world) for x in xs)
         # materialized outputs: each process reads its 1/world slice (rh_program_step_host)
         d2h = gp.local_bytes(out, rank) * world if reduce_outputs else prog.full_bytes(out)
         gp.close()
@@ -370,6 +376,8 @@ def main():
             "e2e": {"value": tok / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "rh_program_run_host (pinned host buffers; copies of neighbouring steps overlap)",
+                    "inputs": "replicated inputs: 1/world slice per process over PCIe + NVLink all-gather"
+                              if any(scattered(x) for x in xs) else "every process copies its inputs whole",
                     "serial": {"value": tok / (e2e_serial_ms * 1e-3), "ms_per_step": e2e_serial_ms,
                                "api": "rh_program_step_host (H2D, run, D2H back to back)"}},
             "gpu_launches": launches,

@@ -8,6 +8,7 @@
 #include <tuple>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -777,6 +778,21 @@ std::pair<size_t, size_t> OutSlice(const rh_program* p, int op, const rh::Tensor
   return {0, t.bytes};
 }
 
+// A fully replicated input in a multi-process run: each process copies only its 1/world
+// contiguous slice over PCIe and the slices are all-gathered over NVLink (every process copying
+// the whole tensor would multiply the host->device traffic by world).  Returns the slice bytes,
+// 0 when the input is copied whole (RH_E2E_SCATTER=0 disables, for A/B).
+size_t ScatterPart(const rh_program* p, const rh::Tensor& t) {
+  const rh_runtime* rt = p->mesh->rt;
+  if (!rt->dist || rt->world <= 1) return 0;
+  const char* env = std::getenv("RH_E2E_SCATTER");
+  if (env && env[0] == '0') return 0;
+  for (int a = 0; a < p->n_axes; ++a)
+    if (t.specs[a].kind != RH_REPLICATED) return 0;
+  if (t.bytes % (static_cast<size_t>(rt->world) * 16) != 0) return 0;
+  return t.bytes / rt->world;
+}
+
 // Pipelined end-to-end steps through host buffers (one local rank per process): step i's H2D
 // (copy-in stream, into a double-buffered device stage) overlaps step i-1's run and step i-2's
 // D2H (copy-out stream); the compute stream moves stage -> arena input (D2D copy, or the slice
@@ -797,6 +813,7 @@ int rh_program_run_host(rh_program* p, int iters, int n_in, const int* in_ops, c
       const rh::Tensor* t;
       size_t bytes;
       void* stage[2];
+      size_t part;  // > 0: scattered (this process copies bytes [part*g, part*(g+1)) over PCIe)
     };
     struct Out {
       const rh::Tensor* t;
@@ -809,6 +826,7 @@ int rh_program_run_host(rh_program* p, int iters, int n_in, const int* in_ops, c
       const rh::Tensor& t = p->tensors[p->out_tensor[in_ops[k]]];
       ins[k].t = &t;
       ins[k].bytes = static_cast<size_t>(Prod(t.gdims)) * rh::ElemBytes(t.dtype);
+      ins[k].part = ScatterPart(p, t);
       for (int b = 0; b < 2; ++b) RH_CUDA(cudaMalloc(&ins[k].stage[b], ins[k].bytes));
     }
     for (int k = 0; k < n_outs; ++k) {
@@ -862,8 +880,12 @@ int rh_program_run_host(rh_program* p, int iters, int n_in, const int* in_ops, c
       for (int it = 0; it < iters; ++it) {
         const int b = it & 1;
         RH_CUDA(cudaStreamWaitEvent(sin, in_free[b], 0));
-        for (auto& x : ins)
-          RH_CUDA(cudaMemcpyAsync(x.stage[b], in_ptrs[&x - ins.data()], x.bytes, cudaMemcpyHostToDevice, sin));
+        for (auto& x : ins) {
+          const size_t off = x.part * static_cast<size_t>(g), n = x.part ? x.part : x.bytes;
+          RH_CUDA(cudaMemcpyAsync(static_cast<char*>(x.stage[b]) + off,
+                                  static_cast<const char*>(in_ptrs[&x - ins.data()]) + off, n,
+                                  cudaMemcpyHostToDevice, sin));
+        }
         RH_CUDA(cudaEventRecord(in_ready[b], sin));
         RH_CUDA(cudaStreamWaitEvent(cs, in_ready[b], 0));
         for (auto& x : ins) {
@@ -874,7 +896,22 @@ int rh_program_run_host(rh_program* p, int iters, int n_in, const int* in_ops, c
             all_rep = all_rep && t.specs[a].kind == RH_REPLICATED;
             if (t.specs[a].kind == RH_PARTIAL && c[a] != 0) partial_zero = true;
           }
-          if (all_rep) {
+          if (x.part) {
+            // own slice into the arena; world barrier (every rank's slice landed, and every
+            // peer finished reading the previous step's slices); pull the peers' slices over
+            // NVLink; world barrier (no rank rewrites its slice while a peer still reads it)
+            const size_t off = x.part * static_cast<size_t>(g);
+            RH_CUDA(cudaMemcpyAsync(p->base[0] + t.offset + off, static_cast<char*>(x.stage[b]) + off, x.part,
+                                    cudaMemcpyDeviceToDevice, cs));
+            WorldSync(p);
+            for (int k = 1; k < rt->world; ++k) {
+              const int q = (g + k) % rt->world;  // rotated: no single source hot spot
+              const size_t qo = x.part * static_cast<size_t>(q);
+              RH_CUDA(cudaMemcpyAsync(p->base[0] + t.offset + qo, p->peer_base[q] + t.offset + qo, x.part,
+                                      cudaMemcpyDeviceToDevice, cs));
+            }
+            WorldSync(p);
+          } else if (all_rep) {
             RH_CUDA(cudaMemcpyAsync(p->base[0] + t.offset, x.stage[b], x.bytes, cudaMemcpyDeviceToDevice, cs));
           } else if (partial_zero) {
             rh::LaunchZero(p->base[0] + t.offset, t.bytes, cs);
