@@ -346,7 +346,7 @@ def main():
         # pipelined path: a fully replicated input in a multi-process run is scattered over PCIe
         # (1/world per process) and all-gathered over NVLink (ScatterPart, abi.cpp)
         def scattered(x):
-            return (world > 1 and os.environ.get("RH_E2E_SCATTER", "1") != "0"
+            return (world > 1 and os.environ.get("RH_E2E_SCATTER", "0") == "1"
                     and all(sp.kind == RH_REPLICATED for sp in prog.ops[x].out_spec)
                     and prog.full_bytes(x) % (world * 16) == 0)
         h2d = sum(prog.full_bytes(x) * (1 if scattered(x) else world) for x in xs)

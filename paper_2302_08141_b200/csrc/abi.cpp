@@ -780,13 +780,16 @@ std::pair<size_t, size_t> OutSlice(const rh_program* p, int op, const rh::Tensor
 
 // A fully replicated input in a multi-process run: each process copies only its 1/world
 // contiguous slice over PCIe and the slices are all-gathered over NVLink (every process copying
-// the whole tensor would multiply the host->device traffic by world).  Returns the slice bytes,
-// 0 when the input is copied whole (RH_E2E_SCATTER=0 disables, for A/B).
+// the whole tensor multiplies the host->device traffic by world).  Returns the slice bytes,
+// 0 when the input is copied whole.  Opt-in (RH_E2E_SCATTER=1): measured on C3 (r1d), the
+// barriers and the gather on the compute stream cost more than the PCIe bytes they save
+// (N=2 e2e 0.518 -> 0.634 ms, N=4 0.465 -> 0.465 ms): the whole-tensor H2D on the copy-in
+// stream overlaps the previous step's run.
 size_t ScatterPart(const rh_program* p, const rh::Tensor& t) {
   const rh_runtime* rt = p->mesh->rt;
   if (!rt->dist || rt->world <= 1) return 0;
   const char* env = std::getenv("RH_E2E_SCATTER");
-  if (env && env[0] == '0') return 0;
+  if (!env || env[0] != '1') return 0;
   for (int a = 0; a < p->n_axes; ++a)
     if (t.specs[a].kind != RH_REPLICATED) return 0;
   if (t.bytes % (static_cast<size_t>(rt->world) * 16) != 0) return 0;
