@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -627,6 +628,129 @@ class Lowerer {
     }
     PlanTransposeFold(uses, consumer, is_out);
     PlanEwChains(is_out, natural_ok, no_partial);
+    PlanRemat(is_out, no_partial);
+  }
+
+  // Rematerialization of forward tanh values (bf16 chain programs).  y = T^p(b), a run of p
+  // tanh ops from a base b whose value is stored, is one ladder-table column away from b (the
+  // table composes the per-op rounding: bit-identical).  A chain program that reads such y's
+  // reads b instead (EwArgs::vlad_*), and a forward chain member y whose every outside consumer
+  // does so is no longer stored.  Opt-in while measured (RH_REMAT=1).
+  struct Remat {
+    int base = -1;
+    Specs spec;
+    std::vector<int> col;     // per chain input: ladder column, -1 = read as is
+    std::vector<int> powers;  // per column
+  };
+  template <typename NoPartial>
+  void PlanRemat(const std::vector<bool>& is_out, NoPartial no_partial) {
+    const int n = static_cast<int>(p_->ops.size());
+    remat_.assign(ew_.size(), Remat{});
+    const char* env = getenv("RH_REMAT");
+    if (!env || env[0] != '1' || ew_.empty() || (p_->flags & RH_FLAG_KEEP_ALL)) return;
+    if (p_->ops[0].dtype != RH_BF16) return;
+    // GEMM-epilogue tails: their value is the fused kernel's stored output (a base, not a
+    // rematerialized value: the pre-epilogue value does not exist)
+    std::vector<bool> epi_tail(n, false);
+    for (int h = 0; h < n; ++h)
+      if (!chain_[h].empty()) epi_tail[chain_[h].back()] = true;
+    std::vector<int> base_of(n, -1), pow_of(n, 0);
+    for (int m : p_->order) {
+      if (!IsElementwiseUnary(m) || UnaryFn(m) != RH_FN_TANH || p_->ops[m].dtype != RH_BF16) continue;
+      const int in = p_->inputs[m][0];
+      if (!SpecsEq(p_->in_specs[m][0], p_->out_specs[in]) || !SpecsEq(p_->out_specs[m], p_->out_specs[in]) ||
+          !no_partial(p_->out_specs[m]) || GDims(m) != GDims(in))
+        continue;
+      if (pow_of[in] > 0 && !epi_tail[in]) {
+        base_of[m] = base_of[in];
+        pow_of[m] = pow_of[in] + 1;
+      } else {
+        base_of[m] = in;
+        pow_of[m] = 1;
+      }
+    }
+    auto member_pos = [&](int op) {
+      const auto& c = ew_[ew_of_[op]];
+      for (size_t j = 0; j < c.members.size(); ++j)
+        if (c.members[j] == op) return static_cast<int>(j);
+      return -1;
+    };
+    // the base's value must exist as a tensor: a source, an unfused kernel output (no epilogue
+    // chain), or a stored chain-program member
+    auto base_ok = [&](int b) {
+      if (b < 0 || !chain_[b].empty()) return false;
+      if (absorbed_[b]) return static_cast<bool>(epi_tail[b]);
+      if (ew_of_[b] >= 0) return static_cast<bool>(ew_[ew_of_[b]].stored[member_pos(b)]);
+      return true;
+    };
+    std::vector<bool> requested(n, false);
+    for (const auto& rq : p_->requests) requested[rq.first] = true;
+    for (size_t ci = 0; ci < ew_.size(); ++ci) {
+      const EwPlan& c = ew_[ci];
+      std::map<int, int> votes;
+      for (const auto& in : c.inputs)
+        if (pow_of[in.first] > 0 && SpecsEq(in.second, p_->out_specs[in.first]) && base_ok(base_of[in.first]))
+          ++votes[base_of[in.first]];
+      int b = -1, best = 0;
+      for (auto& kv : votes)
+        if (kv.second > best) {
+          best = kv.second;
+          b = kv.first;
+        }
+      if (b < 0) continue;
+      Remat r;
+      r.base = b;
+      r.spec = p_->out_specs[b];
+      r.col.assign(c.inputs.size(), -1);
+      // ladder columns in ascending power (TanhLadderTable composes column to column)
+      std::set<int> pw;
+      for (size_t k = 0; k < c.inputs.size(); ++k) {
+        const int y = c.inputs[k].first;
+        if (base_of[y] == b && pow_of[y] > 0 && SpecsEq(c.inputs[k].second, p_->out_specs[y]) &&
+            (static_cast<int>(pw.size()) < kLadderWidth || pw.count(pow_of[y])))
+          pw.insert(pow_of[y]);
+      }
+      r.powers.assign(pw.begin(), pw.end());
+      for (size_t k = 0; k < c.inputs.size(); ++k) {
+        const int y = c.inputs[k].first;
+        if (base_of[y] != b || pow_of[y] <= 0 || !SpecsEq(c.inputs[k].second, p_->out_specs[y])) continue;
+        const auto it = std::find(r.powers.begin(), r.powers.end(), pow_of[y]);
+        if (it != r.powers.end()) r.col[k] = static_cast<int>(it - r.powers.begin());
+      }
+      remat_[ci] = std::move(r);
+    }
+    // forward members no longer stored: every consumer outside their own chain rematerializes
+    std::vector<std::vector<int>> cons(n);
+    for (int i = 0; i < n; ++i)
+      for (int sidx : p_->inputs[i]) cons[sidx].push_back(i);
+    for (size_t fi = 0; fi < ew_.size(); ++fi) {
+      EwPlan& f = ew_[fi];
+      for (size_t j = 0; j + 1 < f.members.size(); ++j) {
+        const int y = f.members[j];
+        if (!f.stored[j] || pow_of[y] <= 0 || is_out[y] || requested[y]) continue;
+        bool all = true;
+        for (int cn : cons[y]) {
+          if (ew_of_[cn] == static_cast<int>(fi)) continue;
+          if (ew_of_[cn] < 0) {
+            if (getenv("RH_REMAT_DEBUG"))
+              fprintf(stderr, "remat: %s kept: consumer %s not in a chain program\n", OpName(y).c_str(), OpName(cn).c_str());
+            all = false;
+            break;
+          }
+          const Remat& r = remat_[ew_of_[cn]];
+          const auto& ci = ew_[ew_of_[cn]].inputs;
+          bool covered = false;
+          for (size_t k = 0; k < ci.size(); ++k)
+            if (ci[k].first == y && r.col.size() > k && r.col[k] >= 0) covered = true;
+          if (!covered && getenv("RH_REMAT_DEBUG"))
+            fprintf(stderr, "remat: %s kept: chain of %s (base %s) does not cover it\n", OpName(y).c_str(),
+                    OpName(cn).c_str(), r.base >= 0 ? OpName(r.base).c_str() : "-");
+          all = all && covered;
+        }
+        if (all) f.stored[j] = false;
+        if (all && getenv("RH_REMAT_DEBUG")) fprintf(stderr, "remat: %s not stored\n", OpName(y).c_str());
+      }
+    }
   }
 
   // Dist runs: a topological order that computes the producers of resharded values as soon as
@@ -999,8 +1123,26 @@ class Lowerer {
     const int h = c.members.front();
     const int dtype = P->ops[h].dtype;
     const bool bf16 = dtype == RH_BF16;
-    std::vector<int> in_t;
-    for (const auto& in : c.inputs) in_t.push_back(GetTensor(in.first, in.second, "edge"));
+    // operand code of each chain input: its in_t index, or kEwSrcVirt + ladder column
+    const int ci = ew_of_[h];
+    const Remat* rm = ci >= 0 && ci < static_cast<int>(remat_.size()) && remat_[ci].base >= 0 ? &remat_[ci] : nullptr;
+    std::vector<int> in_t, opnd(c.inputs.size(), -1);
+    int vbase = -1;
+    for (size_t k = 0; k < c.inputs.size(); ++k) {
+      if (rm && rm->col[k] >= 0) {
+        opnd[k] = kEwSrcVirt + rm->col[k];
+        continue;
+      }
+      opnd[k] = static_cast<int>(in_t.size());
+      in_t.push_back(GetTensor(c.inputs[k].first, c.inputs[k].second, "edge"));
+      if (rm && c.inputs[k].first == rm->base && SpecsEq(c.inputs[k].second, rm->spec)) vbase = opnd[k];
+    }
+    if (rm && vbase < 0) {
+      vbase = static_cast<int>(in_t.size());
+      in_t.push_back(GetTensor(rm->base, rm->spec, "edge"));
+    }
+    if (static_cast<int>(in_t.size()) > kMaxEwIn) Fail("internal: rematerialized chain has too many inputs");
+    auto opx = [&](int v) { return v >= 0 && v < kEwSrcKeep ? opnd[v] : v; };
     // tensors of the stored values
     std::vector<int> out_t;
     std::vector<int> out_slot(c.members.size(), -1);
@@ -1068,7 +1210,7 @@ class Lowerer {
     for (size_t j = 0; j < c.members.size(); ++j) {
       const int m = c.members[j];
       const auto& src = c.src[j];
-      if (j == 0) code.push_back(EwIns(kEwLoad, src[0]));
+      if (j == 0) code.push_back(EwIns(kEwLoad, opx(src[0])));
       if (IsElementwiseUnary(m)) {
         if (bf16 && in_run[j]) {
           if (run_len[j] == 0) continue;  // inside a run: covered by its first member
@@ -1084,7 +1226,7 @@ class Lowerer {
         code.push_back(EwIns(kEwUnary, UnaryFn(m)));
       } else {
         const int other = j == 0 ? src[1] : (src[0] == -1 ? src[1] : src[0]);
-        code.push_back(EwIns(p_->ops[m].kind == RH_OP_MUL ? kEwMul : kEwAdd, other));
+        code.push_back(EwIns(p_->ops[m].kind == RH_OP_MUL ? kEwMul : kEwAdd, opx(other)));
       }
       emit_after(j);
     }
@@ -1103,7 +1245,7 @@ class Lowerer {
     };
     for (size_t q = 0; q + 4 < code.size(); ++q) {
       const int32_t m = code[q + 1];
-      const bool mm = (m & 0xff) == kEwMul && (m >> 8) < kMaxEwIn && code[q + 2] == m &&
+      const bool mm = (m & 0xff) == kEwMul && ((m >> 8) < kMaxEwIn || (m >> 8) >= kEwSrcVirt) && code[q + 2] == m &&
                       code[q + 3] == EwIns(kEwUnary, RH_FN_NEG);
       if (!mm) continue;
       if (code[q] == EwIns(kEwKeep, 0) && code[q + 4] == EwIns(kEwAdd, kEwSrcKeep)) {
@@ -1148,6 +1290,11 @@ class Lowerer {
         a.lad_off = LadderTable(powers);
       }
     }
+    if (rm) {
+      a.vlad_in = vbase;
+      a.vlad_n = static_cast<int32_t>(rm->powers.size());
+      a.vlad_off = LadderTable(rm->powers);
+    }
     a.n_code = static_cast<int32_t>(code.size());
     a.n_in = static_cast<int32_t>(in_t.size());
     std::copy(code.begin(), code.end(), a.code);
@@ -1157,7 +1304,8 @@ class Lowerer {
     st.launches = 1;
     st.name = "ew_chain " + OpName(h) + ".." + OpName(c.members.back()) + " (" +
               std::to_string(c.members.size()) + " ops, " + std::to_string(in_t.size()) + " in, " +
-              std::to_string(out_t.size()) + " out)" + (a.lad_n ? " [ladder]" : "");
+              std::to_string(out_t.size()) + " out)" + (a.lad_n ? " [ladder]" : "") +
+              (a.vlad_n ? " [remat " + std::to_string(a.vlad_n) + "]" : "");
     for (int t : in_t) st.alg_bytes += static_cast<double>(P->tensors[t].bytes);
     for (int t : out_t) st.alg_bytes += static_cast<double>(P->tensors[t].bytes);
     const int first = rt_->first_rank;
@@ -1169,6 +1317,7 @@ class Lowerer {
       for (int t = 0; t < x.n_tab; ++t)
         x.tab[t] = reinterpret_cast<const uint16_t*>(P->peer_base[r] + x.tab_off[t]);
       if (x.lad_n) x.lad = reinterpret_cast<const uint4*>(P->peer_base[r] + x.lad_off);
+      if (x.vlad_n) x.vlad = reinterpret_cast<const uint4*>(P->peer_base[r] + x.vlad_off);
       LaunchEwProg(x, dtype, s);
       return 1;
     };
@@ -1537,6 +1686,7 @@ class Lowerer {
   std::map<std::vector<int>, size_t> ladder_tables_;
   std::vector<int> remote_read_;  // tensors read by peers (transition sources)
   std::vector<EwPlan> ew_;
+  std::vector<Remat> remat_;  // per chain program (PlanRemat)
   std::vector<int> ew_of_;  // op -> elementwise chain id (-1: none)
 };
 

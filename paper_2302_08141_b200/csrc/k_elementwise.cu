@@ -269,13 +269,89 @@ __device__ __forceinline__ uint32_t TanhRunLookup2(uint32_t p, const uint16_t* t
   return (p & 0x80008000u) | rlo | (rhi << 16);
 }
 
-template <bool kBf16>
+// Ladder rows of 8 packed bf16 values (2 x 16-byte shared loads each; |x| < 2^-5 and NaN pass
+// through every T^c unchanged, as in EwLadderKernel).
+__device__ __forceinline__ void LadderRows(const uint4 v, const uint4* lad_s, uint4 (&r)[8][2]) {
+  constexpr uint32_t kLo = 122u << 7, kSpan = 0x7f80u - (122u << 7), kLast = kTanhRunEntries - 1;
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const uint32_t ab = ((e & 1) ? (w[e >> 1] >> 16) : w[e >> 1]) & 0x7fffu;
+    const uint32_t u = ab - kLo;
+    const uint32_t row = min(u, kLast);
+    r[e][0] = lad_s[2 * row];
+    r[e][1] = lad_s[2 * row + 1];
+    if (u > kSpan) {
+      const uint32_t rep = ab | (ab << 16);
+      r[e][0] = r[e][1] = make_uint4(rep, rep, rep, rep);
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t U32OfRow(const uint4 (&r)[2], int w) {
+  const uint4 q = r[w >> 2];
+  return (w & 3) == 0 ? q.x : (w & 3) == 1 ? q.y : (w & 3) == 2 ? q.z : q.w;
+}
+
+template <int S>
+__device__ __forceinline__ uint4 LadderCol(const uint4 (&r)[8][2], uint4 base) {
+  constexpr uint32_t sel = (S & 1) ? 0x7632u : 0x5410u;
+  const uint32_t b[4] = {base.x, base.y, base.z, base.w};
+  uint32_t p[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    p[q] = __byte_perm(U32OfRow(r[2 * q], S >> 1), U32OfRow(r[2 * q + 1], S >> 1), sel) | (b[q] & 0x80008000u);
+  return make_uint4(p[0], p[1], p[2], p[3]);
+}
+
+// Operand k of the program: an input vector, or (k >= kEwSrcVirt) a ladder column of the
+// rematerialization base (warp-uniform switch: static register indices).
+__device__ __forceinline__ uint4 EwOperand(const uint4 (&raw)[kMaxEwIn], const uint4 (&r)[8][2], uint4 base,
+                                           int k) {
+  if (k < kEwSrcVirt) return EwPick(raw, k);
+  switch (k - kEwSrcVirt) {
+    case 0: return LadderCol<0>(r, base);
+    case 1: return LadderCol<1>(r, base);
+    case 2: return LadderCol<2>(r, base);
+    case 3: return LadderCol<3>(r, base);
+    case 4: return LadderCol<4>(r, base);
+    case 5: return LadderCol<5>(r, base);
+    case 6: return LadderCol<6>(r, base);
+    case 7: return LadderCol<7>(r, base);
+    case 8: return LadderCol<8>(r, base);
+    case 9: return LadderCol<9>(r, base);
+    case 10: return LadderCol<10>(r, base);
+    case 11: return LadderCol<11>(r, base);
+    case 12: return LadderCol<12>(r, base);
+    case 13: return LadderCol<13>(r, base);
+    case 14: return LadderCol<14>(r, base);
+    default: return LadderCol<15>(r, base);
+  }
+}
+
+// Scalar form of a ladder column (tail elements; the table in global memory).
+__device__ __forceinline__ float LadderScalar(float x, const uint4* lad, int s) {
+  constexpr uint32_t kLo = 122u << 7, kSpan = 0x7f80u - (122u << 7), kLast = kTanhRunEntries - 1;
+  const uint32_t bits = __float_as_uint(x) >> 16;
+  const uint32_t ab = bits & 0x7fffu, u = ab - kLo;
+  const uint16_t* t = reinterpret_cast<const uint16_t*>(lad);
+  const uint32_t v = u > kSpan ? ab : t[min(u, kLast) * kLadderWidth + s];
+  return __uint_as_float(((bits & 0x8000u) | v) << 16);
+}
+
+template <bool kBf16, bool kRemat = false>
 __device__ __forceinline__ void EwRunVec(const EwArgs& a, int64_t i, const uint16_t* tabs, int pc_end,
-                                         uint32_t (&acc)[4]) {
+                                         uint32_t (&acc)[4], const uint4* vlad_s = nullptr) {
   uint4 raw[kMaxEwIn];
 #pragma unroll
   for (int k = 0; k < kMaxEwIn; ++k)
     if (k < a.n_in) raw[k] = reinterpret_cast<const uint4*>(a.in[k])[i];
+  uint4 vr[8][2];
+  uint4 vbase = make_uint4(0, 0, 0, 0);
+  if constexpr (kBf16 && kRemat) {
+    vbase = EwPick(raw, a.vlad_in);
+    LadderRows(vbase, vlad_s, vr);
+  }
   uint32_t keep[4] = {0, 0, 0, 0};
 #pragma unroll
   for (int e = 0; e < 4; ++e) acc[e] = 0;
@@ -283,7 +359,7 @@ __device__ __forceinline__ void EwRunVec(const EwArgs& a, int64_t i, const uint1
     const int ins = a.code[pc], op = ins & 0xff, arg = ins >> 8;
     switch (op) {
       case kEwLoad: {
-        const uint4 v = EwPick(raw, arg);
+        const uint4 v = (kRemat ? EwOperand(raw, vr, vbase, arg) : EwPick(raw, arg));
         acc[0] = v.x; acc[1] = v.y; acc[2] = v.z; acc[3] = v.w;
         break;
       }
@@ -295,7 +371,7 @@ __device__ __forceinline__ void EwRunVec(const EwArgs& a, int64_t i, const uint1
         reinterpret_cast<uint4*>(a.out[arg])[i] = make_uint4(acc[0], acc[1], acc[2], acc[3]);
         break;
       case kEwTanhBwd: {
-        const uint4 v = EwPick(raw, arg);
+        const uint4 v = (kRemat ? EwOperand(raw, vr, vbase, arg) : EwPick(raw, arg));
         const uint32_t y[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -321,7 +397,7 @@ __device__ __forceinline__ void EwRunVec(const EwArgs& a, int64_t i, const uint1
 #pragma unroll
           for (int e = 0; e < 4; ++e) w[e] = acc[e];
         } else {
-          const uint4 v = EwPick(raw, arg);
+          const uint4 v = (kRemat ? EwOperand(raw, vr, vbase, arg) : EwPick(raw, arg));
           w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
         }
         if constexpr (kBf16) {
@@ -361,16 +437,22 @@ __device__ __forceinline__ void EwRunVec(const EwArgs& a, int64_t i, const uint1
 
 // Scalar tail (n not a multiple of the vector): same semantics on unpacked values.
 template <bool kBf16>
+__device__ __forceinline__ float EwScalarOperand(const EwArgs& a, int64_t i, int k) {
+  if (k < kEwSrcVirt) return LoadScalar<kBf16>(a.in[k], i);
+  return LadderScalar(LoadScalar<kBf16>(a.in[a.vlad_in], i), a.vlad, k - kEwSrcVirt);
+}
+
+template <bool kBf16>
 __device__ __forceinline__ void EwRunScalar(const EwArgs& a, int64_t i, const uint16_t* tabs) {
   float acc = 0.0f, keep = 0.0f;
   for (int pc = 0; pc < a.n_code; ++pc) {
     const int ins = a.code[pc], op = ins & 0xff, arg = ins >> 8;
     switch (op) {
-      case kEwLoad: acc = LoadScalar<kBf16>(a.in[arg], i); break;
+      case kEwLoad: acc = EwScalarOperand<kBf16>(a, i, arg); break;
       case kEwKeep: keep = acc; break;
       case kEwStore: StoreScalar<kBf16>(a.out[arg], i, acc); break;
       case kEwTanhBwd: {
-        const float y = LoadScalar<kBf16>(a.in[arg], i);
+        const float y = EwScalarOperand<kBf16>(a, i, arg);
         keep = acc;
         float t = __fmul_rn(acc, y);
         if (kBf16) t = RoundBf16(t);
@@ -382,7 +464,7 @@ __device__ __forceinline__ void EwRunScalar(const EwArgs& a, int64_t i, const ui
       }
       case kEwAdd:
       case kEwMul: {
-        const float w = arg == kEwSrcKeep ? keep : arg == kEwSrcAcc ? acc : LoadScalar<kBf16>(a.in[arg], i);
+        const float w = arg == kEwSrcKeep ? keep : arg == kEwSrcAcc ? acc : EwScalarOperand<kBf16>(a, i, arg);
         acc = op == kEwAdd ? __fadd_rn(acc, w) : __fmul_rn(acc, w);
         if (kBf16) acc = RoundBf16(acc);
         break;
@@ -398,13 +480,16 @@ __device__ __forceinline__ void EwRunScalar(const EwArgs& a, int64_t i, const ui
   }
 }
 
-template <bool kBf16>
+template <bool kBf16, bool kRemat>
 __global__ void __launch_bounds__(256) EwProgKernel(const __grid_constant__ EwArgs a) {
   PdlTrigger();
   __shared__ uint16_t tab_s[kBf16 ? kMaxTanhRuns * kTanhRunEntries : 1];
+  extern __shared__ uint4 vlad_s[];  // rematerialization ladder (vlad_n > 0)
   if constexpr (kBf16) {
     for (int t = 0; t < a.n_tab; ++t)
       for (int i = threadIdx.x; i < kTanhRunEntries; i += blockDim.x) tab_s[t * kTanhRunEntries + i] = a.tab[t][i];
+    if (kRemat)
+      for (int i = threadIdx.x; i < kTanhRunEntries * 2; i += blockDim.x) vlad_s[i] = a.vlad[i];
     __syncthreads();
   }
   PdlWait();
@@ -413,7 +498,7 @@ __global__ void __launch_bounds__(256) EwProgKernel(const __grid_constant__ EwAr
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nv; i += stride) {
     uint32_t acc[4];
-    EwRunVec<kBf16>(a, i, tab_s, a.n_code, acc);
+    EwRunVec<kBf16, kRemat>(a, i, tab_s, a.n_code, acc, vlad_s);
   }
   for (int64_t i = nv * E + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.n; i += stride)
     EwRunScalar<kBf16>(a, i, tab_s);
@@ -429,13 +514,17 @@ __device__ __forceinline__ uint32_t U32Of(const uint4 (&r)[2], int w) {
   return (w & 3) == 0 ? q.x : (w & 3) == 1 ? q.y : (w & 3) == 2 ? q.z : q.w;
 }
 
-__global__ void __launch_bounds__(256, 2) EwLadderKernel(const __grid_constant__ EwArgs a) {
+template <bool kRemat>
+__global__ void __launch_bounds__(256, kRemat ? 1 : 2) EwLadderKernel(const __grid_constant__ EwArgs a) {
   PdlTrigger();
   extern __shared__ uint4 lad_s[];  // kTanhRunEntries rows x 2 uint4
   __shared__ uint16_t tab_s[kMaxTanhRuns * kTanhRunEntries];
   for (int t = 0; t < a.n_tab; ++t)
     for (int i = threadIdx.x; i < kTanhRunEntries; i += blockDim.x) tab_s[t * kTanhRunEntries + i] = a.tab[t][i];
   for (int i = threadIdx.x; i < kTanhRunEntries * 2; i += blockDim.x) lad_s[i] = a.lad[i];
+  uint4* vlad_s = lad_s + kTanhRunEntries * 2;  // rematerialization ladder (vlad_n > 0)
+  if (kRemat)
+    for (int i = threadIdx.x; i < kTanhRunEntries * 2; i += blockDim.x) vlad_s[i] = a.vlad[i];
   __syncthreads();
   PdlWait();
   constexpr uint32_t kLo = 122u << 7, kSpan = 0x7f80u - (122u << 7), kLast = kTanhRunEntries - 1;
@@ -443,7 +532,7 @@ __global__ void __launch_bounds__(256, 2) EwLadderKernel(const __grid_constant__
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nv; i += stride) {
     uint32_t acc[4];
-    EwRunVec<true>(a, i, tab_s, a.lad_pc, acc);
+    EwRunVec<true, kRemat>(a, i, tab_s, a.lad_pc, acc, vlad_s);
     uint4 r[8][2];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
@@ -643,22 +732,33 @@ void LaunchSoftmaxRows(void* out, const void* in, int64_t rows, int64_t cols, in
 
 void LaunchEwProg(const EwArgs& a, int dtype, cudaStream_t s) {
   if (a.n == 0) return;
+  constexpr int kLadSmem = kTanhRunEntries * kLadderWidth * 2;
+  const int vsmem = dtype == RH_BF16 && a.vlad_n > 0 ? kLadSmem : 0;
+  int dev = 0;
+  RH_CUDA(cudaGetDevice(&dev));
   if (dtype == RH_BF16 && a.lad_n > 0) {
-    constexpr int kLadSmem = kTanhRunEntries * kLadderWidth * 2;
     static bool attr[64] = {};
-    int dev = 0;
-    RH_CUDA(cudaGetDevice(&dev));
     if (dev < 64 && !attr[dev]) {
-      RH_CUDA(cudaFuncSetAttribute(EwLadderKernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLadSmem));
+      RH_CUDA(cudaFuncSetAttribute(EwLadderKernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLadSmem));
+      RH_CUDA(cudaFuncSetAttribute(EwLadderKernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kLadSmem));
       attr[dev] = true;
     }
     // persistent-ish grid: each block stages the 28 KB ladder table once
     const int blocks = std::min(Blocks(a.n, 8), 148 * 4);
-    LaunchPdl(EwLadderKernel, blocks, 256, kLadSmem, s, a);
+    if (vsmem) LaunchPdl(EwLadderKernel<true>, blocks, 256, kLadSmem + vsmem, s, a);
+    else LaunchPdl(EwLadderKernel<false>, blocks, 256, kLadSmem, s, a);
+  } else if (dtype == RH_BF16 && vsmem) {
+    static bool attr[64] = {};
+    if (dev < 64 && !attr[dev]) {
+      RH_CUDA(cudaFuncSetAttribute(EwProgKernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, vsmem));
+      attr[dev] = true;
+    }
+    // the 28 KB rematerialization table is staged per block: persistent-ish grid
+    LaunchPdl(EwProgKernel<true, true>, std::min(Blocks(a.n, 8), 148 * 2), 256, vsmem, s, a);
   } else if (dtype == RH_BF16) {
-    LaunchPdl(EwProgKernel<true>, Blocks(a.n, 8), 256, 0, s, a);
+    LaunchPdl(EwProgKernel<true, false>, Blocks(a.n, 8), 256, 0, s, a);
   } else {
-    LaunchPdl(EwProgKernel<false>, Blocks(a.n, 4), 256, 0, s, a);
+    LaunchPdl(EwProgKernel<false, false>, Blocks(a.n, 4), 256, 0, s, a);
   }
   RH_CUDA(cudaGetLastError());
 }

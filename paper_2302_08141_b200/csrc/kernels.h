@@ -130,7 +130,14 @@ struct EwArgs {
   int32_t lad_out[kMaxEwOut];
   uint64_t lad_off;  // arena offset (host side)
   const uint4* lad;  // device pointer, patched per rank at launch
+  // rematerialized operands (bf16): operand kEwSrcVirt + s = T^{powers[s]}(in[vlad_in]), read
+  // from column s of a ladder table (the forward tanh values the backward would otherwise load;
+  // the table composes the per-op rounding, so the value is bit-identical).  vlad_n = 0: none.
+  int32_t vlad_in, vlad_n;
+  uint64_t vlad_off;  // arena offset (host side)
+  const uint4* vlad;  // device pointer, patched per rank at launch
 };
+constexpr int kEwSrcVirt = 32;
 // Ladder rows: kTanhRunEntries rows x kLadderWidth u16; row r, column s = T^{powers[s]} of the
 // row's representative |x| (the TanhRunTable indexing).
 constexpr int kLadderWidth = 16;

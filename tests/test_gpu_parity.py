@@ -358,3 +358,29 @@ def test_gpt_block_bf16(rx, oracle_lib, name):
     # same rule as fp32: within max(2e-2, 2 x the bf16 oracle's own accumulation-order error)
     tol = max(TOL_BF16, 2.0 * normwise(ref["f32"], ref["f64"]))
     assert normwise(got, ref["f64"]) <= tol, (normwise(got, ref["f64"]), tol)
+
+
+@pytest.mark.parametrize("name", ["c5_gpt_small_d2", "c5_gpt_small_d4", "c5_big_gpt1_d1"])
+def test_remat_bit_exact(rx, name, monkeypatch):
+    """Rematerialized forward tanh values (RH_REMAT=1: a chain program reads T^p(b) as a ladder
+    column of its base b instead of the stored y) give outputs bit-identical to the
+    one-op-per-kernel schedule, and the forward chains store fewer tensors."""
+    prog = LoweredProgram.load(name).with_dtype(RH_BF16)
+    outs, steps = {}, {}
+    for key, flags, remat in (("remat", 0, "1"), ("fused", 0, "0"), ("ref", RH_FLAG_NO_FUSION, "0")):
+        monkeypatch.setenv("RH_REMAT", remat)
+        rt, mesh, gp = load(rx, prog, flags)
+        try:
+            gp.init_synthetic(9)
+            gp.run(1)
+            outs[key] = [gp.read_full(o) for o in prog.outputs]
+            steps[key] = gp.steps()
+        finally:
+            close(rt, mesh, gp)
+    for o, a, b in zip(prog.outputs, outs["remat"], outs["ref"]):
+        np.testing.assert_array_equal(a, b, err_msg=f"{name}:{prog.ops[o].id}")
+    assert any("[remat" in s["name"] for s in steps["remat"]), [s["name"] for s in steps["remat"]][:30]
+
+    def ew_bytes(ss):
+        return sum(s["alg_bytes"] for s in ss if s["name"].startswith("ew_chain"))
+    assert ew_bytes(steps["remat"]) < ew_bytes(steps["fused"])
