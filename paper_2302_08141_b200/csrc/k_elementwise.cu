@@ -497,6 +497,14 @@ __global__ void __launch_bounds__(256) EwProgKernel(const __grid_constant__ EwAr
   const int64_t nv = a.n / E;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nv; i += stride) {
+    if constexpr (kRemat) {
+      // few warps per SM (128 registers): L2-prefetch the next iteration's vectors so their
+      // loads do not wait on HBM latency (no registers held)
+      const int64_t nx = i + stride;
+      if (nx < nv)
+        for (int k = 0; k < a.n_in; ++k)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint4*>(a.in[k]) + nx));
+    }
     uint32_t acc[4];
     EwRunVec<kBf16, kRemat>(a, i, tab_s, a.n_code, acc, vlad_s);
   }
