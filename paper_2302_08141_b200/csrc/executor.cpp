@@ -1257,6 +1257,27 @@ class Lowerer {
         code.erase(code.begin() + q + 2, code.begin() + q + 5);
       }
     }
+    // runs of TBWD on descending consecutive ladder columns -> one unrolled instruction
+    if (rm && !getenv("RH_REMAT_NO_RUNS")) {
+      std::vector<int32_t> fused;
+      for (size_t q = 0; q < code.size();) {
+        const int op = code[q] & 0xff, arg = code[q] >> 8;
+        size_t e = q + 1;
+        if (op == kEwTanhBwd && arg >= kEwSrcVirt) {
+          while (e < code.size() && (code[e] & 0xff) == kEwTanhBwd &&
+                 (code[e] >> 8) == arg - static_cast<int>(e - q))
+            ++e;
+        }
+        if (e - q >= 2) {
+          fused.push_back(EwIns(kEwTanhBwdLad, (arg - kEwSrcVirt) | (static_cast<int>(e - q) << 4)));
+        } else {
+          fused.push_back(code[q]);
+          e = q + 1;
+        }
+        q = e;
+      }
+      code.swap(fused);
+    }
     if (static_cast<int>(code.size()) > kMaxEwCode) Fail("internal: elementwise chain code too long");
     // tanh ladder (bf16): the maximal suffix of tanh runs and stores, from its first tanh run
     // on (stores before it belong to the prefix), with >= 3 stores -> one ladder-table row per

@@ -293,6 +293,17 @@ __device__ __forceinline__ uint32_t U32OfRow(const uint4 (&r)[2], int w) {
   return (w & 3) == 0 ? q.x : (w & 3) == 1 ? q.y : (w & 3) == 2 ? q.z : q.w;
 }
 
+// S must fold to a constant (template argument, or an unrolled loop index): static registers.
+__device__ __forceinline__ uint4 LadderColI(const uint4 (&r)[8][2], uint4 base, const int S) {
+  const uint32_t sel = (S & 1) ? 0x7632u : 0x5410u;
+  const uint32_t b[4] = {base.x, base.y, base.z, base.w};
+  uint32_t p[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    p[q] = __byte_perm(U32OfRow(r[2 * q], S >> 1), U32OfRow(r[2 * q + 1], S >> 1), sel) | (b[q] & 0x80008000u);
+  return make_uint4(p[0], p[1], p[2], p[3]);
+}
+
 template <int S>
 __device__ __forceinline__ uint4 LadderCol(const uint4 (&r)[8][2], uint4 base) {
   constexpr uint32_t sel = (S & 1) ? 0x7632u : 0x5410u;
@@ -370,6 +381,24 @@ __device__ __forceinline__ void EwRunVec(const EwArgs& a, int64_t i, const uint1
       case kEwStore:
         reinterpret_cast<uint4*>(a.out[arg])[i] = make_uint4(acc[0], acc[1], acc[2], acc[3]);
         break;
+      case kEwTanhBwdLad: {
+        if constexpr (kBf16 && kRemat) {
+          const int hi = arg & 15, cnt = arg >> 4;
+#pragma unroll
+          for (int S = 15; S >= 0; --S) {
+            if (S > hi || S <= hi - cnt) continue;
+            const uint4 v = LadderColI(vr, vbase, S);
+            const uint32_t y[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              keep[e] = acc[e];
+              const uint32_t t = MulBf16x2(MulBf16x2(acc[e], y[e]), y[e]);
+              acc[e] = AddBf16x2(keep[e], t ^ 0x80008000u);
+            }
+          }
+        }
+        break;
+      }
       case kEwTanhBwd: {
         const uint4 v = (kRemat ? EwOperand(raw, vr, vbase, arg) : EwPick(raw, arg));
         const uint32_t y[4] = {v.x, v.y, v.z, v.w};
@@ -451,6 +480,21 @@ __device__ __forceinline__ void EwRunScalar(const EwArgs& a, int64_t i, const ui
       case kEwLoad: acc = EwScalarOperand<kBf16>(a, i, arg); break;
       case kEwKeep: keep = acc; break;
       case kEwStore: StoreScalar<kBf16>(a.out[arg], i, acc); break;
+      case kEwTanhBwdLad: {
+        const int hi = arg & 15, cnt = arg >> 4;
+        const float b = LoadScalar<kBf16>(a.in[a.vlad_in], i);
+        for (int c = 0; c < cnt; ++c) {
+          const float y = LadderScalar(b, a.vlad, hi - c);
+          keep = acc;
+          float t = __fmul_rn(acc, y);
+          if (kBf16) t = RoundBf16(t);
+          t = __fmul_rn(t, y);
+          if (kBf16) t = RoundBf16(t);
+          acc = __fadd_rn(keep, -t);
+          if (kBf16) acc = RoundBf16(acc);
+        }
+        break;
+      }
       case kEwTanhBwd: {
         const float y = EwScalarOperand<kBf16>(a, i, arg);
         keep = acc;

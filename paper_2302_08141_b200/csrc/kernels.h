@@ -110,7 +110,9 @@ void LaunchSoftmaxRows(void* out, const void* in, int64_t rows, int64_t cols, in
 // Every op result is rounded to the program dtype, as in the one-op-per-kernel path.
 constexpr int kMaxEwIn = 8, kMaxEwOut = 16, kMaxEwCode = 192;
 enum EwOpcode : int32_t { kEwLoad = 0, kEwUnary = 1, kEwAdd = 2, kEwMul = 3, kEwKeep = 4, kEwStore = 5,
-                          kEwTanhBwd = 6 };
+                          kEwTanhBwd = 6, kEwTanhBwdLad = 7 };
+// kEwTanhBwdLad (rematerializing programs): a run of TBWD on ladder columns hi, hi-1, ..,
+// hi-cnt+1 (arg = hi | cnt << 4), unrolled over compile-time columns.
 constexpr int kEwSrcKeep = 30, kEwSrcAcc = 31;
 inline int32_t EwIns(int op, int arg) { return op | (arg << 8); }
 struct EwArgs {
