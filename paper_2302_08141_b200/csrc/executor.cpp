@@ -635,7 +635,7 @@ class Lowerer {
   // tanh ops from a base b whose value is stored, is one ladder-table column away from b (the
   // table composes the per-op rounding: bit-identical).  A chain program that reads such y's
   // reads b instead (EwArgs::vlad_*), and a forward chain member y whose every outside consumer
-  // does so is no longer stored.  Opt-in while measured (RH_REMAT=1).
+  // does so is no longer stored.  RH_REMAT=0 disables (A/B).
   struct Remat {
     int base = -1;
     Specs spec;
@@ -647,7 +647,7 @@ class Lowerer {
     const int n = static_cast<int>(p_->ops.size());
     remat_.assign(ew_.size(), Remat{});
     const char* env = getenv("RH_REMAT");
-    if (!env || env[0] != '1' || ew_.empty() || (p_->flags & RH_FLAG_KEEP_ALL)) return;
+    if ((env && env[0] == '0') || ew_.empty() || (p_->flags & RH_FLAG_KEEP_ALL)) return;
     if (p_->ops[0].dtype != RH_BF16) return;
     // GEMM-epilogue tails: their value is the fused kernel's stored output (a base, not a
     // rematerialized value: the pre-epilogue value does not exist)
