@@ -635,7 +635,7 @@ class Lowerer {
   // tanh ops from a base b whose value is stored, is one ladder-table column away from b (the
   // table composes the per-op rounding: bit-identical).  A chain program that reads such y's
   // reads b instead (EwArgs::vlad_*), and a forward chain member y whose every outside consumer
-  // does so is no longer stored.  RH_REMAT=0 disables (A/B).
+  // does so is no longer stored.  RH_REMAT=0 disables (A/B), RH_REMAT=1 forces it on.
   struct Remat {
     int base = -1;
     Specs spec;
@@ -646,8 +646,11 @@ class Lowerer {
   void PlanRemat(const std::vector<bool>& is_out, NoPartial no_partial) {
     const int n = static_cast<int>(p_->ops.size());
     remat_.assign(ew_.size(), Remat{});
+    // Default: on for single-process runs (one GPU, or emulated ranks); multi-process meshes
+    // need RH_REMAT=1 until the N=2 C5 hang with rematerialization is found.
     const char* env = getenv("RH_REMAT");
-    if ((env && env[0] == '0') || ew_.empty() || (p_->flags & RH_FLAG_KEEP_ALL)) return;
+    const bool on = env ? env[0] != '0' : !(rt_->dist && rt_->world > 1);
+    if (!on || ew_.empty() || (p_->flags & RH_FLAG_KEEP_ALL)) return;
     if (p_->ops[0].dtype != RH_BF16) return;
     // GEMM-epilogue tails: their value is the fused kernel's stored output (a base, not a
     // rematerialized value: the pre-epilogue value does not exist)
