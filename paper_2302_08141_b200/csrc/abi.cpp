@@ -344,6 +344,10 @@ void DestroyProgram(rh_program* p) {
       if (r != rt->first_rank && p->peer_base[r]) cudaIpcCloseMemHandle(p->peer_base[r]);
   }
   if (p->graph) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(p->graph));
+  for (auto& st : p->steps)
+    if (st.fini)
+      for (int li = 0; li < rt->n_local() && li < static_cast<int>(p->base.size()); ++li)
+        if (p->base[li]) st.fini(li);
   for (auto e : p->fork_ev) cudaEventDestroy(e);
   for (auto e : p->done_ev) cudaEventDestroy(e);
   if (p->side) cudaStreamDestroy(p->side);
@@ -632,6 +636,12 @@ int LoadProgram(rh_mesh* mesh, const rh_op* ops, int n_ops, const int* outputs, 
     p->order = q;
     rh::LowerProgram(p.get());
     Allocate(p.get());
+    for (auto& st : p->steps)  // one-time device tables (arena pointers are final now)
+      if (st.init)
+        for (int li = 0; li < p->mesh->rt->n_local(); ++li) {
+          DeviceGuard dg(p->mesh->rt->device_of(li));
+          st.init(li);
+        }
     raw = p.release();
   });
   if (rc == RH_OK) *out = raw;

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <set>
 #include <sstream>
 
@@ -249,7 +250,9 @@ class Lowerer {
     const bool eager = rt_->dist && rt_->world > 1 && !(p_->flags & RH_FLAG_NO_OVERLAP) &&
                        !getenv("RH_NO_EAGER_TRANSITIONS");
     if (eager) TransitionFirstOrder();
+    PlanGemmGroups();
     PlanFusion();
+    RefineGemmGroups();
     for (int i : p_->order) {
       const rh_op& op = p_->ops[i];
       if (op.kind == RH_OP_PARAMETER || op.kind == RH_OP_INPUT) {
@@ -264,6 +267,15 @@ class Lowerer {
           if (eager)
             for (size_t j = 0; j < c.members.size(); ++j)
               if (c.stored[j]) EagerTransitions(c.members[j]);
+        }
+        continue;
+      }
+      if (!group_of_.empty() && group_of_[i] >= 0) {  // grouped GEMM: one launch at its first member
+        const std::vector<int>& g = groups_[group_of_[i]];
+        if (g.front() == i) {
+          EmitGemmGroup(g);
+          if (eager)
+            for (int m : g) EagerTransitions(chain_[m].empty() ? m : chain_[m].back());
         }
         continue;
       }
@@ -295,7 +307,9 @@ class Lowerer {
       p_->sync_off = Alloc(static_cast<size_t>(p_->n_sync_slots) * rt_->world * 4);
       p_->epoch_off = Alloc(4);
     }
+    MergeTransitions();
     PlanAsync();
+    FinalizePulls();
     PlanArena();
     p_->arena_bytes = arena_;
     // Barrier elision: transition sources are persistent (never recycled by the arena planner)
@@ -395,6 +409,106 @@ class Lowerer {
   int Root(int t) const {
     while (p_->tensors[t].alias >= 0) t = p_->tensors[t].alias;
     return t;
+  }
+
+  // Grouped transitions: a run of consecutive peer-memory transitions on one mesh axis, none
+  // reading another's result (the per-head K / V all-gathers feeding one grouped GEMM), becomes
+  // one step: one fused barrier and one launch (PullMultiKernel) instead of one ~15-20 us
+  // latency-bound transition each.  RH_NO_GROUP_TRANSITIONS=1 disables (A/B).
+  void MergeTransitions() {
+    static const bool off = getenv("RH_NO_GROUP_TRANSITIONS") != nullptr;
+    if (off || (p_->flags & RH_FLAG_NO_FUSION)) return;
+    std::vector<Step> out;
+    std::vector<int> count;
+    for (auto& st : p_->steps) {
+      if (!out.empty() && st.kind == Step::kTransition && !st.pulls.empty()) {
+        Step& pv = out.back();
+        bool ok = pv.kind == Step::kTransition && !pv.pulls.empty() && pv.axis == st.axis &&
+                  (pv.sync_slot >= 0) == (st.sync_slot >= 0);
+        for (int r : st.reads)
+          for (int w : pv.writes) ok = ok && Root(r) != Root(w);
+        if (ok) {
+          for (auto& f : st.pulls) pv.pulls.push_back(std::move(f));
+          pv.reads.insert(pv.reads.end(), st.reads.begin(), st.reads.end());
+          pv.writes.insert(pv.writes.end(), st.writes.begin(), st.writes.end());
+          pv.wire_bytes += st.wire_bytes;
+          pv.alg_bytes += st.alg_bytes;
+          ++count.back();
+          continue;
+        }
+      }
+      out.push_back(std::move(st));
+      count.push_back(1);
+    }
+    for (size_t i = 0; i < out.size(); ++i)
+      if (count[i] > 1) out[i].name = "grouped[" + std::to_string(count[i]) + "] " + out[i].name;
+    p_->steps = std::move(out);
+  }
+
+  // Launch closures of the peer-memory transitions (after merging and overlap planning): the
+  // fused pre-barrier unless the step is overlapped (side stream: a 1-CTA barrier kernel instead
+  // of a grid spinning next to the main stream's kernels), a capped grid on the side stream,
+  // and for merged steps the grouped launch (its segment table written at load).
+  void FinalizePulls() {
+    rh_program* P = p_;
+    for (size_t i = 0; i < p_->steps.size(); ++i) {
+      Step& st = p_->steps[i];
+      if (st.pulls.empty()) continue;
+      const bool async = st.async;
+      const int slot = async ? -1 : st.sync_slot;
+      const int axis = st.axis;
+      const int n = static_cast<int>(st.pulls.size());
+      st.launches = 1;
+      auto sync_of = [P, axis, slot](int li) {
+        PeerSync y{};
+        if (slot < 0) return y;
+        const int g = P->mesh->rt->first_rank + li;
+        const std::vector<int> members = P->mesh->Group(axis, g);
+        const size_t row = P->sync_off + static_cast<size_t>(slot) * P->mesh->rt->world * 4;
+        y.d = static_cast<int>(members.size());
+        y.me = g;
+        for (size_t k = 0; k < members.size(); ++k) {
+          y.members[k] = members[k];
+          y.peer_slot[k] = reinterpret_cast<uint32_t*>(P->peer_base[members[k]] + row);
+        }
+        y.my_slot = reinterpret_cast<uint32_t*>(P->peer_base[g] + row);
+        y.epoch = reinterpret_cast<const uint32_t*>(P->peer_base[g] + P->epoch_off);
+        return y;
+      };
+      const std::vector<std::function<PullArgs(int)>> pulls = st.pulls;
+      const int cap = async ? SideBlocks() : 0;
+      if (n == 1) {
+        st.run = [pulls, sync_of, cap](int li, cudaStream_t s) {
+          PullArgs a = pulls[0](li);
+          a.max_blocks = cap;
+          a.sync = sync_of(li);
+          return LaunchPull(a, s);
+        };
+        continue;
+      }
+      const size_t off = Alloc(PullMultiTableBytes(n));
+      auto ok = std::make_shared<std::vector<char>>(rt_->n_local(), 0);
+      st.init = [P, pulls, cap, off, ok](int li) {
+        std::vector<PullArgs> v;
+        for (const auto& f : pulls) v.push_back(f(li));
+        (*ok)[li] = PreparePullMulti(v.data(), static_cast<int>(v.size()), cap,
+                                     P->peer_base[P->mesh->rt->first_rank + li] + off);
+      };
+      st.fini = [P, off](int li) { ReleasePullMulti(P->peer_base[P->mesh->rt->first_rank + li] + off); };
+      st.run = [P, pulls, sync_of, cap, off, ok](int li, cudaStream_t s) {
+        if ((*ok)[li]) return LaunchPullMulti(P->peer_base[P->mesh->rt->first_rank + li] + off, sync_of(li), s);
+        // not groupable (zero-fill / staged / mixed kinds): one pull each, the first one's
+        // barrier orders all of them (every source was produced before the step)
+        int launches = 0;
+        for (size_t k = 0; k < pulls.size(); ++k) {
+          PullArgs a = pulls[k](li);
+          a.max_blocks = cap;
+          if (k == 0) a.sync = sync_of(li);
+          launches += LaunchPull(a, s);
+        }
+        return launches;
+      };
+    }
   }
 
   // Arena planner: tensor storage is placed after lowering, from the schedule's liveness.
@@ -630,6 +744,193 @@ class Lowerer {
     PlanEwChains(is_out, natural_ok, no_partial);
     PlanRemat(is_out, no_partial);
   }
+
+  // Horizontal fusion of independent MatMuls (the per-head q/k/v, score and context GEMMs of
+  // the 32-head block: 96 + 32 + 32 rank-2 matmuls, each far below a wave): MatMuls with the
+  // same local shapes, transposes, specs and DAG depth (no path can join two ops of equal depth)
+  // run as one grouped tcgen05 launch (GemmTcGroup).  The schedule order is re-derived on the
+  // DAG with every group contracted to one node, so each group's members are contiguous and
+  // all their inputs precede the first of them.  Membership is refined after fusion planning
+  // (equal epilogue chains and folded-transpose flags).  RH_NO_GEMM_GROUP=1 disables (A/B).
+  void PlanGemmGroups() {
+    const int n = static_cast<int>(p_->ops.size());
+    group_of_.assign(n, -1);
+    groups_.clear();
+    if ((p_->flags & (RH_FLAG_NO_FUSION | RH_FLAG_SIMT_GEMM)) || getenv("RH_NO_GEMM_GROUP")) return;
+    std::vector<int> depth(n, 0);
+    for (int i : p_->order)
+      for (int s : p_->inputs[i]) depth[i] = std::max(depth[i], depth[s] + 1);
+    std::map<std::string, std::vector<int>> cand;
+    for (int i : p_->order) {
+      const rh_op& op = p_->ops[i];
+      if (op.kind != RH_OP_MATMUL || op.dtype != RH_BF16 || p_->inputs[i].size() != 2) continue;
+      try {
+        if (!SpecsEq(NaturalSpecs(i, p_->in_specs[i]), p_->out_specs[i])) continue;
+      } catch (const Error&) {
+        continue;
+      }
+      std::ostringstream key;
+      key << depth[i] << '|' << op.transpose_a << op.transpose_b << '|' << SpecsStr(p_->out_specs[i]);
+      for (int sl = 0; sl < 2; ++sl) {
+        key << '|' << SpecsStr(p_->in_specs[i][sl]);
+        for (auto x : LocalDims(GDims(p_->inputs[i][sl]), p_->in_specs[i][sl], mesh_, p_->n_axes)) key << ',' << x;
+      }
+      cand[key.str()].push_back(i);
+    }
+    for (auto& kv : cand) {
+      if (kv.second.size() < 2) continue;
+      for (int m : kv.second) group_of_[m] = static_cast<int>(groups_.size());
+      groups_.push_back(kv.second);
+    }
+    if (groups_.empty()) return;
+    // contracted topological order (ties: the earliest member's position in the current order)
+    std::vector<int> pos(n);
+    for (int k = 0; k < n; ++k) pos[p_->order[k]] = k;
+    auto node = [&](int i) { return group_of_[i] >= 0 ? n + group_of_[i] : i; };
+    const int nn = n + static_cast<int>(groups_.size());
+    std::vector<std::vector<int>> members(nn);
+    for (int k = 0; k < n; ++k) members[node(p_->order[k])].push_back(p_->order[k]);
+    std::vector<int> prio(nn, n), indeg(nn, 0);
+    std::vector<std::vector<int>> succ(nn);
+    for (int i = 0; i < n; ++i) {
+      prio[node(i)] = std::min(prio[node(i)], pos[i]);
+      for (int s : p_->inputs[i]) {
+        succ[node(s)].push_back(node(i));
+        ++indeg[node(i)];
+      }
+    }
+    std::set<std::pair<int, int>> ready;
+    for (int v = 0; v < nn; ++v)
+      if (!members[v].empty() && indeg[v] == 0) ready.insert({prio[v], v});
+    std::vector<int> order;
+    while (!ready.empty()) {
+      const int v = ready.begin()->second;
+      ready.erase(ready.begin());
+      for (int m : members[v]) order.push_back(m);
+      for (int w : succ[v])
+        if (--indeg[w] == 0) ready.insert({prio[w], w});
+    }
+    if (static_cast<int>(order.size()) != n) Fail("internal: grouped schedule is not a topological order");
+    p_->order = order;
+    for (auto& g : groups_) std::sort(g.begin(), g.end(), [&](int a, int b) {
+      return std::find(order.begin(), order.end(), a) < std::find(order.begin(), order.end(), b);
+    });
+  }
+
+  // After fusion planning: members of one launch must share the epilogue chain (unary fns of
+  // the fused tail) and the folded-transpose flags.  Singletons fall back to a plain GEMM.
+  void RefineGemmGroups() {
+    if (groups_.empty()) return;
+    std::vector<std::vector<int>> out;
+    std::fill(group_of_.begin(), group_of_.end(), -1);
+    for (const auto& g : groups_) {
+      std::map<std::string, std::vector<int>> parts;
+      std::vector<std::string> keys;
+      for (int m : g) {
+        std::ostringstream k;
+        for (int v : chain_[m]) k << UnaryFn(v) << ',';
+        if (!fold_t_.empty()) k << '|' << fold_t_[m][0] << fold_t_[m][1];
+        if (!parts.count(k.str())) keys.push_back(k.str());
+        parts[k.str()].push_back(m);
+      }
+      for (const auto& k : keys) {
+        if (parts[k].size() < 2) continue;
+        for (int m : parts[k]) group_of_[m] = static_cast<int>(out.size());
+        out.push_back(parts[k]);
+      }
+    }
+    groups_ = std::move(out);
+  }
+
+  // One grouped tcgen05 launch for the members (all inputs already computed: they precede the
+  // group in the schedule).  Falls back to one GEMM per member when the grouped kernel cannot
+  // take the shape.
+  void EmitGemmGroup(const std::vector<int>& mem) {
+    rh_program* P = p_;
+    const int n = static_cast<int>(mem.size());
+    std::vector<std::array<int, 2>> in_t(n);
+    std::vector<int> out_t(n);
+    for (int k = 0; k < n; ++k) {
+      const int i = mem[k];
+      for (int sl = 0; sl < 2; ++sl) {
+        if (!fold_t_.empty() && fold_t_[i][sl]) {
+          const int t = p_->inputs[i][sl];
+          in_t[k][sl] = GetTensor(p_->inputs[t][0], Transposed(p_->in_specs[i][sl]), "edge");
+        } else {
+          in_t[k][sl] = GetTensor(p_->inputs[i][sl], p_->in_specs[i][sl], "edge");
+        }
+      }
+      p_->in_tensor[i] = {in_t[k][0], in_t[k][1]};
+      for (int sl = 0; sl < 2; ++sl)
+        if (!fold_t_.empty() && fold_t_[i][sl]) p_->in_tensor[i][sl] = -1;
+    }
+    for (int k = 0; k < n; ++k) {
+      const int i = mem[k];
+      const int tail = chain_[i].empty() ? i : chain_[i].back();
+      out_t[k] = NewTensor(tail, p_->out_specs[i]);
+      if (tail != i) p_->tensors[out_t[k]].gdims = GDims(i);
+      p_->out_tensor[tail] = out_t[k];
+    }
+    const int i0 = mem[0];
+    const rh_op& op = P->ops[i0];
+    const Dims ad = P->tensors[in_t[0][0]].ldims, bd = P->tensors[in_t[0][1]].ldims;
+    const bool fa = !fold_t_.empty() && fold_t_[i0][0], fb = !fold_t_.empty() && fold_t_[i0][1];
+    GemmArgs g{};
+    g.ta = op.transpose_a != fa;
+    g.tb = op.transpose_b != fb;
+    g.m = g.ta ? ad[1] : ad[0];
+    g.k = g.ta ? ad[0] : ad[1];
+    g.n = g.tb ? bd[0] : bd[1];
+    g.dtype = op.dtype;
+    g.epi = ChainOf(i0, false);
+    bool shared_a = true;
+    for (int k = 1; k < n; ++k) shared_a = shared_a && in_t[k][0] == in_t[0][0];
+    if (!GemmTcGroupSupported(g, n, shared_a)) {
+      for (int k = 0; k < n; ++k) EmitKernel(mem[k], {in_t[k][0], in_t[k][1]}, out_t[k]);
+      return;
+    }
+    const size_t off = Alloc(GemmTcGroupTableBytes(n));
+    Step st;
+    st.kind = Step::kKernel;
+    st.launches = 1;
+    st.name = "gemm_tc_group[" + std::to_string(n) + "] " + OpName(mem.front()) + ".." + OpName(mem.back()) +
+              (fa || fb ? " [T-folded]" : "") + GemmTcGroupSchedule(g, n, shared_a);
+    st.alg_flops = 2.0 * g.m * g.n * g.k * n;
+    std::set<int> rd;
+    for (int k = 0; k < n; ++k) {
+      rd.insert(in_t[k][0]);
+      rd.insert(in_t[k][1]);
+    }
+    for (int t : rd) st.alg_bytes += static_cast<double>(P->tensors[t].bytes);
+    for (int t : out_t) st.alg_bytes += static_cast<double>(P->tensors[t].bytes);
+    const int first = rt_->first_rank;
+    st.init = [P, g, in_t, out_t, off, first, n](int li) {
+      const int r = first + li;
+      std::vector<const void*> a(n), b(n);
+      std::vector<void*> c(n);
+      for (int k = 0; k < n; ++k) {
+        a[k] = P->Ptr(P->tensors[in_t[k][0]], r);
+        b[k] = P->Ptr(P->tensors[in_t[k][1]], r);
+        c[k] = P->Ptr(P->tensors[out_t[k]], r);
+      }
+      GemmArgs x = g;
+      x.epi = Patch(P, g.epi, r);
+      PrepareGemmTcGroup(x, n, a.data(), b.data(), c.data(), P->peer_base[r] + off);
+    };
+    st.fini = [P, off, first](int li) { ReleaseGemmTcGroup(P->peer_base[first + li] + off); };
+    st.run = [P, g, off, first](int li, cudaStream_t s) {
+      const int r = first + li;
+      GemmArgs x = g;
+      x.epi = Patch(P, g.epi, r);
+      LaunchGemmTcGroup(x, P->peer_base[r] + off, s);
+      return 1;
+    };
+    st.reads.assign(rd.begin(), rd.end());
+    st.writes = out_t;
+    AddStep(std::move(st));
+  }
+  std::vector<int> group_of_;             // op -> grouped GEMM id (-1: none)
+  std::vector<std::vector<int>> groups_;  // members in schedule order
 
   // Rematerialization of forward tanh values (bf16 chain programs).  y = T^p(b), a run of p
   // tanh ops from a base b whose value is stored, is one ladder-table column away from b (the
@@ -1612,37 +1913,21 @@ class Lowerer {
     // (not for zero-fill targets, whose non-zero-coordinate ranks launch no kernel).
     if (st.p2p && rt_->dist && rt_->world > 1 && to.kind != RH_PARTIAL) st.sync_slot = p_->n_sync_slots++;
     if (!nccl) {
-      const int slot = st.sync_slot;
-      const size_t si = p_->steps.size();  // this step's index
-      st.run = [P, src, dst, axis, fv, tv, dtype, slot, si](int li, cudaStream_t s) {
+      // the launch (and the fused barrier) is set up by FinalizePulls once transitions are
+      // merged and the overlap plan is known
+      st.pulls.push_back([P, src, dst, axis, fv, tv, dtype](int li) {
         const int g = P->mesh->rt->first_rank + li;
         const std::vector<int> members = P->mesh->Group(axis, g);
-        const int coord = P->mesh->Coords(g)[axis];
         PullArgs a{};
         a.dst = P->Ptr(P->tensors[dst], g);
         for (size_t k = 0; k < members.size(); ++k) a.src[k] = P->Ptr(P->tensors[src], members[k]);
         a.from = fv;
         a.to = tv;
-        a.coord = coord;
+        a.coord = P->mesh->Coords(g)[axis];
         a.n_dst = P->tensors[dst].elems();
         a.dtype = dtype;
-        const bool async = P->steps[si].async;
-        if (async) a.max_blocks = SideBlocks();  // side stream: leave SMs to compute
-        // async: the pre-barrier is a 1-CTA kernel before the pull (no grid-wide spinning next
-        // to the main stream's kernels)
-        if (slot >= 0 && !async) {
-          const size_t row = P->sync_off + static_cast<size_t>(slot) * P->mesh->rt->world * 4;
-          a.sync.d = static_cast<int>(members.size());
-          a.sync.me = g;
-          for (size_t k = 0; k < members.size(); ++k) {
-            a.sync.members[k] = members[k];
-            a.sync.peer_slot[k] = reinterpret_cast<uint32_t*>(P->peer_base[members[k]] + row);
-          }
-          a.sync.my_slot = reinterpret_cast<uint32_t*>(P->peer_base[g] + row);
-          a.sync.epoch = reinterpret_cast<const uint32_t*>(P->peer_base[g] + P->epoch_off);
-        }
-        return LaunchPull(a, s);
-      };
+        return a;
+      });
     } else {
       // Baseline: NCCL collective on this axis's communicator (+ pack/unpack pull kernels).
       const size_t chunk = static_cast<size_t>(Prod(LocalDims(D, {from.kind == RH_SHARD ? from : to}, {d}, 1)));

@@ -77,6 +77,12 @@ struct Step {
   int async_id = -1;   // index into the program's fork/done events
   // Enqueue this step for local rank `li` on stream `s`; returns the launches issued.
   std::function<int(int li, cudaStream_t s)> run;
+  // Optional one-time setup after the arena is allocated (device tables that hold arena
+  // pointers, e.g. a grouped GEMM's TMA maps) and its teardown at program destruction.
+  std::function<void(int li)> init, fini;
+  // Peer-memory transitions (p2p, not NCCL): one pull per single-axis transition; several
+  // independent transitions of one axis merged into this step run as one grouped launch.
+  std::vector<std::function<PullArgs(int li)>> pulls;
 };
 
 }  // namespace rh

@@ -20,6 +20,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <vector>
 
 #include "kernels.h"
 #include "launch.cuh"
@@ -171,6 +172,15 @@ __global__ void __launch_bounds__(256) SplitReduceBf16(__nv_bfloat16* __restrict
   }
 }
 
+// Grouped launches (GemmTcGroup): independent problems of equal shape, laid side by side along
+// a virtual N = n_prob * seg_n.  Tables live in device memory (written once at program load).
+struct GroupDev {
+  const CUtensorMap* b;       // [n_prob] B maps
+  const CUtensorMap* a;       // [n_prob] A maps, or nullptr: every problem reads the kernel's A
+  __nv_bfloat16* const* c;    // [n_prob] outputs, row pitch seg_n
+  int seg_n;                  // columns per problem
+};
+
 template <int BN, bool kBKMajor, bool kAKMajor, int KB = BK>
 struct TcCfg {
   static constexpr int kABytes = BM * KB * 2;
@@ -192,11 +202,11 @@ struct TcCfg {
 // non-transposed-B layouts) — the MMA reads both straight from the swizzled tiles, no
 // transpose pass.  KB = K elements per pipeline stage: 64, or 128 for the 128-wide tiles (twice
 // the MMA work per barrier round trip: their 128 x 128 x 64 k-blocks were issue-latency-bound).
-template <int BN, bool kBKMajor, bool kAKMajor, int KB>
+template <int BN, bool kBKMajor, bool kAKMajor, int KB, bool kGroup = false>
 __global__ void __launch_bounds__(kThreads, 1)
     GemmTcKernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                  __nv_bfloat16* __restrict__ C, int M, int N, int K, ChainArgs epi, int ksplit,
-                 float* __restrict__ ws) {
+                 float* __restrict__ ws, GroupDev grp) {
   PdlTrigger();
   // Work unit = (m tile, n tile, k split).  ksplit > 1 (few tiles: the sharded GEMMs at N >= 4)
   // writes fp32 partial tiles to ws[split][M][N]; SplitReduceBf16 finishes them.
@@ -214,8 +224,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kblocks = K / KB / ksplit;  // per split
 
   if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
+    if (!kGroup) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
+    }
     for (int s = 0; s < Cfg::kStages; ++s) {
       MbarInit(&full[s], 1);
       MbarInit(&empty[s], 1);
@@ -244,6 +256,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         const int t = tile % mn, ks = tile / mn;
         const int m_blk = t % num_m, n_blk = t / num_m;
+        // operand maps of this tile: grouped launches pick each problem's map (the B column
+        // chunk's problem; A per problem unless shared) from the device table
+        const CUtensorMap* ma = &tma_a;
+        const CUtensorMap* mb[BN / 64];
+        int cb[BN / 64];
+#pragma unroll
+        for (int j = 0; j < BN / 64; ++j) {
+          const int col = n_blk * BN + (kBKMajor ? 0 : j * 64);
+          mb[j] = &tma_b;
+          cb[j] = col;
+          if constexpr (kGroup) {
+            mb[j] = grp.b + col / grp.seg_n;
+            cb[j] = col % grp.seg_n;
+          }
+        }
+        if constexpr (kGroup) {
+          if (grp.a) ma = grp.a + (n_blk * BN) / grp.seg_n;
+        }
         for (int kb = ks * kblocks; kb < (ks + 1) * kblocks; ++kb) {
           MbarWait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::kStage;
@@ -252,20 +282,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (kAKMajor) {
 #pragma unroll
             for (int q = 0; q < KB / 64; ++q)
-              TmaLoad2D(sa + q * (BM * 128), &tma_a, &full[stage], kb * KB + q * 64, m_blk * BM);
+              TmaLoad2D(sa + q * (BM * 128), ma, &full[stage], kb * KB + q * 64, m_blk * BM);
           } else {
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j)
-              TmaLoad2D(sa + j * (64 * KB * 2), &tma_a, &full[stage], m_blk * BM + j * 64, kb * KB);
+              TmaLoad2D(sa + j * (64 * KB * 2), ma, &full[stage], m_blk * BM + j * 64, kb * KB);
           }
           if constexpr (kBKMajor) {
 #pragma unroll
             for (int q = 0; q < KB / 64; ++q)
-              TmaLoad2D(sb + q * (BN * 128), &tma_b, &full[stage], kb * KB + q * 64, n_blk * BN);
+              TmaLoad2D(sb + q * (BN * 128), mb[0], &full[stage], kb * KB + q * 64, cb[0]);
           } else {
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
-              TmaLoad2D(sb + j * (64 * KB * 2), &tma_b, &full[stage], n_blk * BN + j * 64, kb * KB);
+              TmaLoad2D(sb + j * (64 * KB * 2), mb[j], &full[stage], cb[j], kb * KB);
           }
           if (++stage == Cfg::kStages) {
             stage = 0;
@@ -326,6 +356,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
         TmemLd32(tmem + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
+        if constexpr (kGroup) {  // this 32-column chunk's problem and column within it
+          const int col = n_blk * BN + c * 32;
+          crow = grp.c[col / grp.seg_n] + static_cast<int64_t>(row) * grp.seg_n + col % grp.seg_n - c * 32;
+        }
         if (wrow) {  // split-K partial (fp32, unrounded)
           float4* dst = reinterpret_cast<float4*>(wrow + c * 32);
 #pragma unroll
@@ -443,11 +477,11 @@ struct Tc2Cfg {
                                      (static_cast<uint32_t>((2 * BM) >> 4) << 24);  // M = 256
 };
 
-template <int BN, bool kBKMajor, bool kAKMajor>
+template <int BN, bool kBKMajor, bool kAKMajor, bool kGroup = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     GemmTcPairKernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                      __nv_bfloat16* __restrict__ C, int M, int N, int K, ChainArgs epi, int ksplit,
-                     float* __restrict__ ws) {
+                     float* __restrict__ ws, GroupDev grp) {
   PdlTrigger();
   using Cfg = Tc2Cfg<BN, kBKMajor, kAKMajor>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -466,8 +500,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int kblocks = K / BK / ksplit;
 
   if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
+    if (!kGroup) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
+    }
     for (int st = 0; st < Cfg::kStages; ++st) {
       MbarInit(&full[st], 1);
       MbarInit(&empty[st], 1);
@@ -498,6 +534,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int m_blk = t % num_m, n_blk = t / num_m;
         const int m0 = m_blk * 2 * BM + static_cast<int>(rank) * BM;
         const int n0 = n_blk * BN + static_cast<int>(rank) * (BN / 2);
+        const CUtensorMap* ma = &tma_a;
+        const CUtensorMap* mb[BN / 128];
+        int cb[BN / 128];
+#pragma unroll
+        for (int j = 0; j < BN / 128; ++j) {
+          const int col = n0 + (kBKMajor ? 0 : j * 64);
+          mb[j] = &tma_b;
+          cb[j] = col;
+          if constexpr (kGroup) {
+            mb[j] = grp.b + col / grp.seg_n;
+            cb[j] = col % grp.seg_n;
+          }
+        }
+        if constexpr (kGroup) {
+          if (grp.a) ma = grp.a + (n_blk * BN) / grp.seg_n;
+        }
         for (int kb = ks * kblocks; kb < (ks + 1) * kblocks; ++kb) {
           MbarWait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::kStage;
@@ -505,16 +557,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint32_t fb = MapaShared(SmemU32(&full[stage]), 0);
           if (leader) MbarExpectTx(&full[stage], 2 * Cfg::kStage);
           if constexpr (kAKMajor) {
-            TmaLoad2D2Sm(sa, &tma_a, fb, kb * BK, m0);
+            TmaLoad2D2Sm(sa, ma, fb, kb * BK, m0);
           } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) TmaLoad2D2Sm(sa + j * (64 * BK * 2), &tma_a, fb, m0 + j * 64, kb * BK);
+            for (int j = 0; j < BM / 64; ++j) TmaLoad2D2Sm(sa + j * (64 * BK * 2), ma, fb, m0 + j * 64, kb * BK);
           }
           if constexpr (kBKMajor) {
-            TmaLoad2D2Sm(sb, &tma_b, fb, kb * BK, n0);
+            TmaLoad2D2Sm(sb, mb[0], fb, kb * BK, cb[0]);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 128; ++j) TmaLoad2D2Sm(sb + j * (64 * BK * 2), &tma_b, fb, n0 + j * 64, kb * BK);
+            for (int j = 0; j < BN / 128; ++j) TmaLoad2D2Sm(sb + j * (64 * BK * 2), mb[j], fb, cb[j], kb * BK);
           }
           if (++stage == Cfg::kStages) {
             stage = 0;
@@ -576,6 +628,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
         TmemLd32(tmem + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
+        if constexpr (kGroup) {
+          const int col = n_blk * BN + c * 32;
+          crow = grp.c[col / grp.seg_n] + static_cast<int64_t>(row) * grp.seg_n + col % grp.seg_n - c * 32;
+        }
         if (wrow) {
           float4* dst = reinterpret_cast<float4*>(wrow + c * 32);
 #pragma unroll
@@ -986,25 +1042,34 @@ int KSplitPair(const GemmArgs& g, int bn) {
   return best;
 }
 
-template <int BN, bool kBK, bool kAK, int KB>
-void LaunchKB(const GemmArgs& g, cudaStream_t s) {
+// A grouped launch (GemmTcGroup): problem 0's maps as the kernel-param maps (the shared A),
+// the device table, and the problem count.
+struct GroupLaunch {
+  Maps m0;
+  GroupDev dev;
+  int n_prob;
+};
+
+template <int BN, bool kBK, bool kAK, int KB, bool kG = false>
+void LaunchKB(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullptr) {
   using Cfg = TcCfg<BN, kBK, kAK, KB>;
   int dev = 0;
   RH_CUDA(cudaGetDevice(&dev));
   static bool attr[64] = {};  // per device (local multi-GPU runtimes)
   if (dev < 64 && !attr[dev]) {
-    RH_CUDA(cudaFuncSetAttribute(GemmTcKernel<BN, kBK, kAK, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RH_CUDA(cudaFuncSetAttribute(GemmTcKernel<BN, kBK, kAK, KB, kG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Cfg::kSmem));
     attr[dev] = true;
   }
-  const Maps& mp = GetMaps(g, BN, KB);
-  const int ks = g.scratch ? KSplit(g, BN) : 1;
-  const int tiles = static_cast<int>((g.m / BM) * (g.n / BN)) * ks;
+  const Maps& mp = kG ? gl->m0 : GetMaps(g, BN, KB);
+  const int64_t n = kG ? g.n * gl->n_prob : g.n;
+  const int ks = g.scratch && !kG ? KSplit(g, BN) : 1;
+  const int tiles = static_cast<int>((g.m / BM) * (n / BN)) * ks;
   const int grid = std::min(tiles, NumSms());
   float* ws = ks > 1 ? static_cast<float*>(g.scratch) : nullptr;
-  LaunchPdl(GemmTcKernel<BN, kBK, kAK, KB>, grid, kThreads, Cfg::kSmem, s, 
-      mp.a, mp.b, static_cast<__nv_bfloat16*>(g.c), static_cast<int>(g.m), static_cast<int>(g.n),
-      static_cast<int>(g.k), g.epi, ks, ws);
+  LaunchPdl(GemmTcKernel<BN, kBK, kAK, KB, kG>, grid, kThreads, Cfg::kSmem, s,
+      mp.a, mp.b, static_cast<__nv_bfloat16*>(g.c), static_cast<int>(g.m), static_cast<int>(n),
+      static_cast<int>(g.k), g.epi, ks, ws, kG ? gl->dev : GroupDev{});
   RH_CUDA(cudaGetLastError());
   if (ws) {
     const int64_t n4 = g.m * g.n / 4;
@@ -1016,28 +1081,29 @@ void LaunchKB(const GemmArgs& g, cudaStream_t s) {
 }
 
 // KB = 128 K elements per stage for 128-wide tiles when every split holds whole 128-chunks.
-template <int BN, bool kBK, bool kAK>
-void Launch(const GemmArgs& g, cudaStream_t s) {
-  const int ks = g.scratch ? KSplit(g, BN) : 1;
-  if (BN == 128 && g.k % (128 * ks) == 0) LaunchKB<BN, kBK, kAK, 128>(g, s);
-  else LaunchKB<BN, kBK, kAK, 64>(g, s);
+template <int BN, bool kBK, bool kAK, bool kG = false>
+void Launch(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullptr) {
+  const int ks = g.scratch && !kG ? KSplit(g, BN) : 1;
+  if (BN == 128 && g.k % (128 * ks) == 0) LaunchKB<BN, kBK, kAK, 128, kG>(g, s, gl);
+  else LaunchKB<BN, kBK, kAK, 64, kG>(g, s, gl);
 }
 
 // Pair-tile (256 x BN) launch: clusters of 2 CTAs, one pair per TPC, persistent over the tiles.
-template <int BN, bool kBK, bool kAK>
-void LaunchPair(const GemmArgs& g, cudaStream_t s) {
+template <int BN, bool kBK, bool kAK, bool kG = false>
+void LaunchPair(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullptr) {
   using Cfg = Tc2Cfg<BN, kBK, kAK>;
   int dev = 0;
   RH_CUDA(cudaGetDevice(&dev));
   static bool attr[64] = {};
   if (dev < 64 && !attr[dev]) {
-    RH_CUDA(cudaFuncSetAttribute(GemmTcPairKernel<BN, kBK, kAK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RH_CUDA(cudaFuncSetAttribute(GemmTcPairKernel<BN, kBK, kAK, kG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Cfg::kSmem));
     attr[dev] = true;
   }
-  const Maps& mp = GetMaps(g, BN / 2);  // B box: half of the pair's columns per CTA
-  const int ks = g.scratch ? KSplitPair(g, BN) : 1;
-  const int tiles = static_cast<int>((g.m / (2 * BM)) * (g.n / BN)) * ks;
+  const Maps& mp = kG ? gl->m0 : GetMaps(g, BN / 2);  // B box: half of the pair's columns per CTA
+  const int64_t n = kG ? g.n * gl->n_prob : g.n;
+  const int ks = g.scratch && !kG ? KSplitPair(g, BN) : 1;
+  const int tiles = static_cast<int>((g.m / (2 * BM)) * (n / BN)) * ks;
   const int pairs = std::min(tiles, NumSms() / 2);
   float* ws = ks > 1 ? static_cast<float*>(g.scratch) : nullptr;
   cudaLaunchConfig_t cfg{};
@@ -1054,8 +1120,9 @@ void LaunchPair(const GemmArgs& g, cudaStream_t s) {
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = PdlEnabled() ? 2 : 1;
-  RH_CUDA(cudaLaunchKernelEx(&cfg, GemmTcPairKernel<BN, kBK, kAK>, mp.a, mp.b, static_cast<__nv_bfloat16*>(g.c),
-                             static_cast<int>(g.m), static_cast<int>(g.n), static_cast<int>(g.k), g.epi, ks, ws));
+  RH_CUDA(cudaLaunchKernelEx(&cfg, GemmTcPairKernel<BN, kBK, kAK, kG>, mp.a, mp.b, static_cast<__nv_bfloat16*>(g.c),
+                             static_cast<int>(g.m), static_cast<int>(n), static_cast<int>(g.k), g.epi, ks, ws,
+                             kG ? gl->dev : GroupDev{}));
   if (ws) {
     const int64_t n4 = g.m * g.n / 4;
     const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 148 * 8)));
@@ -1190,6 +1257,131 @@ const char* GemmTcSchedule(const GemmArgs& g) {
 int GemmTcLaunches(const GemmArgs& g) {
   if (g.dtype == RH_F32) return 3;
   return ScheduleOf(g).ks > 1 ? 2 : 1;
+}
+
+// ------------------------------- grouped GEMM (horizontal fusion) -------------------------------
+namespace {
+// Problems side by side along a virtual N = n_prob * g.n.  A tile may span problems only when
+// they share A; B column chunks (64 wide, MN-major) or boxes (K-major: bn or bn/2 rows) must not
+// straddle two problems; no split-K (the partials' reduce would need the same scatter).
+Sched GroupScheduleOf(const GemmArgs& g, int n_prob, bool shared_a) {
+  GemmArgs v = g;
+  v.n = g.n * n_prob;
+  auto ok = [&](int bn, bool pair) {
+    const int64_t half = pair ? bn / 2 : bn;
+    if (v.n % bn || g.n % 64) return false;
+    if (!shared_a && g.n % bn) return false;
+    if (g.tb && g.n % half) return false;
+    return true;
+  };
+  static const int force = EnvInt("RH_GEMM_BN", 0);
+  if (UsePair(v) && ok(256, true)) {
+    const int64_t ctas = (v.m / BM) * (v.n / 256);
+    if (ctas >= 148 || force == 256) return {true, 256, 1};
+  }
+  if (force != 128 && (v.m / BM) * (v.n / 256) >= 96 && ok(256, false)) return {false, 256, 1};
+  if (ok(128, false)) return {false, 128, 1};
+  return {false, 0, 1};
+}
+
+struct GroupHost {
+  GroupLaunch gl;
+  Sched sc;
+};
+std::mutex g_group_mu;
+std::map<const void*, GroupHost> g_groups;  // device table -> launch parameters
+}  // namespace
+
+bool GemmTcGroupSupported(const GemmArgs& g, int n_prob, bool shared_a) {
+  if (g.dtype != RH_BF16 || n_prob < 2 || !GemmTcSupported(g)) return false;
+  if (g.n * n_prob > (int64_t{1} << 30)) return false;
+  return GroupScheduleOf(g, n_prob, shared_a).bn != 0;
+}
+
+size_t GemmTcGroupTableBytes(int n_prob) {
+  return static_cast<size_t>(n_prob) * (2 * sizeof(CUtensorMap) + sizeof(void*));
+}
+
+const char* GemmTcGroupSchedule(const GemmArgs& g, int n_prob, bool shared_a) {
+  const Sched sc = GroupScheduleOf(g, n_prob, shared_a);
+  if (sc.pair) return " [pair]";
+  return sc.bn == 256 ? " [256]" : " [128]";
+}
+
+void PrepareGemmTcGroup(const GemmArgs& g, int n_prob, const void* const* a, const void* const* b,
+                        void* const* c, void* table) {
+  const bool shared_a = std::all_of(a, a + n_prob, [&](const void* x) { return x == a[0]; });
+  if (!GemmTcGroupSupported(g, n_prob, shared_a)) Fail("tcgen05 grouped GEMM: unsupported shape/layout", RH_ERR_UNSUPPORTED);
+  GroupHost h{};
+  h.sc = GroupScheduleOf(g, n_prob, shared_a);
+  const int box_n = h.sc.pair ? h.sc.bn / 2 : h.sc.bn;
+  const int kb = !h.sc.pair && h.sc.bn == 128 && g.k % 128 == 0 ? 128 : 64;
+  std::vector<char> host(GemmTcGroupTableBytes(n_prob));
+  CUtensorMap* bm = reinterpret_cast<CUtensorMap*>(host.data());
+  CUtensorMap* am = bm + n_prob;
+  void** cp = reinterpret_cast<void**>(am + n_prob);
+  for (int p = 0; p < n_prob; ++p) {
+    GemmArgs gp = g;
+    gp.a = a[p];
+    gp.b = b[p];
+    const Maps& mp = GetMaps(gp, box_n, kb);
+    if (p == 0) h.gl.m0 = mp;
+    bm[p] = mp.b;
+    am[p] = mp.a;
+    cp[p] = c[p];
+    if (reinterpret_cast<uintptr_t>(c[p]) % 16) Fail("tcgen05 grouped GEMM: unaligned output");
+  }
+  RH_CUDA(cudaMemcpy(table, host.data(), host.size(), cudaMemcpyHostToDevice));
+  const CUtensorMap* tb = static_cast<const CUtensorMap*>(table);
+  h.gl.dev.b = tb;
+  h.gl.dev.a = shared_a ? nullptr : tb + n_prob;
+  h.gl.dev.c = reinterpret_cast<__nv_bfloat16* const*>(tb + 2 * n_prob);
+  h.gl.dev.seg_n = static_cast<int>(g.n);
+  h.gl.n_prob = n_prob;
+  std::lock_guard<std::mutex> lk(g_group_mu);
+  g_groups[table] = h;
+}
+
+void ReleaseGemmTcGroup(const void* table) {
+  std::lock_guard<std::mutex> lk(g_group_mu);
+  g_groups.erase(table);
+}
+
+void LaunchGemmTcGroup(const GemmArgs& g, const void* table, cudaStream_t s) {
+  GroupHost h;
+  {
+    std::lock_guard<std::mutex> lk(g_group_mu);
+    auto it = g_groups.find(table);
+    if (it == g_groups.end()) Fail("tcgen05 grouped GEMM: table not prepared", RH_ERR_STATE);
+    h = it->second;
+  }
+  for (int i = 0; i < g.epi.n_fn; ++i) {
+    const int fn = g.epi.fns[i];
+    if (fn != RH_FN_RELU && fn != RH_FN_NEG && fn != RH_FN_IDENTITY && !(fn >= kFnTanhRun && fn - kFnTanhRun < g.epi.n_tab))
+      Fail("tcgen05 bf16 GEMM epilogue takes only relu / neg / identity / tanh runs", RH_ERR_UNSUPPORTED);
+  }
+  const GroupLaunch* gl = &h.gl;
+  const int v = (h.sc.bn == 256 ? 4 : 0) | (g.tb ? 2 : 0) | (g.ta ? 0 : 1);
+  if (h.sc.pair) {
+    switch (v) {
+      case 4: LaunchPair<256, false, false, true>(g, s, gl); break;
+      case 5: LaunchPair<256, false, true, true>(g, s, gl); break;
+      case 6: LaunchPair<256, true, false, true>(g, s, gl); break;
+      case 7: LaunchPair<256, true, true, true>(g, s, gl); break;
+      default: Fail("internal: grouped pair schedule");
+    }
+    return;
+  }
+  switch (v) {
+    case 0: Launch<128, false, false, true>(g, s, gl); break;
+    case 1: Launch<128, false, true, true>(g, s, gl); break;
+    case 2: Launch<128, true, false, true>(g, s, gl); break;
+    case 3: Launch<128, true, true, true>(g, s, gl); break;
+    case 4: Launch<256, false, false, true>(g, s, gl); break;
+    case 5: Launch<256, false, true, true>(g, s, gl); break;
+    case 6: Launch<256, true, false, true>(g, s, gl); break;
+    default: Launch<256, true, true, true>(g, s, gl); break;
+  }
 }
 
 void LaunchGemmTc(const GemmArgs& g, cudaStream_t s) {

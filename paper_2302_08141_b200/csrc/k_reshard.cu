@@ -10,6 +10,10 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cmath>
+#include <map>
+#include <mutex>
+#include <vector>
 
 #include "kernels.h"
 
@@ -65,6 +69,8 @@ struct PullDev {
   uint32_t rot; // traversal start (units): coord * n / d, so that at any moment the d ranks of a
                 // group read from d different sources instead of all hammering the same peer
   PeerSync sync;
+  uint32_t blk0, nblk;  // grouped launches (PullMultiKernel): this segment's block range
+  int32_t d_sum;        // Partial sources: members summed
 };
 
 __device__ __forceinline__ uint32_t Rotate(uint32_t i, uint32_t rot, uint32_t n) {
@@ -115,14 +121,14 @@ __device__ __forceinline__ uint32_t DstToGlobal(const PullDev& a, uint32_t i) {
   return (p * a.dd.d + a.coord) * a.qst.d + u;
 }
 
-// Shard / Replicated sources: a pure copy of VB-byte units.
+// Shard / Replicated sources: a pure copy of VB-byte units.  `bid` / `nb`: this block's index
+// among the blocks working on this transition (the whole grid, or a grouped launch's segment).
 template <int VB, bool kFromShard>
-__global__ void __launch_bounds__(256) PullCopyKernel(PullDev a) {
+__device__ __forceinline__ void PullCopyBody(const PullDev& a, uint32_t bid, uint32_t nb) {
   using V = typename VecT<VB>::T;
   constexpr int U = 4;
-  ArriveAndWait(a.sync);
-  const uint32_t stride = gridDim.x * blockDim.x;
-  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t stride = nb * blockDim.x;
+  uint32_t i = bid * blockDim.x + threadIdx.x;
   for (; i < a.n; i += U * stride) {
     V v[U];
 #pragma unroll
@@ -148,6 +154,12 @@ __global__ void __launch_bounds__(256) PullCopyKernel(PullDev a) {
   }
 }
 
+template <int VB, bool kFromShard>
+__global__ void __launch_bounds__(256) PullCopyKernel(PullDev a) {
+  ArriveAndWait(a.sync);
+  PullCopyBody<VB, kFromShard>(a, blockIdx.x, gridDim.x);
+}
+
 template <typename T>
 __device__ __forceinline__ float ToF(T x);
 template <>
@@ -171,12 +183,11 @@ __device__ __forceinline__ __nv_bfloat16 FromF<__nv_bfloat16>(float x) {
 
 // Partial sources: sum of the d members' values at the same global position, rank order.
 template <typename T, int VB>
-__global__ void __launch_bounds__(256) PullSumKernel(PullDev a, int d) {
+__device__ __forceinline__ void PullSumBody(const PullDev& a, int d, uint32_t bid, uint32_t nb) {
   using V = typename VecT<VB>::T;
   constexpr int E = VB / sizeof(T);
-  ArriveAndWait(a.sync);
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < a.n; i0 += stride) {
+  const uint32_t stride = nb * blockDim.x;
+  for (uint32_t i0 = bid * blockDim.x + threadIdx.x; i0 < a.n; i0 += stride) {
     const uint32_t i = Rotate(i0, a.rot, a.n);
     const uint32_t f = DstToGlobal(a, i);
     float acc[E];
@@ -191,6 +202,33 @@ __global__ void __launch_bounds__(256) PullSumKernel(PullDev a, int d) {
 #pragma unroll
     for (int e = 0; e < E; ++e) t[e] = FromF<T>(acc[e]);
     reinterpret_cast<V*>(a.dst)[i] = o;
+  }
+}
+
+template <typename T, int VB>
+__global__ void __launch_bounds__(256) PullSumKernel(PullDev a, int d) {
+  ArriveAndWait(a.sync);
+  PullSumBody<T, VB>(a, d, blockIdx.x, gridDim.x);
+}
+
+// Grouped transitions: independent single-axis transitions of one mesh axis (the per-head K / V
+// all-gathers of an attention block) as ONE launch behind ONE fused barrier.  Segment k owns
+// blocks [blk0, blk0 + nblk); the segment table lives in device memory (written at load).
+// kKind: 0 Shard-source copy, 1 Replicated-source copy, 2 Partial-source sum.
+template <int VB, int kKind, typename T>
+__global__ void __launch_bounds__(256) PullMultiKernel(const PullDev* __restrict__ seg, int n, PeerSync sync) {
+  ArriveAndWait(sync);
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (seg[mid].blk0 <= blockIdx.x) lo = mid;
+    else hi = mid - 1;
+  }
+  const PullDev& a = seg[lo];
+  if constexpr (kKind == 2) {
+    PullSumBody<T, VB>(a, a.d_sum, blockIdx.x - a.blk0, a.nblk);
+  } else {
+    PullCopyBody<VB, kKind == 0>(a, blockIdx.x - a.blk0, a.nblk);
   }
 }
 
@@ -340,19 +378,10 @@ void LaunchPullVB(const PullArgs& a, PullDev& dv, cudaStream_t s) {
   RH_CUDA(cudaGetLastError());
 }
 
-}  // namespace
-
-int LaunchPull(const PullArgs& a, cudaStream_t s) {
+// Vector width of a plain pull: the largest power-of-two unit (<= 16 B) that divides every
+// contiguous run and every buffer alignment.
+int PullVB(const PullArgs& a) {
   const int eb = ElemBytes(a.dtype);
-  if (a.n_dst == 0) return 0;
-  if (a.to.kind == RH_PARTIAL && a.coord != 0) {  // zero-fill (sharding.cpp:132-135)
-    if (a.sync.d) Fail("internal: fused barrier on a zero-fill transition");
-    RH_CUDA(cudaMemsetAsync(a.dst, 0, a.n_dst * eb, s));
-    return 1;
-  }
-  if (TryLaunchStaged(a, s)) return 1;
-  // Vector width: the largest power-of-two unit (<= 16 B) that divides every contiguous run and
-  // every buffer alignment.
   int64_t g = a.n_dst;
   if (a.to.kind == RH_SHARD) g = Gcd(g, a.to.Qs);
   if (a.from.kind == RH_SHARD) g = Gcd(g, a.from.Qs);
@@ -366,6 +395,11 @@ int LaunchPull(const PullArgs& a, cudaStream_t s) {
     if (ok) break;
     vb /= 2;
   }
+  return vb;
+}
+
+PullDev MakePullDev(const PullArgs& a, int vb) {
+  const int eb = ElemBytes(a.dtype);
   const int64_t units_per = vb / eb;
   PullDev dv{};
   dv.dst = static_cast<char*>(a.dst);
@@ -382,12 +416,106 @@ int LaunchPull(const PullArgs& a, cudaStream_t s) {
   dv.coord = static_cast<uint32_t>(a.coord);
   dv.rot = static_cast<uint32_t>((static_cast<uint64_t>(dv.n) / std::max(d, 1)) * a.coord % std::max<uint32_t>(dv.n, 1));
   dv.sync = a.sync;
+  dv.d_sum = a.from.d;
+  return dv;
+}
+
+}  // namespace
+
+int LaunchPull(const PullArgs& a, cudaStream_t s) {
+  const int eb = ElemBytes(a.dtype);
+  if (a.n_dst == 0) return 0;
+  if (a.to.kind == RH_PARTIAL && a.coord != 0) {  // zero-fill (sharding.cpp:132-135)
+    if (a.sync.d) Fail("internal: fused barrier on a zero-fill transition");
+    RH_CUDA(cudaMemsetAsync(a.dst, 0, a.n_dst * eb, s));
+    return 1;
+  }
+  if (TryLaunchStaged(a, s)) return 1;
+  const int vb = PullVB(a);
+  PullDev dv = MakePullDev(a, vb);
   switch (vb) {
     case 16: LaunchPullVB<16>(a, dv, s); break;
     case 8: LaunchPullVB<8>(a, dv, s); break;
     case 4: LaunchPullVB<4>(a, dv, s); break;
     default: LaunchPullVB<2>(a, dv, s); break;
   }
+  return 1;
+}
+
+// Grouped transitions (one launch, one fused barrier).  Eligible when every segment is a plain
+// pull (no zero-fill, no staged fine-grained source) of the same source kind and dtype; the
+// common vector width is the smallest segment's.
+namespace {
+struct MultiHost {
+  int vb, kind, dtype, blocks, n;
+};
+std::mutex g_multi_mu;
+std::map<const void*, MultiHost> g_multi;
+}  // namespace
+
+size_t PullMultiTableBytes(int n) { return static_cast<size_t>(n) * sizeof(PullDev); }
+
+bool PreparePullMulti(const PullArgs* a, int n, int max_blocks, void* table) {
+  if (n < 2) return false;
+  int vb = 16;
+  for (int k = 0; k < n; ++k) {
+    if (a[k].n_dst == 0 || a[k].to.kind == RH_PARTIAL || a[k].from.kind != a[0].from.kind ||
+        a[k].dtype != a[0].dtype)
+      return false;
+    if (a[k].from.kind == RH_SHARD && a[k].from.Qs * ElemBytes(a[k].dtype) < 16) return false;  // staged
+    vb = std::min(vb, PullVB(a[k]));
+  }
+  if (a[0].from.kind == RH_PARTIAL && vb < (a[0].dtype == RH_BF16 ? 2 : 4)) return false;
+  std::vector<PullDev> seg(n);
+  double units = 0;
+  for (int k = 0; k < n; ++k) {
+    seg[k] = MakePullDev(a[k], vb);
+    units += seg[k].n;
+  }
+  const int cap = max_blocks > 0 ? max_blocks : 148 * 6;
+  const double per_blk = a[0].from.kind == RH_PARTIAL ? 256.0 : 1024.0;
+  const double scale = std::min(1.0, cap / std::max(1.0, units / per_blk));
+  uint32_t b0 = 0;
+  for (int k = 0; k < n; ++k) {
+    const uint32_t want = static_cast<uint32_t>(std::ceil(seg[k].n / per_blk * scale));
+    seg[k].blk0 = b0;
+    seg[k].nblk = std::max<uint32_t>(1, want);
+    b0 += seg[k].nblk;
+  }
+  RH_CUDA(cudaMemcpy(table, seg.data(), seg.size() * sizeof(PullDev), cudaMemcpyHostToDevice));
+  std::lock_guard<std::mutex> lk(g_multi_mu);
+  g_multi[table] = MultiHost{vb, a[0].from.kind, a[0].dtype, static_cast<int>(b0), n};
+  return true;
+}
+
+void ReleasePullMulti(const void* table) {
+  std::lock_guard<std::mutex> lk(g_multi_mu);
+  g_multi.erase(table);
+}
+
+int LaunchPullMulti(const void* table, const PeerSync& sync, cudaStream_t s) {
+  MultiHost h;
+  {
+    std::lock_guard<std::mutex> lk(g_multi_mu);
+    auto it = g_multi.find(table);
+    if (it == g_multi.end()) Fail("grouped transition: table not prepared", RH_ERR_STATE);
+    h = it->second;
+  }
+  const PullDev* seg = static_cast<const PullDev*>(table);
+  const bool bf = h.dtype == RH_BF16;
+#define RH_MULTI(VB)                                                                                  \
+  if (h.kind == RH_SHARD) PullMultiKernel<VB, 0, float><<<h.blocks, 256, 0, s>>>(seg, h.n, sync);     \
+  else if (h.kind == RH_REPLICATED) PullMultiKernel<VB, 1, float><<<h.blocks, 256, 0, s>>>(seg, h.n, sync); \
+  else if (bf) PullMultiKernel<VB, 2, __nv_bfloat16><<<h.blocks, 256, 0, s>>>(seg, h.n, sync);       \
+  else if (VB >= 4) PullMultiKernel<(VB >= 4 ? VB : 4), 2, float><<<h.blocks, 256, 0, s>>>(seg, h.n, sync);
+  switch (h.vb) {
+    case 16: RH_MULTI(16) break;
+    case 8: RH_MULTI(8) break;
+    case 4: RH_MULTI(4) break;
+    default: RH_MULTI(2) break;
+  }
+#undef RH_MULTI
+  RH_CUDA(cudaGetLastError());
   return 1;
 }
 

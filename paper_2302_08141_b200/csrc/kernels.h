@@ -66,6 +66,14 @@ struct PullArgs {
 void LaunchEpochTick(uint32_t* epoch, cudaStream_t s);
 // Returns the number of kernel launches (0 or 1).
 int LaunchPull(const PullArgs& a, cudaStream_t s);
+// Grouped transitions: n independent pulls of one mesh axis as ONE launch behind ONE fused
+// barrier (`sync` of LaunchPullMulti; the PullArgs' own sync is ignored).  PreparePullMulti
+// writes the segment table (PullMultiTableBytes) once and returns false when the pulls cannot
+// share a launch (zero-fill, staged fine-grained sources, mixed source kinds or dtypes).
+size_t PullMultiTableBytes(int n);
+bool PreparePullMulti(const PullArgs* a, int n, int max_blocks, void* table);
+void ReleasePullMulti(const void* table);
+int LaunchPullMulti(const void* table, const PeerSync& sync, cudaStream_t s);
 
 // dst_local[l] = full[ComposedLocalToGlobal(m, l)]  (R -> any composed spec slice)
 void LaunchSliceComposed(void* dst, const void* full, const ComposedMap& m, int64_t n, int dtype,
@@ -188,6 +196,18 @@ void LaunchGemmTc(const GemmArgs& g, cudaStream_t s);
 // Launches LaunchGemmTc issues: 3xTF32 3 (two splits + GEMM), bf16 split-K 2 (+ reduce), else 1.
 int GemmTcLaunches(const GemmArgs& g);
 const char* GemmTcSchedule(const GemmArgs& g);  // " [split-k]" or ""
+// Grouped tcgen05 GEMM: n_prob independent problems of g's shape (m, n, k, ta, tb, dtype, epi)
+// in ONE persistent launch (the per-head q/k/v, score and context GEMMs of an attention block),
+// laid side by side along a virtual N; a tile spans problems when they all read the same A.
+// PrepareGemmTcGroup writes the device table (GemmTcGroupTableBytes: per-problem TMA maps and
+// output pointers) once; LaunchGemmTcGroup replays it.
+bool GemmTcGroupSupported(const GemmArgs& g, int n_prob, bool shared_a);
+size_t GemmTcGroupTableBytes(int n_prob);
+const char* GemmTcGroupSchedule(const GemmArgs& g, int n_prob, bool shared_a);
+void PrepareGemmTcGroup(const GemmArgs& g, int n_prob, const void* const* a, const void* const* b,
+                        void* const* c, void* table);
+void ReleaseGemmTcGroup(const void* table);
+void LaunchGemmTcGroup(const GemmArgs& g, const void* table, cudaStream_t s);
 
 // --------------------------------------- cross-GPU sync --------------------------------------
 // Group barrier over CUDA-IPC-mapped flag arrays (one process per GPU only: every member runs on

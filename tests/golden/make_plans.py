@@ -23,9 +23,11 @@ PROG = os.path.join(HERE, "programs")
 OUT = os.path.join(HERE, "plans")
 
 
-def gpt_heads_ir(heads=32, hidden=4096, seq=2048, head_dim=128):
+def gpt_heads_ir(heads=32, hidden=4096, seq=2048, head_dim=128, score_chain=14):
     """C3 per-head variant: the gpt_like block (proj/src/fixtures.cpp:101-137)
-    with attention split into `heads` rank-2 heads joined by Concat (ir.cpp:205-220)."""
+    with attention split into `heads` rank-2 heads joined by Concat (ir.cpp:205-220).  Chain
+    lengths are the fixture's own (kGptLn1/kGptScore/kGptMix/kGptGate/kGptLn2/kGptGelu =
+    12/14/4/36/12/12, fixtures.cpp:90-99); every head carries the full 14-op score chain."""
     H, B, F, D = hidden, seq, 4 * hidden, head_dim
     L = [f"x = input f32[{B},{H}]"]
     for n in ("wo",):
@@ -51,7 +53,7 @@ def gpt_heads_ir(heads=32, hidden=4096, seq=2048, head_dim=128):
         L.append(f"{p}_k = matmul({n1}, {p}_wk)")
         L.append(f"{p}_v = matmul({n1}, {p}_wv)")
         L.append(f"{p}_score = matmul({p}_q, {p}_k^T)")
-        sm = chain(f"{p}_smax", f"{p}_score", 2, f"{B},{B}")
+        sm = chain(f"{p}_smax", f"{p}_score", score_chain, f"{B},{B}")
         L.append(f"{p}_ctx = matmul({sm}, {p}_v)")
         ctxs.append(f"{p}_ctx")
     L.append(f"attn = concat({', '.join(ctxs)}) : f32[{B},{H}] {{axis=1}}")
@@ -99,7 +101,7 @@ def jobs():
             J.append((f"rand_{short}_{mesh.replace(',', 'x')}_s{seed}",
                       ["--fixture", fam, "--random-choice", str(seed), "--mesh", mesh]))
     heads = os.path.join(PROG, "c3_gpt_heads32.ir")
-    for d in (8,):
+    for d in (1, 2, 4, 8):
         J.append((f"c3_gpt_heads32_d{d}", ["--text", heads, "--devices", str(d)]))
     return J
 

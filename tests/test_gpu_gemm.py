@@ -125,3 +125,105 @@ def test_simt_fp32_gemm_vs_fp64():
     assert any("gemm_simt" in s for s in names)
     ref = a.astype(np.float64) @ b.astype(np.float64).T
     assert np.abs(c - ref).max() / np.abs(ref).max() <= 1e-5
+
+
+def group_doc(P, m, k, n, shared_a, ta=False, tb=False, chain=()):
+    """P independent MatMuls of one shape (the per-head GEMMs of an attention block): with
+    shared_a every problem reads the same A (q/k/v projections), else each its own (score, ctx)."""
+    R = ["replicated"]
+    ops = []
+    ash = [k, m] if ta else [m, k]
+    bsh = [n, k] if tb else [k, n]
+    if shared_a:
+        ops.append({"id": "a", "kind": "input", "inputs": [], "shape": ash, "out_spec": R, "in_specs": [[]]})
+    outs = []
+    for p in range(P):
+        if not shared_a:
+            ops.append({"id": f"a{p}", "kind": "input", "inputs": [], "shape": ash, "out_spec": R, "in_specs": [[]]})
+        ai = 0 if shared_a else len(ops) - 1
+        ops.append({"id": f"b{p}", "kind": "param", "inputs": [], "shape": bsh, "out_spec": R, "in_specs": [[]]})
+        ops.append({"id": f"c{p}", "kind": "matmul", "inputs": [ai, len(ops) - 1], "shape": [m, n],
+                    "transpose_a": ta, "transpose_b": tb, "out_spec": R, "in_specs": [R * 2]})
+        for i, fn in enumerate(chain):
+            ops.append({"id": f"u{p}_{i}", "kind": "unary", "fn": fn, "inputs": [len(ops) - 1], "shape": [m, n],
+                        "out_spec": R, "in_specs": [R]})
+        outs.append(len(ops) - 1)
+    return {"schema": "rhino-lowered/1", "name": "group", "mesh": [1], "dtype": "bf16", "ops": ops,
+            "outputs": outs}
+
+
+def run_group(doc, env_off=False, monkeypatch=None):
+    from paper_2302_08141_b200 import runtime as rx
+    if monkeypatch is not None:
+        if env_off:
+            monkeypatch.setenv("RH_NO_GEMM_GROUP", "1")
+        else:
+            monkeypatch.delenv("RH_NO_GEMM_GROUP", raising=False)
+    prog = LoweredProgram(doc)
+    rt = rx.Runtime(devices=[0])
+    mesh = rx.Mesh(rt, [1])
+    gp = rx.Program(mesh, prog)
+    try:
+        gp.init_synthetic(21)
+        gp.run(2)
+        vals = {op.index: gp.read_full(op.index) for op in prog.ops if op.kind in (0, 1)}
+        outs = [gp.read_full(o) for o in prog.outputs]
+        names = [s["name"] for s in gp.steps()]
+    finally:
+        gp.close()
+        mesh.close()
+        rt.close()
+    return prog, vals, outs, names
+
+
+# q/k/v-like (shared A, N = head_dim 128: tiles span two problems), score-like (own A, tb),
+# ctx-like (own A, N = 128), and MN-major / transposed-A variants
+@pytest.mark.parametrize("P,m,k,n,shared_a,ta,tb", [
+    (24, 2048, 512, 128, True, False, False),   # CTA-pair 256-wide tiles: one problem per CTA
+    (24, 2048, 256, 128, True, False, True),
+    (64, 384, 256, 128, True, False, False),    # single-CTA 256-wide tiles spanning two problems
+    (12, 512, 1024, 128, True, False, False),
+    (6, 256, 512, 256, True, False, True),
+    (4, 512, 128, 512, False, False, True),
+    (5, 256, 512, 128, False, False, False),
+    (3, 256, 256, 256, False, True, False),
+    (8, 2048, 256, 128, True, True, True),
+])
+def test_tc_grouped_gemm(monkeypatch, P, m, k, n, shared_a, ta, tb):
+    """One grouped tcgen05 launch for P independent MatMuls (per-problem TMA maps and output
+    pointers from a device table) against fp64, and against the one-launch-per-GEMM schedule."""
+    doc = group_doc(P, m, k, n, shared_a, ta, tb)
+    prog, vals, outs, names = run_group(doc, monkeypatch=monkeypatch)
+    assert any(s.startswith("gemm_tc_group[%d]" % P) for s in names), names
+    _, _, outs0, names0 = run_group(doc, env_off=True, monkeypatch=monkeypatch)
+    assert not any("group" in s for s in names0)
+    for p, o in enumerate(prog.outputs):
+        mm = prog.ops[o]
+        A, B = bf16_to_f64(vals[mm.inputs[0]]), bf16_to_f64(vals[mm.inputs[1]])
+        ref = (A.T if ta else A) @ (B.T if tb else B)
+        got = bf16_to_f64(outs[p])
+        assert np.abs(got - ref).max() / np.abs(ref).max() <= 1e-2, p
+        y = bf16_to_f64(outs0[p])
+        assert np.abs(got - y).max() <= 2.0 ** -8 * np.abs(y).max(), p
+
+
+def test_tc_grouped_gemm_epilogue_bit_exact(monkeypatch):
+    """Grouped launches keep the fused tanh-run epilogue: bit-identical to NO_FUSION."""
+    from paper_2302_08141_b200.abi import RH_FLAG_NO_FUSION
+    from paper_2302_08141_b200 import runtime as rx
+    doc = group_doc(6, 256, 512, 256, False, False, True, chain=("", "", "tanh"))
+    prog, _, outs, names = run_group(doc, monkeypatch=monkeypatch)
+    assert names[0].startswith("gemm_tc_group[6]") and len(names) == 1, names
+    rt = rx.Runtime(devices=[0])
+    mesh = rx.Mesh(rt, [1])
+    gp = rx.Program(mesh, LoweredProgram(doc), RH_FLAG_NO_FUSION)
+    try:
+        gp.init_synthetic(21)
+        gp.run(1)
+        ref = [gp.read_full(o) for o in prog.outputs]
+    finally:
+        gp.close()
+        mesh.close()
+        rt.close()
+    for a, b in zip(outs, ref):
+        np.testing.assert_array_equal(a, b)
