@@ -1815,8 +1815,24 @@ class Lowerer {
         st.name = "concat " + id;
         st.launches = static_cast<int>(in_t.size());
         const std::vector<int> ins = in_t;
-        st.run = [P, ins, out_t, first, outer, orow, rows, offs, dtype](int li, cudaStream_t s) {
+        bool vec = static_cast<int>(ins.size()) <= kMaxConcat && (orow * eb) % 16 == 0;
+        for (size_t k = 0; k < ins.size(); ++k) vec = vec && (rows[k] * eb) % 16 == 0 && (offs[k] * eb) % 16 == 0;
+        if (vec) st.launches = 1;
+        st.run = [P, ins, out_t, first, outer, orow, rows, offs, dtype, vec, eb](int li, cudaStream_t s) {
           const int r = first + li;
+          if (vec) {  // one launch for every piece
+            ConcatArgs a{};
+            a.out = P->Ptr(P->tensors[out_t], r);
+            a.n = static_cast<int>(ins.size());
+            a.outer = outer;
+            a.orow16 = orow * eb / 16;
+            for (size_t k = 0; k < ins.size(); ++k) {
+              a.in[k] = P->Ptr(P->tensors[ins[k]], r);
+              a.row16[k] = rows[k] * eb / 16;
+              a.off16[k] = offs[k] * eb / 16;
+            }
+            if (LaunchConcat(a, s)) return 1;
+          }
           for (size_t k = 0; k < ins.size(); ++k)
             LaunchConcatPiece(P->Ptr(P->tensors[out_t], r), P->Ptr(P->tensors[ins[k]], r), outer,
                               rows[k], orow, offs[k], dtype, s);

@@ -748,6 +748,22 @@ __global__ void ConcatPieceKernel(T* out, const T* in, int64_t outer, int64_t ro
   }
 }
 
+// All pieces of a concat in one launch: blockIdx.y = piece, 16-byte units (every piece row,
+// output row and column offset a multiple of 16 bytes).
+__global__ void __launch_bounds__(256) ConcatKernel(ConcatArgs a) {
+  PdlTrigger();
+  PdlWait();
+  const int p = blockIdx.y;
+  const uint32_t row = static_cast<uint32_t>(a.row16[p]);
+  const uint32_t n = static_cast<uint32_t>(a.outer) * row;
+  const uint4* in = static_cast<const uint4*>(a.in[p]);
+  uint4* out = static_cast<uint4*>(a.out) + a.off16[p];
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const uint32_t o = t / row;
+    out[static_cast<int64_t>(o) * a.orow16 + (t - o * row)] = in[t];
+  }
+}
+
 int Blocks(int64_t n, int per_thread = 1) {
   static const int per_sm = [] {  // A/B knob (profiles/): grid cap in blocks per SM
     const char* v = getenv("RH_EW_BLOCKS_PER_SM");
@@ -879,6 +895,20 @@ void LaunchBroadcast(void* out, const void* in, int64_t n_out, int64_t n_in, int
   if (dtype == RH_BF16) LaunchPdl(BroadcastKernel<uint16_t>, Blocks(n_out), 256, 0, s, static_cast<uint16_t*>(out), static_cast<const uint16_t*>(in), n_out, n_in);
   else LaunchPdl(BroadcastKernel<uint32_t>, Blocks(n_out), 256, 0, s, static_cast<uint32_t*>(out), static_cast<const uint32_t*>(in), n_out, n_in);
   RH_CUDA(cudaGetLastError());
+}
+
+bool LaunchConcat(const ConcatArgs& a, cudaStream_t s) {
+  if (a.n < 1 || a.n > kMaxConcat || a.outer == 0) return false;
+  int64_t most = 0;
+  for (int p = 0; p < a.n; ++p) {
+    if (reinterpret_cast<uintptr_t>(a.in[p]) % 16) return false;
+    most = std::max(most, a.outer * a.row16[p]);
+  }
+  if (reinterpret_cast<uintptr_t>(a.out) % 16 || most >= (int64_t{1} << 32)) return false;
+  const int bx = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((most + 1023) / 1024, 148 * 8 / a.n + 1)));
+  LaunchPdl(ConcatKernel, dim3(bx, a.n), 256, 0, s, a);
+  RH_CUDA(cudaGetLastError());
+  return true;
 }
 
 void LaunchConcatPiece(void* out, const void* in, int64_t outer, int64_t row, int64_t orow,

@@ -67,6 +67,45 @@ __device__ __forceinline__ void TmaLoad2D(void* dst, const CUtensorMap* map, uin
       : "memory");
 }
 
+// Epilogue output: 32 x 32 bf16 boxes (64-byte rows, 64-byte swizzle) staged in shared memory and
+// written by the TMA engine (cp.async.bulk.tensor store): fully coalesced, asynchronous global
+// writes instead of one 16-byte store per row per thread (32 rows per store instruction).
+__device__ __forceinline__ void TmaStore2D(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+               "r"(SmemU32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void BulkCommit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void BulkWaitRead() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void BulkWaitAll() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void FenceProxyAsyncSmem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+constexpr int kEpiStageBytes = 4 * 2 * 2048;  // 4 epilogue warps x 2 buffers x (32 x 64 B)
+
+// One 32-row x 32-column bf16 box of the epilogue (lane = row, p = its 16 packed pairs) through
+// staging buffer `buf` (of 2, alternating) and a TMA store at (c0, c1).  `cnt` = boxes this warp
+// stored before: the buffer's previous store must have been read out before it is rewritten.
+__device__ __forceinline__ void EpiStoreBox(uint8_t* stage, uint32_t cnt, const uint32_t (&p)[16],
+                                            const CUtensorMap* map, int c0, int c1, int lane) {
+  uint8_t* sb = stage + (cnt & 1) * 2048;
+  if (lane == 0 && cnt >= 2) BulkWaitRead<1>();
+  __syncwarp();
+  const int sw = (lane >> 1) & 3;  // 64-byte swizzle: 16-byte chunk ^= address bits [7,9)
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    *reinterpret_cast<uint4*>(sb + lane * 64 + ((q ^ sw) << 4)) = make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
+  FenceProxyAsyncSmem();
+  __syncwarp();
+  if (lane == 0) {
+    TmaStore2D(map, sb, c0, c1);
+    BulkCommit();
+  }
+}
+
 __device__ __forceinline__ void FenceBefore() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void FenceAfter() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -177,7 +216,7 @@ __global__ void __launch_bounds__(256) SplitReduceBf16(__nv_bfloat16* __restrict
 struct GroupDev {
   const CUtensorMap* b;       // [n_prob] B maps
   const CUtensorMap* a;       // [n_prob] A maps, or nullptr: every problem reads the kernel's A
-  __nv_bfloat16* const* c;    // [n_prob] outputs, row pitch seg_n
+  const CUtensorMap* cm;      // [n_prob] output maps (TMA-store epilogue)
   int seg_n;                  // columns per problem
 };
 
@@ -188,7 +227,7 @@ struct TcCfg {
   static constexpr int kStage = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered fp32 accumulator
   static constexpr int kStages = (192 * 1024) / kStage;  // 4 (BN 256, KB 64) / 3 (BN 128, KB 128)
-  static constexpr int kSmem = kStages * kStage + 1024 /*barriers*/ + kEpiTabBytes + 1024 /*align*/;
+  static constexpr int kSmem = kStages * kStage + 1024 /*barriers*/ + kEpiTabBytes + kEpiStageBytes + 1024 /*align*/;
   static constexpr uint32_t kIdesc = (1u << 4)                     // D = F32
                                      | (1u << 7) | (1u << 10)      // A, B = BF16
                                      | ((kAKMajor ? 0u : 1u) << 15)  // A major
@@ -205,7 +244,7 @@ struct TcCfg {
 template <int BN, bool kBKMajor, bool kAKMajor, int KB, bool kGroup = false>
 __global__ void __launch_bounds__(kThreads, 1)
     GemmTcKernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                 __nv_bfloat16* __restrict__ C, int M, int N, int K, ChainArgs epi, int ksplit,
+                 const __grid_constant__ CUtensorMap tma_c, int M, int N, int K, ChainArgs epi, int ksplit,
                  float* __restrict__ ws, GroupDev grp) {
   PdlTrigger();
   // Work unit = (m tile, n tile, k split).  ksplit > 1 (few tiles: the sharded GEMMs at N >= 4)
@@ -342,6 +381,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - 4;  // TMEM lanes [32*ew, 32*ew+32)
     const uint16_t* tp[kMaxTanhRuns];
     StageEpiTables(epi, reinterpret_cast<uint16_t*>(smem + Cfg::kStages * Cfg::kStage + 1024), threadIdx.x - 128, tp);
+    uint8_t* stage_c = smem + Cfg::kStages * Cfg::kStage + 1024 + kEpiTabBytes + ew * 4096;
+    uint32_t boxes = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
@@ -350,16 +391,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       MbarWait(&tfull[acc], acc_phase);
       FenceAfter();
       const int row = m_blk * BM + ew * 32 + lane;
-      __nv_bfloat16* crow = C + static_cast<int64_t>(row) * N + n_blk * BN;
       float* wrow = ws ? ws + (static_cast<int64_t>(ks) * M + row) * N + n_blk * BN : nullptr;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
         TmemLd32(tmem + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
-        if constexpr (kGroup) {  // this 32-column chunk's problem and column within it
-          const int col = n_blk * BN + c * 32;
-          crow = grp.c[col / grp.seg_n] + static_cast<int64_t>(row) * grp.seg_n + col % grp.seg_n - c * 32;
-        }
         if (wrow) {  // split-K partial (fp32, unrounded)
           float4* dst = reinterpret_cast<float4*>(wrow + c * 32);
 #pragma unroll
@@ -375,9 +411,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) p[j] = PackBf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
         EpiPackedBf16(epi, p, tp);
-        uint4* dst = reinterpret_cast<uint4*>(crow + c * 32);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) dst[q] = make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
+        int col = n_blk * BN + c * 32;
+        const CUtensorMap* cmap = &tma_c;
+        if constexpr (kGroup) {  // this 32-column chunk's problem and column within it
+          cmap = grp.cm + col / grp.seg_n;
+          col %= grp.seg_n;
+        }
+        EpiStoreBox(stage_c, boxes++, p, cmap, col, m_blk * BM + ew * 32, lane);
       }
       FenceBefore();
       __syncwarp();
@@ -387,6 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) BulkWaitAll();  // staged outputs written before the CTA retires
   }
   FenceBefore();
   __syncthreads();
@@ -433,8 +474,12 @@ __device__ __forceinline__ void MbarWaitCluster(uint64_t* bar, uint32_t parity) 
       "r"(parity)
       : "memory");
 }
+// Release at CTA scope (the PTX default): the epilogue's TMEM reads are ordered by
+// tcgen05.wait::ld + fence::before_thread_sync.  A .release.cluster arrive compiles to
+// MEMBAR.GPU, which waits for the warp's 16 KB of epilogue stores to drain on every tile (the
+// K = 128 score GEMMs of the 32-head block spent most of their time there).
 __device__ __forceinline__ void MbarArriveRemote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void TmaLoad2D2Sm(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
                                              int c1) {
@@ -469,7 +514,7 @@ struct Tc2Cfg {
   static constexpr int kStage = kABytes + kBBytes;
   static constexpr int kStages = (192 * 1024) / kStage;  // 6 (BN 256) / 8 (BN 128)
   static constexpr int kTmemCols = 2 * BN;
-  static constexpr int kSmem = kStages * kStage + 1024 + kEpiTabBytes + 1024;
+  static constexpr int kSmem = kStages * kStage + 1024 + kEpiTabBytes + kEpiStageBytes + 1024;
   static constexpr uint32_t kIdesc = (1u << 4)                     // D = F32
                                      | (1u << 7) | (1u << 10)      // A, B = BF16
                                      | ((kAKMajor ? 0u : 1u) << 15) | ((kBKMajor ? 0u : 1u) << 16) |
@@ -480,7 +525,7 @@ struct Tc2Cfg {
 template <int BN, bool kBKMajor, bool kAKMajor, bool kGroup = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     GemmTcPairKernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                     __nv_bfloat16* __restrict__ C, int M, int N, int K, ChainArgs epi, int ksplit,
+                     const __grid_constant__ CUtensorMap tma_c, int M, int N, int K, ChainArgs epi, int ksplit,
                      float* __restrict__ ws, GroupDev grp) {
   PdlTrigger();
   using Cfg = Tc2Cfg<BN, kBKMajor, kAKMajor>;
@@ -614,6 +659,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint16_t* tp[kMaxTanhRuns];
     StageEpiTables(epi, reinterpret_cast<uint16_t*>(smem + Cfg::kStages * Cfg::kStage + 1024), threadIdx.x - 128, tp);
     const uint32_t tempty_leader[2] = {MapaShared(SmemU32(&tempty[0]), 0), MapaShared(SmemU32(&tempty[1]), 0)};
+    uint8_t* stage_c = smem + Cfg::kStages * Cfg::kStage + 1024 + kEpiTabBytes + ew * 4096;
+    uint32_t boxes = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = pair; tile < tiles; tile += n_pairs) {
@@ -621,17 +668,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int m_blk = t % num_m, n_blk = t / num_m;
       MbarWait(&tfull[acc], acc_phase);
       FenceAfter();
-      const int row = m_blk * 2 * BM + static_cast<int>(rank) * BM + ew * 32 + lane;
-      __nv_bfloat16* crow = C + static_cast<int64_t>(row) * N + n_blk * BN;
+      const int row0 = m_blk * 2 * BM + static_cast<int>(rank) * BM + ew * 32;
+      const int row = row0 + lane;
       float* wrow = ws ? ws + (static_cast<int64_t>(ks) * M + row) * N + n_blk * BN : nullptr;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
         TmemLd32(tmem + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
-        if constexpr (kGroup) {
-          const int col = n_blk * BN + c * 32;
-          crow = grp.c[col / grp.seg_n] + static_cast<int64_t>(row) * grp.seg_n + col % grp.seg_n - c * 32;
-        }
         if (wrow) {
           float4* dst = reinterpret_cast<float4*>(wrow + c * 32);
 #pragma unroll
@@ -644,9 +687,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) p[j] = PackBf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
         EpiPackedBf16(epi, p, tp);
-        uint4* dst = reinterpret_cast<uint4*>(crow + c * 32);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) dst[q] = make_uint4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
+        int col = n_blk * BN + c * 32;
+        const CUtensorMap* cmap = &tma_c;
+        if constexpr (kGroup) {
+          cmap = grp.cm + col / grp.seg_n;
+          col %= grp.seg_n;
+        }
+        EpiStoreBox(stage_c, boxes++, p, cmap, col, row0, lane);
       }
       FenceBefore();
       __syncwarp();
@@ -656,6 +703,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) BulkWaitAll();
   }
   FenceBefore();
   __syncthreads();
@@ -936,7 +984,8 @@ EncodeFn GetEncode() {
 // 2-D tensor map (bf16 or fp32): inner dim `d0` (contiguous), outer `d1` with row pitch `pitch`
 // elements, 128-byte swizzle.
 CUtensorMap MakeMap(const void* base, uint64_t d0, uint64_t d1, uint64_t pitch, uint32_t box0,
-                    uint32_t box1, bool f32 = false) {
+                    uint32_t box1, bool f32 = false,
+                    CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   cuuint64_t dims[2] = {d0, d1};
   cuuint64_t strides[1] = {pitch * (f32 ? 4 : 2)};
@@ -944,23 +993,23 @@ CUtensorMap MakeMap(const void* base, uint64_t d0, uint64_t d1, uint64_t pitch, 
   cuuint32_t es[2] = {1, 1};
   CUresult r = GetEncode()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                            2, const_cast<void*>(base), dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) Fail("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")", RH_ERR_CUDA);
   return m;
 }
 
 struct Maps {
-  CUtensorMap a, b;
+  CUtensorMap a, b, c;  // c: output, 32 x 32 boxes, 64-byte swizzle (TMA-store epilogue)
 };
 
 // Tensor maps depend only on (pointer, shape); arena pointers are static, so cache them.
 // bn = B rows per CTA tile (K-major box), kb = K rows per stage (MN-major box).
 const Maps& GetMaps(const GemmArgs& g, int bn, int kb = BK) {
   static std::mutex mu;
-  static std::map<std::tuple<const void*, const void*, int64_t, int64_t, int64_t, bool, bool, int, int>, Maps> cache;
+  static std::map<std::tuple<const void*, const void*, const void*, int64_t, int64_t, int64_t, bool, bool, int, int>, Maps> cache;
   std::lock_guard<std::mutex> lk(mu);
-  auto key = std::make_tuple(g.a, g.b, g.m, g.n, g.k, g.ta, g.tb, bn, kb);
+  auto key = std::make_tuple(g.a, g.b, g.c, g.m, g.n, g.k, g.ta, g.tb, bn, kb);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   Maps m;
@@ -974,6 +1023,7 @@ const Maps& GetMaps(const GemmArgs& g, int bn, int kb = BK) {
   } else {
     m.b = MakeMap(g.b, g.n, g.k, g.n, 64, kb);  // B stored [K,N]: MN-major, 64-wide chunks
   }
+  m.c = MakeMap(g.c, g.n, g.m, g.n, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
   return cache.emplace(key, m).first->second;
 }
 
@@ -1068,7 +1118,7 @@ void LaunchKB(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullptr
   const int grid = std::min(tiles, NumSms());
   float* ws = ks > 1 ? static_cast<float*>(g.scratch) : nullptr;
   LaunchPdl(GemmTcKernel<BN, kBK, kAK, KB, kG>, grid, kThreads, Cfg::kSmem, s,
-      mp.a, mp.b, static_cast<__nv_bfloat16*>(g.c), static_cast<int>(g.m), static_cast<int>(n),
+      mp.a, mp.b, mp.c, static_cast<int>(g.m), static_cast<int>(n),
       static_cast<int>(g.k), g.epi, ks, ws, kG ? gl->dev : GroupDev{});
   RH_CUDA(cudaGetLastError());
   if (ws) {
@@ -1120,7 +1170,7 @@ void LaunchPair(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullp
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = PdlEnabled() ? 2 : 1;
-  RH_CUDA(cudaLaunchKernelEx(&cfg, GemmTcPairKernel<BN, kBK, kAK, kG>, mp.a, mp.b, static_cast<__nv_bfloat16*>(g.c),
+  RH_CUDA(cudaLaunchKernelEx(&cfg, GemmTcPairKernel<BN, kBK, kAK, kG>, mp.a, mp.b, mp.c,
                              static_cast<int>(g.m), static_cast<int>(n), static_cast<int>(g.k), g.epi, ks, ws,
                              kG ? gl->dev : GroupDev{}));
   if (ws) {
@@ -1299,7 +1349,7 @@ bool GemmTcGroupSupported(const GemmArgs& g, int n_prob, bool shared_a) {
 }
 
 size_t GemmTcGroupTableBytes(int n_prob) {
-  return static_cast<size_t>(n_prob) * (2 * sizeof(CUtensorMap) + sizeof(void*));
+  return static_cast<size_t>(n_prob) * 3 * sizeof(CUtensorMap);
 }
 
 const char* GemmTcGroupSchedule(const GemmArgs& g, int n_prob, bool shared_a) {
@@ -1319,23 +1369,24 @@ void PrepareGemmTcGroup(const GemmArgs& g, int n_prob, const void* const* a, con
   std::vector<char> host(GemmTcGroupTableBytes(n_prob));
   CUtensorMap* bm = reinterpret_cast<CUtensorMap*>(host.data());
   CUtensorMap* am = bm + n_prob;
-  void** cp = reinterpret_cast<void**>(am + n_prob);
+  CUtensorMap* cm = am + n_prob;
   for (int p = 0; p < n_prob; ++p) {
     GemmArgs gp = g;
     gp.a = a[p];
     gp.b = b[p];
+    gp.c = c[p];
     const Maps& mp = GetMaps(gp, box_n, kb);
     if (p == 0) h.gl.m0 = mp;
     bm[p] = mp.b;
     am[p] = mp.a;
-    cp[p] = c[p];
+    cm[p] = mp.c;
     if (reinterpret_cast<uintptr_t>(c[p]) % 16) Fail("tcgen05 grouped GEMM: unaligned output");
   }
   RH_CUDA(cudaMemcpy(table, host.data(), host.size(), cudaMemcpyHostToDevice));
   const CUtensorMap* tb = static_cast<const CUtensorMap*>(table);
   h.gl.dev.b = tb;
   h.gl.dev.a = shared_a ? nullptr : tb + n_prob;
-  h.gl.dev.c = reinterpret_cast<__nv_bfloat16* const*>(tb + 2 * n_prob);
+  h.gl.dev.cm = tb + 2 * n_prob;
   h.gl.dev.seg_n = static_cast<int>(g.n);
   h.gl.n_prob = n_prob;
   std::lock_guard<std::mutex> lk(g_group_mu);

@@ -162,6 +162,17 @@ void LaunchTranspose(void* out, const void* in, int nd, const int64_t* in_dims, 
                      int dtype, cudaStream_t s);
 void LaunchBroadcast(void* out, const void* in, int64_t n_out, int64_t n_in, int dtype,
                      cudaStream_t s);
+// Concat of every piece in one launch (16-byte units): row16/off16/orow16 in 16-byte units.
+// Returns false when a row, offset or pointer is not 16-byte aligned (use the per-piece form).
+constexpr int kMaxConcat = 64;
+struct ConcatArgs {
+  void* out;
+  const void* in[kMaxConcat];
+  int64_t row16[kMaxConcat], off16[kMaxConcat];
+  int64_t outer, orow16;
+  int n;
+};
+bool LaunchConcat(const ConcatArgs& a, cudaStream_t s);
 // Concat: copies `in` ([outer, row] contiguous) into out at column offset `off` of rows `orow`.
 void LaunchConcatPiece(void* out, const void* in, int64_t outer, int64_t row, int64_t orow,
                        int64_t off, int dtype, cudaStream_t s);
