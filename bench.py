@@ -31,6 +31,10 @@ NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
 WORKLOADS = {
     "gpt_block": dict(plan="c3_gpt_block_d{n}", name="gpt_block_h4096_s2048", dtype="bf16",
                       metric="partitioned-program tokens/s (GPT block, hidden 4096, seq 2048)"),
+    # C3 with attention split into 32 rank-2 heads joined by concat (tests/golden/make_plans.py
+    # gpt_heads_ir: 96 q/k/v + 32 score + 32 context GEMMs per block, 790 ops)
+    "gpt_heads32": dict(plan="c3_gpt_heads32_d{n}", name="gpt_block_h4096_s2048_heads32", dtype="bf16",
+                        metric="partitioned-program tokens/s (GPT block, hidden 4096, seq 2048, 32 heads)"),
     # C5: 24-layer GPT forward + backward (tests/golden/make_fwd_bwd.py); the CPU sample is one
     # layer of the same shapes (the full 24-layer step is minutes of CPU), scaled by 1/24
     "gpt24_train": dict(plan="c5_big_gpt24_d{n}", name="gpt24_fwd_bwd_h2048_t2048", dtype="bf16",
@@ -71,7 +75,149 @@ def peaks():
             j = json.load(f)
         p.update({k: j[k] for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in j})
         p["source"] = "measured"
+    # fp32 denominators (not in MEASURED_PEAKS.json): cuBLAS TF32 / CUDA-core fp32, measured by
+    # tools/measure_peaks.py on this pool's B200s
+    extra = os.path.join(REPO, "profiles", "peaks_extra.json")
+    if os.path.exists(extra):
+        with open(extra) as f:
+            j = json.load(f)
+        p.update({k: j[k] for k in ("tf32_tflops", "fp32_tflops") if k in j})
     return p
+
+
+def roofline_of(steps, ms_prof, pk, clk_sum, f32):
+    """Roofline of the dominant kernel class (the largest share of the step): achieved =
+    algorithmic flops (or bytes) summed over its launches / their summed device time."""
+    kern = [s for s in steps if s["kind"] == 0]
+    classes = {}
+    for s in kern:
+        c = classes.setdefault(s["name"].split(" ")[0], {"ms": 0.0, "alg_flops": 0.0, "alg_bytes": 0.0, "n": 0})
+        c["ms"] += s["ms"]
+        c["alg_flops"] += s["alg_flops"]
+        c["alg_bytes"] += s["alg_bytes"]
+        c["n"] += 1
+    # the tcgen05 GEMM kernels (single launches and grouped launches) are one class
+    gemm = {"ms": 0.0, "alg_flops": 0.0, "alg_bytes": 0.0, "n": 0}
+    for k in [k for k in classes if k.startswith("gemm_tc")]:
+        for f in gemm:
+            gemm[f] += classes[k][f]
+    if gemm["n"]:
+        classes = {k: v for k, v in classes.items() if not k.startswith("gemm_tc")}
+        classes["gemm_tc" + ("_3xtf32" if f32 else "")] = gemm
+    cname, c = max(classes.items(), key=lambda kv: kv[1]["ms"])
+    if "gemm_tc" in cname:
+        achieved = c["alg_flops"] / (c["ms"] * 1e-3) / 1e12
+        # B200_PROFILING.md: the burst peak for a kernel that runs at full clocks, the
+        # sustained (power-capped, ~1340 MHz) one when the timed region ran below max clocks
+        at_max = bool(clk_sum.get("sm_mhz") and clk_sum.get("sm_max_mhz")
+                      and clk_sum["sm_mhz"] >= 0.95 * clk_sum["sm_max_mhz"])
+        kind = "burst" if at_max else "sustained"
+        if f32 and "tf32_tflops" in pk:
+            peak = pk["tf32_tflops"] / 3
+            note = ("3xTF32: measured cuBLAS TF32 peak (profiles/peaks_extra.json, tools/measure_peaks.py) "
+                    "/ 3 products")
+        elif f32:
+            peak = pk["bf16_tflops" if at_max else "bf16_tflops_sustained"] / 6
+            note = f"3xTF32 effective fp32 = {kind} bf16 / 2 (tf32 rate) / 3 (products) of MEASURED_PEAKS.json"
+        else:
+            peak = pk["bf16_tflops" if at_max else "bf16_tflops_sustained"]
+            note = (f"{kind} bf16 (timed region at {clk_sum.get('sm_mhz')} of {clk_sum.get('sm_max_mhz')} MHz)"
+                    f" of MEASURED_PEAKS.json ({pk['source']})")
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None, "kernel": cname, "peak_note": note,
+                "launches": c["n"], "share_of_step": c["ms"] / ms_prof}
+    else:
+        achieved = c["alg_bytes"] / (c["ms"] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "traffic": None, "kernel": cname,
+                "launches": c["n"], "share_of_step": c["ms"] / ms_prof}
+    return roof, classes
+
+
+def normwise(a, b):
+    import numpy as np
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+
+
+def variant_run(D, rx, rt, pname, dtype, steps, warmup, pk, clk_sum, check_oracle=False):
+    """One more program on the same runtime (the default line's sub-records): device ms per step
+    (max over ranks), the dominant kernel's roofline and, optionally (rank 0), the normwise error
+    of its output against the CPU oracle with fp64-accumulated GEMMs."""
+    from paper_2302_08141_b200.abi import RH_F32
+    from paper_2302_08141_b200.program import LoweredProgram
+    prog = LoweredProgram.load(pname).with_dtype(dtype)
+    mesh = rx.Mesh(rt, prog.mesh)
+    gp = rx.Program(mesh, prog, 0)
+    try:
+        gp.init_synthetic(0)
+        gp.run(warmup)
+        D.barrier()
+        ms = D.max_over_ranks(gp.run(steps))
+        prof = gp.profile(min(steps, 3))
+        roof, _ = roofline_of(gp.steps(), prof, pk, clk_sum, dtype == RH_F32)
+        out = gp.read_full(prog.outputs[0]) if check_oracle and rt.first_rank == 0 else None
+    finally:
+        gp.close()
+        mesh.close()
+    tok = tokens_of(prog)
+    rec = {"plan": pname, "dtype": "f32" if dtype == RH_F32 else "bf16", "ms_per_step": ms,
+           "value": tok / (ms * 1e-3), "unit": "tokens/s", "gflop_per_step": prog.flops() / 1e9,
+           "roofline": roof}
+    if out is not None:
+        from oracle import pyoracle
+        o = pyoracle.OracleProgram(prog, flags=pyoracle.OracleProgram.GEMM_F64)
+        o.init_synthetic(0)
+        o.run_unpartitioned(os.cpu_count() or 1)
+        want = o.read_full(prog.outputs[0], partitioned=False)
+        conv = (lambda a: a) if dtype == RH_F32 else pyoracle.bf16_to_f32
+        rec["normwise_err_vs_oracle_f64"] = normwise(conv(out), conv(want))
+    return rec
+
+
+def reshard_hbm(rx, pk, d=4, size=256 << 20):
+    """HBM-bound pack / unpack / slice kernels of the resharding transitions (K9-K13) with d ranks
+    emulated on this GPU (every source and destination in local HBM), 256 MiB bf16 [rows, 4096]:
+    algorithmic bytes (each rank's reads + writes) / device time against the HBM copy peak."""
+    import torch
+    from paper_2302_08141_b200.abi import RH_BF16, AxisSpec
+    rt = rx.Runtime(devices=[0] * d)
+    mesh = rx.Mesh(rt, [d])
+    eb = 2
+    rows = size // (4096 * eb)
+    dims = [rows, 4096]
+    pairs = [("replicated", "shard(0,max)"), ("replicated", "shard(1,64)"), ("replicated", "shard(1,1)"),
+             ("shard(0,max)", "shard(1,max)"), ("shard(1,max)", "shard(0,max)"), ("shard(1,1)", "shard(0,max)"),
+             ("shard(0,max)", "shard(1,1)"), ("shard(1,1)", "shard(1,64)"), ("shard(0,max)", "replicated"),
+             ("partial", "shard(0,max)")]
+    out = []
+    try:
+        for fname, tname in pairs:
+            def spec(s):
+                if "max" in s:
+                    dim = int(s[6])
+                    return AxisSpec.shard(dim, dims[dim] // d)
+                return AxisSpec.from_string(s)
+            fs, ts = spec(fname), spec(tname)
+            n_src = size // eb // (d if fs.kind == 0 else 1)
+            n_dst = size // eb // (d if ts.kind == 0 else 1)
+            src = [torch.randn(n_src, device="cuda", dtype=torch.bfloat16) for _ in range(d)]
+            dst = [torch.empty(n_dst, device="cuda", dtype=torch.bfloat16) for _ in range(d)]
+            torch.cuda.synchronize()
+            mesh.reshard(0, fs, ts, dims, RH_BF16, [x.data_ptr() for x in src], [x.data_ptr() for x in dst], 0, 3)
+            ms = mesh.reshard(0, fs, ts, dims, RH_BF16, [x.data_ptr() for x in src], [x.data_ptr() for x in dst], 0, 10)
+            reads = n_dst * eb * (d if fs.kind == 2 else 1)
+            alg = (reads + n_dst * eb) * d
+            gbs = alg / (ms * 1e-3) / 1e9
+            out.append({"from": fname, "to": tname, "ms": ms, "alg_bytes": alg, "hbm_gbs": gbs,
+                        "frac": gbs / pk["hbm_gbs"]})
+            del src, dst
+            torch.cuda.empty_cache()
+    finally:
+        mesh.close()
+        rt.close()
+    return {"d": d, "bytes": size, "dtype": "bf16", "mode": f"{d} ranks emulated on one GPU (local HBM)",
+            "peak_gbs": pk["hbm_gbs"], "transitions": out}
 
 
 class Clocks:
@@ -198,6 +344,8 @@ def main():
     ap.add_argument("--no-overlap", action="store_true", help="keep every transition on the main stream")
     ap.add_argument("--simt", action="store_true", help="force the CUDA-core GEMM (comparison)")
     ap.add_argument("--no-pdl", action="store_true", help="no programmatic dependent launch (A/B)")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the default line's sub-records (fp32 C3, 32-head C3, HBM resharding)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.dtype is None:
@@ -276,43 +424,12 @@ def main():
         D.barrier()
         e2e_ms = D.max_over_ranks(gp.run_host(max(args.steps, 2), xs, ptrs, [yout.data_ptr()]))
 
-        # Roofline of the dominant kernel (the kernel class with the largest share of the step:
-        # achieved = algorithmic flops or bytes summed over its launches / their summed time).
         pk = peaks()
-        kern = [s for s in steps if s["kind"] == 0]
-        classes = {}
-        for s in kern:
-            c = classes.setdefault(s["name"].split(" ")[0], {"ms": 0.0, "alg_flops": 0.0, "alg_bytes": 0.0, "n": 0})
-            c["ms"] += s["ms"]
-            c["alg_flops"] += s["alg_flops"]
-            c["alg_bytes"] += s["alg_bytes"]
-            c["n"] += 1
-        cname, c = max(classes.items(), key=lambda kv: kv[1]["ms"])
-        dom = dict(c, name=cname)
-        gemm_ms = sum(s["ms"] for s in kern if "gemm" in s["name"])
         clk_sum = clk.summary()
-        if "gemm_tc" in dom["name"]:
-            achieved = dom["alg_flops"] / (dom["ms"] * 1e-3) / 1e12
-            f32 = dtype == RH_F32
-            # B200_PROFILING.md: the burst peak for a kernel that runs at full clocks, the
-            # sustained (power-capped, ~1340 MHz) one when the timed region ran below max clocks
-            at_max = bool(clk_sum.get("sm_mhz") and clk_sum.get("sm_max_mhz")
-                          and clk_sum["sm_mhz"] >= 0.95 * clk_sum["sm_max_mhz"])
-            key = "bf16_tflops" if at_max else "bf16_tflops_sustained"
-            peak = pk[key] / 6 if f32 else pk[key]
-            kind = "burst" if at_max else "sustained"
-            roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": None, "kernel": dom["name"],
-                    "peak_note": (f"3xTF32 effective fp32 = {kind} bf16 / 2 (tf32 rate) / 3 (products)"
-                                  if f32 else f"{kind} bf16 (timed region at "
-                                  f"{clk_sum.get('sm_mhz')} of {clk_sum.get('sm_max_mhz')} MHz)")
-                                 + f" of MEASURED_PEAKS.json ({pk['source']})",
-                    "launches": dom["n"], "share_of_step": dom["ms"] / ms_prof}
-        else:
-            achieved = dom["alg_bytes"] / (dom["ms"] * 1e-3) / 1e9
-            roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                    "frac": achieved / pk["hbm_gbs"], "traffic": None, "kernel": dom["name"],
-                    "launches": dom["n"], "share_of_step": dom["ms"] / ms_prof}
+        kern = [s for s in steps if s["kind"] == 0]
+        gemm_ms = sum(s["ms"] for s in kern if "gemm" in s["name"])
+        roof, classes = roofline_of(steps, ms_prof, pk, clk_sum, dtype == RH_F32)
+        dom = {"name": roof["kernel"]}
         tr_path = os.path.join(REPO, "profiles", "ncu_traffic.json")
         if os.path.exists(tr_path):
             with open(tr_path) as f:
@@ -354,7 +471,20 @@ def main():
         d2h = gp.local_bytes(out, rank) * world if reduce_outputs else prog.full_bytes(out)
         gp.close()
         mesh.close()
+        # Sub-records of the default line: the reference program's own precision (fp32, with its
+        # end-to-end error against the oracle), the 32-head variant of the block, and (N=1) the
+        # HBM-bound resharding kernels
+        variants = None
+        if args.workload == "gpt_block" and not args.no_variants and dtype == RH_BF16:
+            variants = {
+                "f32": variant_run(D, rx, rt, plan_name("gpt_block", world), RH_F32, max(3, args.steps // 4),
+                                   3, pk, clk_sum, check_oracle=(world == 1)),
+                "gpt_heads32": variant_run(D, rx, rt, plan_name("gpt_heads32", world), RH_BF16, args.steps,
+                                           args.warmup, pk, clk_sum),
+            }
         rt.close()
+        if variants is not None and world == 1:
+            variants["reshard_hbm"] = reshard_hbm(rx, pk)
     if rank == 0:
         line = {
             "metric": wl["metric"], "value": tok / (ms_step * 1e-3), "unit": "tokens/s", "n_gpus": world,
@@ -383,6 +513,7 @@ def main():
             "gpu_launches": launches,
             "roofline": roof,
             "reshard": reshard,
+            "variants": variants,
             "cpu_baseline": cpu,
             "clocks": clk_sum,
             "kernel_classes": {k: {"ms": round(v["ms"], 4), "launches": v["n"]} for k, v in

@@ -37,7 +37,9 @@ typedef enum {
   RH_ERR_CUDA = -2,        /* CUDA runtime failure */
   RH_ERR_NCCL = -3,        /* NCCL failure */
   RH_ERR_STATE = -4,       /* call out of order */
-  RH_ERR_UNSUPPORTED = -5  /* valid per the reference, not executable by this build */
+  RH_ERR_UNSUPPORTED = -5, /* valid per the reference, not executable by this build */
+  RH_ERR_TIMEOUT = -6      /* a cross-GPU barrier did not complete within RH_SYNC_TIMEOUT_MS
+                              (default 20 s): a peer died or the schedules diverged */
 } rh_status;
 
 /* parashard::AxisSpec::Kind (sharding.h:33) — note the reference enum order is
@@ -205,6 +207,14 @@ int rh_program_step_info(const rh_program* prog, int i, rh_step_info* out);
 int rh_program_profile(rh_program* prog, int iters, double* ms_per_iter);
 /* Kernel launches per run summed over this process's ranks. */
 int rh_program_launch_count(const rh_program* prog, int64_t* launches);
+
+/* The executor's local-op rule table on its own (host only, no device): the output spec per mesh
+ * axis that op `op`'s local computation produces when its inputs arrive in the specs its
+ * strategy demands (ops[op].in_specs) — the local side of FollowInput / ProduceOutput
+ * (proj/src/sharding.cpp:225-388), composed over axes as EffectiveShapes does (:390-403).  A
+ * planned out_spec that differs from it is executed by the pin fallback (compute, then slice,
+ * sharding.cpp:477-487).  Fails (RH_ERR_INVALID) when no local rule exists. */
+int rh_op_natural_specs(const rh_op* ops, int n_ops, int op, int n_axes, const int* mesh_dims, rh_spec* out);
 
 /* Microbenchmark entry (config C4): one transition `from -> to` on mesh axis `axis` of a
  * tensor of global shape dims (dtype), src/dst = device buffers of every LOCAL rank (in local

@@ -510,7 +510,7 @@ bool Passthrough(const Dims& in, const Dims& out, const rh_spec& s, int d, rh_sp
 // (sharding.cpp:225-388).  `in_dims` are the per-slot shapes on this axis, `out_dims` the
 // output's.
 rh_spec Natural(const Op& op, const std::vector<rh_spec>& in, const std::vector<Dims>& in_dims,
-                const Dims& out_dims, int d) {
+                const Dims& out_dims, int d, const rh_spec& planned) {
   auto bad = [&]() -> rh_spec {
     std::string m = "op kind " + std::to_string(op.raw.kind) + ": no local rule for inputs";
     for (auto& s : in) m += " " + SpecStr(s);
@@ -518,6 +518,12 @@ rh_spec Natural(const Op& op, const std::vector<rh_spec>& in, const std::vector<
   };
   bool all_rep = true;
   for (auto& s : in) all_rep &= s.kind == RH_REPLICATED;
+  // ProduceOutput, Broadcast with want.dim < off (sharding.cpp:360-367): a replicated input and
+  // an output sharded on a broadcast (leading) dim — each rank holds its rows of the broadcast
+  if (all_rep && op.raw.kind == RH_OP_BROADCAST && planned.kind == RH_SHARD && !in_dims.empty() &&
+      planned.dim < static_cast<int>(out_dims.size() - in_dims[0].size()) &&
+      out_dims[planned.dim] % (static_cast<int64_t>(d) * planned.stride) == 0)
+    return planned;
   if (all_rep) return Rep();
   for (auto& s : in)
     if (s.kind == RH_PARTIAL) bad();
@@ -629,7 +635,7 @@ struct Exec {
                             Specs(ispecs[s].begin(), ispecs[s].begin() + a), mesh);
       }
       Dims od = LocalDims(op.dims, Specs(nat.begin(), nat.begin() + a), mesh);
-      nat[a] = Natural(op, in_a, in_d, od, mesh.dims[a]);
+      nat[a] = Natural(op, in_a, in_d, od, mesh.dims[a], out[a]);
     }
     std::vector<std::vector<float>> res(world);
     for (int r = 0; r < world; ++r) {

@@ -110,6 +110,12 @@ class AxisSpec:
     def to_c(self):
         return RhSpec(self.kind, self.dim, self.stride)
 
+    @staticmethod
+    def from_c(c):
+        if c.kind == RH_SHARD:
+            return AxisSpec.shard(c.dim, c.stride)
+        return AxisSpec(c.kind)
+
     @property
     def is_shard(self):
         return self.kind == RH_SHARD

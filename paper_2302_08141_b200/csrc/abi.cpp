@@ -114,6 +114,8 @@ void GroupSync(rh_program* p, int axis, bool side = false) {
     b.my_flags = reinterpret_cast<uint32_t*>(p->base[0] + flags_off);
     b.counter = reinterpret_cast<uint32_t*>(p->base[0] + counter_off);
     b.me = g;
+    b.err = reinterpret_cast<uint32_t*>(p->base[0] + p->err_off);
+    b.timeout_ns = rh::SyncTimeoutNs();
     rh::LaunchBarrier(b, side ? p->side : rt->streams[0]);
     return;
   }
@@ -148,6 +150,8 @@ void WorldSync(rh_program* p) {
   b.my_flags = reinterpret_cast<uint32_t*>(p->base[0] + p->flags_off);
   b.counter = reinterpret_cast<uint32_t*>(p->base[0] + p->counter_off);
   b.me = rt->first_rank;
+  b.err = reinterpret_cast<uint32_t*>(p->base[0] + p->err_off);
+  b.timeout_ns = rh::SyncTimeoutNs();
   rh::LaunchBarrier(b, rt->streams[0]);
 }
 
@@ -260,6 +264,23 @@ void SyncAll(rh_runtime* rt) {
     DeviceGuard dg(rt->devs[i]);
     RH_CUDA(cudaStreamSynchronize(rt->streams[i]));
   }
+}
+
+// After a run (dist mode): a cross-GPU wait that gave up (PeerSync.err) fails the call.
+void CheckSync(rh_program* p) {
+  rh_runtime* rt = p->mesh->rt;
+  if (!rt->dist || rt->world == 1 || p->base.empty()) return;
+  uint32_t e = 0;
+  DeviceGuard dg(rt->devs[0]);
+  if (p->side) RH_CUDA(cudaStreamSynchronize(p->side));
+  RH_CUDA(cudaMemcpy(&e, p->base[0] + p->err_off, 4, cudaMemcpyDeviceToHost));
+  if (!e) return;
+  const uint32_t zero = 0;
+  RH_CUDA(cudaMemcpy(p->base[0] + p->err_off, &zero, 4, cudaMemcpyHostToDevice));
+  Fail("cross-GPU barrier timed out: rank " + std::to_string((e >> 8) & 0xff) + " waited more than " +
+           std::to_string(rh::SyncTimeoutNs() / 1000000) + " ms for rank " + std::to_string(e & 0xff) +
+           " (RH_SYNC_TIMEOUT_MS); the run's results are invalid",
+       RH_ERR_TIMEOUT);
 }
 
 // Host-side barrier over the world communicator (dist) — used around setup only.
@@ -651,6 +672,15 @@ int LoadProgram(rh_mesh* mesh, const rh_op* ops, int n_ops, const int* outputs, 
 
 extern "C" {
 
+int rh_op_natural_specs(const rh_op* ops, int n_ops, int op, int n_axes, const int* mesh_dims, rh_spec* out) {
+  return Guard([&] {
+    if (n_axes < 1 || n_axes > RH_MAX_AXES) Fail("bad mesh");
+    const std::vector<int> mesh(mesh_dims, mesh_dims + n_axes);
+    const Specs nat = rh::NaturalSpecsOf(ops, n_ops, op, mesh);
+    for (int a = 0; a < n_axes; ++a) out[a] = nat[a];
+  });
+}
+
 int rh_program_load(rh_mesh* mesh, const rh_op* ops, int n_ops, const int* outputs, int n_out,
                     uint32_t flags, rh_program** out) {
   return LoadProgram(mesh, ops, n_ops, outputs, n_out, flags, {}, out);
@@ -729,6 +759,7 @@ int rh_program_run(rh_program* p, int iters, double* ms_per_iter) {
       cudaEventDestroy(ev0[i]);
       cudaEventDestroy(ev1[i]);
     }
+    CheckSync(p);
     if (ms_per_iter) *ms_per_iter = iters > 0 ? worst / iters : 0.0;
   });
 }
@@ -754,6 +785,7 @@ int rh_program_profile(rh_program* p, int iters, double* ms_per_iter) {
       for (int it = 0; it < iters; ++it) RunOnce(p, &ev[it]);
     }
     SyncAll(rt);
+    CheckSync(p);
     std::vector<double> acc(n, 0.0);
     for (int it = 0; it < iters; ++it)
       for (size_t i = 0; i < n; ++i) {
@@ -955,6 +987,7 @@ int rh_program_run_host(rh_program* p, int iters, int n_in, const int* in_ops, c
       throw;
     }
     cleanup();
+    CheckSync(p);
   });
 }
 
@@ -1012,6 +1045,7 @@ int rh_program_step_host(rh_program* p, int n_in, const int* in_ops, const void*
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    CheckSync(p);
     if (ms) *ms = std::max<double>(dev_ms, host_ms);
   });
 }

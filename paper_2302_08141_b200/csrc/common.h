@@ -32,6 +32,20 @@ struct Error : std::runtime_error {
 
 inline int ElemBytes(int dtype) { return dtype == RH_BF16 ? 2 : 4; }
 
+// SMs of the current device (148 on B200; queried once per device, so persistent grids and wave
+// heuristics follow the part they run on: another SKU, a MIG slice or a green context).
+inline int SmCount() {
+  static int cache[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
+
 // ---------------------------------------------------------------------------------------------
 // Single-axis block-cyclic view (sharding.cpp:61-72).  Shard(dim, s) on an axis of size d over
 // a tensor of `dims`: write the flat index as f = ((p * d + r) * Qs + u) with

@@ -134,8 +134,11 @@ const char* KindName(int k) {
 }
 
 // The output spec (one mesh axis) the local computation produces from the given input specs.
+// `planned`: the op's planned output spec on this axis — it decides the one rule whose output is
+// not a function of the inputs: ProduceOutput's Broadcast R -> Shard(y < off) (sharding.cpp:
+// 360-367), where every rank writes only its own rows of the broadcast.
 rh_spec Natural(const rh_op& op, const std::vector<rh_spec>& in, const std::vector<Dims>& in_dims,
-                const Dims& out_dims, int d) {
+                const Dims& out_dims, int d, const rh_spec& planned) {
   auto bad = [&]() -> rh_spec {
     std::string m = std::string("no local rule for ") + KindName(op.kind) + " with inputs";
     for (auto& s : in) m += " " + SpecStr(s);
@@ -143,6 +146,9 @@ rh_spec Natural(const rh_op& op, const std::vector<rh_spec>& in, const std::vect
   };
   bool all_rep = true;
   for (auto& s : in) all_rep = all_rep && s.kind == RH_REPLICATED;
+  if (all_rep && op.kind == RH_OP_BROADCAST && planned.kind == RH_SHARD && !in_dims.empty() &&
+      planned.dim < static_cast<int>(out_dims.size() - in_dims[0].size()) && Valid(planned, out_dims, d))
+    return planned;
   if (all_rep) return Rep();
   for (auto& s : in)
     if (s.kind == RH_PARTIAL) bad();
@@ -195,7 +201,7 @@ rh_spec Natural(const rh_op& op, const std::vector<rh_spec>& in, const std::vect
 int SideBlocks() {
   static const int n = [] {
     const char* e = std::getenv("RH_SIDE_BLOCKS");
-    return e ? std::max(1, std::atoi(e)) : 148 * 2;
+    return e ? std::max(1, std::atoi(e)) : SmCount() * 2;
   }();
   return n;
 }
@@ -246,6 +252,7 @@ class Lowerer {
     // flags + barrier counter live at the front of the arena
     p_->flags_off = Alloc(static_cast<size_t>(rt_->world) * 4);
     p_->counter_off = Alloc(4);
+    p_->err_off = Alloc(4);
     ValidateSpecs();
     const bool eager = rt_->dist && rt_->world > 1 && !(p_->flags & RH_FLAG_NO_OVERLAP) &&
                        !getenv("RH_NO_EAGER_TRANSITIONS");
@@ -353,6 +360,10 @@ class Lowerer {
       }
       if (ok) p_->steps[l].post_sync = false;
     }
+    for (auto& st : p_->steps) {
+      if (st.post_mode == 1) st.post_sync = true;
+      if (st.post_mode == 2) st.post_sync = false;
+    }
   }
 
  private:
@@ -381,7 +392,7 @@ class Lowerer {
     };
     for (int i = 0; i < ns; ++i) {
       Step& st = S[i];
-      if (st.kind != Step::kTransition || !st.p2p || st.sync_slot < 0 || st.writes.size() != 1) continue;
+      if (st.kind != Step::kTransition || !st.p2p || st.sync_slot < 0 || st.writes.size() != 1 || st.no_async) continue;
       const int y = Root(st.writes[0]);
       int j = -1;
       for (int k = i + 1; k < ns && j < 0; ++k)
@@ -453,7 +464,7 @@ class Lowerer {
     rh_program* P = p_;
     for (size_t i = 0; i < p_->steps.size(); ++i) {
       Step& st = p_->steps[i];
-      if (st.pulls.empty()) continue;
+      if (st.pulls.empty() && !st.fine) continue;
       const bool async = st.async;
       const int slot = async ? -1 : st.sync_slot;
       const int axis = st.axis;
@@ -473,10 +484,17 @@ class Lowerer {
         }
         y.my_slot = reinterpret_cast<uint32_t*>(P->peer_base[g] + row);
         y.epoch = reinterpret_cast<const uint32_t*>(P->peer_base[g] + P->epoch_off);
+        y.err = reinterpret_cast<uint32_t*>(P->peer_base[g] + P->err_off);
+        y.timeout_ns = SyncTimeoutNs();
         return y;
       };
       const std::vector<std::function<PullArgs(int)>> pulls = st.pulls;
       const int cap = async ? SideBlocks() : 0;
+      if (st.fine) {
+        const auto fine = st.fine;
+        st.run = [fine, sync_of, cap](int li, cudaStream_t s) { return fine(li, s, sync_of(li), cap); };
+        continue;
+      }
       if (n == 1) {
         st.run = [pulls, sync_of, cap](int li, cudaStream_t s) {
           PullArgs a = pulls[0](li);
@@ -654,7 +672,7 @@ class Lowerer {
         in_a.push_back(ins[s][a]);
         in_d.push_back(LocalDims(GDims(p_->inputs[i][s]), ins[s], mesh_, a));
       }
-      nat[a] = Natural(op, in_a, in_d, LocalDims(GDims(i), nat, mesh_, a), mesh_[a]);
+      nat[a] = Natural(op, in_a, in_d, LocalDims(GDims(i), nat, mesh_, a), mesh_[a], p_->out_specs[i][a]);
     }
     return nat;
   }
@@ -947,10 +965,11 @@ class Lowerer {
   void PlanRemat(const std::vector<bool>& is_out, NoPartial no_partial) {
     const int n = static_cast<int>(p_->ops.size());
     remat_.assign(ew_.size(), Remat{});
-    // Default: on for single-process runs (one GPU, or emulated ranks); multi-process meshes
-    // need RH_REMAT=1 until the N=2 C5 hang with rematerialization is found.
+    // Default: on when every rank runs on one physical GPU (one rank, or emulated ranks);
+    // meshes over several GPUs need RH_REMAT=1 until the N=2 C5 hang seen with it is explained
+    // (the cross-GPU waits are bounded, so it now fails as RH_ERR_TIMEOUT).
     const char* env = getenv("RH_REMAT");
-    const bool on = env ? env[0] != '0' : !(rt_->dist && rt_->world > 1);
+    const bool on = env ? env[0] != '0' : !(rt_->dist && rt_->world > 1) && rt_->devs.size() == 1;
     if (!on || ew_.empty() || (p_->flags & RH_FLAG_KEEP_ALL)) return;
     if (p_->ops[0].dtype != RH_BF16) return;
     // GEMM-epilogue tails: their value is the fused kernel's stored output (a base, not a
@@ -1909,6 +1928,12 @@ class Lowerer {
     const AxisView tv = MakeAxisView(to, static_cast<int>(D.size()), D.data(), d);
     const int eb = ElemBytes(X.dtype);
     const double S = static_cast<double>(Prod(D)) * eb;
+    {
+      static const bool no_fine = getenv("RH_NO_FINE") != nullptr;  // A/B knob (profiles/)
+      const bool nccl_t = (p_->flags & RH_FLAG_TRANSPORT_NCCL) && rt_->dist;
+      const FinePlan fp = ClassifyFine(fv, tv, eb, d, Prod(D));
+      if (fp.mode && !no_fine && !nccl_t) return EmitFine(fp, src, dst, axis, fv, tv, S, why);
+    }
     Step st;
     st.kind = Step::kTransition;
     st.axis = axis;
@@ -2018,5 +2043,27 @@ class Lowerer {
 }  // namespace
 
 void LowerProgram(rh_program* p) { Lowerer(p).Lower(); }
+
+// The local-op rule table on its own (rh_op_natural_specs): composed over the mesh axes exactly
+// as the lowering does (axis a sees the shapes left by axes < a, sharding.cpp:390-403).
+Specs NaturalSpecsOf(const rh_op* ops, int n_ops, int i, const std::vector<int>& mesh) {
+  if (i < 0 || i >= n_ops) Fail("bad op index");
+  const rh_op& op = ops[i];
+  const int n_axes = static_cast<int>(mesh.size());
+  auto gdims = [&](int k) { return Dims(ops[k].dims, ops[k].dims + ops[k].rank); };
+  Specs nat(n_axes), out(op.out_spec, op.out_spec + n_axes);
+  for (int a = 0; a < n_axes; ++a) {
+    std::vector<rh_spec> in_a;
+    std::vector<Dims> in_d;
+    for (int sl = 0; sl < op.n_in; ++sl) {
+      Specs ins(n_axes);
+      for (int b = 0; b < n_axes; ++b) ins[b] = op.in_specs[b * op.n_in + sl];
+      in_a.push_back(ins[a]);
+      in_d.push_back(LocalDims(gdims(op.inputs[sl]), ins, mesh, a));
+    }
+    nat[a] = Natural(op, in_a, in_d, LocalDims(gdims(i), nat, mesh, a), mesh[a], out[a]);
+  }
+  return nat;
+}
 
 }  // namespace rh

@@ -73,6 +73,10 @@ struct Step {
   double ms = 0;             // from the last profile
   std::vector<int> reads, writes;  // tensors (for the arena planner's liveness)
   bool async = false;  // dist p2p transition on the side stream, overlapping the compute
+  int post_mode = 0;   // p2p post-barrier: 0 planned (elided when a later barrier orders it),
+                       // 1 always (push: peers wrote this rank's destination), 2 never (the
+                       // push phase of a two-phase transition: its unpack step's barrier orders it)
+  bool no_async = false;  // must stay on the main stream (a two-phase transition's steps)
   int join = -1;       // async: main-stream step that first needs the result (-1: end of run)
   int async_id = -1;   // index into the program's fork/done events
   // Enqueue this step for local rank `li` on stream `s`; returns the launches issued.
@@ -83,7 +87,12 @@ struct Step {
   // Peer-memory transitions (p2p, not NCCL): one pull per single-axis transition; several
   // independent transitions of one axis merged into this step run as one grouped launch.
   std::vector<std::function<PullArgs(int li)>> pulls;
+  // Fine-grained layouts (LaunchFine): launch with the step's fused barrier and grid cap.
+  std::function<int(int li, cudaStream_t s, const PeerSync& sync, int max_blocks)> fine;
 };
+
+// Output specs (one per mesh axis) of op i's local computation from its demanded input specs.
+Specs NaturalSpecsOf(const rh_op* ops, int n_ops, int i, const std::vector<int>& mesh);
 
 }  // namespace rh
 
@@ -111,6 +120,7 @@ struct rh_program {
   size_t arena_bytes = 0;
   size_t pool_bytes = 0;  // liveness-planned part of the arena (recycled intermediates)
   size_t flags_off = 0, counter_off = 0;
+  size_t err_off = 0;  // bounded cross-GPU waits: first timed-out (me, member) pair (PeerSync)
   size_t sync_off = 0, epoch_off = 0;  // fused-barrier flag rows [slots][world] + run counter
   int n_sync_slots = 0;
   std::vector<char*> base;       // per local rank

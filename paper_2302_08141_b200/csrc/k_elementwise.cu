@@ -396,6 +396,8 @@ __device__ __forceinline__ void EwRunVec(const EwArgs& a, int64_t i, const uint1
               acc[e] = AddBf16x2(keep[e], t ^ 0x80008000u);
             }
           }
+        } else {
+          __trap();  // emitted only for bf16 rematerializing programs (EmitEwChain): misrouted
         }
         break;
       }
@@ -770,7 +772,7 @@ int Blocks(int64_t n, int per_thread = 1) {
     return v && *v ? atoi(v) : 16;
   }();
   return static_cast<int>(
-      std::max<int64_t>(1, std::min<int64_t>((n / per_thread + 255) / 256, 148 * per_sm)));
+      std::max<int64_t>(1, std::min<int64_t>((n / per_thread + 255) / 256, SmCount() * per_sm)));
 }
 
 }  // namespace
@@ -812,7 +814,7 @@ void LaunchEwProg(const EwArgs& a, int dtype, cudaStream_t s) {
       attr[dev] = true;
     }
     // persistent-ish grid: each block stages the 28 KB ladder table once
-    const int blocks = std::min(Blocks(a.n, 8), 148 * 4);
+    const int blocks = std::min(Blocks(a.n, 8), SmCount() * 4);
     if (vsmem) LaunchPdl(EwLadderKernel<true>, blocks, 256, kLadSmem + vsmem, s, a);
     else LaunchPdl(EwLadderKernel<false>, blocks, 256, kLadSmem, s, a);
   } else if (dtype == RH_BF16 && vsmem) {
@@ -822,7 +824,7 @@ void LaunchEwProg(const EwArgs& a, int dtype, cudaStream_t s) {
       attr[dev] = true;
     }
     // the 28 KB rematerialization table is staged per block: persistent-ish grid
-    LaunchPdl(EwProgKernel<true, true>, std::min(Blocks(a.n, 8), 148 * 2), 256, vsmem, s, a);
+    LaunchPdl(EwProgKernel<true, true>, std::min(Blocks(a.n, 8), SmCount() * 2), 256, vsmem, s, a);
   } else if (dtype == RH_BF16) {
     LaunchPdl(EwProgKernel<true, false>, Blocks(a.n, 8), 256, 0, s, a);
   } else {
@@ -905,7 +907,7 @@ bool LaunchConcat(const ConcatArgs& a, cudaStream_t s) {
     most = std::max(most, a.outer * a.row16[p]);
   }
   if (reinterpret_cast<uintptr_t>(a.out) % 16 || most >= (int64_t{1} << 32)) return false;
-  const int bx = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((most + 1023) / 1024, 148 * 8 / a.n + 1)));
+  const int bx = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((most + 1023) / 1024, SmCount() * 8 / a.n + 1)));
   LaunchPdl(ConcatKernel, dim3(bx, a.n), 256, 0, s, a);
   RH_CUDA(cudaGetLastError());
   return true;

@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(256) SplitReduceKernel(T* __restrict__ C, cons
 
 int SplitsFor(const GemmArgs& g) {
   const int64_t tiles = ((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN);
-  if (tiles >= 148 || g.k < 128) return 1;
+  if (tiles >= SmCount() || g.k < 128) return 1;
   int64_t splits = (296 + tiles - 1) / tiles;
   splits = std::min<int64_t>(splits, std::min<int64_t>(g.k / 64, 32));
   return static_cast<int>(std::max<int64_t>(splits, 1));
@@ -190,7 +190,7 @@ int Dispatch(const GemmArgs& g, cudaStream_t s) {
   else LaunchPdl(GemmSimtKernel<T, true, true>, grid, 256, 0, s, c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws);
   if (!ws) return 1;
   const int64_t n = g.m * g.n;
-  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)));
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, SmCount() * 8)));
   LaunchPdl(SplitReduceKernel<T>, blocks, 256, 0, s, c, ws, n, z, g.epi);
   return 2;
 }
@@ -213,7 +213,7 @@ int LaunchGemmSimt(const GemmArgs& g, cudaStream_t s) {
   if (g.m == 0 || g.n == 0) return 0;
   if (g.k == 0) {  // empty contraction: C = 0 (a kernel, not a memset node: PDL edges link kernels)
     const int64_t words = g.m * g.n * ElemBytes(g.dtype) / 4;
-    LaunchPdl(ZeroWordsKernel, static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((words + 255) / 256, 148 * 8))),
+    LaunchPdl(ZeroWordsKernel, static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((words + 255) / 256, SmCount() * 8))),
               256, 0, s, static_cast<uint32_t*>(g.c), words);
     return 1;
   }

@@ -1027,15 +1027,7 @@ const Maps& GetMaps(const GemmArgs& g, int bn, int kb = BK) {
   return cache.emplace(key, m).first->second;
 }
 
-int NumSms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return n;
-}
+int NumSms() { return SmCount(); }
 
 // Experiment knobs (profiles/gemm_shapes.py A/B runs): RH_GEMM_BN forces the tile width,
 // RH_GEMM_MAX_SPLIT caps split-K.  Unset in production.
@@ -1068,7 +1060,7 @@ int KSplit(const GemmArgs& g, int bn) {
   if (tiles >= 96) return 1;
   int best = 1;
   for (int ks = 2; ks <= max_split; ks *= 2) {
-    if (kb % ks || kb / ks < 8 || tiles * (ks / 2) > 148) break;
+    if (kb % ks || kb / ks < 8 || tiles * (ks / 2) > SmCount()) break;
     best = ks;
   }
   return best;
@@ -1086,7 +1078,7 @@ int KSplitPair(const GemmArgs& g, int bn) {
   if (ctas >= 96) return 1;
   int best = 1;
   for (int ks = 2; ks <= max_split; ks *= 2) {
-    if (kb % ks || kb / ks < 8 || ctas * (ks / 2) > 148) break;
+    if (kb % ks || kb / ks < 8 || ctas * (ks / 2) > SmCount()) break;
     best = ks;
   }
   return best;
@@ -1123,7 +1115,7 @@ void LaunchKB(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullptr
   RH_CUDA(cudaGetLastError());
   if (ws) {
     const int64_t n4 = g.m * g.n / 4;
-    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 148 * 8)));
+    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, SmCount() * 8)));
     LaunchPdl(SplitReduceBf16, blocks, 256, 0, s, static_cast<__nv_bfloat16*>(g.c), reinterpret_cast<const float4*>(ws),
                                            n4, ks, g.epi);
     RH_CUDA(cudaGetLastError());
@@ -1175,7 +1167,7 @@ void LaunchPair(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullp
                              kG ? gl->dev : GroupDev{}));
   if (ws) {
     const int64_t n4 = g.m * g.n / 4;
-    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 148 * 8)));
+    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, SmCount() * 8)));
     LaunchPdl(SplitReduceBf16, blocks, 256, 0, s, static_cast<__nv_bfloat16*>(g.c), reinterpret_cast<const float4*>(ws),
               n4, ks, g.epi);
     RH_CUDA(cudaGetLastError());
@@ -1204,7 +1196,7 @@ void LaunchTf32x3(const GemmArgs& g, cudaStream_t s) {
   float* b_hi = a_lo + na;
   float* b_lo = b_hi + nb;
   const int threads = 256;
-  auto blocks = [](int64_t n4) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, 148 * 8))); };
+  auto blocks = [](int64_t n4) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, SmCount() * 8))); };
   if (!g.ta) {
     LaunchPdl(SplitTf32Kernel, blocks(na / 4), threads, 0, s, static_cast<const float4*>(g.a), reinterpret_cast<float4*>(a_hi),
                                                        reinterpret_cast<float4*>(a_lo), na / 4);
@@ -1267,7 +1259,7 @@ Sched ScheduleOf(const GemmArgs& g) {
   if (UsePair(g) && g.n % 256 == 0) {
     static const int force = EnvInt("RH_GEMM_BN", 0);
     const int64_t ctas = (g.m / BM) * (g.n / 256);
-    if (force == 256 || ctas >= 148) return {true, 256, 1};
+    if (force == 256 || ctas >= SmCount()) return {true, 256, 1};
     if (force == 128 && EnvInt("RH_GEMM_PAIR128", 0)) return {true, 128, 1};
     if (ctas < 96 && g.k / BK >= 128) return {true, 256, KSplitPair(g, 256)};
   }
@@ -1327,7 +1319,7 @@ Sched GroupScheduleOf(const GemmArgs& g, int n_prob, bool shared_a) {
   static const int force = EnvInt("RH_GEMM_BN", 0);
   if (UsePair(v) && ok(256, true)) {
     const int64_t ctas = (v.m / BM) * (v.n / 256);
-    if (ctas >= 148 || force == 256) return {true, 256, 1};
+    if (ctas >= SmCount() || force == 256) return {true, 256, 1};
   }
   if (force != 128 && (v.m / BM) * (v.n / 256) >= 96 && ok(256, false)) return {false, 256, 1};
   if (ok(128, false)) return {false, 128, 1};

@@ -10,6 +10,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <map>
 #include <mutex>
@@ -94,6 +95,29 @@ __device__ __forceinline__ uint32_t LdAcquireSysU32(const uint32_t* p) {
   return v;
 }
 
+__device__ __forceinline__ uint64_t GlobalTimerNs() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Spin until *f reaches `want` (wrapping compare), at most timeout_ns: on timeout record the
+// (me, member) pair in *err (first one wins) and give up — the run then fails loudly on the
+// host (RH_ERR_TIMEOUT) instead of hanging the GPU.
+__device__ __forceinline__ void WaitFlag(const uint32_t* f, uint32_t want, uint32_t* err, uint64_t timeout_ns,
+                                         int me, int member, bool sleep) {
+  if (static_cast<int32_t>(LdAcquireSysU32(f) - want) >= 0) return;
+  const uint64_t t0 = GlobalTimerNs();
+  uint32_t n = 0;
+  while (static_cast<int32_t>(LdAcquireSysU32(f) - want) < 0) {
+    if (sleep) __nanosleep(64);
+    if ((++n & 1023) == 0 && timeout_ns && GlobalTimerNs() - t0 > timeout_ns) {
+      if (err) atomicCAS(err, 0u, SyncErrorCode(me, member));
+      return;
+    }
+  }
+}
+
 // Block 0 publishes the arrival (it is dispatched first; every other CTA only polls its own,
 // local flag row, so no CTA waits on a CTA of its own grid that might not be resident).
 __device__ __forceinline__ void ArriveAndWait(const PeerSync& s) {
@@ -105,9 +129,7 @@ __device__ __forceinline__ void ArriveAndWait(const PeerSync& s) {
       __threadfence_system();  // this rank's producer writes precede the signal
       StRelaxedSys(s.peer_slot[t] + s.me, e);
     }
-    const uint32_t* f = s.my_slot + s.members[t];
-    while (static_cast<int32_t>(LdAcquireSysU32(f) - e) < 0) {
-    }
+    WaitFlag(s.my_slot + s.members[t], e, s.err, s.timeout_ns, s.me, s.members[t], false);
   }
   __syncthreads();
 }
@@ -340,7 +362,7 @@ bool TryLaunchStaged(const PullArgs& a, cudaStream_t s) {
   sd.chunks = static_cast<uint32_t>(a.n_dst / L);
   sd.cpb = static_cast<uint32_t>(std::max<int64_t>(1, 4096 / L));
   const int64_t groups = (sd.chunks + sd.cpb - 1) / sd.cpb;
-  const int blocks = static_cast<int>(std::min<int64_t>(groups, a.max_blocks > 0 ? a.max_blocks : 148 * 6));
+  const int blocks = static_cast<int>(std::min<int64_t>(groups, a.max_blocks > 0 ? a.max_blocks : SmCount() * 6));
   const size_t smem = static_cast<size_t>(sd.cpb) * L * eb;
   if (eb == 2) PullStagedKernel<uint16_t><<<blocks, 256, smem, s>>>(sd);
   else PullStagedKernel<uint32_t><<<blocks, 256, smem, s>>>(sd);
@@ -360,7 +382,7 @@ int Gcd(int64_t a, int64_t b) {
 template <int VB>
 void LaunchPullVB(const PullArgs& a, PullDev& dv, cudaStream_t s) {
   const uint32_t n = dv.n;
-  const int cap = a.max_blocks > 0 ? a.max_blocks : 148 * 6;
+  const int cap = a.max_blocks > 0 ? a.max_blocks : SmCount() * 6;
   int blocks = static_cast<int>(std::min<int64_t>((n + 1023) / 1024, cap));
   blocks = std::max(blocks, 1);
   if (a.from.kind == RH_PARTIAL) {
@@ -377,6 +399,199 @@ void LaunchPullVB(const PullArgs& a, PullDev& dv, cudaStream_t s) {
   }
   RH_CUDA(cudaGetLastError());
 }
+
+// ------------------------ fine-grained layouts: unit (de)interleave ------------------------
+// Block-cyclic layouts whose runs are shorter than a sector (Shard(1,1) of a [N,4096] tensor:
+// 2-byte runs) make a plain pull read or write 2..16-byte pieces across NVLink.  Instead:
+//   De-interleave (push, run by source rank c): a thread reads D*W contiguous bytes of its local
+//     buffer (W = max(16, UB) bytes per member; UB = the pattern's unit), unit m of them belongs
+//     to member m % D at position m / D, and writes W contiguous bytes to each member's target
+//     (the member's destination directly, or its staging stream for this source).
+//   Interleave (pull, run by destination rank c): a thread reads W contiguous bytes from each
+//     member's stream, unit m of its output comes from member m % D, and writes D*W contiguous
+//     bytes.
+// The unit permutation runs in registers (compile-time D and UB: register moves / PRMT), every
+// global access is a 16-byte vector and every warp access 512 contiguous bytes per stream.
+// Offsets (elements) of super-vector s on the strided side: lin ? s*Wel
+//   : f0 / D with i0 = s*D*Wel, f0 = ((i0 / R)*D + c)*R + i0 % R   (R: that side's run length).
+struct FineDev {
+  const char* in[kMaxGroup];
+  char* out[kMaxGroup];
+  uint32_t n_sv;   // super-vectors
+  uint32_t sv;     // elements per super-vector (D * Wel)
+  FastDiv run;     // R (elements), non-linear offsets only
+  uint32_t c;      // coordinate of the running rank
+  uint32_t eb;     // element bytes
+  int lin;
+  int only;        // de-interleave: write member `only` only (local slice), -1: every member
+  PeerSync sync;
+};
+
+__device__ __forceinline__ uint64_t FineOffset(const FineDev& a, uint32_t s, uint32_t d) {
+  const uint32_t wel = a.sv / d;
+  if (a.lin) return static_cast<uint64_t>(s) * wel;
+  const uint64_t i0 = static_cast<uint64_t>(s) * a.sv;
+  const uint32_t q = Div(a.run, static_cast<uint32_t>(i0));  // i0 < 2^32 (host-checked)
+  const uint64_t f0 = (static_cast<uint64_t>(q) * d + a.c) * a.run.d + (i0 - static_cast<uint64_t>(q) * a.run.d);
+  return f0 / d;
+}
+
+// 16-bit unit x of a word array (compile-time x after unrolling)
+template <int N>
+__device__ __forceinline__ uint32_t Half2(const uint32_t (&w)[N], int lo, int hi) {
+  // halfword lo -> bits 0..15, halfword hi -> bits 16..31
+  const uint32_t sel = ((lo & 1) ? 0x32u : 0x10u) | (((hi & 1) ? 0x76u : 0x54u) << 8);
+  return __byte_perm(w[lo >> 1], w[hi >> 1], sel);
+}
+
+template <int D, int UB>
+__global__ void __launch_bounds__(256) FineDeinterleaveKernel(FineDev a) {
+  constexpr int W = UB < 16 ? 16 : UB;  // bytes per member per super-vector
+  constexpr int NV = W / 16;            // uint4 per member
+  ArriveAndWait(a.sync);
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < a.n_sv; s += gridDim.x * blockDim.x) {
+    const uint4* src = reinterpret_cast<const uint4*>(a.in[0]) + static_cast<size_t>(s) * D * NV;
+    uint32_t w[4 * D * NV];
+#pragma unroll
+    for (int j = 0; j < D * NV; ++j) {
+      const uint4 v = src[j];
+      w[4 * j] = v.x;
+      w[4 * j + 1] = v.y;
+      w[4 * j + 2] = v.z;
+      w[4 * j + 3] = v.w;
+    }
+    const uint64_t off = FineOffset(a, s, D) * a.eb;
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      if (a.only >= 0 && a.only != r) continue;
+      uint32_t o[4 * NV];
+      if constexpr (UB >= 16) {  // unit = NV uint4, unit m -> member m
+#pragma unroll
+        for (int q = 0; q < 4 * NV; ++q) o[q] = w[r * 4 * NV + q];
+      } else if constexpr (UB == 8) {  // 2 units of 2 words per member
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          o[2 * e] = w[2 * (e * D + r)];
+          o[2 * e + 1] = w[2 * (e * D + r) + 1];
+        }
+      } else if constexpr (UB == 4) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[e] = w[e * D + r];
+      } else {  // UB == 2: 8 halfwords per member
+#pragma unroll
+        for (int q = 0; q < 4; ++q) o[q] = Half2(w, (2 * q) * D + r, (2 * q + 1) * D + r);
+      }
+      uint4* dst = reinterpret_cast<uint4*>(a.out[r] + off);
+#pragma unroll
+      for (int q = 0; q < NV; ++q) dst[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+    }
+  }
+}
+
+template <int D, int UB>
+__global__ void __launch_bounds__(256) FineInterleaveKernel(FineDev a) {
+  constexpr int W = UB < 16 ? 16 : UB;
+  constexpr int NV = W / 16;
+  ArriveAndWait(a.sync);
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < a.n_sv; s += gridDim.x * blockDim.x) {
+    const uint64_t off = FineOffset(a, s, D) * a.eb;
+    uint32_t w[4 * D * NV];  // member-major: member r's W bytes at w[r*4*NV ..]
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      const uint4* src = reinterpret_cast<const uint4*>(a.in[r] + off);
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        const uint4 v = src[q];
+        w[r * 4 * NV + 4 * q] = v.x;
+        w[r * 4 * NV + 4 * q + 1] = v.y;
+        w[r * 4 * NV + 4 * q + 2] = v.z;
+        w[r * 4 * NV + 4 * q + 3] = v.w;
+      }
+    }
+    uint32_t o[4 * D * NV];
+    if constexpr (UB >= 16) {  // unit m <- member m
+#pragma unroll
+      for (int q = 0; q < 4 * D * NV; ++q) o[q] = w[q];
+    } else if constexpr (UB == 8) {  // output unit m (2 words) <- member m % D, its unit m / D
+#pragma unroll
+      for (int m = 0; m < 2 * D; ++m) {
+        o[2 * m] = w[(m % D) * 4 + 2 * (m / D)];
+        o[2 * m + 1] = w[(m % D) * 4 + 2 * (m / D) + 1];
+      }
+    } else if constexpr (UB == 4) {
+#pragma unroll
+      for (int m = 0; m < 4 * D; ++m) o[m] = w[(m % D) * 4 + m / D];
+    } else {  // UB == 2: output halfword x <- member x % D, its halfword x / D
+#pragma unroll
+      for (int q = 0; q < 4 * D; ++q) {
+        const int x0 = 2 * q, x1 = 2 * q + 1;
+        o[q] = Half2(w, (x0 % D) * 8 + x0 / D, (x1 % D) * 8 + x1 / D);
+      }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(a.out[0]) + static_cast<size_t>(s) * D * NV;
+#pragma unroll
+    for (int j = 0; j < D * NV; ++j) dst[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+  }
+}
+
+template <int D>
+bool LaunchFineD(const FineArgs& a, const FineDev& dv, int blocks, cudaStream_t s) {
+#define RH_FINE(UBV)                                                                      \
+  case UBV:                                                                               \
+    if (a.kind == 0) FineDeinterleaveKernel<D, UBV><<<blocks, 256, 0, s>>>(dv);          \
+    else FineInterleaveKernel<D, UBV><<<blocks, 256, 0, s>>>(dv);                        \
+    return true;
+  switch (a.unit_bytes) {
+    RH_FINE(2)
+    RH_FINE(4)
+    RH_FINE(8)
+    RH_FINE(16)
+    RH_FINE(32)
+    default:
+      return false;
+  }
+#undef RH_FINE
+}
+
+}  // namespace
+
+bool FineSupported(int d, int unit_bytes, int eb, int64_t n_contig) {
+  if (d != 2 && d != 4 && d != 8) return false;
+  if (unit_bytes != 2 && unit_bytes != 4 && unit_bytes != 8 && unit_bytes != 16 && unit_bytes != 32) return false;
+  if (unit_bytes < eb) return false;
+  const int64_t sv = static_cast<int64_t>(d) * std::max(16, unit_bytes) / eb;
+  return n_contig > 0 && n_contig % sv == 0 && n_contig < (int64_t{1} << 32);
+}
+
+int LaunchFine(const FineArgs& a, cudaStream_t s) {
+  if (!FineSupported(a.d, a.unit_bytes, a.eb, a.n)) Fail("fine-grained reshard: unsupported pattern");
+  FineDev dv{};
+  for (int k = 0; k < kMaxGroup; ++k) {
+    dv.in[k] = static_cast<const char*>(a.in[k]);
+    dv.out[k] = static_cast<char*>(a.out[k]);
+  }
+  dv.sv = static_cast<uint32_t>(static_cast<int64_t>(a.d) * std::max(16, a.unit_bytes) / a.eb);
+  dv.n_sv = static_cast<uint32_t>(a.n / dv.sv);
+  dv.run = MakeFastDiv(static_cast<uint32_t>(a.lin ? 1 : a.run));
+  dv.c = static_cast<uint32_t>(a.c);
+  dv.eb = static_cast<uint32_t>(a.eb);
+  dv.lin = a.lin;
+  dv.only = a.only;
+  dv.sync = a.sync;
+  const int cap = a.max_blocks > 0 ? a.max_blocks : SmCount() * 6;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((dv.n_sv + 255) / 256, cap)));
+  bool ok = false;
+  switch (a.d) {
+    case 2: ok = LaunchFineD<2>(a, dv, blocks, s); break;
+    case 4: ok = LaunchFineD<4>(a, dv, blocks, s); break;
+    default: ok = LaunchFineD<8>(a, dv, blocks, s); break;
+  }
+  if (!ok) Fail("fine-grained reshard: unsupported unit");
+  RH_CUDA(cudaGetLastError());
+  return 1;
+}
+
+namespace {
 
 // Vector width of a plain pull: the largest power-of-two unit (<= 16 B) that divides every
 // contiguous run and every buffer alignment.
@@ -472,7 +687,7 @@ bool PreparePullMulti(const PullArgs* a, int n, int max_blocks, void* table) {
     seg[k] = MakePullDev(a[k], vb);
     units += seg[k].n;
   }
-  const int cap = max_blocks > 0 ? max_blocks : 148 * 6;
+  const int cap = max_blocks > 0 ? max_blocks : SmCount() * 6;
   const double per_blk = a[0].from.kind == RH_PARTIAL ? 256.0 : 1024.0;
   const double scale = std::min(1.0, cap / std::max(1.0, units / per_blk));
   uint32_t b0 = 0;
@@ -586,13 +801,12 @@ __global__ void BarrierKernel(BarrierArgs b) {
   if (t < b.d) {
     __threadfence_system();
     StReleaseSys(b.peer_flags[t] + b.me, seq);
-    const uint32_t* f = b.my_flags + b.members[t];
-    while (static_cast<int32_t>(LdAcquireSys(f) - seq) < 0) __nanosleep(64);
+    WaitFlag(b.my_flags + b.members[t], seq, b.err, b.timeout_ns, b.me, b.members[t], true);
   }
   __syncthreads();
 }
 
-int Blocks(int64_t n) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16))); }
+int Blocks(int64_t n) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, SmCount() * 16))); }
 
 }  // namespace
 
@@ -619,6 +833,15 @@ void LaunchSynthetic(void* dst, const ComposedMap& m, int64_t n, uint64_t seed, 
     SyntheticKernel<<<Blocks(n), 256, 0, s>>>(static_cast<float*>(dst), m, n, seed, op_index, scale);
   }
   RH_CUDA(cudaGetLastError());
+}
+
+uint64_t SyncTimeoutNs() {
+  static const uint64_t ns = [] {
+    const char* e = std::getenv("RH_SYNC_TIMEOUT_MS");
+    const double ms = e && *e ? std::atof(e) : 20000.0;
+    return static_cast<uint64_t>(std::max(0.0, ms) * 1e6);
+  }();
+  return ns;
 }
 
 void LaunchBarrier(const BarrierArgs& b, cudaStream_t s) {

@@ -48,7 +48,17 @@ struct PeerSync {
   int members[kMaxGroup];
   int d;                           // 0: no fused barrier
   int me;
+  // Bounded wait: a peer that has not arrived within timeout_ns (globaltimer) records
+  // SyncErrorCode(me, member) in *err and the kernel proceeds; the host turns it into
+  // RH_ERR_TIMEOUT after the run instead of hanging the GPU.
+  uint32_t* err;
+  uint64_t timeout_ns;
 };
+// Host: RH_SYNC_TIMEOUT_MS (default 20000) in ns; error word encoding / decoding.
+uint64_t SyncTimeoutNs();
+__host__ __device__ inline uint32_t SyncErrorCode(int me, int member) {
+  return 0x80000000u | (static_cast<uint32_t>(me & 0xff) << 8) | static_cast<uint32_t>(member & 0xff);
+}
 
 struct PullArgs {
   void* dst;
@@ -66,6 +76,29 @@ struct PullArgs {
 void LaunchEpochTick(uint32_t* epoch, cudaStream_t s);
 // Returns the number of kernel launches (0 or 1).
 int LaunchPull(const PullArgs& a, cudaStream_t s);
+// Fine-grained block-cyclic layouts (runs shorter than a sector): register-permute kernels that
+// keep every global access a 16-byte vector (k_reshard.cu, FineDeinterleaveKernel /
+// FineInterleaveKernel).  kind 0 = de-interleave (push: the running rank c splits n contiguous
+// local elements into d targets, unit m -> member m % d); kind 1 = interleave (pull: d streams
+// into n contiguous elements).  The strided side's element offset of super-vector s is s * n/(d*
+// n_sv) when `lin`, else f0/d with i0 = s*sv, f0 = ((i0/run)*d + c)*run + i0%run.
+struct FineArgs {
+  int kind;
+  int d;
+  int unit_bytes;  // 2, 4, 8, 16 or 32
+  int eb;
+  const void* in[kMaxGroup];
+  void* out[kMaxGroup];
+  int64_t n;       // elements on the contiguous side
+  int lin;
+  int64_t run;
+  int c;
+  int only = -1;   // de-interleave: write only member `only` (a local slice)
+  PeerSync sync;
+  int max_blocks = 0;
+};
+bool FineSupported(int d, int unit_bytes, int eb, int64_t n_contig);
+int LaunchFine(const FineArgs& a, cudaStream_t s);
 // Grouped transitions: n independent pulls of one mesh axis as ONE launch behind ONE fused
 // barrier (`sync` of LaunchPullMulti; the PullArgs' own sync is ignored).  PreparePullMulti
 // writes the segment table (PullMultiTableBytes) once and returns false when the pulls cannot
@@ -230,6 +263,8 @@ struct BarrierArgs {
   int members[kMaxGroup];           // global ranks of the group
   int d;
   int me;                           // my global rank
+  uint32_t* err;                    // bounded wait (PeerSync)
+  uint64_t timeout_ns;
 };
 void LaunchBarrier(const BarrierArgs& b, cudaStream_t s);
 

@@ -5,6 +5,7 @@ A lowered program is the reference TensorProgram (proj/include/parashard/ir.h:97
 op and mesh axis, the OpStrategy the planner chose (proj/include/parashard/sharding.h:99-111).
 """
 import ctypes
+import gzip
 import json
 import math
 import os
@@ -12,8 +13,11 @@ import os
 from .abi import (OP_KINDS, RH_BF16, RH_F32, RH_MAX_AXES, RH_MAX_RANK, UNARY_FNS, AxisSpec, RhOp,
                   RhSpec, composed_local_shape)
 
-PLANS_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests",
-                         "golden", "plans")
+# Lowered-program library searched by LoweredProgram.load(name): RH_PLANS_DIR, else the fixtures
+# the reference-side tool wrote for the BASELINE configs (tests/golden/plans).  A caller with its
+# own plan passes a path instead of a name.
+PLANS_DIR = os.environ.get("RH_PLANS_DIR") or os.path.join(
+    os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden", "plans")
 
 
 class LoweredOp:
@@ -54,10 +58,14 @@ class LoweredProgram:
 
     @staticmethod
     def load(path_or_name):
+        """A plan file (.json or .json.gz) or the name of one in PLANS_DIR."""
         path = path_or_name
         if not os.path.exists(path):
             path = os.path.join(PLANS_DIR, path_or_name + ".json")
-        with open(path) as f:
+            if not os.path.exists(path) and os.path.exists(path + ".gz"):
+                path += ".gz"
+        opener = gzip.open if path.endswith(".gz") else open
+        with opener(path, "rt") as f:
             return LoweredProgram(json.load(f))
 
     @property

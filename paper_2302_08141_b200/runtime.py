@@ -20,6 +20,7 @@ EXPORTS = [
     "rh_program_write_full", "rh_program_run", "rh_program_step_host", "rh_program_run_host", "rh_program_read_local",
     "rh_program_read_full", "rh_program_read_input_full", "rh_program_local_bytes", "rh_program_memory", "rh_program_num_steps",
     "rh_program_step_info", "rh_program_profile", "rh_program_launch_count", "rh_reshard",
+    "rh_op_natural_specs",
 ]
 
 _lib = None
@@ -50,6 +51,7 @@ def lib():
     L.rh_mesh_destroy.argtypes = [vp]
     L.rh_mesh_destroy.restype = None
     L.rh_program_load.argtypes = [vp, P(RhOp), i, P(i), i, u32, P(vp)]
+    L.rh_op_natural_specs.argtypes = [P(RhOp), i, i, i, P(i), P(RhSpec)]
     L.rh_program_destroy.argtypes = [vp]
     L.rh_program_destroy.restype = None
     L.rh_program_init_synthetic.argtypes = [vp, u64]
@@ -81,6 +83,18 @@ def unique_id():
     buf = (ctypes.c_uint8 * RH_UID_BYTES)()
     check(lib().rh_get_unique_id(buf))
     return bytes(buf)
+
+
+def natural_specs(prog: LoweredProgram, op: int):
+    """rh_op_natural_specs: the executor's own local-op rule (host only): the per-axis output spec
+    op `op` computes locally from the input specs its strategy demands."""
+    ops, _ = prog.to_c()
+    n = len(prog.mesh)
+    dims = (ctypes.c_int * n)(*prog.mesh)
+    out = (RhSpec * n)()
+    check(lib().rh_op_natural_specs(ops, len(prog.ops), op, n, dims, out))
+    from .abi import AxisSpec
+    return [AxisSpec.from_c(out[a]) for a in range(n)]
 
 
 class Runtime:

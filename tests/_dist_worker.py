@@ -76,6 +76,19 @@ def check(rt, name, flags, dtype=None):
             ge.close()
             mesh_e.close()
             rt_e.close()
+            if rt.first_rank == 0 and not (flags & RH_FLAG_TRANSPORT_NCCL):
+                # ... and that result against the bf16 oracle of the same partitioned program
+                # (rule of test_gpu_parity.test_gpt_block_bf16), on rank 0 with every host core
+                ref = {}
+                for key_, fl in (("f64", pyoracle.OracleProgram.GEMM_F64), ("f32", 0)):
+                    oo = pyoracle.OracleProgram(prog, flags=fl)
+                    oo.init_synthetic(21)
+                    oo.run_partitioned(os.cpu_count() or 1)
+                    ref[key_] = conv(oo.read_full(prog.outputs[0], partitioned=True))
+                tol_o = max(2e-2, 2.0 * normwise(ref["f32"], ref["f64"]))
+                e = normwise(conv(gp.read_full(prog.outputs[0])), ref["f64"])
+                res["oracle_err"] = e
+                res["ok"] &= e <= tol_o
         else:
             for out in prog.outputs:
                 e = normwise(conv(gp.read_full(out)), conv(o.read_full(out, partitioned=False)))

@@ -15,6 +15,7 @@ dtype side channel).
     python tests/golden/make_fwd_bwd.py gpt_like:2:256:128 --devices 1,2,4 [--name c5_small]
 """
 import argparse
+import gzip
 import json
 import os
 import subprocess
@@ -167,6 +168,15 @@ def main():
         j = json.load(open(out))
         print(f"{name}_d{d}: ops={len(j['ops'])} {[x['ilp_status'] for x in j['recovery']]} "
               f"{time.time() - t:.1f}s")
+        gzip_if_large(out)
+
+
+def gzip_if_large(path, limit=1 << 20):
+    """Plans over 1 MB are committed gzipped (LoweredProgram.load reads NAME.json.gz)."""
+    if os.path.getsize(path) > limit:
+        with open(path, "rb") as f, gzip.open(path + ".gz", "wb", compresslevel=9) as g:
+            g.write(f.read())
+        os.remove(path)
 
 
 if __name__ == "__main__":

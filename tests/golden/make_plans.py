@@ -10,6 +10,7 @@ Each fixture is "rhino-lowered/1" JSON: the program graph, the planner's output 
 mesh axis, the OpStrategy recovered by replaying the search (paper_2302_08141_b200/host/rh_lower.cpp).
 """
 import argparse
+import gzip
 import json
 import os
 import subprocess
@@ -100,6 +101,8 @@ def jobs():
             short = fam.split(":")[0]
             J.append((f"rand_{short}_{mesh.replace(',', 'x')}_s{seed}",
                       ["--fixture", fam, "--random-choice", str(seed), "--mesh", mesh]))
+    # C5's forward pass alone (24 layers, H 2048, 2048 tokens): the oracle-checked forward
+    J.append(("c5_big_gpt24_fwd_d1", ["--fixture", "gpt_like:24:2048:2048", "--devices", "1"]))
     heads = os.path.join(PROG, "c3_gpt_heads32.ir")
     for d in (1, 2, 4, 8):
         J.append((f"c3_gpt_heads32_d{d}", ["--text", heads, "--devices", str(d)]))
@@ -126,6 +129,10 @@ def main():
         rec = ",".join(f"{x['ilp_status']}/{'ok' if x['replay_matched'] else 'fallback'}"
                        for x in j["recovery"])
         print(f"{name:32s} mesh={j['mesh']} ops={len(j['ops'])} {rec} {time.time() - t:.1f}s")
+        if os.path.getsize(out) > (1 << 20):  # large plans are committed gzipped
+            with open(out, "rb") as f, gzip.open(out + ".gz", "wb", compresslevel=9) as g:
+                g.write(f.read())
+            os.remove(out)
 
 
 if __name__ == "__main__":

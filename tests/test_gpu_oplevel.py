@@ -45,9 +45,9 @@ def as_f64(a):
     return a.astype(np.float64)
 
 
-@pytest.mark.parametrize("name", ["c3_gpt_block_d1", "c3_gpt_block_d8", "c3_gpt_block_2x4",
-                                  "c5_gpt_small_d2", "c5_gpt_small_d4"])
-@pytest.mark.parametrize("dtype", [RH_BF16, RH_F32])
+@pytest.mark.parametrize("name,dtype", [(n, d) for n in ("c3_gpt_block_d1", "c3_gpt_block_d8", "c3_gpt_block_2x4",
+                                                        "c5_gpt_small_d2", "c5_gpt_small_d4")
+                                         for d in (RH_BF16, RH_F32)] + [("c3_gpt_heads32_d4", RH_BF16)])
 def test_gpt_block_op_level(oracle_lib, name, dtype):
     from paper_2302_08141_b200 import runtime as rx
     prog = LoweredProgram.load(name).with_dtype(dtype)

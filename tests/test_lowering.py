@@ -9,12 +9,14 @@ import pytest
 from paper_2302_08141_b200.abi import AxisSpec, composed_local_shape, spec_valid
 from paper_2302_08141_b200.program import PLANS_DIR, LoweredProgram
 
-PLANS = sorted(os.path.basename(p)[:-5] for p in glob.glob(os.path.join(PLANS_DIR, "*.json")))
+PLANS = sorted({os.path.basename(p).split(".json")[0]
+                for p in glob.glob(os.path.join(PLANS_DIR, "*.json")) + glob.glob(os.path.join(PLANS_DIR, "*.json.gz"))})
 
 
 def test_fixtures_present():
     for need in ["c1_mlp_d4", "c2_mlp_reshape_d4", "c2_mlp_pinned_d8", "c3_gpt_block_d8",
-                 "c3_gpt_block_2x4", "c3_gpt_heads32_d8"]:
+                 "c3_gpt_block_2x4", "c3_gpt_heads32_d1", "c3_gpt_heads32_d2", "c3_gpt_heads32_d4",
+                 "c3_gpt_heads32_d8", "c5_big_gpt24_d4"]:
         assert need in PLANS
 
 
