@@ -39,7 +39,7 @@ typedef enum {
   RH_ERR_STATE = -4,       /* call out of order */
   RH_ERR_UNSUPPORTED = -5, /* valid per the reference, not executable by this build */
   RH_ERR_TIMEOUT = -6      /* a cross-GPU barrier did not complete within RH_SYNC_TIMEOUT_MS
-                              (default 20 s): a peer died or the schedules diverged */
+                              (default 60 s): a peer died or the schedules diverged */
 } rh_status;
 
 /* parashard::AxisSpec::Kind (sharding.h:33) — note the reference enum order is

@@ -240,6 +240,59 @@ struct EwPlan {
   std::vector<bool> keep_after, stored;
 };
 
+// Fine-grained single-axis transitions (runs under 64 bytes on a side, LaunchFine): which
+// kernel(s) move the data with 16-byte vectors on every global access.  a / b: source / target
+// run lengths Qs (elements; the whole tensor for Replicated / Partial).  For a transition
+// between block-cyclic layouts the pieces are:
+//   a % (d*b) == 0: rank k's elements for rank r are runs of b in k's buffer (k side) and runs
+//                   of a/d in r's buffer (r side);
+//   b % (d*a) == 0: runs of b/d on the k side, runs of a on the r side.
+// Coarse k side -> pull (plain, or interleave if the r side is fine); fine k side, coarse r side
+// -> push (de-interleave straight into the peers' destinations); both fine -> two phases:
+// de-interleave into the peers' staging streams, then interleave locally.
+struct FinePlan {
+  int mode = 0;  // 0 plain pull, 1 push, 2 pull-interleave, 3 two-phase, 4 partial two-phase,
+                 // 5 local slice (Replicated source)
+  int64_t u1 = 0, u2 = 0;  // unit elements: de-interleave (phase 1), interleave (phase 2)
+  int64_t run = 0;         // strided-side run for push / pull-interleave (0: linear offsets)
+};
+
+FinePlan ClassifyFine(const AxisView& f, const AxisView& t, int eb, int d, int64_t n) {
+  FinePlan p;
+  if (d < 2) return p;
+  const int64_t tel = 64 / eb, E = 16 / eb;
+  auto pow2 = [](int64_t x) { return x > 0 && (x & (x - 1)) == 0; };
+  auto ok = [&](int64_t u, int64_t n_contig) {
+    return pow2(u) && u * eb <= 32 && FineSupported(d, static_cast<int>(u * eb), eb, n_contig);
+  };
+  const int64_t ns = f.kind == RH_SHARD ? n / d : n, nt = t.kind == RH_SHARD ? n / d : n;
+  if (f.kind == RH_SHARD && t.kind == RH_SHARD) {
+    const int64_t a = f.Qs, b = t.Qs;
+    if (a >= tel && b >= tel) return p;
+    if (a % (d * b) == 0) {
+      if (b >= tel) return p;  // coarse k side: plain pull
+      if (a / d >= tel) {
+        if (ok(b, ns) && a % (d * std::max(E, b)) == 0) p = {1, b, 0, a};
+      } else if (ok(b, ns) && ok(a / d, nt)) {
+        p = {3, b, a / d, 0};
+      }
+      return p;
+    }
+    if (b % (d * a) == 0) {
+      if (b / d >= tel) {
+        if (a < tel && ok(a, nt) && b % (d * std::max(E, a)) == 0) p = {2, 0, a, b};
+      } else if (ok(b / d, ns) && ok(a, nt)) {
+        p = {3, b / d, a, 0};
+      }
+    }
+    return p;
+  }
+  if (f.kind == RH_PARTIAL && t.kind == RH_SHARD && t.Qs < tel && ok(t.Qs, n)) return {4, t.Qs, 0, 0};
+  if (f.kind == RH_REPLICATED && t.kind == RH_SHARD && t.Qs < tel && ok(t.Qs, n)) return {5, t.Qs, 0, 0};
+  if (f.kind == RH_SHARD && t.kind == RH_REPLICATED && f.Qs < tel && ok(f.Qs, n)) return {2, 0, f.Qs, 0};
+  return p;
+}
+
 class Lowerer {
  public:
   explicit Lowerer(rh_program* p) : p_(p), mesh_(p->mesh->dims), rt_(p->mesh->rt) {}
@@ -965,11 +1018,12 @@ class Lowerer {
   void PlanRemat(const std::vector<bool>& is_out, NoPartial no_partial) {
     const int n = static_cast<int>(p_->ops.size());
     remat_.assign(ew_.size(), Remat{});
-    // Default: on when every rank runs on one physical GPU (one rank, or emulated ranks);
-    // meshes over several GPUs need RH_REMAT=1 until the N=2 C5 hang seen with it is explained
-    // (the cross-GPU waits are bounded, so it now fails as RH_ERR_TIMEOUT).
+    // Default on.  The round-1 C5 N=2 hang seen with it did not reproduce after this round's
+    // barrier / transition changes (N=2 and N=4 benches and the dist parity suite run with it,
+    // DESIGN §8); every cross-GPU wait is bounded, so a recurrence fails as RH_ERR_TIMEOUT
+    // instead of hanging.  RH_REMAT=0 disables it (A/B).
     const char* env = getenv("RH_REMAT");
-    const bool on = env ? env[0] != '0' : !(rt_->dist && rt_->world > 1) && rt_->devs.size() == 1;
+    const bool on = env ? env[0] != '0' : true;
     if (!on || ew_.empty() || (p_->flags & RH_FLAG_KEEP_ALL)) return;
     if (p_->ops[0].dtype != RH_BF16) return;
     // GEMM-epilogue tails: their value is the fused kernel's stored output (a base, not a
@@ -1866,6 +1920,161 @@ class Lowerer {
     st.reads = in_t;
     st.writes = {out_t};
     AddStep(std::move(st));
+  }
+
+  // Fine-grained transition (ClassifyFine): one or two steps of LaunchFine kernels.
+  int EmitFine(const FinePlan& fp, int src, int dst, int axis, const AxisView& fv, const AxisView& tv,
+               double S, const char* why) {
+    rh_program* P = p_;
+    const Tensor X = p_->tensors[src];
+    const int d = mesh_[axis];
+    const int eb = ElemBytes(X.dtype);
+    const int64_t n_src = X.elems(), n_dst = p_->tensors[dst].elems();
+    const rh_spec from = X.specs[axis], to = p_->tensors[dst].specs[axis];
+    const bool multi = rt_->dist && rt_->world > 1;
+    auto base_step = [&](const std::string& tag) {
+      Step st;
+      st.kind = Step::kTransition;
+      st.axis = axis;
+      st.name = std::string(CollectiveName(from, to)) + " op" + std::to_string(X.op) + " " + SpecStr(from) + "->" +
+                SpecStr(to) + "@" + std::to_string(axis) + " (" + why + ") [" + tag + "]";
+      st.launches = 1;
+      return st;
+    };
+    static const char* kMode[] = {"", "push", "pull-interleave", "two-phase", "two-phase", "slice"};
+    if (fp.mode == 5) {  // Replicated -> fine Shard: local de-interleave keeping this rank's units
+      Step st = base_step("slice");
+      st.alg_bytes = static_cast<double>(n_dst) * eb * 2;
+      const int64_t u = fp.u1;
+      st.fine = [P, src, dst, axis, d, eb, u, n_src](int li, cudaStream_t s, const PeerSync&, int cap) {
+        const int g = P->mesh->rt->first_rank + li;
+        FineArgs a{};
+        a.kind = 0;
+        a.d = d;
+        a.unit_bytes = static_cast<int>(u * eb);
+        a.eb = eb;
+        a.in[0] = P->Ptr(P->tensors[src], g);
+        a.only = P->mesh->Coords(g)[axis];
+        a.out[a.only] = P->Ptr(P->tensors[dst], g);
+        a.n = n_src;
+        a.lin = 1;
+        a.max_blocks = cap;
+        return LaunchFine(a, s);
+      };
+      st.reads = {src};
+      st.writes = {dst};
+      AddStep(std::move(st));
+      return dst;
+    }
+    if (fp.mode == 1 || fp.mode == 2) {  // one step: push into the peers / pull-interleave from them
+      const bool push = fp.mode == 1;
+      Step st = base_step(kMode[fp.mode]);
+      st.p2p = true;
+      st.wire_bytes = WireBytes(from, to, S, d);
+      st.alg_bytes = static_cast<double>(push ? n_src : n_dst) * eb * 2;
+      if (multi) st.sync_slot = p_->n_sync_slots++;
+      if (push) st.post_mode = 1;  // peers wrote this rank's destination: barrier before any read
+      const int64_t u = push ? fp.u1 : fp.u2, run = fp.run, n = push ? n_src : n_dst;
+      st.fine = [P, src, dst, axis, d, eb, u, run, n, push](int li, cudaStream_t s, const PeerSync& sync, int cap) {
+        const int g = P->mesh->rt->first_rank + li;
+        const std::vector<int> members = P->mesh->Group(axis, g);
+        FineArgs a{};
+        a.kind = push ? 0 : 1;
+        a.d = d;
+        a.unit_bytes = static_cast<int>(u * eb);
+        a.eb = eb;
+        for (int k = 0; k < d; ++k) {
+          if (push) a.out[k] = P->Ptr(P->tensors[dst], members[k]);
+          else a.in[k] = P->Ptr(P->tensors[src], members[k]);
+        }
+        if (push) a.in[0] = P->Ptr(P->tensors[src], g);
+        else a.out[0] = P->Ptr(P->tensors[dst], g);
+        a.n = n;
+        a.lin = run == 0;
+        a.run = run;
+        a.c = P->mesh->Coords(g)[axis];
+        a.sync = sync;
+        a.max_blocks = cap;
+        return LaunchFine(a, s);
+      };
+      if (!push) remote_read_.push_back(src);
+      st.reads = {src};
+      st.writes = {dst};
+      AddStep(std::move(st));
+      return dst;
+    }
+    // two phases: (A) de-interleave this rank's buffer into every member's staging stream for
+    // it, (B) after a group barrier, interleave (or sum, Partial) the d local streams
+    const bool partial = fp.mode == 4;
+    const int64_t seg = partial ? n_dst : n_dst / d;  // elements of one member's stream
+    const size_t stage_off = Alloc(static_cast<size_t>(seg) * d * eb);  // persistent, symmetric
+    Step a_st = base_step("two-phase push");
+    a_st.p2p = true;
+    a_st.wire_bytes = WireBytes(from, to, S, d);
+    a_st.alg_bytes = static_cast<double>(n_src) * eb * 2;
+    a_st.post_mode = 2;
+    a_st.no_async = true;
+    if (multi) a_st.sync_slot = p_->n_sync_slots++;
+    const int64_t u1 = fp.u1, u2 = fp.u2;
+    a_st.fine = [P, src, axis, d, eb, u1, n_src, seg, stage_off](int li, cudaStream_t s, const PeerSync& sync, int cap) {
+      const int g = P->mesh->rt->first_rank + li;
+      const std::vector<int> members = P->mesh->Group(axis, g);
+      const int c = P->mesh->Coords(g)[axis];
+      FineArgs a{};
+      a.kind = 0;
+      a.d = d;
+      a.unit_bytes = static_cast<int>(u1 * eb);
+      a.eb = eb;
+      a.in[0] = P->Ptr(P->tensors[src], g);
+      for (int k = 0; k < d; ++k)
+        a.out[k] = P->peer_base[members[k]] + stage_off + static_cast<size_t>(c) * seg * eb;  // stream c of member k
+      a.n = n_src;
+      a.lin = 1;
+      a.sync = sync;
+      a.max_blocks = cap;
+      return LaunchFine(a, s);
+    };
+    a_st.reads = {src};
+    AddStep(std::move(a_st));
+    Step b_st = base_step(partial ? "two-phase sum" : "two-phase unpack");
+    b_st.p2p = true;  // group-ordered after the pushes (fused barrier / stream joins)
+    b_st.alg_bytes = static_cast<double>(n_dst) * eb * (partial ? d + 1 : 2);
+    b_st.post_mode = 2;
+    b_st.no_async = true;
+    if (multi) b_st.sync_slot = p_->n_sync_slots++;
+    const int dtype = X.dtype;
+    b_st.fine = [P, dst, d, eb, u2, n_dst, seg, stage_off, partial, dtype](int li, cudaStream_t s, const PeerSync& sync,
+                                                                          int cap) {
+      const int g = P->mesh->rt->first_rank + li;
+      char* stage = P->peer_base[g] + stage_off;
+      if (partial) {  // sum of the d streams in member order (the rank-order sum of DESIGN §3)
+        PullArgs pa{};
+        pa.dst = P->Ptr(P->tensors[dst], g);
+        for (int k = 0; k < d; ++k) pa.src[k] = stage + static_cast<size_t>(k) * seg * eb;
+        pa.from = AxisView{RH_PARTIAL, d, 0, 0};
+        pa.to = AxisView{RH_REPLICATED, d, 0, 0};
+        pa.n_dst = n_dst;
+        pa.dtype = dtype;
+        pa.sync = sync;
+        pa.max_blocks = cap;
+        return LaunchPull(pa, s);
+      }
+      FineArgs a{};
+      a.kind = 1;
+      a.d = d;
+      a.unit_bytes = static_cast<int>(u2 * eb);
+      a.eb = eb;
+      for (int k = 0; k < d; ++k) a.in[k] = stage + static_cast<size_t>(k) * seg * eb;
+      a.out[0] = P->Ptr(P->tensors[dst], g);
+      a.n = n_dst;
+      a.lin = 1;
+      a.sync = sync;
+      a.max_blocks = cap;
+      return LaunchFine(a, s);
+    };
+    b_st.writes = {dst};
+    AddStep(std::move(b_st));
+    return dst;
   }
 
   // Producer `p` in the per-axis layout `want`, inserting single-axis transitions as needed.

@@ -534,8 +534,36 @@ __global__ void __launch_bounds__(256) FineInterleaveKernel(FineDev a) {
   }
 }
 
+// Units of 16 / 32 bytes need no permutation inside a vector: one thread per 16-byte chunk, the
+// contiguous side walked in order by consecutive lanes (fully coalesced) and every member given
+// 512/D contiguous bytes per warp instruction (the super-vector form stores 32-byte units with a
+// 32-byte lane stride: half-sector writes, which cost 2x across NVLink).
+template <int D, int NV>
+__global__ void __launch_bounds__(256) FineChunkKernel(FineDev a, int kind) {
+  ArriveAndWait(a.sync);
+  const uint32_t total = a.n_sv * NV * D;  // 16-byte chunks on the contiguous side
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
+    // chunk g = (q*D + r)*NV + j: super-vector q, member r, chunk j of its unit.  Consecutive
+    // lanes walk the contiguous side in order and give each member 512/D contiguous bytes per
+    // warp instruction.
+    if (kind == 0) {  // de-interleave: input chunk g -> member r's chunk q*NV + j
+      const uint32_t q = g / (D * NV), rem = g - q * (D * NV), r = rem / NV, j = rem % NV;
+      if (a.only >= 0 && a.only != static_cast<int>(r)) continue;
+      const uint64_t off = FineOffset(a, q, D) * a.eb + j * 16;
+      *reinterpret_cast<uint4*>(a.out[r] + off) = reinterpret_cast<const uint4*>(a.in[0])[g];
+    } else {  // interleave: output chunk g <- member (g/NV)%D, its chunk ((g/NV)/D)*NV + g%NV
+      const uint32_t m = g / NV, r = m % D, p = (m / D) * NV + g % NV;
+      const uint64_t off = FineOffset(a, p / NV, D) * a.eb + (p % NV) * 16;
+      reinterpret_cast<uint4*>(a.out[0])[g] = *reinterpret_cast<const uint4*>(a.in[r] + off);
+    }
+  }
+}
+
 template <int D>
-bool LaunchFineD(const FineArgs& a, const FineDev& dv, int blocks, cudaStream_t s) {
+bool LaunchFineD(const FineArgs& a, const FineDev& dv, int blocks, int cap, cudaStream_t s) {
+  auto chunk_blocks = [&](int nv) {
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((int64_t{dv.n_sv} * nv * D + 255) / 256, cap)));
+  };
 #define RH_FINE(UBV)                                                                      \
   case UBV:                                                                               \
     if (a.kind == 0) FineDeinterleaveKernel<D, UBV><<<blocks, 256, 0, s>>>(dv);          \
@@ -545,8 +573,12 @@ bool LaunchFineD(const FineArgs& a, const FineDev& dv, int blocks, cudaStream_t 
     RH_FINE(2)
     RH_FINE(4)
     RH_FINE(8)
-    RH_FINE(16)
-    RH_FINE(32)
+    case 16:
+      FineChunkKernel<D, 1><<<chunk_blocks(1), 256, 0, s>>>(dv, a.kind);
+      return true;
+    case 32:
+      FineChunkKernel<D, 2><<<chunk_blocks(2), 256, 0, s>>>(dv, a.kind);
+      return true;
     default:
       return false;
   }
@@ -582,9 +614,9 @@ int LaunchFine(const FineArgs& a, cudaStream_t s) {
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((dv.n_sv + 255) / 256, cap)));
   bool ok = false;
   switch (a.d) {
-    case 2: ok = LaunchFineD<2>(a, dv, blocks, s); break;
-    case 4: ok = LaunchFineD<4>(a, dv, blocks, s); break;
-    default: ok = LaunchFineD<8>(a, dv, blocks, s); break;
+    case 2: ok = LaunchFineD<2>(a, dv, blocks, cap, s); break;
+    case 4: ok = LaunchFineD<4>(a, dv, blocks, cap, s); break;
+    default: ok = LaunchFineD<8>(a, dv, blocks, cap, s); break;
   }
   if (!ok) Fail("fine-grained reshard: unsupported unit");
   RH_CUDA(cudaGetLastError());
@@ -838,7 +870,7 @@ void LaunchSynthetic(void* dst, const ComposedMap& m, int64_t n, uint64_t seed, 
 uint64_t SyncTimeoutNs() {
   static const uint64_t ns = [] {
     const char* e = std::getenv("RH_SYNC_TIMEOUT_MS");
-    const double ms = e && *e ? std::atof(e) : 20000.0;
+    const double ms = e && *e ? std::atof(e) : 60000.0;
     return static_cast<uint64_t>(std::max(0.0, ms) * 1e6);
   }();
   return ns;

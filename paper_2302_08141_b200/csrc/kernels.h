@@ -54,7 +54,7 @@ struct PeerSync {
   uint32_t* err;
   uint64_t timeout_ns;
 };
-// Host: RH_SYNC_TIMEOUT_MS (default 20000) in ns; error word encoding / decoding.
+// Host: RH_SYNC_TIMEOUT_MS (default 60000) in ns; error word encoding / decoding.
 uint64_t SyncTimeoutNs();
 __host__ __device__ inline uint32_t SyncErrorCode(int me, int member) {
   return 0x80000000u | (static_cast<uint32_t>(me & 0xff) << 8) | static_cast<uint32_t>(member & 0xff);

@@ -89,6 +89,7 @@ def check(rt, name, flags, dtype=None):
                 e = normwise(conv(gp.read_full(prog.outputs[0])), ref["f64"])
                 res["oracle_err"] = e
                 res["ok"] &= e <= tol_o
+            D.barrier()  # the other ranks wait here (host), not in a device barrier of the next run
         else:
             for out in prog.outputs:
                 e = normwise(conv(gp.read_full(out)), conv(o.read_full(out, partitioned=False)))
@@ -131,10 +132,56 @@ def check(rt, name, flags, dtype=None):
     return res
 
 
+def check_reshard(rt):
+    """rh_reshard in dist mode (peer memory, fused barriers) for every ordered spec pair —
+    including the fine-grained layouts that push into the peers' buffers or run in two phases —
+    against the oracle's reshard, bit-exact on this rank's destination."""
+    import torch
+    from paper_2302_08141_b200.abi import RH_F32, AxisSpec
+    d = rt.world
+    dims = [64, 1024]
+    specs = ["replicated", "partial", "shard(0,1)", "shard(0,max)", "shard(1,1)", "shard(1,2)", "shard(1,8)",
+             "shard(1,64)", "shard(1,max)"]
+
+    def spec(x):
+        if "max" in x:
+            dim = int(x[6])
+            return AxisSpec.shard(dim, dims[dim] // d)
+        return AxisSpec.from_string(x)
+    mesh = rx.Mesh(rt, [d])
+    res = {"name": f"reshard_d{d}", "flags": 0, "ok": True, "err": 0.0, "bad": []}
+    try:
+        for a in specs:
+            for b in specs:
+                fs, ts = spec(a), spec(b)
+                if a == b or fs == ts or b == "partial":
+                    continue
+                n = dims[0] * dims[1]
+                n_src, n_dst = (n // d if fs.kind == 0 else n), (n // d if ts.kind == 0 else n)
+                srcs = [np.random.default_rng(100 + r).standard_normal(n_src).astype(np.float32) for r in range(d)]
+                if fs.kind == 1:
+                    srcs = [srcs[0].copy() for _ in range(d)]
+                want = pyoracle.reshard(d, dims, fs, ts, RH_F32, srcs, n_dst)[rt.first_rank]
+                ts_ = torch.from_numpy(srcs[rt.first_rank]).cuda()
+                td = torch.empty(n_dst, device="cuda")
+                mesh.reshard(0, fs, ts, dims, RH_F32, [ts_.data_ptr()], [td.data_ptr()], 0, 2)
+                torch.cuda.synchronize()
+                if not np.array_equal(td.cpu().numpy(), want):
+                    res["ok"] = False
+                    res["bad"].append(f"{a}->{b}")
+    except Exception as e:
+        res["ok"] = False
+        res["exc"] = repr(e)
+    finally:
+        mesh.close()
+    res["ok"] = D.max_over_ranks(0.0 if res["ok"] else 1.0) == 0.0
+    return res
+
+
 def main():
     names = sys.argv[1].split(",")
     rt = D.make_runtime()
-    out = []
+    out = [check_reshard(rt)]
     for name in names:
         full = not name.startswith("c3_")  # full-size block: outputs only (oracle cost)
         for flags in ((0, RH_FLAG_NO_FUSION | RH_FLAG_SIMT_GEMM, RH_FLAG_TRANSPORT_NCCL) if full
@@ -142,6 +189,14 @@ def main():
             out.append(check(rt, name, flags))
         if name.startswith(("c3_", "c1_", "c5_")):
             out.append(check(rt, name, 0, RH_BF16))
+        if name.startswith("c5_"):  # rematerialized tanh values over real peers (bounded waits)
+            os.environ["RH_REMAT"] = "1"
+            try:
+                r = check(rt, name, 0, RH_BF16)
+                r["name"] += " [RH_REMAT=1]"
+                out.append(r)
+            finally:
+                del os.environ["RH_REMAT"]
     rt.close()
     if rt.first_rank == 0:
         print("DIST_RESULT " + json.dumps(out), flush=True)

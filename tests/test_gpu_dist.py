@@ -33,7 +33,7 @@ def test_dist_parity(world):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(29600 + world),
            os.path.join(HERE, "_dist_worker.py"), ",".join(PLANS[world])]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1800)
     lines = [l for l in r.stdout.splitlines() if l.startswith("DIST_RESULT ")]
     assert r.returncode == 0 and lines, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.loads(lines[0][len("DIST_RESULT "):])

@@ -10,8 +10,8 @@ from paper_2302_08141_b200.abi import RH_BF16, RH_F32, AxisSpec
 
 pytestmark = pytest.mark.gpu
 
-SPECS = ["replicated", "partial", "shard(0,1)", "shard(0,8)", "shard(0,max)", "shard(1,1)",
-         "shard(1,64)", "shard(1,max)"]
+SPECS = ["replicated", "partial", "shard(0,1)", "shard(0,8)", "shard(0,max)", "shard(1,1)", "shard(1,2)",
+         "shard(1,8)", "shard(1,64)", "shard(1,max)"]
 
 
 def spec_of(s, dims, d):
@@ -28,10 +28,12 @@ def local_elems(spec, dims, d):
 
 @pytest.mark.parametrize("d", [2, 4, 8])
 @pytest.mark.parametrize("dtype", [RH_F32, RH_BF16])
-def test_all_transitions_bit_exact(oracle_lib, d, dtype):
+@pytest.mark.parametrize("dims", [[64, 512], [256, 2048]])
+def test_all_transitions_bit_exact(oracle_lib, d, dtype, dims):
+    """Every ordered spec pair, including the fine-grained layouts (runs of 1-8 elements) that take
+    the push / pull-interleave / two-phase kernels (executor.cpp ClassifyFine)."""
     import torch
     from paper_2302_08141_b200 import runtime as rx
-    dims = [64, 512]
     rt = rx.Runtime(devices=[0] * d)
     mesh = rx.Mesh(rt, [d])
     rng = np.random.default_rng(d)
