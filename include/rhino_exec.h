@@ -102,7 +102,18 @@ typedef struct {
   int32_t perm[RH_MAX_RANK];
   rh_spec out_spec[RH_MAX_AXES];
   const rh_spec* in_specs;       /* [n_axes][n_in], axis-major */
+  /* Pipeline programs only (rh_program_load_pipeline; ignored by rh_program_load): the stage
+   * that computes the op (ExecutionPlan.stages.stage_of, planner.h:69-84), its microbatch
+   * (1..m) and its task in the stage's 1F1B order (proj/src/taskgraph.cpp:173-211):
+   * RH_PHASE_FWD / RH_PHASE_BWD / RH_PHASE_ACC (LocalAccumulate, taskgraph.cpp:149-160). */
+  int32_t stage;
+  int32_t microbatch;
+  int32_t phase;
 } rh_op;
+
+#define RH_PHASE_FWD 0
+#define RH_PHASE_BWD 1
+#define RH_PHASE_ACC 2
 
 /* rh_program_load flags */
 #define RH_FLAG_UNLABELED_IDENTITY 0x1u /* unlabeled unary = identity instead of tanh */
@@ -145,6 +156,18 @@ void rh_runtime_destroy(rh_runtime* rt);
 /* Device mesh (parashard::DeviceMesh::dims, mesh.h:44-57); prod(dims) == world. */
 int rh_mesh_create(rh_runtime* rt, int n_axes, const int* dims, rh_mesh** out);
 void rh_mesh_destroy(rh_mesh* mesh);
+
+/* A pipeline-parallel program (ExecutionPlan.pipeline_axis >= 0): mesh axis `pipeline_axis`
+ * holds the S stages (every spec Replicated on it); a rank with pipeline coordinate s runs only
+ * the ops of stage s, SPMD over the other axes; a value consumed by a later (or earlier) stage
+ * moves between the two ranks with equal non-pipeline coordinates (Send/Recv, taskgraph.cpp:
+ * 115-130) and is then resharded within the receiving stage (cut placeholders, planner.cpp:
+ * 84-91).  Each stage runs its tasks in 1F1B order (taskgraph.cpp:173-211).  `apply` (n_apply
+ * pairs {gradient op, parameter op}, may be 0): after the step, every parameter is updated in
+ * place, p -= lr * g (ApplyGradients, taskgraph.cpp:161-165), by its stage. */
+int rh_program_load_pipeline(rh_mesh* mesh, int pipeline_axis, const rh_op* ops, int n_ops, const int* outputs,
+                             int n_out, const int* apply, int n_apply, float lr, uint32_t flags,
+                             rh_program** out);
 
 /* Lower + allocate a partitioned program.  `outputs` are the program outputs
  * (TensorProgram::output_indices, ir.cpp:321-330); unless RH_FLAG_NO_MATERIALIZE they are

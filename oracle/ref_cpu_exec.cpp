@@ -525,6 +525,8 @@ rh_spec Natural(const Op& op, const std::vector<rh_spec>& in, const std::vector<
       out_dims[planned.dim] % (static_cast<int64_t>(d) * planned.stride) == 0)
     return planned;
   if (all_rep) return Rep();
+  // P + P -> P (local accumulation of partial sums; the executor's LocalAccumulate extension)
+  if (op.raw.kind == RH_OP_ADD && in.size() == 2 && in[0].kind == RH_PARTIAL && in[1].kind == RH_PARTIAL) return Par();
   for (auto& s : in)
     if (s.kind == RH_PARTIAL) bad();
   switch (op.raw.kind) {

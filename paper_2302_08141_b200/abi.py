@@ -53,6 +53,9 @@ class RhOp(ctypes.Structure):
         ("perm", ctypes.c_int32 * RH_MAX_RANK),
         ("out_spec", RhSpec * RH_MAX_AXES),
         ("in_specs", ctypes.POINTER(RhSpec)),
+        ("stage", ctypes.c_int32),
+        ("microbatch", ctypes.c_int32),
+        ("phase", ctypes.c_int32),
     ]
 
 

@@ -179,7 +179,7 @@ int64_t RunOnce(rh_program* p, std::vector<cudaEvent_t>* prof) {
       RH_CUDA(cudaStreamWaitEvent(p->side, p->fork_ev[k], 0));
       if (prof) RH_CUDA(cudaEventRecordWithFlags((*prof)[n + 1 + 2 * k], p->side, cudaEventRecordExternal));
       GroupSync(p, st.axis, /*side=*/true);
-      launches += st.run(0, p->side);
+      if (st.stage < 0 || p->StageOf(rt->first_rank) == st.stage) launches += st.run(0, p->side);
       GroupSync(p, st.axis, /*side=*/true);
       launches += 2;
       if (prof) RH_CUDA(cudaEventRecordWithFlags((*prof)[n + 2 + 2 * k], p->side, cudaEventRecordExternal));
@@ -194,6 +194,7 @@ int64_t RunOnce(rh_program* p, std::vector<cudaEvent_t>* prof) {
     rh::SetPdl(pdl);
     try {
       for (int li = 0; li < rt->n_local(); ++li) {
+        if (st.stage >= 0 && p->StageOf(rt->first_rank + li) != st.stage) continue;  // another stage's step
         if (multi_dev) RH_CUDA(cudaSetDevice(rt->device_of(li)));
         launches += st.run(li, rt->stream_of(li));
       }
@@ -432,6 +433,10 @@ void AssembleFull(rh_program* p, const rh::Tensor& t, void* dst) {
     const std::vector<int> c = p->mesh->Coords(r);
     bool skip = false, first = true;
     for (int a = 0; a < p->n_axes; ++a) {
+      if (a == p->pipeline_axis) {  // the tensor lives on the ranks of its stage only
+        if (c[a] != t.stage) skip = true;
+        continue;
+      }
       if (t.specs[a].kind == RH_REPLICATED && c[a] != 0) skip = true;
       if (t.specs[a].kind == RH_PARTIAL && c[a] != 0) first = false;
     }
@@ -609,9 +614,15 @@ void rh_mesh_destroy(rh_mesh* mesh) {
 }  // extern "C"
 
 namespace {
+struct PipelineArgs {
+  int axis = -1;
+  std::vector<std::pair<int, int>> apply;
+  float lr = 0.f;
+};
+
 int LoadProgram(rh_mesh* mesh, const rh_op* ops, int n_ops, const int* outputs, int n_out,
                 uint32_t flags, const std::vector<std::pair<int, Specs>>& requests,
-                rh_program** out) {
+                rh_program** out, const PipelineArgs& pp = PipelineArgs{}) {
   rh_program* raw = nullptr;
   int rc = Guard([&] {
     auto p = std::make_unique<rh_program>();
@@ -619,6 +630,15 @@ int LoadProgram(rh_mesh* mesh, const rh_op* ops, int n_ops, const int* outputs, 
     p->mesh = mesh;
     p->flags = flags;
     p->n_axes = static_cast<int>(mesh->dims.size());
+    if (pp.axis >= 0) {
+      if (pp.axis >= p->n_axes) Fail("pipeline axis out of range");
+      p->pipeline_axis = pp.axis;
+      p->n_stages = mesh->dims[pp.axis];
+      p->apply = pp.apply;
+      p->lr = pp.lr;
+      for (const auto& ap : pp.apply)
+        if (ap.first < 0 || ap.first >= n_ops || ap.second < 0 || ap.second >= n_ops) Fail("apply: bad op index");
+    }
     p->ops.assign(ops, ops + n_ops);
     p->inputs.resize(n_ops);
     p->in_specs.resize(n_ops);
@@ -684,6 +704,20 @@ int rh_op_natural_specs(const rh_op* ops, int n_ops, int op, int n_axes, const i
 int rh_program_load(rh_mesh* mesh, const rh_op* ops, int n_ops, const int* outputs, int n_out,
                     uint32_t flags, rh_program** out) {
   return LoadProgram(mesh, ops, n_ops, outputs, n_out, flags, {}, out);
+}
+
+int rh_program_load_pipeline(rh_mesh* mesh, int pipeline_axis, const rh_op* ops, int n_ops, const int* outputs,
+                             int n_out, const int* apply, int n_apply, float lr, uint32_t flags,
+                             rh_program** out) {
+  PipelineArgs pp;
+  pp.axis = pipeline_axis;
+  pp.lr = lr;
+  for (int k = 0; k < n_apply; ++k) pp.apply.emplace_back(apply[2 * k], apply[2 * k + 1]);
+  if (pipeline_axis < 0) {
+    g_err = "rh_program_load_pipeline: pipeline_axis must be a mesh axis";
+    return RH_ERR_INVALID;
+  }
+  return LoadProgram(mesh, ops, n_ops, outputs, n_out, flags, {}, out, pp);
 }
 
 void rh_program_destroy(rh_program* prog) { DestroyProgram(prog); }
@@ -1082,6 +1116,8 @@ int rh_program_read_local(rh_program* p, int op, int rank, void* dst, size_t byt
     if (bytes != t.bytes) Fail("rh_program_read_local: size mismatch");
     RequireLive(t);
     const int li = p->LocalIndex(rank);
+    if (t.stage >= 0 && p->StageOf(rank) != t.stage)
+      Fail("op is held by pipeline stage " + std::to_string(t.stage) + ", not by rank " + std::to_string(rank));
     SyncAll(p->mesh->rt);
     DeviceGuard dg(p->mesh->rt->device_of(li));
     RH_CUDA(cudaMemcpy(dst, p->base[li] + t.offset, bytes, cudaMemcpyDeviceToHost));
@@ -1100,8 +1136,15 @@ int rh_program_read_full(rh_program* p, int op, void* dst, size_t bytes) {
     if (bytes != static_cast<size_t>(n) * eb) Fail("rh_program_read_full: size mismatch");
     if (p->mat_tensor[op] >= 0) {
       const rh::Tensor& t = p->tensors[p->mat_tensor[op]];
-      DeviceGuard dg(rt->device_of(0));
-      RH_CUDA(cudaMemcpy(dst, p->base[0] + t.offset, bytes, cudaMemcpyDeviceToHost));
+      int li = 0;  // a local rank that holds it (pipeline programs: of the output's stage)
+      if (t.stage >= 0) {
+        li = -1;
+        for (int k = 0; k < rt->n_local() && li < 0; ++k)
+          if (p->StageOf(rt->first_rank + k) == t.stage) li = k;
+        if (li < 0) Fail("output is held by pipeline stage " + std::to_string(t.stage) + ", not by this process");
+      }
+      DeviceGuard dg(rt->device_of(li));
+      RH_CUDA(cudaMemcpy(dst, p->base[li] + t.offset, bytes, cudaMemcpyDeviceToHost));
       return;
     }
     if (p->out_tensor[op] < 0) Fail("op was fused into its consumer's kernel (use RH_FLAG_NO_FUSION)");

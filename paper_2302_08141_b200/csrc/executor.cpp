@@ -150,6 +150,11 @@ rh_spec Natural(const rh_op& op, const std::vector<rh_spec>& in, const std::vect
       planned.dim < static_cast<int>(out_dims.size() - in_dims[0].size()) && Valid(planned, out_dims, d))
     return planned;
   if (all_rep) return Rep();
+  // Accumulating partial sums (P + P -> P: the sum of per-rank addends is linear): the local
+  // gradient accumulation of a microbatched step (LocalAccumulate, taskgraph.cpp:149-160) adds
+  // unreduced data-parallel gradients and reduces once.  Not in the reference's rule table
+  // (ProduceOutput never yields Partial from an add, sharding.cpp:313-329): executor extension.
+  if (op.kind == RH_OP_ADD && in.size() == 2 && in[0].kind == RH_PARTIAL && in[1].kind == RH_PARTIAL) return Par();
   for (auto& s : in)
     if (s.kind == RH_PARTIAL) bad();
   switch (op.kind) {
@@ -307,14 +312,18 @@ class Lowerer {
     p_->counter_off = Alloc(4);
     p_->err_off = Alloc(4);
     ValidateSpecs();
+    const bool pipeline = p_->pipeline_axis >= 0;
     const bool eager = rt_->dist && rt_->world > 1 && !(p_->flags & RH_FLAG_NO_OVERLAP) &&
-                       !getenv("RH_NO_EAGER_TRANSITIONS");
+                       !getenv("RH_NO_EAGER_TRANSITIONS") && !pipeline;
     if (eager) TransitionFirstOrder();
     PlanGemmGroups();
+    if (pipeline) PipelineOrder();
+    SortGroupMembers();
     PlanFusion();
     RefineGemmGroups();
     for (int i : p_->order) {
       const rh_op& op = p_->ops[i];
+      cur_stage_ = StageOfOp(i);
       if (op.kind == RH_OP_PARAMETER || op.kind == RH_OP_INPUT) {
         p_->out_tensor[i] = NewTensor(i, p_->out_specs[i]);
         continue;
@@ -346,6 +355,7 @@ class Lowerer {
       // training-step outputs: reduce Partial axes (the gradient all-reduce / reduce of a
       // data-parallel step), keep sharded axes sharded (the optimizer updates shards in place)
       for (int o : p_->outputs) {
+        cur_stage_ = StageOfOp(o);
         Specs fin = p_->tensors[p_->out_tensor[o]].specs;
         bool rep = true;
         for (auto& x : fin) {
@@ -357,11 +367,16 @@ class Lowerer {
       }
     } else if (!(p_->flags & RH_FLAG_NO_MATERIALIZE)) {
       for (int o : p_->outputs) {
+        cur_stage_ = StageOfOp(o);
         Specs rep(p_->n_axes, Rep());
         p_->mat_tensor[o] = GetTensor(o, rep, "materialize");
       }
     }
-    for (const auto& rq : p_->requests) p_->request_tensors.push_back(GetTensor(rq.first, rq.second, "request"));
+    for (const auto& rq : p_->requests) {
+      cur_stage_ = StageOfOp(rq.first);
+      p_->request_tensors.push_back(GetTensor(rq.first, rq.second, "request"));
+    }
+    EmitApply();
     if (p_->gemm_scratch_bytes) p_->gemm_scratch_off = Alloc(p_->gemm_scratch_bytes);
     if (p_->n_sync_slots) {
       p_->sync_off = Alloc(static_cast<size_t>(p_->n_sync_slots) * rt_->world * 4);
@@ -378,23 +393,28 @@ class Lowerer {
     // post-barrier: the next p2p transition on that axis begins with a barrier of the same
     // group, which peers cannot pass before we finished.  Async (side-stream) transitions keep
     // their post-barrier (on the side stream's own barrier state).
-    std::vector<int> last(p_->n_axes, -1);
+    // (keyed by axis and pipeline stage: the ranks of one stage run only that stage's steps;
+    // cross-stage transfers (stage -2) carry their own pairwise rendezvous)
+    const int n_st = std::max(1, p_->n_stages) + 1;
+    auto slot_of = [&](const Step& st) { return st.axis * n_st + (st.stage < 0 ? 0 : st.stage + 1); };
+    std::vector<int> last(static_cast<size_t>(p_->n_axes) * n_st, -1);
     for (size_t i = 0; i < p_->steps.size(); ++i)
-      if (p_->steps[i].p2p && !p_->steps[i].async) last[p_->steps[i].axis] = static_cast<int>(i);
+      if (p_->steps[i].p2p && !p_->steps[i].async && p_->steps[i].stage != -2)
+        last[slot_of(p_->steps[i])] = static_cast<int>(i);
     for (size_t i = 0; i < p_->steps.size(); ++i)
-      if (p_->steps[i].p2p)
-        p_->steps[i].post_sync = p_->steps[i].async || static_cast<int>(i) == last[p_->steps[i].axis];
+      if (p_->steps[i].p2p && p_->steps[i].stage != -2)
+        p_->steps[i].post_sync = p_->steps[i].async || static_cast<int>(i) == last[slot_of(p_->steps[i])];
     // The last one on an axis: the NEXT run's first main-stream p2p transition on that axis
     // begins with the same group's barrier.  If it comes before the step that (re)writes every
     // tensor the last transition reads (kernel-written, own storage: not a source op, which the
     // host may overwrite between runs, nor an alias), peers cannot overwrite what we read before
     // we passed that barrier, and the post-barrier kernel can go too.
-    std::vector<int> first(p_->n_axes, -1);
+    std::vector<int> first(last.size(), -1);
     for (size_t i = 0; i < p_->steps.size(); ++i) {
       const Step& st = p_->steps[i];
-      if (st.p2p && !st.async && first[st.axis] < 0) first[st.axis] = static_cast<int>(i);
+      if (st.p2p && !st.async && st.stage != -2 && first[slot_of(st)] < 0) first[slot_of(st)] = static_cast<int>(i);
     }
-    for (int a = 0; a < p_->n_axes; ++a) {
+    for (size_t a = 0; a < last.size(); ++a) {
       const int l = last[a];
       if (l < 0 || getenv("RH_KEEP_LAST_POST_SYNC")) continue;
       bool ok = true;
@@ -438,7 +458,7 @@ class Lowerer {
     auto& S = p_->steps;
     const int ns = static_cast<int>(S.size());
     p_->joins_at.assign(ns, {});
-    if (!rt_->dist || rt_->world < 2 || (p_->flags & RH_FLAG_NO_OVERLAP)) return;
+    if (!rt_->dist || rt_->world < 2 || (p_->flags & RH_FLAG_NO_OVERLAP) || p_->pipeline_axis >= 0) return;
     auto est = [&](const Step& s) {
       if (s.kind == Step::kTransition) return s.wire_bytes / 5e11 + 15e-6;
       return std::max(s.alg_flops / 1.2e15, s.alg_bytes / 5e12) + 2e-6;
@@ -488,7 +508,7 @@ class Lowerer {
       if (!out.empty() && st.kind == Step::kTransition && !st.pulls.empty()) {
         Step& pv = out.back();
         bool ok = pv.kind == Step::kTransition && !pv.pulls.empty() && pv.axis == st.axis &&
-                  (pv.sync_slot >= 0) == (st.sync_slot >= 0);
+                  (pv.sync_slot >= 0) == (st.sync_slot >= 0) && pv.stage == st.stage;
         for (int r : st.reads)
           for (int w : pv.writes) ok = ok && Root(r) != Root(w);
         if (ok) {
@@ -682,9 +702,11 @@ class Lowerer {
 
   Dims GDims(int i) const { return Dims(p_->ops[i].dims, p_->ops[i].dims + p_->ops[i].rank); }
 
-  int NewTensor(int op, const Specs& specs, bool alloc = true) {
+  static constexpr int kOpStage = -3;  // NewTensor: the stage that computes the op
+  int NewTensor(int op, const Specs& specs, bool alloc = true, int stage = kOpStage) {
     Tensor t;
     t.op = op;
+    t.stage = stage == kOpStage ? StageOfOp(op) : stage;
     t.specs = specs;
     t.gdims = GDims(op);
     t.ldims = LocalDims(t.gdims, specs, mesh_, specs.size());
@@ -693,11 +715,21 @@ class Lowerer {
     t.storage = alloc;  // placed by PlanArena
     p_->tensors.push_back(t);
     const int idx = static_cast<int>(p_->tensors.size()) - 1;
-    cache_[Key(op, specs)] = idx;
+    cache_[Key(op, specs, p_->tensors[idx].stage)] = idx;
     return idx;
   }
 
-  static std::string Key(int op, const Specs& s) { return std::to_string(op) + "|" + SpecsStr(s); }
+  static std::string Key(int op, const Specs& s, int stage) {
+    return std::to_string(op) + "|" + SpecsStr(s) + "@" + std::to_string(stage);
+  }
+  int StageOfOp(int i) const { return p_->pipeline_axis >= 0 ? p_->ops[i].stage : -1; }
+  // pipeline programs: one kernel never spans two tasks (stage, microbatch, phase) of the 1F1B
+  // order — fusion would move an op out of its task
+  bool SameTask(int a, int b) const {
+    if (p_->pipeline_axis < 0) return true;
+    const rh_op &x = p_->ops[a], &y = p_->ops[b];
+    return x.stage == y.stage && x.microbatch == y.microbatch && x.phase == y.phase;
+  }
 
   void ValidateSpecs() {
     for (size_t i = 0; i < p_->ops.size(); ++i) {
@@ -712,6 +744,144 @@ class Lowerer {
       check(p_->out_specs[i], g, "output");
       for (size_t s = 0; s < p_->inputs[i].size(); ++s)
         check(p_->in_specs[i][s], GDims(p_->inputs[i][s]), "input");
+      if (p_->pipeline_axis >= 0) {  // the pipeline axis places stages, it shards nothing
+        const int pa = p_->pipeline_axis;
+        bool rep = p_->out_specs[i][pa].kind == RH_REPLICATED;
+        for (const auto& sp : p_->in_specs[i]) rep = rep && sp[pa].kind == RH_REPLICATED;
+        if (!rep) Fail("op " + std::to_string(i) + ": spec on the pipeline axis must be replicated");
+        const rh_op& op = p_->ops[i];
+        if (op.stage < 0 || op.stage >= p_->n_stages) Fail("op " + std::to_string(i) + ": stage out of range");
+      }
+    }
+  }
+
+  // 1F1B (taskgraph.cpp:173-211): stage s runs min(m, S - s) forward microbatches, then
+  // alternates backward(b) [+ LocalAccumulate(b)] and the next forward.  The op order is a
+  // topological order in which every stage's ops come task by task in that sequence (an op is
+  // eligible when its inputs are done and every earlier task of its stage is); ops of tasks the
+  // sequence does not list (no backward, accumulations of microbatch 1) follow their stage's
+  // last listed task.  Cross-stage transfers are emitted at their consumer, so each Send/Recv
+  // rendezvous sits at one point of this global order.
+  void PipelineOrder() {
+    const int n = static_cast<int>(p_->ops.size()), S = p_->n_stages;
+    int m = 1;
+    for (const auto& op : p_->ops) m = std::max(m, static_cast<int>(op.microbatch));
+    std::vector<std::map<std::pair<int, int>, int>> seq(S);  // (phase, microbatch) -> index
+    for (int s = 0; s < S; ++s) {
+      int k = 0;
+      auto put = [&](int ph, int mb) { seq[s].emplace(std::make_pair(ph, mb), k++); };
+      const int warm = std::min(m, S - s);
+      int next = 1;
+      for (; next <= warm; ++next) put(RH_PHASE_FWD, next);
+      for (int b = 1; b <= m; ++b) {
+        put(RH_PHASE_BWD, b);
+        if (b >= 2) put(RH_PHASE_ACC, b);
+        if (next <= m) put(RH_PHASE_FWD, next++);
+      }
+    }
+    std::vector<int> task(n);
+    for (int i = 0; i < n; ++i) {
+      const rh_op& op = p_->ops[i];
+      if (op.kind == RH_OP_PARAMETER || op.kind == RH_OP_INPUT) {
+        task[i] = -1;  // sources: before everything
+        continue;
+      }
+      auto it = seq[op.stage].find({op.phase, op.microbatch});
+      task[i] = it != seq[op.stage].end() ? it->second : static_cast<int>(seq[op.stage].size());
+    }
+    // nodes: single ops, or a grouped-GEMM group (same stage and task) as one node
+    auto node = [&](int i) { return group_of_.empty() || group_of_[i] < 0 ? i : n + group_of_[i]; };
+    const int nn = n + static_cast<int>(groups_.size());
+    std::vector<std::vector<int>> members(nn);
+    std::vector<int> pos(n);
+    for (int k = 0; k < n; ++k) pos[p_->order[k]] = k;
+    for (int k = 0; k < n; ++k) members[node(p_->order[k])].push_back(p_->order[k]);
+    std::vector<int> prio(nn, n), indeg(nn, 0), ntask(nn, -1), nstage(nn, 0);
+    std::vector<std::vector<int>> succ(nn);
+    for (int i = 0; i < n; ++i) {
+      const int v = node(i);
+      prio[v] = std::min(prio[v], pos[i]);
+      ntask[v] = task[i];
+      nstage[v] = p_->ops[i].stage;
+      for (int x : p_->inputs[i]) {
+        succ[node(x)].push_back(v);
+        ++indeg[v];
+      }
+    }
+    std::vector<std::vector<int>> left(S);  // ops left per (stage, task)
+    for (int s = 0; s < S; ++s) left[s].assign(seq[s].size() + 1, 0);
+    for (int i = 0; i < n; ++i)
+      if (task[i] >= 0) ++left[p_->ops[i].stage][task[i]];
+    std::vector<int> cur(S, 0);
+    auto advance = [&](int s) {
+      while (cur[s] < static_cast<int>(left[s].size()) && left[s][cur[s]] == 0) ++cur[s];
+    };
+    for (int s = 0; s < S; ++s) advance(s);
+    std::set<std::pair<int, int>> ready, parked;  // (priority, node)
+    auto offer = [&](int v) {
+      if (ntask[v] < 0 || ntask[v] == cur[nstage[v]]) ready.insert({prio[v], v});
+      else parked.insert({prio[v], v});
+    };
+    for (int v = 0; v < nn; ++v)
+      if (!members[v].empty() && !indeg[v]) offer(v);
+    std::vector<int> order;
+    while (!ready.empty()) {
+      const int v = ready.begin()->second;
+      ready.erase(ready.begin());
+      for (int i : members[v]) order.push_back(i);
+      if (ntask[v] >= 0) {
+        const int s = nstage[v];
+        left[s][ntask[v]] -= static_cast<int>(members[v].size());
+        const int before = cur[s];
+        advance(s);
+        if (cur[s] != before) {  // the stage's next task opened: release its parked nodes
+          for (auto it = parked.begin(); it != parked.end();) {
+            if (nstage[it->second] == s && ntask[it->second] == cur[s]) {
+              ready.insert(*it);
+              it = parked.erase(it);
+            } else {
+              ++it;
+            }
+          }
+        }
+      }
+      for (int w : succ[v])
+        if (--indeg[w] == 0) offer(w);
+    }
+    if (static_cast<int>(order.size()) != n)
+      Fail("pipeline program: the 1F1B task order contradicts the data dependencies");
+    p_->order = order;
+  }
+
+  // ApplyGradients (taskgraph.cpp:161-165): each parameter is updated in place by its stage,
+  // p -= lr * g, with the gradient brought to the parameter's own layout first (Partial axes
+  // reduced, shards matched).
+  void EmitApply() {
+    rh_program* P = p_;
+    for (const auto& ap : p_->apply) {
+      const int g = ap.first, w = ap.second;
+      if (p_->ops[w].kind != RH_OP_PARAMETER) Fail("apply: op " + std::to_string(w) + " is not a parameter");
+      if (GDims(g) != GDims(w) || p_->ops[g].dtype != p_->ops[w].dtype) Fail("apply: gradient / parameter mismatch");
+      cur_stage_ = StageOfOp(w);
+      const int wt = p_->out_tensor[w];
+      const int gt = GetTensor(g, p_->tensors[wt].specs, "apply");
+      Step st;
+      st.kind = Step::kKernel;
+      st.name = "apply_sgd op" + std::to_string(w);
+      st.launches = 1;
+      st.alg_bytes = 3.0 * p_->tensors[wt].bytes;
+      st.alg_flops = 2.0 * p_->tensors[wt].elems();
+      const float lr = p_->lr;
+      const int first = rt_->first_rank;
+      st.run = [P, wt, gt, lr, first](int li, cudaStream_t s) {
+        const int r = first + li;
+        LaunchSgd(P->Ptr(P->tensors[wt], r), P->Ptr(P->tensors[gt], r), P->tensors[wt].elems(), lr,
+                  P->tensors[wt].dtype, s);
+        return 1;
+      };
+      st.reads = {gt, wt};
+      st.writes = {wt};
+      AddStep(std::move(st));
     }
   }
 
@@ -771,7 +941,7 @@ class Lowerer {
       while (true) {
         if (uses[cur] != 1 || is_out[cur]) break;
         const int v = consumer[cur];
-        if (!IsElementwiseUnary(v) || p_->ops[v].dtype != op.dtype) break;
+        if (!IsElementwiseUnary(v) || p_->ops[v].dtype != op.dtype || !SameTask(v, h)) break;
         if (!SpecsEq(p_->in_specs[v][0], p_->out_specs[cur])) break;
         if (!no_partial(p_->out_specs[cur]) || !natural_ok(cur) || !natural_ok(v)) break;
         if (static_cast<int>(chain_[h].size()) + 1 >= kMaxChain) break;
@@ -842,6 +1012,7 @@ class Lowerer {
       }
       std::ostringstream key;
       key << depth[i] << '|' << op.transpose_a << op.transpose_b << '|' << SpecsStr(p_->out_specs[i]);
+      if (p_->pipeline_axis >= 0) key << "|s" << op.stage << '.' << op.microbatch << '.' << op.phase;
       for (int sl = 0; sl < 2; ++sl) {
         key << '|' << SpecsStr(p_->in_specs[i][sl]);
         for (auto x : LocalDims(GDims(p_->inputs[i][sl]), p_->in_specs[i][sl], mesh_, p_->n_axes)) key << ',' << x;
@@ -853,7 +1024,7 @@ class Lowerer {
       for (int m : kv.second) group_of_[m] = static_cast<int>(groups_.size());
       groups_.push_back(kv.second);
     }
-    if (groups_.empty()) return;
+    if (groups_.empty() || p_->pipeline_axis >= 0) return;  // pipeline: PipelineOrder contracts them
     // contracted topological order (ties: the earliest member's position in the current order)
     std::vector<int> pos(n);
     for (int k = 0; k < n; ++k) pos[p_->order[k]] = k;
@@ -883,9 +1054,12 @@ class Lowerer {
     }
     if (static_cast<int>(order.size()) != n) Fail("internal: grouped schedule is not a topological order");
     p_->order = order;
-    for (auto& g : groups_) std::sort(g.begin(), g.end(), [&](int a, int b) {
-      return std::find(order.begin(), order.end(), a) < std::find(order.begin(), order.end(), b);
-    });
+  }
+
+  void SortGroupMembers() {
+    std::vector<int> pos(p_->ops.size());
+    for (size_t k = 0; k < p_->order.size(); ++k) pos[p_->order[k]] = static_cast<int>(k);
+    for (auto& g : groups_) std::sort(g.begin(), g.end(), [&](int a, int b) { return pos[a] < pos[b]; });
   }
 
   // After fusion planning: members of one launch must share the epilogue chain (unary fns of
@@ -1074,7 +1248,7 @@ class Lowerer {
           best = kv.second;
           b = kv.first;
         }
-      if (b < 0) continue;
+      if (b < 0 || StageOfOp(b) != StageOfOp(c.members.front())) continue;
       Remat r;
       r.base = b;
       r.spec = p_->out_specs[b];
@@ -1219,7 +1393,7 @@ class Lowerer {
       for (int c : users[t]) {
         const auto& ins = p_->inputs[c];
         ok = ok && p_->ops[c].kind == RH_OP_MATMUL && !absorbed_[c] && p_->ops[c].dtype == op.dtype &&
-             ins.size() == 2 && ins[0] != ins[1];
+             ins.size() == 2 && ins[0] != ins[1] && StageOfOp(c) == StageOfOp(t);
       }
       if (!ok) continue;
       for (int c : users[t]) fold_t_[c][p_->inputs[c][0] == t ? 0 : 1] = true;
@@ -1290,6 +1464,7 @@ class Lowerer {
         for (int cand : cons[cur]) {
           if (!IsEw(cand) || absorbed_[cand] || ew_of_[cand] >= 0 || member_index(cand) >= 0) continue;
           if (p_->ops[cand].dtype != p_->ops[h].dtype || GDims(cand) != GDims(cur) || !natural_ok(cand)) continue;
+          if (!SameTask(cand, h)) continue;
           bool edge_ok = false;
           for (size_t sl = 0; sl < p_->inputs[cand].size(); ++sl)
             if (p_->inputs[cand][sl] == cur && SpecsEq(p_->in_specs[cand][sl], p_->out_specs[cur])) edge_ok = true;
@@ -1454,7 +1629,10 @@ class Lowerer {
 
   std::string OpName(int i) const { return "op" + std::to_string(i); }
 
-  void AddStep(Step s) { p_->steps.push_back(std::move(s)); }
+  void AddStep(Step s) {
+    if (s.stage == -1) s.stage = cur_stage_;  // pipeline programs: run by the current op's stage
+    p_->steps.push_back(std::move(s));
+  }
 
   void EmitOp(int i) {
     const rh_op& op = p_->ops[i];
@@ -1534,7 +1712,7 @@ class Lowerer {
     for (int m : c.members) {
       std::vector<int> ins;
       for (size_t sl = 0; sl < p_->inputs[m].size(); ++sl) {
-        auto it = cache_.find(Key(p_->inputs[m][sl], p_->in_specs[m][sl]));
+        auto it = cache_.find(Key(p_->inputs[m][sl], p_->in_specs[m][sl], cur_stage_));
         ins.push_back(it != cache_.end() ? it->second : -1);
       }
       p_->in_tensor[m] = ins;
@@ -2079,10 +2257,14 @@ class Lowerer {
 
   // Producer `p` in the per-axis layout `want`, inserting single-axis transitions as needed.
   int GetTensor(int p, const Specs& want, const char* why) {
-    auto it = cache_.find(Key(p, want));
+    auto it = cache_.find(Key(p, want, cur_stage_));
     if (it != cache_.end()) return it->second;
     int cur = p_->out_tensor[p];
     if (cur < 0) Fail("internal: producer " + std::to_string(p) + " has no buffer");
+    if (p_->tensors[cur].stage != cur_stage_) {  // produced by another pipeline stage
+      auto jt = cache_.find(Key(p, p_->tensors[cur].specs, cur_stage_));
+      cur = jt != cache_.end() ? jt->second : Transfer(cur, cur_stage_);
+    }
     Specs cs = p_->tensors[cur].specs;
     if (SpecsEq(cs, want)) return cur;
     int m = 0;
@@ -2106,8 +2288,85 @@ class Lowerer {
     return cur;
   }
 
+  // Cross-stage Send/Recv (taskgraph.cpp:115-130): the receiving stage's rank pulls the tensor,
+  // in its producer's layout, from the rank of the producing stage with the same non-pipeline
+  // coordinates (same local layout: a plain copy), between two pairwise rendezvous — before:
+  // the sender has produced it; after: the receiver has read it (the sender may overwrite it in
+  // its next run).  Both sides run the step at the consumer's position in the schedule, so every
+  // rendezvous is one point of the global order (deadlock-free).  Within the receiving stage
+  // the usual transitions take it to the consumer's demanded layout (the cut placeholder's
+  // reshard, planner.cpp:84-91).
+  int Transfer(int src, int to_stage) {
+    rh_program* P = p_;
+    const Tensor X = p_->tensors[src];
+    const int dst = NewTensor(X.op, X.specs, true, to_stage);
+    const int from_stage = X.stage, paxis = p_->pipeline_axis;
+    Step st;
+    st.kind = Step::kTransition;
+    st.stage = -2;
+    st.axis = paxis;
+    st.p2p = true;
+    st.post_mode = 2;  // the closure's own pairwise rendezvous
+    st.no_async = true;
+    st.name = "send_recv op" + std::to_string(X.op) + " stage " + std::to_string(from_stage) + "->" +
+              std::to_string(to_stage);
+    st.wire_bytes = static_cast<double>(X.bytes);
+    st.alg_bytes = 2.0 * X.bytes;
+    const bool multi = rt_->dist && rt_->world > 1;
+    const int slot_a = multi ? p_->n_sync_slots++ : -1, slot_b = multi ? p_->n_sync_slots++ : -1;
+    st.sync_slot = -1;  // no group barrier / fused group sync: the pair rendezvous below
+    st.run = [P, src, dst, from_stage, to_stage, paxis, slot_a, slot_b](int li, cudaStream_t s) {
+      const int g = P->mesh->rt->first_rank + li;
+      std::vector<int> c = P->mesh->Coords(g);
+      const int me = c[paxis];
+      if (me != from_stage && me != to_stage) return 0;
+      c[paxis] = me == to_stage ? from_stage : to_stage;
+      int peer = 0;
+      for (size_t a = 0; a < c.size(); ++a) peer = peer * P->mesh->dims[a] + c[a];
+      auto pair = [&](int slot) {
+        PeerSync y{};
+        if (slot < 0) return y;
+        const size_t row = P->sync_off + static_cast<size_t>(slot) * P->mesh->rt->world * 4;
+        const int mem[2] = {std::min(g, peer), std::max(g, peer)};
+        y.d = 2;
+        y.me = g;
+        for (int k = 0; k < 2; ++k) {
+          y.members[k] = mem[k];
+          y.peer_slot[k] = reinterpret_cast<uint32_t*>(P->peer_base[mem[k]] + row);
+        }
+        y.my_slot = reinterpret_cast<uint32_t*>(P->peer_base[g] + row);
+        y.epoch = reinterpret_cast<const uint32_t*>(P->peer_base[g] + P->epoch_off);
+        y.err = reinterpret_cast<uint32_t*>(P->peer_base[g] + P->err_off);
+        y.timeout_ns = SyncTimeoutNs();
+        return y;
+      };
+      if (me == from_stage) {  // sender: rendezvous before and after the receiver's read
+        LaunchPeerSync(pair(slot_a), s);
+        LaunchPeerSync(pair(slot_b), s);
+        return slot_a >= 0 ? 2 : 0;
+      }
+      PullArgs a{};
+      a.dst = P->Ptr(P->tensors[dst], g);
+      for (int k = 0; k < kMaxGroup; ++k) a.src[k] = P->Ptr(P->tensors[src], peer);
+      a.from = AxisView{RH_REPLICATED, 1, 0, 0};
+      a.to = AxisView{RH_REPLICATED, 1, 0, 0};
+      a.coord = 0;
+      a.n_dst = P->tensors[dst].elems();
+      a.dtype = P->tensors[dst].dtype;
+      a.sync = pair(slot_a);
+      int n = LaunchPull(a, s);
+      LaunchPeerSync(pair(slot_b), s);
+      return n + (slot_b >= 0 ? 1 : 0);
+    };
+    remote_read_.push_back(src);
+    st.reads = {src};
+    st.writes = {dst};
+    AddStep(std::move(st));
+    return dst;
+  }
+
   int Move(int src, int axis, const Specs& to_specs, const char* why) {
-    auto it = cache_.find(Key(p_->tensors[src].op, to_specs));
+    auto it = cache_.find(Key(p_->tensors[src].op, to_specs, p_->tensors[src].stage));
     if (it != cache_.end()) return it->second;
     const Tensor X = p_->tensors[src];
     {
@@ -2127,7 +2386,7 @@ class Lowerer {
         }
       }
     }
-    const int dst = NewTensor(X.op, to_specs);
+    const int dst = NewTensor(X.op, to_specs, true, X.stage);
     const Tensor Y = p_->tensors[dst];
     const int d = mesh_[axis];
     const Dims D = LocalDims(X.gdims, X.specs, mesh_, axis);  // axis-local tensor
@@ -2247,6 +2506,7 @@ class Lowerer {
   std::vector<EwPlan> ew_;
   std::vector<Remat> remat_;  // per chain program (PlanRemat)
   std::vector<int> ew_of_;  // op -> elementwise chain id (-1: none)
+  int cur_stage_ = -1;      // pipeline programs: stage of the op being emitted
 };
 
 }  // namespace

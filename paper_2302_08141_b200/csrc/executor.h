@@ -52,6 +52,7 @@ struct Tensor {
   int alias = -1;      // reshape pass-through: shares the storage of this tensor
   bool storage = true; // owns arena storage (false: alias or bufferless chain member)
   bool recycled = false;  // storage is reused by later tensors within a run (arena planner)
+  int stage = -1;         // pipeline programs: the stage whose ranks hold it (-1: every rank)
   int64_t elems() const {
     int64_t n = 1;
     for (auto x : ldims) n *= x;
@@ -63,6 +64,8 @@ struct Step {
   enum Kind { kKernel = 0, kTransition = 1, kSync = 2 };
   int kind = kKernel;
   std::string name;
+  int stage = -1;            // pipeline programs: ranks of this stage run it (-1 every rank,
+                             // -2 a cross-stage transfer: its closure knows sender / receiver)
   int axis = -1;             // transitions: mesh axis (group) that must be synchronised
   bool p2p = false;          // transition reads peer buffers (needs pre/post group sync)
   bool post_sync = true;     // p2p only: false when a later p2p step on the same axis (same
@@ -143,4 +146,12 @@ struct rh_program {
 
   char* Ptr(const rh::Tensor& t, int global_rank) const { return peer_base[global_rank] + t.offset; }
   int LocalIndex(int global_rank) const;
+  // pipeline programs (rh_program_load_pipeline)
+  int pipeline_axis = -1;
+  int n_stages = 1;
+  std::vector<std::pair<int, int>> apply;  // {gradient op, parameter op}
+  float lr = 0.f;
+  int StageOf(int global_rank) const {
+    return pipeline_axis < 0 ? -1 : mesh->Coords(global_rank)[pipeline_axis];
+  }
 };

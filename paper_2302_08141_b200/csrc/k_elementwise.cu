@@ -899,6 +899,32 @@ void LaunchBroadcast(void* out, const void* in, int64_t n_out, int64_t n_in, int
   RH_CUDA(cudaGetLastError());
 }
 
+namespace {
+template <bool kBf16>
+__global__ void __launch_bounds__(256) SgdKernel(void* w, const void* g, int64_t n, float lr) {
+  PdlTrigger();
+  PdlWait();
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    if constexpr (kBf16) {
+      __nv_bfloat16* wp = static_cast<__nv_bfloat16*>(w);
+      const float v = __fsub_rn(__bfloat162float(wp[i]),
+                                __fmul_rn(lr, __bfloat162float(static_cast<const __nv_bfloat16*>(g)[i])));
+      wp[i] = __float2bfloat16_rn(v);
+    } else {
+      float* wp = static_cast<float*>(w);
+      wp[i] = __fsub_rn(wp[i], __fmul_rn(lr, static_cast<const float*>(g)[i]));
+    }
+  }
+}
+}  // namespace
+
+void LaunchSgd(void* w, const void* g, int64_t n, float lr, int dtype, cudaStream_t s) {
+  if (n == 0) return;
+  if (dtype == RH_BF16) LaunchPdl(SgdKernel<true>, Blocks(n), 256, 0, s, w, g, n, lr);
+  else LaunchPdl(SgdKernel<false>, Blocks(n), 256, 0, s, w, g, n, lr);
+  RH_CUDA(cudaGetLastError());
+}
+
 bool LaunchConcat(const ConcatArgs& a, cudaStream_t s) {
   if (a.n < 1 || a.n > kMaxConcat || a.outer == 0) return false;
   int64_t most = 0;

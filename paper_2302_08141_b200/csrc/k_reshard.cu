@@ -136,6 +136,8 @@ __device__ __forceinline__ void ArriveAndWait(const PeerSync& s) {
 
 __global__ void EpochTickKernel(uint32_t* epoch) { *epoch += 1; }
 
+__global__ void PeerSyncKernel(PeerSync s) { ArriveAndWait(s); }
+
 __device__ __forceinline__ uint32_t DstToGlobal(const PullDev& a, uint32_t i) {
   if (!a.to_shard) return i;
   const uint32_t p = Div(a.qst, i);
@@ -878,6 +880,12 @@ uint64_t SyncTimeoutNs() {
 
 void LaunchBarrier(const BarrierArgs& b, cudaStream_t s) {
   BarrierKernel<<<1, 32, 0, s>>>(b);
+  RH_CUDA(cudaGetLastError());
+}
+
+void LaunchPeerSync(const PeerSync& sync, cudaStream_t s) {
+  if (sync.d == 0) return;
+  PeerSyncKernel<<<1, 32, 0, s>>>(sync);
   RH_CUDA(cudaGetLastError());
 }
 

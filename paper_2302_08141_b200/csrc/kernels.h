@@ -210,6 +210,11 @@ bool LaunchConcat(const ConcatArgs& a, cudaStream_t s);
 void LaunchConcatPiece(void* out, const void* in, int64_t outer, int64_t row, int64_t orow,
                        int64_t off, int dtype, cudaStream_t s);
 void LaunchZero(void* dst, size_t bytes, cudaStream_t s);
+// ApplyGradients (taskgraph.cpp:161-165): w -= lr * g elementwise, in place (fp32 arithmetic,
+// bf16 rounded once).
+void LaunchSgd(void* w, const void* g, int64_t n, float lr, int dtype, cudaStream_t s);
+// A fused-barrier rendezvous on its own (one CTA): the sending side of a cross-stage transfer.
+void LaunchPeerSync(const PeerSync& sync, cudaStream_t s);
 
 // ------------------------------------------ GEMM (K1) ----------------------------------------
 // C[m,n] = op(A)[m,k] . op(B)[k,n]; A stored [m,k] (ta=0) or [k,m] (ta=1), B stored [k,n]

@@ -28,15 +28,32 @@ struct AxisRecovery {
   std::vector<std::string> fallback_ops;  // ops recovered by the output-spec fallback
 };
 
+// A pipeline plan's cut placeholder (proj/src/planner.cpp:84-91): producer `producer` (of an
+// earlier stage), read by stage `stage` as input "__cut_<id>", in the per-axis specs the stage's
+// own search chose for the placeholder (the plan does not record them, planner.cpp:219-221).
+struct CutSpec {
+  int stage = 0;
+  int producer = 0;
+  std::vector<parashard::AxisSpec> specs;  // [axis]
+};
+
 struct LoweredProgram {
   std::vector<int> mesh;                                    // DeviceMesh::dims
   std::vector<std::vector<parashard::OpStrategy>> strat;   // [axis][op]
   std::vector<AxisRecovery> recovery;
   std::string descriptor;
+  // pipeline plans (ExecutionPlan.pipeline_axis >= 0): stage of every op, microbatches, cuts
+  int pipeline_axis = -1;
+  int microbatches = 1;
+  std::vector<int> stage_of;
+  std::vector<CutSpec> cuts;
 };
 
-// Recovers every op's OpStrategy on every mesh axis of `plan` (SPMD plans only; pipeline plans
-// are SURVEY §8f-1).  `opts` must be the PlanOptions the plan was made with.
+// Recovers every op's OpStrategy on every mesh axis of `plan`.  Pipeline plans: per stage, the
+// stage subprogram (ExtractStage, planner.cpp:75-110) is searched again on the non-pipeline axes
+// (SpmdSearchAllAxes with skip_axis, planner.cpp:122-167); ops get their stage and the cut
+// placeholders their specs; every op is Replicated on the pipeline axis.  `opts` must be the
+// PlanOptions the plan was made with.
 LoweredProgram RecoverStrategies(const parashard::TensorProgram& g,
                                  const parashard::ExecutionPlan& plan,
                                  const parashard::PlanOptions& opts);

@@ -7,7 +7,7 @@
 //   rh_plan (--text F | --json F | --fixture family:layers:hidden:batch)
 //           [--devices N | --machines M --gpus G] [--equal-bw] [--ilp-time-limit S]
 //           [--random-choice SEED --mesh d0[,d1]] [--dtype f32|bf16] [--name NAME]
-//           [--plan-out PLAN.json] -o OUT.json
+//           [--pipeline-stages S --microbatches M] [--plan-out PLAN.json] -o OUT.json
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -107,7 +107,7 @@ rhino::LoweredProgram PlanFwdGreedyBwd(const TensorProgram& g, int k_fwd, const 
   for (size_t axis = 0; axis < mesh.size(); ++axis) {
     const int d = mesh[axis];
     std::vector<AxisSpec> specs(g.size(), AxisSpec::Replicated());
-    if (d < 2) {
+    if (d < 2 || static_cast<int>(axis) == pf.pipeline_axis) {  // pipeline axis: all Replicated
       for (int i = 0; i < g.size(); ++i) {
         strat[axis][i].input_specs.assign(g.input_indices(i).size(), AxisSpec::Replicated());
         strat[axis][i].output_spec = AxisSpec::Replicated();
@@ -154,6 +154,13 @@ rhino::LoweredProgram PlanFwdGreedyBwd(const TensorProgram& g, int k_fwd, const 
                               {"recovery_matched", lf.recovery.empty() || lf.recovery[0].replay_matched}};
   rhino::LoweredProgram lp = rhino::StrategiesFromChoice(g, mesh, chosen, strat);
   lp.descriptor = pf.descriptor + "+greedy-bwd";
+  if (pf.pipeline_axis >= 0) {  // forward stages from the plan; backward ops staged by the caller
+    lp.pipeline_axis = lf.pipeline_axis;
+    lp.microbatches = lf.microbatches;
+    lp.stage_of.assign(g.size(), -1);
+    for (int i = 0; i < k_fwd; ++i) lp.stage_of[i] = lf.stage_of[i];
+    lp.cuts = lf.cuts;
+  }
   return lp;
 }
 
@@ -167,6 +174,7 @@ int main(int argc, char** argv) {
   double ilp_limit = 60.0;
   int opt_level = 0;  // PlanOptions.opt_level: 0 auto (O3 below 5000 ops), 2 = O2, 3 = O3
   int greedy_after = 0;  // > 0: plan the first N ops (forward) with the planner, rest greedy
+  int pipeline_stages = -1, microbatches = 0;  // SPMD plans unless --pipeline-stages
   for (int i = 1; i < argc; ++i) {
     std::string a = argv[i];
     auto next = [&]() -> std::string {
@@ -184,6 +192,8 @@ int main(int argc, char** argv) {
     else if (a == "--opt-level") opt_level = std::stoi(next());
     else if (a == "--greedy-after") greedy_after = std::stoi(next());
     else if (a == "--random-choice") random_seed = std::stoll(next());
+    else if (a == "--pipeline-stages") pipeline_stages = std::stoi(next());
+    else if (a == "--microbatches") microbatches = std::stoi(next());
     else if (a == "--mesh") mesh_s = next();
     else if (a == "--dtype") dtype = next();
     else if (a == "--name") name = next();
@@ -236,7 +246,8 @@ int main(int argc, char** argv) {
         cluster.inter_alpha = cluster.intra_alpha;
       }
       PlanOptions opts;
-      opts.pipeline_stages = -1;  // SPMD plans (pipeline execution is SURVEY §8f-1)
+      opts.pipeline_stages = pipeline_stages;  // -1: SPMD plans; S > 0: S pipeline stages
+      opts.microbatches = microbatches;
       opts.ilp_time_limit = ilp_limit;
       opts.opt_level = opt_level;
       if (greedy_after > 0) {

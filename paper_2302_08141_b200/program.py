@@ -22,7 +22,7 @@ PLANS_DIR = os.environ.get("RH_PLANS_DIR") or os.path.join(
 
 class LoweredOp:
     __slots__ = ("index", "id", "kind", "inputs", "shape", "fn", "transpose_a", "transpose_b",
-                 "axis", "perm", "out_spec", "in_specs", "flops")
+                 "axis", "perm", "out_spec", "in_specs", "flops", "stage", "microbatch", "phase")
 
     def local_shape(self, mesh):
         return composed_local_shape(self.shape, self.out_spec, mesh)
@@ -30,8 +30,8 @@ class LoweredOp:
 
 class LoweredProgram:
     def __init__(self, doc):
-        if doc.get("schema") != "rhino-lowered/1":
-            raise ValueError("not a rhino-lowered/1 document")
+        if doc.get("schema") not in ("rhino-lowered/1", "rhino-lowered/2"):
+            raise ValueError("not a rhino-lowered/1|2 document")
         self.doc = doc
         self.name = doc.get("name", "")
         self.mesh = list(doc["mesh"])
@@ -53,7 +53,16 @@ class LoweredProgram:
             op.out_spec = [AxisSpec.from_string(s) for s in o["out_spec"]]
             op.in_specs = [[AxisSpec.from_string(s) for s in axis] for axis in o["in_specs"]]
             op.flops = float(o.get("flops", 0.0))
+            op.stage = int(o.get("stage", 0))
+            op.microbatch = int(o.get("microbatch", 1))
+            op.phase = {"fwd": 0, "bwd": 1, "acc": 2}.get(o.get("phase", "fwd"), 0)
             self.ops.append(op)
+        # wire format v2 (pipeline plans): pipeline axis, microbatches, cut placeholder specs,
+        # and the ApplyGradients pairs {gradient op, parameter op} with the learning rate
+        self.pipeline_axis = int(doc.get("pipeline_axis", -1))
+        self.microbatches = int(doc.get("microbatches", 1))
+        self.apply = [tuple(x) for x in doc.get("apply", [])]
+        self.lr = float(doc.get("lr", 0.0))
         self._keep = None
 
     @staticmethod
@@ -132,6 +141,9 @@ class LoweredProgram:
                     specs[a * len(op.inputs) + s] = op.in_specs[a][s].to_c()
             keep.append(specs)
             r.in_specs = specs
+            r.stage = op.stage
+            r.microbatch = op.microbatch
+            r.phase = op.phase
         outs = (ctypes.c_int * max(1, len(self.outputs)))(*self.outputs)
         keep.append(outs)
         self._keep = keep

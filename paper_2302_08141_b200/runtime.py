@@ -20,7 +20,7 @@ EXPORTS = [
     "rh_program_write_full", "rh_program_run", "rh_program_step_host", "rh_program_run_host", "rh_program_read_local",
     "rh_program_read_full", "rh_program_read_input_full", "rh_program_local_bytes", "rh_program_memory", "rh_program_num_steps",
     "rh_program_step_info", "rh_program_profile", "rh_program_launch_count", "rh_reshard",
-    "rh_op_natural_specs",
+    "rh_op_natural_specs", "rh_program_load_pipeline",
 ]
 
 _lib = None
@@ -52,6 +52,7 @@ def lib():
     L.rh_mesh_destroy.restype = None
     L.rh_program_load.argtypes = [vp, P(RhOp), i, P(i), i, u32, P(vp)]
     L.rh_op_natural_specs.argtypes = [P(RhOp), i, i, i, P(i), P(RhSpec)]
+    L.rh_program_load_pipeline.argtypes = [vp, i, P(RhOp), i, P(i), i, P(i), i, ctypes.c_float, u32, P(vp)]
     L.rh_program_destroy.argtypes = [vp]
     L.rh_program_destroy.restype = None
     L.rh_program_init_synthetic.argtypes = [vp, u64]
@@ -157,8 +158,15 @@ class Program:
             raise RhinoError(f"mesh {mesh.dims} does not match the plan's mesh {prog.mesh}")
         arr, outs = prog.to_c()
         h = ctypes.c_void_p()
-        check(lib().rh_program_load(mesh.h, arr, len(prog.ops), outs, len(prog.outputs), flags,
-                                    ctypes.byref(h)))
+        if getattr(prog, "pipeline_axis", -1) >= 0:  # rh_program_load_pipeline (wire format v2)
+            ap = [x for pair in prog.apply for x in pair]
+            apc = (ctypes.c_int * max(1, len(ap)))(*ap)
+            check(lib().rh_program_load_pipeline(mesh.h, prog.pipeline_axis, arr, len(prog.ops), outs,
+                                                 len(prog.outputs), apc, len(prog.apply), prog.lr, flags,
+                                                 ctypes.byref(h)))
+        else:
+            check(lib().rh_program_load(mesh.h, arr, len(prog.ops), outs, len(prog.outputs), flags,
+                                        ctypes.byref(h)))
         self.h, self.mesh, self.prog = h, mesh, prog
 
     def close(self):

@@ -178,10 +178,57 @@ def check_reshard(rt):
     return res
 
 
+def check_pipeline(rt, name, dtype):
+    """A pipeline step program (2 stages on the pipeline axis, 1F1B, Send/Recv over NVLink,
+    LocalAccumulate + in-place ApplyGradients): one eager step, then every output this process's
+    stage holds against the oracle's unpartitioned run of the same step program."""
+    from paper_2302_08141_b200.abi import RH_FLAG_NO_GRAPH
+    prog = LoweredProgram.load(name)
+    prog = prog.with_dtype(dtype) if dtype is not None else prog
+    mesh = rx.Mesh(rt, prog.mesh)
+    res = {"name": name + (" bf16" if dtype == RH_BF16 else ""), "flags": RH_FLAG_NO_GRAPH, "ok": True, "err": 0.0}
+    gp = rx.Program(mesh, prog, RH_FLAG_NO_GRAPH)
+    try:
+        gp.init_synthetic(7)
+        gp.run(1)
+        coords, r = [], rt.first_rank
+        for dim in reversed(prog.mesh):
+            coords.insert(0, r % dim)
+            r //= dim
+        stage = coords[prog.pipeline_axis]
+        conv = pyoracle.bf16_to_f32 if dtype == RH_BF16 else (lambda a: a)
+        mine = [o for o in prog.outputs if prog.ops[o].stage == stage]
+        got = {o: conv(gp.read_full(o)) for o in mine}
+        key = (name, dtype)
+        if key not in _ORACLES:
+            o = pyoracle.OracleProgram(prog)
+            o.init_synthetic(7)
+            o.run_unpartitioned(max(1, (os.cpu_count() or 2) // max(1, rt.world)))
+            _ORACLES[key] = o
+        tol = 2e-2 if dtype == RH_BF16 else 1e-5
+        for o in mine:
+            e = normwise(got[o], conv(_ORACLES[key].read_full(o, partitioned=False)))
+            res["err"] = max(res["err"], e)
+            res["ok"] &= e <= tol
+        res["outputs_checked"] = len(mine)
+    except Exception as e:
+        res["ok"] = False
+        res["exc"] = repr(e)
+    finally:
+        gp.close()
+        mesh.close()
+    res["ok"] = D.max_over_ranks(0.0 if res["ok"] else 1.0) == 0.0
+    return res
+
+
 def main():
     names = sys.argv[1].split(",")
     rt = D.make_runtime()
     out = [check_reshard(rt)]
+    for name in [n for n in names if n.startswith("pp_")]:
+        out.append(check_pipeline(rt, name, None))
+        out.append(check_pipeline(rt, name, RH_BF16))
+    names = [n for n in names if not n.startswith("pp_")]
     for name in names:
         full = not name.startswith("c3_")  # full-size block: outputs only (oracle cost)
         for flags in ((0, RH_FLAG_NO_FUSION | RH_FLAG_SIMT_GEMM, RH_FLAG_TRANSPORT_NCCL) if full

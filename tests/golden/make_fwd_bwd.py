@@ -36,11 +36,24 @@ def forward_graph(fixture):
         return json.load(open(out))
 
 
-def fwd_bwd_ir(g):
+def fwd_bwd_ir(g, origin=None):
+    """Forward + backward text IR.  `origin` (optional dict) receives, for every op the backward
+    emits, the id of the forward op it differentiates (gradient accumulations: the op whose
+    gradient they sum; parameter gradients: the parameter) — pipeline programs give a backward
+    op the stage of its forward op (make_pipeline.py)."""
     ops = g["ops"]
+    if origin is None:
+        origin = {}
+    cur_fwd = [None]
+
+    class _L(list):
+        def append(self, line):
+            if cur_fwd[0] is not None:
+                origin[line.split(" = ", 1)[0]] = cur_fwd[0]
+            super().append(line)
     n = len(ops)
     shape = {o["id"]: o["shape"] for o in ops}
-    lines = []
+    lines = _L()
 
     def sh(dims):
         return "f32[" + ",".join(str(d) for d in dims) + "]"
@@ -70,6 +83,7 @@ def fwd_bwd_ir(g):
         return f"{prefix}_{cnt[0]:05d}"
 
     def grad_of(oid):
+        cur_fwd[0] = oid
         parts = grads.get(oid)
         if not parts:
             return None
@@ -100,6 +114,7 @@ def fwd_bwd_ir(g):
         dy = grad_of(oid)
         if dy is None:
             continue
+        cur_fwd[0] = oid
         if k == "param":
             gname = f"d_{oid}"  # same-shape reshape: names the gradient (metadata only)
             lines.append(f"{gname} = reshape({dy}) : {sh(o['shape'])}")

@@ -22,7 +22,7 @@ PLANS = {
         "skipnet_small_d2", "c3_gpt_block_d2", "c3_gpt_heads32_d2", "c5_gpt_small_d2"],
     4: ["c1_mlp_d4", "c2_mlp_reshape_d4", "c2_mlp_pinned_d4", "moe_small_d4", "gpt_small_2x2",
         "rand_gpt_like_2x2_s0", "rand_moe_like_4_s2", "c3_gpt_block_d4", "c3_gpt_heads32_d4", "c3_gpt_block_2x2",
-        "c5_gpt_small_d4"],
+        "c5_gpt_small_d4", "pp_gpt_small_2x2_m2", "pp_gpt_small_2x2_m4"],
 }
 
 

@@ -20,8 +20,10 @@ from paper_2302_08141_b200.program import PLANS_DIR, LoweredProgram
 pytestmark = pytest.mark.gpu
 
 TOL_F32, TOL_BF16 = 1e-5, 2e-2
+# (pipeline step programs are stateful — ApplyGradients — and have their own tests:
+# test_gpu_pipeline.py)
 SMALL = sorted(os.path.basename(p)[:-5] for p in glob.glob(os.path.join(PLANS_DIR, "*.json"))
-               if not os.path.basename(p).startswith(("c3_", "c5_big")))
+               if not os.path.basename(p).startswith(("c3_", "c5_big", "pp_")))
 DATA_MOVEMENT_KINDS = {0, 1, 6, 7, 9, 10}  # param, input, reshape, transpose, broadcast, concat
 
 

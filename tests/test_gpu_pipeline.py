@@ -1,0 +1,94 @@
+"""Pipeline-parallel training steps: a plan of the reference planner with
+pipeline_stages = 2 on a 2x2 mesh (pipeline axis + one SPMD axis), m microbatches, 1F1B.
+
+Executed with the 4 ranks emulated on cuda:0 (dist mode: tests/test_gpu_dist.py).  Checked
+against the CPU oracle running the same step program unpartitioned: every loss-side output
+and every LocalAccumulate gradient sum; the in-place ApplyGradients update p -= lr * g of every
+parameter; the cross-stage Send/Recv steps; and each stage's task order against the reference's
+1F1B sequence (proj/src/taskgraph.cpp:173-211)."""
+import re
+
+import numpy as np
+import pytest
+
+from paper_2302_08141_b200.abi import RH_BF16, RH_F32, RH_FLAG_NO_GRAPH
+from paper_2302_08141_b200.program import LoweredProgram
+
+pytestmark = pytest.mark.gpu
+
+
+def normwise(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-30)
+
+
+def one_f_one_b(S, m, s):
+    """The task sequence of stage s (schedule_1f1b, taskgraph.cpp:173-211)."""
+    seq, nxt = [], 1
+    warm = min(m, S - s)
+    for _ in range(warm):
+        seq.append(("fwd", nxt))
+        nxt += 1
+    for b in range(1, m + 1):
+        seq.append(("bwd", b))
+        if b >= 2:
+            seq.append(("acc", b))
+        if nxt <= m:
+            seq.append(("fwd", nxt))
+            nxt += 1
+    return seq
+
+
+@pytest.mark.parametrize("name", ["pp_gpt_small_2x2_m2", "pp_gpt_small_2x2_m4"])
+@pytest.mark.parametrize("dtype", [RH_F32, RH_BF16])
+def test_pipeline_step(oracle_lib, name, dtype):
+    from paper_2302_08141_b200 import runtime as rx
+    prog = LoweredProgram.load(name).with_dtype(dtype)
+    assert prog.pipeline_axis >= 0 and prog.apply
+    conv = oracle_lib.bf16_to_f32 if dtype == RH_BF16 else (lambda a: a)
+    rt = rx.Runtime(devices=[0] * prog.world)
+    mesh = rx.Mesh(rt, prog.mesh)
+    gp = rx.Program(mesh, prog, RH_FLAG_NO_GRAPH)  # eager: exactly one step (the step is stateful)
+    try:
+        gp.init_synthetic(7)
+        w0 = {w: conv(gp.read_full(w)).astype(np.float64) for _, w in prog.apply}
+        gp.run(1)
+        outs = {o: conv(gp.read_full(o)) for o in prog.outputs}
+        w1 = {w: conv(gp.read_full(w)).astype(np.float64) for _, w in prog.apply}
+        steps = gp.steps()
+    finally:
+        gp.close()
+        mesh.close()
+        rt.close()
+    names = [s["name"] for s in steps]
+    assert any(n.startswith("send_recv") for n in names), names[:20]
+    assert sum(n.startswith("apply_sgd") for n in names) == len(prog.apply)
+    # every stage's compute steps follow the 1F1B task sequence
+    S, m = prog.mesh[prog.pipeline_axis], prog.microbatches
+    tag = {0: "fwd", 1: "bwd", 2: "acc"}
+    seen = {s: [] for s in range(S)}
+    for st in steps:
+        mo = re.search(r"\bop(\d+)", st["name"])
+        if st["kind"] != 0 or not mo or st["name"].startswith("apply"):
+            continue
+        op = prog.ops[int(mo.group(1))]
+        t = (tag[op.phase], op.microbatch)
+        if op.kind in (0, 1):
+            continue
+        if not seen[op.stage] or seen[op.stage][-1] != t:
+            seen[op.stage].append(t)
+    for s in range(S):
+        want = [t for t in one_f_one_b(S, m, s) if t in seen[s]]
+        assert seen[s] == want, (s, seen[s], want)
+    o = oracle_lib.OracleProgram(prog)
+    o.init_synthetic(7)
+    o.run_unpartitioned()
+    tol = 2e-2 if dtype == RH_BF16 else 1e-5
+    for out in prog.outputs:
+        want = conv(o.read_full(out, partitioned=False))
+        assert normwise(outs[out], want) <= tol, (prog.ops[out].id, normwise(outs[out], want))
+    for g, w in prog.apply:  # ApplyGradients with the executor's own gradient sum
+        want = w0[w] - prog.lr * outs[g].astype(np.float64)
+        err = np.abs(w1[w] - want).max()
+        step = np.abs(want).max() * (2.0 ** -8 if dtype == RH_BF16 else 1e-6)
+        assert err <= step, (prog.ops[w].id, err)

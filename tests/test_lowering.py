@@ -23,7 +23,7 @@ def test_fixtures_present():
 @pytest.mark.parametrize("name", PLANS)
 def test_plan_fixture_consistent(name):
     p = LoweredProgram.load(name)
-    assert p.doc["schema"] == "rhino-lowered/1"
+    assert p.doc["schema"] == ("rhino-lowered/2" if name.startswith("pp_") else "rhino-lowered/1")
     for rec in p.doc["recovery"]:
         assert rec["replay_matched"], rec
     if "plan_sharding" in p.doc:  # recovered strategies emit exactly the planner's specs
@@ -50,3 +50,25 @@ def test_axis_spec_strings():
     assert AxisSpec.from_string("P") == AxisSpec.partial()
     with pytest.raises(ValueError):
         AxisSpec.from_string("shard(x)")
+
+
+PIPELINE = [p for p in PLANS if p.startswith("pp_")]
+
+
+@pytest.mark.parametrize("name", PIPELINE)
+def test_pipeline_plan_fixture(name):
+    """Wire format v2: stages, microbatches, cut placeholder specs and the
+    ApplyGradients pairs; every op Replicated on the pipeline axis (it places stages)."""
+    p = LoweredProgram.load(name)
+    assert p.doc["schema"] == "rhino-lowered/2" and p.pipeline_axis >= 0
+    S = p.mesh[p.pipeline_axis]
+    assert all(0 <= op.stage < S for op in p.ops)
+    assert all(str(op.out_spec[p.pipeline_axis]) == "replicated" for op in p.ops)
+    assert {op.microbatch for op in p.ops} == set(range(1, p.microbatches + 1))
+    assert p.doc["cuts"] and all(c["id"].startswith("__cut_") for c in p.doc["cuts"])
+    for g, w in p.apply:
+        assert p.ops[w].kind == 0 and p.ops[g].shape == p.ops[w].shape
+        assert p.ops[g].stage == p.ops[w].stage
+    # each stage's ops read only values of their own stage or of cut producers (Send/Recv)
+    cut_producers = {c["producer"] for c in p.doc["cuts"]}
+    assert cut_producers

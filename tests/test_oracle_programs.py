@@ -12,7 +12,7 @@ from paper_2302_08141_b200.abi import RH_BF16
 from paper_2302_08141_b200.program import PLANS_DIR, LoweredProgram
 
 SMALL = sorted(os.path.basename(p)[:-5] for p in glob.glob(os.path.join(PLANS_DIR, "*.json"))
-               if not os.path.basename(p).startswith(("c3_", "c5_big")))
+               if not os.path.basename(p).startswith(("c3_", "c5_big", "pp_")))
 TOL_F32, TOL_BF16 = 1e-5, 2e-2
 
 
