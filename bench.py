@@ -40,6 +40,11 @@ WORKLOADS = {
     "gpt24_train": dict(plan="c5_big_gpt24_d{n}", name="gpt24_fwd_bwd_h2048_t2048", dtype="bf16",
                         metric="partitioned-program tokens/s (24-layer GPT fwd+bwd, hidden 2048, 2048 tokens)",
                         cpu_plan="c5_big_gpt1_d1", cpu_scale=24, reduce_outputs=True),
+    # C5 with the planner's pipeline: 2 stages x 2-way SPMD on a 2x2 mesh, 4 microbatches of 512
+    # tokens, 1F1B, LocalAccumulate + ApplyGradients (tests/golden/make_pipeline.py); N=4 only
+    "gpt24_train_pp": dict(plan="pp_gpt24_2x2_m4", name="gpt24_fwd_bwd_h2048_t2048_pp2x2_m4", dtype="bf16",
+                           metric="partitioned-program tokens/s (24-layer GPT fwd+bwd, hidden 2048, 2048 tokens)",
+                           cpu_plan="c5_big_gpt1_d1", cpu_scale=24, reduce_outputs=True, fixed_n=4),
     "mlp": dict(plan="c1_mlp_d{n}", name="mlp2_b64_h1024", dtype="f32",
                 metric="partitioned-program tokens/s (2-layer MLP, batch 64, hidden 1024)"),
     "mlp_strided": dict(plan="c2_mlp_reshape_d{n}", name="mlp_reshape_strided_b64_h1024", dtype="f32",
@@ -209,8 +214,16 @@ def reshard_hbm(rx, pk, d=4, size=256 << 20):
             reads = n_dst * eb * (d if fs.kind == 2 else 1)
             alg = (reads + n_dst * eb) * d
             gbs = alg / (ms * 1e-3) / 1e9
+            # DRAM moves 32-byte sectors: a target whose runs are shorter than d*32 bytes makes
+            # every rank read every sector of a replicated source (R -> S(1,1) reads the whole
+            # tensor for 1/d of it), which bounds the algorithmic-byte fraction at ~(2/d)/(1+1/d)
+            src_full = size if fs.kind != 0 else size // d
+            run_t = (ts.stride * (dims[1] if ts.dim == 0 else 1) * eb) if ts.kind == 0 else size
+            touched = min(1.0, max(1.0 / d, 32.0 / (run_t * d))) if fs.kind == 1 and ts.kind == 0 else None
+            dram = (src_full * touched + n_dst * eb) * d if touched is not None else alg
             out.append({"from": fname, "to": tname, "ms": ms, "alg_bytes": alg, "hbm_gbs": gbs,
-                        "frac": gbs / pk["hbm_gbs"]})
+                        "frac": gbs / pk["hbm_gbs"], "sector_min_bytes": dram,
+                        "sector_frac": dram / (ms * 1e-3) / 1e9 / pk["hbm_gbs"]})
             del src, dst
             torch.cuda.empty_cache()
     finally:
@@ -291,7 +304,9 @@ def cpu_baseline(prog, threads):
 
 
 def tokens_of(prog):
-    return prog.ops[prog.op_index("x")].shape[0]
+    """Rows of the program input x (pipeline step programs: summed over the microbatch inputs)."""
+    xs = [op for op in prog.ops if op.kind == 1 and op.id.split("@")[0] == "x"]
+    return sum(op.shape[0] for op in xs)
 
 
 def run_reference(args):

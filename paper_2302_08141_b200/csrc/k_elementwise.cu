@@ -918,10 +918,43 @@ __global__ void __launch_bounds__(256) SgdKernel(void* w, const void* g, int64_t
 }
 }  // namespace
 
+// 16-byte vectors (8 bf16 / 4 fp32 per thread and iteration): a write-back pass of the whole
+// parameter set is HBM-bound.
+template <bool kBf16>
+__global__ void __launch_bounds__(256) SgdVecKernel(uint4* w, const uint4* g, int64_t n16, float lr) {
+  PdlTrigger();
+  PdlWait();
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n16; i += int64_t(gridDim.x) * blockDim.x) {
+    uint4 a = w[i];
+    const uint4 b = g[i];
+    uint32_t* x = reinterpret_cast<uint32_t*>(&a);
+    const uint32_t* y = reinterpret_cast<const uint32_t*>(&b);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if constexpr (kBf16) {
+        const float lo = __fsub_rn(__uint_as_float(x[k] << 16), __fmul_rn(lr, __uint_as_float(y[k] << 16)));
+        const float hi = __fsub_rn(__uint_as_float(x[k] & 0xffff0000u), __fmul_rn(lr, __uint_as_float(y[k] & 0xffff0000u)));
+        x[k] = PackBf16x2(lo, hi);
+      } else {
+        x[k] = __float_as_uint(__fsub_rn(__uint_as_float(x[k]), __fmul_rn(lr, __uint_as_float(y[k]))));
+      }
+    }
+    w[i] = a;
+  }
+}
+
 void LaunchSgd(void* w, const void* g, int64_t n, float lr, int dtype, cudaStream_t s) {
   if (n == 0) return;
-  if (dtype == RH_BF16) LaunchPdl(SgdKernel<true>, Blocks(n), 256, 0, s, w, g, n, lr);
-  else LaunchPdl(SgdKernel<false>, Blocks(n), 256, 0, s, w, g, n, lr);
+  const int eb = ElemBytes(dtype);
+  if ((n * eb) % 16 == 0 && (reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g)) % 16 == 0) {
+    const int64_t n16 = n * eb / 16;
+    if (dtype == RH_BF16) LaunchPdl(SgdVecKernel<true>, Blocks(n16), 256, 0, s, static_cast<uint4*>(w), static_cast<const uint4*>(g), n16, lr);
+    else LaunchPdl(SgdVecKernel<false>, Blocks(n16), 256, 0, s, static_cast<uint4*>(w), static_cast<const uint4*>(g), n16, lr);
+  } else if (dtype == RH_BF16) {
+    LaunchPdl(SgdKernel<true>, Blocks(n), 256, 0, s, w, g, n, lr);
+  } else {
+    LaunchPdl(SgdKernel<false>, Blocks(n), 256, 0, s, w, g, n, lr);
+  }
   RH_CUDA(cudaGetLastError());
 }
 
