@@ -247,6 +247,21 @@ __device__ __forceinline__ uint4 EwPick(const uint4 (&r)[kMaxEwIn], int k) {
   }
 }
 
+// Programs with at most 4 inputs (the rematerializing backward chains): 4 input vectors live,
+// not 8 — the registers buy a third / fourth resident block per SM.
+template <int N>
+__device__ __forceinline__ uint4 EwPickN(const uint4 (&r)[kMaxEwIn], int k) {
+  if constexpr (N <= 4) {
+    switch (k) {
+      case 0: return r[0];
+      case 1: return r[1];
+      case 2: return r[2];
+      default: return r[3];
+    }
+  }
+  return EwPick(r, k);
+}
+
 __device__ __forceinline__ uint32_t AddBf16x2(uint32_t a, uint32_t b) {
   uint32_t d;
   asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
@@ -271,6 +286,9 @@ __device__ __forceinline__ uint32_t TanhRunLookup2(uint32_t p, const uint16_t* t
 
 // Ladder rows of 8 packed bf16 values (2 x 16-byte shared loads each; |x| < 2^-5 and NaN pass
 // through every T^c unchanged, as in EwLadderKernel).
+// kHalf: a table of half rows (columns 0..7 only, 16 bytes per row): programs whose
+// rematerialized operands use at most 8 powers fetch one 16-byte row per element, not two.
+template <bool kHalf = false>
 __device__ __forceinline__ void LadderRows(const uint4 v, const uint4* lad_s, uint4 (&r)[8][2]) {
   constexpr uint32_t kLo = 122u << 7, kSpan = 0x7f80u - (122u << 7), kLast = kTanhRunEntries - 1;
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -279,11 +297,19 @@ __device__ __forceinline__ void LadderRows(const uint4 v, const uint4* lad_s, ui
     const uint32_t ab = ((e & 1) ? (w[e >> 1] >> 16) : w[e >> 1]) & 0x7fffu;
     const uint32_t u = ab - kLo;
     const uint32_t row = min(u, kLast);
-    r[e][0] = lad_s[2 * row];
-    r[e][1] = lad_s[2 * row + 1];
-    if (u > kSpan) {
-      const uint32_t rep = ab | (ab << 16);
-      r[e][0] = r[e][1] = make_uint4(rep, rep, rep, rep);
+    if constexpr (kHalf) {
+      r[e][0] = lad_s[row];
+      if (u > kSpan) {
+        const uint32_t rep = ab | (ab << 16);
+        r[e][0] = make_uint4(rep, rep, rep, rep);
+      }
+    } else {
+      r[e][0] = lad_s[2 * row];
+      r[e][1] = lad_s[2 * row + 1];
+      if (u > kSpan) {
+        const uint32_t rep = ab | (ab << 16);
+        r[e][0] = r[e][1] = make_uint4(rep, rep, rep, rep);
+      }
     }
   }
 }
@@ -317,9 +343,22 @@ __device__ __forceinline__ uint4 LadderCol(const uint4 (&r)[8][2], uint4 base) {
 
 // Operand k of the program: an input vector, or (k >= kEwSrcVirt) a ladder column of the
 // rematerialization base (warp-uniform switch: static register indices).
+template <bool kHalf = false>
 __device__ __forceinline__ uint4 EwOperand(const uint4 (&raw)[kMaxEwIn], const uint4 (&r)[8][2], uint4 base,
                                            int k) {
-  if (k < kEwSrcVirt) return EwPick(raw, k);
+  if (k < kEwSrcVirt) return EwPickN<kHalf ? 4 : kMaxEwIn>(raw, k);
+  if constexpr (kHalf) {
+    switch (k - kEwSrcVirt) {
+      case 0: return LadderCol<0>(r, base);
+      case 1: return LadderCol<1>(r, base);
+      case 2: return LadderCol<2>(r, base);
+      case 3: return LadderCol<3>(r, base);
+      case 4: return LadderCol<4>(r, base);
+      case 5: return LadderCol<5>(r, base);
+      case 6: return LadderCol<6>(r, base);
+      default: return LadderCol<7>(r, base);
+    }
+  }
   switch (k - kEwSrcVirt) {
     case 0: return LadderCol<0>(r, base);
     case 1: return LadderCol<1>(r, base);
@@ -350,18 +389,19 @@ __device__ __forceinline__ float LadderScalar(float x, const uint4* lad, int s) 
   return __uint_as_float(((bits & 0x8000u) | v) << 16);
 }
 
-template <bool kBf16, bool kRemat = false>
+template <bool kBf16, bool kRemat = false, bool kHalf = false>
 __device__ __forceinline__ void EwRunVec(const EwArgs& a, int64_t i, const uint16_t* tabs, int pc_end,
                                          uint32_t (&acc)[4], const uint4* vlad_s = nullptr) {
+  constexpr int kIn = kHalf ? 4 : kMaxEwIn;  // kHalf programs have at most 4 inputs (launcher)
   uint4 raw[kMaxEwIn];
 #pragma unroll
-  for (int k = 0; k < kMaxEwIn; ++k)
+  for (int k = 0; k < kIn; ++k)
     if (k < a.n_in) raw[k] = reinterpret_cast<const uint4*>(a.in[k])[i];
   uint4 vr[8][2];
   uint4 vbase = make_uint4(0, 0, 0, 0);
   if constexpr (kBf16 && kRemat) {
-    vbase = EwPick(raw, a.vlad_in);
-    LadderRows(vbase, vlad_s, vr);
+    vbase = EwPickN<kIn>(raw, a.vlad_in);
+    LadderRows<kHalf>(vbase, vlad_s, vr);
   }
   uint32_t keep[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -370,7 +410,7 @@ __device__ __forceinline__ void EwRunVec(const EwArgs& a, int64_t i, const uint1
     const int ins = a.code[pc], op = ins & 0xff, arg = ins >> 8;
     switch (op) {
       case kEwLoad: {
-        const uint4 v = (kRemat ? EwOperand(raw, vr, vbase, arg) : EwPick(raw, arg));
+        const uint4 v = (kRemat ? EwOperand<kHalf>(raw, vr, vbase, arg) : EwPickN<kIn>(raw, arg));
         acc[0] = v.x; acc[1] = v.y; acc[2] = v.z; acc[3] = v.w;
         break;
       }
@@ -385,7 +425,7 @@ __device__ __forceinline__ void EwRunVec(const EwArgs& a, int64_t i, const uint1
         if constexpr (kBf16 && kRemat) {
           const int hi = arg & 15, cnt = arg >> 4;
 #pragma unroll
-          for (int S = 15; S >= 0; --S) {
+          for (int S = kHalf ? 7 : 15; S >= 0; --S) {
             if (S > hi || S <= hi - cnt) continue;
             const uint4 v = LadderColI(vr, vbase, S);
             const uint32_t y[4] = {v.x, v.y, v.z, v.w};
@@ -402,7 +442,7 @@ __device__ __forceinline__ void EwRunVec(const EwArgs& a, int64_t i, const uint1
         break;
       }
       case kEwTanhBwd: {
-        const uint4 v = (kRemat ? EwOperand(raw, vr, vbase, arg) : EwPick(raw, arg));
+        const uint4 v = (kRemat ? EwOperand<kHalf>(raw, vr, vbase, arg) : EwPickN<kIn>(raw, arg));
         const uint32_t y[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -428,7 +468,7 @@ __device__ __forceinline__ void EwRunVec(const EwArgs& a, int64_t i, const uint1
 #pragma unroll
           for (int e = 0; e < 4; ++e) w[e] = acc[e];
         } else {
-          const uint4 v = (kRemat ? EwOperand(raw, vr, vbase, arg) : EwPick(raw, arg));
+          const uint4 v = (kRemat ? EwOperand<kHalf>(raw, vr, vbase, arg) : EwPickN<kIn>(raw, arg));
           w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
         }
         if constexpr (kBf16) {
@@ -526,16 +566,20 @@ __device__ __forceinline__ void EwRunScalar(const EwArgs& a, int64_t i, const ui
   }
 }
 
-template <bool kBf16, bool kRemat>
-__global__ void __launch_bounds__(256) EwProgKernel(const __grid_constant__ EwArgs a) {
+template <bool kBf16, bool kRemat, bool kHalf = false>
+__global__ void __launch_bounds__(256, kHalf ? 4 : 1) EwProgKernel(const __grid_constant__ EwArgs a) {
   PdlTrigger();
   __shared__ uint16_t tab_s[kBf16 ? kMaxTanhRuns * kTanhRunEntries : 1];
-  extern __shared__ uint4 vlad_s[];  // rematerialization ladder (vlad_n > 0)
+  extern __shared__ uint4 vlad_s[];  // rematerialization ladder (vlad_n > 0); kHalf: half rows
   if constexpr (kBf16) {
     for (int t = 0; t < a.n_tab; ++t)
       for (int i = threadIdx.x; i < kTanhRunEntries; i += blockDim.x) tab_s[t * kTanhRunEntries + i] = a.tab[t][i];
-    if (kRemat)
-      for (int i = threadIdx.x; i < kTanhRunEntries * 2; i += blockDim.x) vlad_s[i] = a.vlad[i];
+    if (kRemat) {
+      if (kHalf)
+        for (int i = threadIdx.x; i < kTanhRunEntries; i += blockDim.x) vlad_s[i] = a.vlad[2 * i];
+      else
+        for (int i = threadIdx.x; i < kTanhRunEntries * 2; i += blockDim.x) vlad_s[i] = a.vlad[i];
+    }
     __syncthreads();
   }
   PdlWait();
@@ -552,7 +596,7 @@ __global__ void __launch_bounds__(256) EwProgKernel(const __grid_constant__ EwAr
           asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint4*>(a.in[k]) + nx));
     }
     uint32_t acc[4];
-    EwRunVec<kBf16, kRemat>(a, i, tab_s, a.n_code, acc, vlad_s);
+    EwRunVec<kBf16, kRemat, kHalf>(a, i, tab_s, a.n_code, acc, vlad_s);
   }
   for (int64_t i = nv * E + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.n; i += stride)
     EwRunScalar<kBf16>(a, i, tab_s);
@@ -817,6 +861,10 @@ void LaunchEwProg(const EwArgs& a, int dtype, cudaStream_t s) {
     const int blocks = std::min(Blocks(a.n, 8), SmCount() * 4);
     if (vsmem) LaunchPdl(EwLadderKernel<true>, blocks, 256, kLadSmem + vsmem, s, a);
     else LaunchPdl(EwLadderKernel<false>, blocks, 256, kLadSmem, s, a);
+  } else if (dtype == RH_BF16 && vsmem && a.vlad_n <= 8 && a.n_in <= 4 && !getenv("RH_REMAT_FULL_ROWS")) {
+    // at most 8 rematerialized powers and 4 inputs: half rows (14 KB table, one 16-byte row per
+    // element) and 3 resident blocks per SM
+    LaunchPdl(EwProgKernel<true, true, true>, std::min(Blocks(a.n, 8), SmCount() * 4), 256, vsmem / 2, s, a);
   } else if (dtype == RH_BF16 && vsmem) {
     static bool attr[64] = {};
     if (dev < 64 && !attr[dev]) {
