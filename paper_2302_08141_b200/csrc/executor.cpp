@@ -2421,7 +2421,30 @@ class Lowerer {
     // One process per GPU: the pre-transition group barrier rides inside the pull kernel
     // (not for zero-fill targets, whose non-zero-coordinate ranks launch no kernel).
     if (st.p2p && rt_->dist && rt_->world > 1 && to.kind != RH_PARTIAL) st.sync_slot = p_->n_sync_slots++;
-    if (!nccl) {
+    static const bool no_push = getenv("RH_NO_PUSH_AG") != nullptr;  // A/B knob (profiles/)
+    if (!nccl && !no_push && st.p2p && from.kind == RH_SHARD && to.kind == RH_REPLICATED &&
+        std::string(why) == "materialize" && (fv.Qs * eb) % 16 == 0) {
+      // Output materialization into its persistent replicated buffer: push (every rank writes
+      // its shard into every member's copy: posted NVLink writes), fused pre-barrier (the
+      // members' copies are free: they reached this step), post-barrier (every push landed).
+      st.name += " [push]";
+      st.post_mode = 1;
+      st.fine = [P, src, dst, axis, fv, tv, dtype](int li, cudaStream_t s, const PeerSync& sync, int cap) {
+        const int g = P->mesh->rt->first_rank + li;
+        const std::vector<int> members = P->mesh->Group(axis, g);
+        PullArgs a{};
+        a.dst = P->Ptr(P->tensors[src], g);  // roles reversed (LaunchPushGather)
+        for (size_t k = 0; k < members.size(); ++k) a.src[k] = P->Ptr(P->tensors[dst], members[k]);
+        a.from = fv;
+        a.to = tv;
+        a.coord = P->mesh->Coords(g)[axis];
+        a.n_dst = P->tensors[dst].elems();
+        a.dtype = dtype;
+        a.sync = sync;
+        a.max_blocks = cap;
+        return LaunchPushGather(a, s);
+      };
+    } else if (!nccl) {
       // the launch (and the fused barrier) is set up by FinalizePulls once transitions are
       // merged and the overlap plan is known
       st.pulls.push_back([P, src, dst, axis, fv, tv, dtype](int li) {

@@ -627,6 +627,66 @@ int LaunchFine(const FineArgs& a, cudaStream_t s) {
 
 namespace {
 
+// Push all-gather (S -> R into a persistent destination, the output materialization): the
+// source rank writes each of its 16-byte local units to its global position in every member's
+// replicated destination — posted NVLink writes instead of round-trip reads.  Unit l of the
+// local buffer: run q = l / Qs, offset u: global (q*d + c)*Qs + u.
+struct PushDev {
+  const uint4* src;
+  uint4* dst[kMaxGroup];
+  FastDiv qs;  // source run (16-byte units)
+  uint32_t d, c, n;
+  PeerSync sync;
+};
+
+__global__ void __launch_bounds__(256) PushGatherKernel(PushDev a) {
+  ArriveAndWait(a.sync);
+  for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < a.n; l += gridDim.x * blockDim.x) {
+    const uint32_t q = Div(a.qs, l);
+    const uint64_t f = (static_cast<uint64_t>(q) * a.d + a.c) * a.qs.d + (l - q * a.qs.d);
+    const uint4 v = a.src[l];
+    for (uint32_t k = 0; k < a.d; ++k) {
+      const uint32_t r = (a.c + k) % a.d;  // rotated: the d ranks start on d different peers
+      a.dst[r][f] = v;
+    }
+  }
+}
+
+}  // namespace
+
+bool PushGatherSupported(const PullArgs& a) {
+  const int eb = ElemBytes(a.dtype);
+  if (a.from.kind != RH_SHARD || a.to.kind != RH_REPLICATED) return false;
+  if ((a.from.Qs * eb) % 16) return false;
+  const int64_t n16 = a.n_dst * eb / 16;
+  if (n16 >= (int64_t{1} << 32)) return false;
+  for (int k = 0; k < a.from.d; ++k)
+    if (reinterpret_cast<uintptr_t>(a.src[k]) % 16) return false;
+  return reinterpret_cast<uintptr_t>(a.dst) % 16 == 0;
+}
+
+// a.src[k]: member k's DESTINATION (replicated) buffer; a.dst: this rank's SOURCE shard (the
+// roles of a pull, reversed); a.n_dst: elements of the replicated destination.
+int LaunchPushGather(const PullArgs& a, cudaStream_t s) {
+  if (!PushGatherSupported(a)) Fail("push all-gather: unsupported layout");
+  const int eb = ElemBytes(a.dtype);
+  PushDev dv{};
+  dv.src = static_cast<const uint4*>(a.dst);
+  for (int k = 0; k < a.from.d; ++k) dv.dst[k] = static_cast<uint4*>(const_cast<void*>(a.src[k]));
+  dv.qs = MakeFastDiv(static_cast<uint32_t>(a.from.Qs * eb / 16));
+  dv.d = static_cast<uint32_t>(a.from.d);
+  dv.c = static_cast<uint32_t>(a.coord);
+  dv.n = static_cast<uint32_t>(a.n_dst / a.from.d * eb / 16);
+  dv.sync = a.sync;
+  const int cap = a.max_blocks > 0 ? a.max_blocks : SmCount() * 6;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((dv.n + 255) / 256, cap)));
+  PushGatherKernel<<<blocks, 256, 0, s>>>(dv);
+  RH_CUDA(cudaGetLastError());
+  return 1;
+}
+
+namespace {
+
 // Vector width of a plain pull: the largest power-of-two unit (<= 16 B) that divides every
 // contiguous run and every buffer alignment.
 int PullVB(const PullArgs& a) {

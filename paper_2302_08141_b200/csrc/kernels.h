@@ -99,6 +99,10 @@ struct FineArgs {
 };
 bool FineSupported(int d, int unit_bytes, int eb, int64_t n_contig);
 int LaunchFine(const FineArgs& a, cudaStream_t s);
+// Push all-gather (S -> R into a persistent destination): a.src[k] = member k's replicated
+// destination, a.dst = this rank's local shard (roles reversed against a pull).
+bool PushGatherSupported(const PullArgs& a);
+int LaunchPushGather(const PullArgs& a, cudaStream_t s);
 // Grouped transitions: n independent pulls of one mesh axis as ONE launch behind ONE fused
 // barrier (`sync` of LaunchPullMulti; the PullArgs' own sync is ignored).  PreparePullMulti
 // writes the segment table (PullMultiTableBytes) once and returns false when the pulls cannot
