@@ -26,7 +26,8 @@ import time
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md): the roofline
+NVLINK_NAMEPLATE_GBS = 900.0  # NVLink 5 per direction per GPU (nameplate), quoted next to it
 
 WORKLOADS = {
     "gpt_block": dict(plan="c3_gpt_block_d{n}", name="gpt_block_h4096_s2048", dtype="bf16",
@@ -460,7 +461,8 @@ def main():
                        "overlapped": len(ov), "overlapped_ms": sum(s["ms"] for s in ov),
                        "exposed_ms": t - sum(s["ms"] for s in ov),
                        "busbw_gbs": wire / (t * 1e-3) / 1e9 if t > 0 else None,
-                       "peak_gbs": NVLINK_PEER_GBS, "transport": args.transport,
+                       "peak_gbs": NVLINK_PEER_GBS, "nameplate_gbs": NVLINK_NAMEPLATE_GBS,
+                       "transport": args.transport,
                        "per_transition": [{"name": s["name"], "ms": s["ms"],
                                            "busbw_gbs": s["wire_bytes"] / (s["ms"] * 1e-3) / 1e9 if s["ms"] else None}
                                           for s in trans]}
