@@ -2421,8 +2421,11 @@ class Lowerer {
     // One process per GPU: the pre-transition group barrier rides inside the pull kernel
     // (not for zero-fill targets, whose non-zero-coordinate ranks launch no kernel).
     if (st.p2p && rt_->dist && rt_->world > 1 && to.kind != RH_PARTIAL) st.sync_slot = p_->n_sync_slots++;
-    static const bool no_push = getenv("RH_NO_PUSH_AG") != nullptr;  // A/B knob (profiles/)
-    if (!nccl && !no_push && st.p2p && from.kind == RH_SHARD && to.kind == RH_REPLICATED &&
+    // Push all-gather of the output materialization: opt-in (RH_PUSH_AG=1).  Measured no faster
+    // than the pull (C3 N=4: 40.2 vs 39.0 us, N=2: 32.3 vs 30.7 us, profiles/r2/push_ag_ab.log):
+    // the posted writes gain nothing over the pull's reads and it needs a post-barrier.
+    static const bool push_ag = getenv("RH_PUSH_AG") && getenv("RH_PUSH_AG")[0] == '1';
+    if (!nccl && push_ag && st.p2p && from.kind == RH_SHARD && to.kind == RH_REPLICATED &&
         std::string(why) == "materialize" && (fv.Qs * eb) % 16 == 0) {
       // Output materialization into its persistent replicated buffer: push (every rank writes
       // its shard into every member's copy: posted NVLink writes), fused pre-barrier (the

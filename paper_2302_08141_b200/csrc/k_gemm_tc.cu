@@ -178,14 +178,15 @@ __device__ __forceinline__ void EpiPackedBf16(const ChainArgs& epi, uint32_t (&p
   }
 }
 
-// Epilogue warps (128 threads, named barrier 1) stage the chain's T^k tables in shared memory.
+// Epilogue warps (`nthreads` threads, named barrier 1) stage the chain's T^k tables in shared
+// memory.
 __device__ __forceinline__ void StageEpiTables(const ChainArgs& epi, uint16_t* tab_s, int t,
-                                               const uint16_t* (&tp)[kMaxTanhRuns]) {
-  for (int i = t; i < epi.n_tab * kTanhRunEntries; i += 128)
+                                               const uint16_t* (&tp)[kMaxTanhRuns], int nthreads = 128) {
+  for (int i = t; i < epi.n_tab * kTanhRunEntries; i += nthreads)
     tab_s[i] = epi.tab[i / kTanhRunEntries][i % kTanhRunEntries];
 #pragma unroll
   for (int k = 0; k < kMaxTanhRuns; ++k) tp[k] = tab_s + k * kTanhRunEntries;
-  asm volatile("bar.sync 1, 128;" ::: "memory");
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 constexpr int kEpiTabBytes = 8192;  // >= kMaxTanhRuns * kTanhRunEntries * 2
 
@@ -507,14 +508,17 @@ __device__ __forceinline__ void CommitPair(uint64_t* bar) {
       : "memory");
 }
 
-template <int BN, bool kBKMajor, bool kAKMajor>
+// kEpi = epilogue warps: 4, or 8 for short-K GEMMs whose epilogue is the critical path (the
+// 32-head block's K = 128 score GEMMs, each output through a T^14 lookup): two warps per TMEM
+// lane quarter, alternate 32-column chunks; one pipeline stage less pays for their staging.
+template <int BN, bool kBKMajor, bool kAKMajor, int kEpi = 4>
 struct Tc2Cfg {
   static constexpr int kABytes = BM * BK * 2;        // own 128 rows
   static constexpr int kBBytes = (BN / 2) * BK * 2;  // own half of the columns
   static constexpr int kStage = kABytes + kBBytes;
-  static constexpr int kStages = (192 * 1024) / kStage;  // 6 (BN 256) / 8 (BN 128)
+  static constexpr int kStages = ((kEpi == 4 ? 192 : 160) * 1024) / kStage;  // 6 / 8 (4 warps), 5 / 6 (8)
   static constexpr int kTmemCols = 2 * BN;
-  static constexpr int kSmem = kStages * kStage + 1024 + kEpiTabBytes + kEpiStageBytes + 1024;
+  static constexpr int kSmem = kStages * kStage + 1024 + kEpiTabBytes + kEpi * 4096 + 1024;
   static constexpr uint32_t kIdesc = (1u << 4)                     // D = F32
                                      | (1u << 7) | (1u << 10)      // A, B = BF16
                                      | ((kAKMajor ? 0u : 1u) << 15) | ((kBKMajor ? 0u : 1u) << 16) |
@@ -522,13 +526,13 @@ struct Tc2Cfg {
                                      (static_cast<uint32_t>((2 * BM) >> 4) << 24);  // M = 256
 };
 
-template <int BN, bool kBKMajor, bool kAKMajor, bool kGroup = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+template <int BN, bool kBKMajor, bool kAKMajor, bool kGroup = false, int kEpi = 4>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpi, 1)
     GemmTcPairKernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                      const __grid_constant__ CUtensorMap tma_c, int M, int N, int K, ChainArgs epi, int ksplit,
                      float* __restrict__ ws, GroupDev grp) {
   PdlTrigger();
-  using Cfg = Tc2Cfg<BN, kBKMajor, kAKMajor>;
+  using Cfg = Tc2Cfg<BN, kBKMajor, kAKMajor, kEpi>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStage);
@@ -555,7 +559,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       MbarInit(&tfull[a], 1);
-      MbarInit(&tempty[a], 8);
+      MbarInit(&tempty[a], 2 * kEpi);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -655,9 +659,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {  // ---------------- epilogue (both CTAs) ----------------
-    const int ew = warp - 4;
+    const int ew = warp - 4, quarter = ew % 4, half = ew / 4;  // TMEM lanes of warp w: 32 * (w % 4)
     const uint16_t* tp[kMaxTanhRuns];
-    StageEpiTables(epi, reinterpret_cast<uint16_t*>(smem + Cfg::kStages * Cfg::kStage + 1024), threadIdx.x - 128, tp);
+    StageEpiTables(epi, reinterpret_cast<uint16_t*>(smem + Cfg::kStages * Cfg::kStage + 1024), threadIdx.x - 128, tp,
+                   32 * kEpi);
     const uint32_t tempty_leader[2] = {MapaShared(SmemU32(&tempty[0]), 0), MapaShared(SmemU32(&tempty[1]), 0)};
     uint8_t* stage_c = smem + Cfg::kStages * Cfg::kStage + 1024 + kEpiTabBytes + ew * 4096;
     uint32_t boxes = 0;
@@ -668,13 +673,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int m_blk = t % num_m, n_blk = t / num_m;
       MbarWait(&tfull[acc], acc_phase);
       FenceAfter();
-      const int row0 = m_blk * 2 * BM + static_cast<int>(rank) * BM + ew * 32;
+      const int row0 = m_blk * 2 * BM + static_cast<int>(rank) * BM + quarter * 32;
       const int row = row0 + lane;
       float* wrow = ws ? ws + (static_cast<int64_t>(ks) * M + row) * N + n_blk * BN : nullptr;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half; c < BN / 32; c += kEpi / 4) {
         uint32_t r[32];
-        TmemLd32(tmem + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
+        TmemLd32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c * 32, r);
         if (wrow) {
           float4* dst = reinterpret_cast<float4*>(wrow + c * 32);
 #pragma unroll
@@ -1131,14 +1136,14 @@ void Launch(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullptr) 
 }
 
 // Pair-tile (256 x BN) launch: clusters of 2 CTAs, one pair per TPC, persistent over the tiles.
-template <int BN, bool kBK, bool kAK, bool kG = false>
+template <int BN, bool kBK, bool kAK, bool kG = false, int kEpi = 4>
 void LaunchPair(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullptr) {
-  using Cfg = Tc2Cfg<BN, kBK, kAK>;
+  using Cfg = Tc2Cfg<BN, kBK, kAK, kEpi>;
   int dev = 0;
   RH_CUDA(cudaGetDevice(&dev));
   static bool attr[64] = {};
   if (dev < 64 && !attr[dev]) {
-    RH_CUDA(cudaFuncSetAttribute(GemmTcPairKernel<BN, kBK, kAK, kG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RH_CUDA(cudaFuncSetAttribute(GemmTcPairKernel<BN, kBK, kAK, kG, kEpi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Cfg::kSmem));
     attr[dev] = true;
   }
@@ -1150,7 +1155,7 @@ void LaunchPair(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullp
   float* ws = ks > 1 ? static_cast<float*>(g.scratch) : nullptr;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(128 + 32 * kEpi);
   cfg.dynamicSmemBytes = Cfg::kSmem;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
@@ -1162,7 +1167,7 @@ void LaunchPair(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullp
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = PdlEnabled() ? 2 : 1;
-  RH_CUDA(cudaLaunchKernelEx(&cfg, GemmTcPairKernel<BN, kBK, kAK, kG>, mp.a, mp.b, mp.c,
+  RH_CUDA(cudaLaunchKernelEx(&cfg, GemmTcPairKernel<BN, kBK, kAK, kG, kEpi>, mp.a, mp.b, mp.c,
                              static_cast<int>(g.m), static_cast<int>(n), static_cast<int>(g.k), g.epi, ks, ws,
                              kG ? gl->dev : GroupDev{}));
   if (ws) {
@@ -1303,6 +1308,12 @@ int GemmTcLaunches(const GemmArgs& g) {
 
 // ------------------------------- grouped GEMM (horizontal fusion) -------------------------------
 namespace {
+// 8 epilogue warps when the main loop is a handful of k-blocks (K <= 256): the epilogue is the
+// critical path there.  RH_GEMM_EPI8=0 disables (A/B).
+bool UseEpi8(const GemmArgs& g) {
+  static const int on = EnvInt("RH_GEMM_EPI8", 1);
+  return on && g.k <= 256;
+}
 // Problems side by side along a virtual N = n_prob * g.n.  A tile may span problems only when
 // they share A; B column chunks (64 wide, MN-major) or boxes (K-major: bn or bn/2 rows) must not
 // straddle two problems; no split-K (the partials' reduce would need the same scatter).
@@ -1406,6 +1417,16 @@ void LaunchGemmTcGroup(const GemmArgs& g, const void* table, cudaStream_t s) {
   const GroupLaunch* gl = &h.gl;
   const int v = (h.sc.bn == 256 ? 4 : 0) | (g.tb ? 2 : 0) | (g.ta ? 0 : 1);
   if (h.sc.pair) {
+    if (UseEpi8(g)) {
+      switch (v) {
+        case 4: LaunchPair<256, false, false, true, 8>(g, s, gl); break;
+        case 5: LaunchPair<256, false, true, true, 8>(g, s, gl); break;
+        case 6: LaunchPair<256, true, false, true, 8>(g, s, gl); break;
+        case 7: LaunchPair<256, true, true, true, 8>(g, s, gl); break;
+        default: Fail("internal: grouped pair schedule");
+      }
+      return;
+    }
     switch (v) {
       case 4: LaunchPair<256, false, false, true>(g, s, gl); break;
       case 5: LaunchPair<256, false, true, true>(g, s, gl); break;
