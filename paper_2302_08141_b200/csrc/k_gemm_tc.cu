@@ -516,7 +516,7 @@ struct Tc2Cfg {
   static constexpr int kABytes = BM * BK * 2;        // own 128 rows
   static constexpr int kBBytes = (BN / 2) * BK * 2;  // own half of the columns
   static constexpr int kStage = kABytes + kBBytes;
-  static constexpr int kStages = ((kEpi == 4 ? 192 : 160) * 1024) / kStage;  // 6 / 8 (4 warps), 5 / 6 (8)
+  static constexpr int kStages = ((kEpi == 4 ? 192 : kEpi == 8 ? 160 : 128) * 1024) / kStage;
   static constexpr int kTmemCols = 2 * BN;
   static constexpr int kSmem = kStages * kStage + 1024 + kEpiTabBytes + kEpi * 4096 + 1024;
   static constexpr uint32_t kIdesc = (1u << 4)                     // D = F32
@@ -1418,6 +1418,17 @@ void LaunchGemmTcGroup(const GemmArgs& g, const void* table, cudaStream_t s) {
   const int v = (h.sc.bn == 256 ? 4 : 0) | (g.tb ? 2 : 0) | (g.ta ? 0 : 1);
   if (h.sc.pair) {
     if (UseEpi8(g)) {
+      static const int w = EnvInt("RH_GEMM_EPI_WARPS", 12);
+      if (w == 12) {
+        switch (v) {
+          case 4: LaunchPair<256, false, false, true, 12>(g, s, gl); break;
+          case 5: LaunchPair<256, false, true, true, 12>(g, s, gl); break;
+          case 6: LaunchPair<256, true, false, true, 12>(g, s, gl); break;
+          case 7: LaunchPair<256, true, true, true, 12>(g, s, gl); break;
+          default: Fail("internal: grouped pair schedule");
+        }
+        return;
+      }
       switch (v) {
         case 4: LaunchPair<256, false, false, true, 8>(g, s, gl); break;
         case 5: LaunchPair<256, false, true, true, 8>(g, s, gl); break;
