@@ -28,7 +28,12 @@ SHAPES = [
     (2048, 8192, 4096, 0, 0), (2048, 16384, 4096, 0, 0),
     # 148-SM-friendly tile counts
     (2048, 4096, 9472, 0, 0), (4736, 4096, 2048, 0, 0),
+    # C3 at N=4 (row-split FFN: 512-row shards) and N=2
+    (512, 16384, 4096, 0, 0), (512, 4096, 16384, 0, 0), (1024, 16384, 4096, 0, 0), (1024, 4096, 16384, 0, 0),
 ]
+
+
+os.environ.setdefault("RH_NO_GEMM_GROUP", "1")  # the reps below would otherwise be one grouped launch
 
 
 def ours(m, k, n, ta, tb, iters, flags, reps=16):
