@@ -187,10 +187,18 @@ int64_t RunOnce(rh_program* p, std::vector<cudaEvent_t>* prof) {
       continue;
     }
     if (st.p2p && st.sync_slot < 0) GroupSync(p, st.axis);
-    // PDL (launch.cuh) only between compute kernels: never after a transition (pull kernels
-    // spin on peers) nor after a cross-stream join or a profiling event
+    // PDL (launch.cuh) after a compute kernel only: for the next compute kernel, and for a
+    // peer-memory pull (its CTAs become resident while the producer drains and publish their
+    // arrival at the fused barrier as soon as griddepcontrol.wait returns).  Never after a
+    // transition (a kernel must not wait on a grid whose CTAs spin on peers), a cross-stream
+    // join or a profiling event; RH_PDL_PULL=0 keeps pulls on plain launches.
+    static const bool pdl_pull = [] {
+      const char* e = std::getenv("RH_PDL_PULL");
+      return !(e && e[0] == '0');
+    }();
     const bool pdl = !(p->flags & RH_FLAG_NO_PDL) && !prof && prev_kernel && p->joins_at[si].empty() &&
-                     st.kind == rh::Step::kKernel;
+                     (st.kind == rh::Step::kKernel ||
+                      (pdl_pull && st.kind == rh::Step::kTransition && !st.pulls.empty() && !st.fine));
     rh::SetPdl(pdl);
     try {
       for (int li = 0; li < rt->n_local(); ++li) {

@@ -385,6 +385,7 @@ class Lowerer {
     MergeTransitions();
     PlanAsync();
     FinalizePulls();
+    EwJitBuild();
     PlanArena();
     p_->arena_bytes = arena_;
     // Barrier elision: transition sources are persistent (never recycled by the arena planner)
@@ -1875,6 +1876,7 @@ class Lowerer {
     a.n_in = static_cast<int32_t>(in_t.size());
     std::copy(code.begin(), code.end(), a.code);
     a.n = P->tensors[out_t[0]].elems();
+    a.jit = EwJitRegister(a, dtype);  // compiled with the program's other chains (EwJitBuild)
     Step st;
     st.kind = Step::kKernel;
     st.launches = 1;

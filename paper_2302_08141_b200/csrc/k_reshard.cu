@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "kernels.h"
+#include "launch.cuh"
 
 namespace rh {
 
@@ -121,6 +122,7 @@ __device__ __forceinline__ void WaitFlag(const uint32_t* f, uint32_t want, uint3
 // Block 0 publishes the arrival (it is dispatched first; every other CTA only polls its own,
 // local flag row, so no CTA waits on a CTA of its own grid that might not be resident).
 __device__ __forceinline__ void ArriveAndWait(const PeerSync& s) {
+  PdlWait();  // launched with PDL after a compute kernel: its writes are complete and visible
   if (s.d == 0) return;
   const int t = threadIdx.x;
   if (t < s.d) {
@@ -390,14 +392,14 @@ void LaunchPullVB(const PullArgs& a, PullDev& dv, cudaStream_t s) {
   if (a.from.kind == RH_PARTIAL) {
     const int sb = static_cast<int>(std::min<int64_t>((n + 255) / 256, cap));
     if (a.dtype == RH_BF16) {
-      if constexpr (VB >= 2) PullSumKernel<__nv_bfloat16, VB><<<sb, 256, 0, s>>>(dv, a.from.d);
+      if constexpr (VB >= 2) LaunchPdl(PullSumKernel<__nv_bfloat16, VB>, sb, 256, 0, s, dv, a.from.d);
     } else {
-      if constexpr (VB >= 4) PullSumKernel<float, VB><<<sb, 256, 0, s>>>(dv, a.from.d);
+      if constexpr (VB >= 4) LaunchPdl(PullSumKernel<float, VB>, sb, 256, 0, s, dv, a.from.d);
     }
   } else if (a.from.kind == RH_SHARD) {
-    PullCopyKernel<VB, true><<<blocks, 256, 0, s>>>(dv);
+    LaunchPdl(PullCopyKernel<VB, true>, blocks, 256, 0, s, dv);
   } else {
-    PullCopyKernel<VB, false><<<blocks, 256, 0, s>>>(dv);
+    LaunchPdl(PullCopyKernel<VB, false>, blocks, 256, 0, s, dv);
   }
   RH_CUDA(cudaGetLastError());
 }
@@ -812,11 +814,11 @@ int LaunchPullMulti(const void* table, const PeerSync& sync, cudaStream_t s) {
   }
   const PullDev* seg = static_cast<const PullDev*>(table);
   const bool bf = h.dtype == RH_BF16;
-#define RH_MULTI(VB)                                                                                  \
-  if (h.kind == RH_SHARD) PullMultiKernel<VB, 0, float><<<h.blocks, 256, 0, s>>>(seg, h.n, sync);     \
-  else if (h.kind == RH_REPLICATED) PullMultiKernel<VB, 1, float><<<h.blocks, 256, 0, s>>>(seg, h.n, sync); \
-  else if (bf) PullMultiKernel<VB, 2, __nv_bfloat16><<<h.blocks, 256, 0, s>>>(seg, h.n, sync);       \
-  else if (VB >= 4) PullMultiKernel<(VB >= 4 ? VB : 4), 2, float><<<h.blocks, 256, 0, s>>>(seg, h.n, sync);
+#define RH_MULTI(VB)                                                                                   \
+  if (h.kind == RH_SHARD) LaunchPdl(PullMultiKernel<VB, 0, float>, h.blocks, 256, 0, s, seg, h.n, sync);       \
+  else if (h.kind == RH_REPLICATED) LaunchPdl(PullMultiKernel<VB, 1, float>, h.blocks, 256, 0, s, seg, h.n, sync); \
+  else if (bf) LaunchPdl(PullMultiKernel<VB, 2, __nv_bfloat16>, h.blocks, 256, 0, s, seg, h.n, sync);         \
+  else if (VB >= 4) LaunchPdl(PullMultiKernel<(VB >= 4 ? VB : 4), 2, float>, h.blocks, 256, 0, s, seg, h.n, sync);
   switch (h.vb) {
     case 16: RH_MULTI(16) break;
     case 8: RH_MULTI(8) break;

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include "common.h"
+#include "ew_defs.h"
 
 namespace rh {
 
@@ -121,12 +122,6 @@ void LaunchSynthetic(void* dst, const ComposedMap& m, int64_t n, uint64_t seed, 
 
 // ----------------------------------------- local ops -----------------------------------------
 constexpr int kMaxChain = 64;
-// bf16 only: a run of k consecutive tanh ops is one lookup in the table of T^k, T = the
-// correctly rounded bf16 tanh (bf16 has 2^16 inputs; T^k composes the per-op-rounded
-// semantics exactly).  fns[i] = kFnTanhRun + j selects table j.
-constexpr int kFnTanhRun = 100;
-constexpr int kMaxTanhRuns = 4;
-constexpr int kTanhRunEntries = 897;  // 896 table binades [2^-5, 4) + the |x| >= 4 constant
 struct ChainArgs {
   int32_t n_fn;
   int32_t fns[kMaxChain];
@@ -153,43 +148,20 @@ void LaunchSoftmaxRows(void* out, const void* in, int64_t rows, int64_t cols, in
 //   TBWD k          keep = acc; acc = keep + -((acc * in[k]) * in[k])  — the backward of tanh
 //                   (peephole of KEEP, MUL k, MUL k, UNARY neg, ADD keep; same roundings)
 // Every op result is rounded to the program dtype, as in the one-op-per-kernel path.
-constexpr int kMaxEwIn = 8, kMaxEwOut = 16, kMaxEwCode = 192;
-enum EwOpcode : int32_t { kEwLoad = 0, kEwUnary = 1, kEwAdd = 2, kEwMul = 3, kEwKeep = 4, kEwStore = 5,
-                          kEwTanhBwd = 6, kEwTanhBwdLad = 7 };
-// kEwTanhBwdLad (rematerializing programs): a run of TBWD on ladder columns hi, hi-1, ..,
-// hi-cnt+1 (arg = hi | cnt << 4), unrolled over compile-time columns.
-constexpr int kEwSrcKeep = 30, kEwSrcAcc = 31;
 inline int32_t EwIns(int op, int arg) { return op | (arg << 8); }
-struct EwArgs {
-  int32_t n_code, n_in;
-  int32_t code[kMaxEwCode];
-  const void* in[kMaxEwIn];
-  void* out[kMaxEwOut];
-  int32_t n_tab;
-  uint64_t tab_off[kMaxTanhRuns];     // arena offsets (host side)
-  const uint16_t* tab[kMaxTanhRuns];  // device pointers, patched per rank at launch
-  int64_t n;
-  // tanh ladder (bf16): code[lad_pc..] is only tanh runs and stores.  Store s of the suffix
-  // holds T^{c_s}(x0) with x0 = acc at lad_pc, so the vector path reads all lad_n outputs of an
-  // element from one 32-byte row of the ladder table (TanhLadderTable) instead of walking the
-  // chain one lookup per op.  lad_n = 0: no ladder.
-  int32_t lad_pc, lad_n;
-  int32_t lad_out[kMaxEwOut];
-  uint64_t lad_off;  // arena offset (host side)
-  const uint4* lad;  // device pointer, patched per rank at launch
-  // rematerialized operands (bf16): operand kEwSrcVirt + s = T^{powers[s]}(in[vlad_in]), read
-  // from column s of a ladder table (the forward tanh values the backward would otherwise load;
-  // the table composes the per-op rounding, so the value is bit-identical).  vlad_n = 0: none.
-  int32_t vlad_in, vlad_n;
-  uint64_t vlad_off;  // arena offset (host side)
-  const uint4* vlad;  // device pointer, patched per rank at launch
-};
-constexpr int kEwSrcVirt = 32;
-// Ladder rows: kTanhRunEntries rows x kLadderWidth u16; row r, column s = T^{powers[s]} of the
-// row's representative |x| (the TanhRunTable indexing).
-constexpr int kLadderWidth = 16;
 void TanhLadderTable(const int* powers, int n, uint16_t* out);
 void LaunchEwProg(const EwArgs& a, int dtype, cudaStream_t s);
+// Kernel family a program runs in (LaunchEwProg's choice; the JIT compiles the same family).
+enum EwKind { kEwKindF32 = 0, kEwKindBf16 = 1, kEwKindRematHalf = 2, kEwKindRematFull = 3, kEwKindLadder = 4,
+              kEwKindLadderRemat = 5 };
+int EwKindOf(const EwArgs& a, int dtype);
+// Per-program kernels (ew_jit.cpp): EwJitRegister returns the EwArgs::jit value for a program
+// (0 when RH_EW_JIT=0); EwJitBuild compiles every registered, not yet compiled program with
+// NVRTC (one call per executor build); EwJitLaunch launches a's compiled kernel and returns
+// false when there is none (compile failure: the interpreter kernel runs instead).
+int32_t EwJitRegister(const EwArgs& a, int dtype);
+void EwJitBuild();
+bool EwJitLaunch(const EwArgs& a, int blocks, size_t smem, cudaStream_t s);
 // out = a (+|*) b, then an optional unary chain (epilogue fusion).
 void LaunchBinary(void* out, const void* a, const void* b, int64_t n, bool mul, const ChainArgs& c,
                   int dtype, cudaStream_t s);

@@ -17,6 +17,7 @@
 #include <utility>
 
 #include "kernels.h"
+#include "pdl.cuh"
 
 namespace rh {
 
@@ -37,8 +38,5 @@ inline void LaunchPdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sm
   }
   RH_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
-
-__device__ __forceinline__ void PdlTrigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void PdlWait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 }  // namespace rh

@@ -9,9 +9,12 @@
 // ones except in rare boundary cases.
 #pragma once
 
+#ifndef __CUDACC_RTC__  // (NVRTC: ew_jit.cpp's prelude provides these)
 #include <cuda_bf16.h>
 
+#include "ew_defs.h"
 #include "rhino_exec.h"
+#endif
 
 namespace rh {
 
