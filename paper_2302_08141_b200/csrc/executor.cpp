@@ -378,6 +378,7 @@ class Lowerer {
     }
     EmitApply();
     if (p_->gemm_scratch_bytes) p_->gemm_scratch_off = Alloc(p_->gemm_scratch_bytes);
+    p_->gemm_flags_off = Alloc(kGemmSkFlagBytes);
     if (p_->n_sync_slots) {
       p_->sync_off = Alloc(static_cast<size_t>(p_->n_sync_slots) * rt_->world * 4);
       p_->epoch_off = Alloc(4);
@@ -1937,6 +1938,7 @@ class Lowerer {
         // fp32 GEMMs run as 3xTF32 and need split scratch: one region shared by all GEMMs of the
         // program (stream-ordered), sized to the largest and placed at the end of lowering.
         if (dtype == RH_F32) g.scratch = reinterpret_cast<void*>(uintptr_t{256});  // support probe
+        g.sk_flags = reinterpret_cast<uint32_t*>(uintptr_t{256});  // stream-K allowed (flags at run)
         const bool tc = !(P->flags & RH_FLAG_SIMT_GEMM) && GemmTcSupported(g);
         if (tc) P->gemm_scratch_bytes = std::max(P->gemm_scratch_bytes, GemmTcScratchBytes(g));
         if (!tc) P->gemm_scratch_bytes = std::max(P->gemm_scratch_bytes, GemmSimtScratchBytes(g));
@@ -1953,6 +1955,7 @@ class Lowerer {
           a.c = P->Ptr(P->tensors[out_t], r);
           a.epi = Patch(P, g.epi, r);
           if (P->gemm_scratch_bytes) a.scratch = P->peer_base[r] + P->gemm_scratch_off;
+          a.sk_flags = reinterpret_cast<uint32_t*>(P->peer_base[r] + P->gemm_flags_off);
           if (!tc) return LaunchGemmSimt(a, s);  // (+ split-K reduce for small M)
           LaunchGemmTc(a, s);
           return GemmTcLaunches(a);

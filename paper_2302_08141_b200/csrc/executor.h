@@ -131,7 +131,8 @@ struct rh_program {
   bool ipc_opened = false;
   std::vector<void*> owned;      // device allocations to free (per distinct device)
   std::vector<std::pair<size_t, std::vector<char>>> uploads;  // constant data (arena offset, bytes)
-  size_t gemm_scratch_bytes = 0, gemm_scratch_off = 0;  // 3xTF32 split scratch (shared)
+  size_t gemm_scratch_bytes = 0, gemm_scratch_off = 0;  // 3xTF32 / split-K / stream-K scratch (shared)
+  size_t gemm_flags_off = 0;                             // stream-K flags (kGemmSkFlagBytes, zeroed)
   void* graph = nullptr;  // cudaGraphExec_t of one captured run (single-stream runtimes)
   // overlap (dist): side stream for async transitions + its own barrier state
   int n_async = 0;

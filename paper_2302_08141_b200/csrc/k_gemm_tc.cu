@@ -15,6 +15,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -508,6 +509,69 @@ __device__ __forceinline__ void CommitPair(uint64_t* bar) {
       : "memory");
 }
 
+// Work units of one CTA pair.  Tile stepping: output tiles pair, pair + n_pairs, .. (tile index
+// includes the split-K index), all k-blocks of each.  Stream-K: the tiles' mn * kbt k-block
+// iterations are cut into n_pairs contiguous ranges, so every pair runs the same number of
+// k-blocks whatever the wave quantization; a range starts and ends inside tiles.  A unit
+// [k0, k1) of a tile with k0 > 0 (at most one per pair: its first) is a contributor: fp32
+// partial accumulator to the pair's workspace slot, then a flag; the unit with k0 == 0 of a
+// split tile (the pair's last) finishes it: waits for the later pairs that contribute to the
+// tile (their first units, so no wait cycle), adds their partials in pair order, and runs the
+// epilogue.  All pairs are co-resident (grid <= cudaOccupancyMaxActiveClusters).
+struct PairWork {
+  int64_t g, end;  // stream-K: [g, end) of the mn * kbt iterations
+  int next, step, tiles, kbt;
+  bool sk;
+};
+__device__ __forceinline__ int64_t SkStart(int pair, int n_pairs, int64_t total) { return total * pair / n_pairs; }
+__device__ __forceinline__ PairWork PairWorkOf(int pair, int n_pairs, int tiles, int kbt, bool sk) {
+  PairWork w;
+  w.sk = sk;
+  w.kbt = kbt;
+  w.next = pair;
+  w.step = n_pairs;
+  w.tiles = tiles;
+  const int64_t total = static_cast<int64_t>(tiles) * kbt;
+  w.g = SkStart(pair, n_pairs, total);
+  w.end = SkStart(pair + 1, n_pairs, total);
+  return w;
+}
+__device__ __forceinline__ bool NextPairWork(PairWork& w, int& tile, int& k0, int& k1) {
+  if (w.sk) {
+    if (w.g >= w.end) return false;
+    tile = static_cast<int>(w.g / w.kbt);
+    k0 = static_cast<int>(w.g - static_cast<int64_t>(tile) * w.kbt);
+    k1 = static_cast<int>(min(static_cast<int64_t>(w.kbt), k0 + (w.end - w.g)));
+    w.g += k1 - k0;
+    return true;
+  }
+  if (w.next >= w.tiles) return false;
+  tile = w.next;
+  w.next += w.step;
+  k0 = 0;
+  k1 = w.kbt;
+  return true;
+}
+__device__ __forceinline__ uint32_t LdAcquireGpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Bounded wait for a stream-K contributor (a schedule bug must not hang the GPU).
+__device__ __forceinline__ void SkWaitFlag(const uint32_t* f) {
+  if (LdAcquireGpu(f)) return;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (uint32_t n = 1;; ++n) {
+    if (LdAcquireGpu(f)) return;
+    if ((n & 1023) == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 5000000000ull) __trap();
+    }
+  }
+}
+
 // kEpi = epilogue warps: 4, or 8 for short-K GEMMs whose epilogue is the critical path (the
 // 32-head block's K = 128 score GEMMs, each output through a T^14 lookup): two warps per TMEM
 // lane quarter, alternate 32-column chunks; one pipeline stage less pays for their staging.
@@ -530,7 +594,7 @@ template <int BN, bool kBKMajor, bool kAKMajor, bool kGroup = false, int kEpi = 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpi, 1)
     GemmTcPairKernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                      const __grid_constant__ CUtensorMap tma_c, int M, int N, int K, ChainArgs epi, int ksplit,
-                     float* __restrict__ ws, GroupDev grp) {
+                     float* __restrict__ ws, GroupDev grp, uint32_t* __restrict__ sk_flags) {
   PdlTrigger();
   using Cfg = Tc2Cfg<BN, kBKMajor, kAKMajor, kEpi>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -547,6 +611,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpi, 1)
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
   const int num_m = M / (2 * BM), num_n = N / BN, mn = num_m * num_n, tiles = mn * ksplit;
   const int kblocks = K / BK / ksplit;
+  const bool sk = sk_flags != nullptr;  // stream-K (ksplit == 1; ws = the pairs' partial slots)
 
   if (warp == 0 && lane == 0) {
     if (!kGroup) {
@@ -578,7 +643,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpi, 1)
     if (lane == 0) {  // ---------------- TMA producer (both CTAs) ----------------
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = pair; tile < tiles; tile += n_pairs) {
+      PairWork w = PairWorkOf(pair, n_pairs, tiles, kblocks, sk);
+      int tile, k0, k1;
+      while (NextPairWork(w, tile, k0, k1)) {
         const int t = tile % mn, ks = tile / mn;
         const int m_blk = t % num_m, n_blk = t / num_m;
         const int m0 = m_blk * 2 * BM + static_cast<int>(rank) * BM;
@@ -599,7 +666,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpi, 1)
         if constexpr (kGroup) {
           if (grp.a) ma = grp.a + (n_blk * BN) / grp.seg_n;
         }
-        for (int kb = ks * kblocks; kb < (ks + 1) * kblocks; ++kb) {
+        for (int kb = ks * kblocks + k0; kb < ks * kblocks + k1; ++kb) {
           MbarWait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::kStage;
           uint8_t* sb = sa + Cfg::kABytes;
@@ -628,11 +695,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpi, 1)
     if (lane == 0 && leader) {  // ---------------- MMA issuer (leader) ----------------
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
-      for (int tile = pair; tile < tiles; tile += n_pairs) {
+      PairWork w = PairWorkOf(pair, n_pairs, tiles, kblocks, sk);
+      int tile, k0, k1;
+      while (NextPairWork(w, tile, k0, k1)) {
         MbarWaitCluster(&tempty[acc], acc_phase ^ 1);
         FenceAfter();
         const uint32_t d_tmem = tmem + acc * BN;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = 0; kb < k1 - k0; ++kb) {
           MbarWait(&full[stage], phase);
           FenceAfter();
           const uint32_t sa = SmemU32(smem + stage * Cfg::kStage);
@@ -668,18 +737,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpi, 1)
     uint32_t boxes = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = pair; tile < tiles; tile += n_pairs) {
+    PairWork w = PairWorkOf(pair, n_pairs, tiles, kblocks, sk);
+    const int64_t sk_total = static_cast<int64_t>(tiles) * kblocks;
+    constexpr int kSlot = BM * BN;  // floats per CTA slot: [BN/32 chunks][128 rows][32]
+    int tile, k0, k1;
+    while (NextPairWork(w, tile, k0, k1)) {
       const int t = tile % mn, ks = tile / mn;
       const int m_blk = t % num_m, n_blk = t / num_m;
+      const bool contrib = sk && k0 > 0, finish = sk && k0 == 0 && k1 < kblocks;
+      // contributors of a finished tile: the next pairs whose ranges start inside it
+      int cp_end = pair + 1;
+      if (finish) {
+        const int64_t tile_end = static_cast<int64_t>(tile + 1) * kblocks;
+        while (cp_end < n_pairs && SkStart(cp_end, n_pairs, sk_total) < tile_end) ++cp_end;
+        if (lane == 0)
+          for (int cp = pair + 1; cp < cp_end; ++cp) SkWaitFlag(sk_flags + 2 * cp + rank);
+        __syncwarp();
+      }
       MbarWait(&tfull[acc], acc_phase);
       FenceAfter();
       const int row0 = m_blk * 2 * BM + static_cast<int>(rank) * BM + quarter * 32;
       const int row = row0 + lane;
-      float* wrow = ws ? ws + (static_cast<int64_t>(ks) * M + row) * N + n_blk * BN : nullptr;
+      float* wrow = ws && !sk ? ws + (static_cast<int64_t>(ks) * M + row) * N + n_blk * BN : nullptr;
 #pragma unroll 1
       for (int c = half; c < BN / 32; c += kEpi / 4) {
         uint32_t r[32];
         TmemLd32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c * 32, r);
+        const int64_t so = (static_cast<int64_t>(c) * BM + quarter * 32 + lane) * 32;
+        if (contrib) {
+          float4* dst = reinterpret_cast<float4*>(ws + static_cast<int64_t>(2 * pair + rank) * kSlot + so);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                 __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+          continue;
+        }
+        if (finish) {
+          for (int cp = pair + 1; cp < cp_end; ++cp) {
+            const float4* src = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(2 * cp + rank) * kSlot + so);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 v = src[q];
+              r[4 * q] = __float_as_uint(__uint_as_float(r[4 * q]) + v.x);
+              r[4 * q + 1] = __float_as_uint(__uint_as_float(r[4 * q + 1]) + v.y);
+              r[4 * q + 2] = __float_as_uint(__uint_as_float(r[4 * q + 2]) + v.z);
+              r[4 * q + 3] = __float_as_uint(__uint_as_float(r[4 * q + 3]) + v.w);
+            }
+          }
+        }
         if (wrow) {
           float4* dst = reinterpret_cast<float4*>(wrow + c * 32);
 #pragma unroll
@@ -706,6 +811,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpi, 1)
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
+      }
+      if (contrib || finish) {
+        if (contrib) __threadfence();  // this thread's partials, before the flag (below)
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * kEpi) : "memory");  // the epilogue warps
+        if (threadIdx.x == 128) {
+          if (contrib) {
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(sk_flags + 2 * pair + rank), "r"(1u) : "memory");
+          } else {  // consumed: re-arm the contributors' flags for the next stream-K GEMM
+            for (int cp = pair + 1; cp < cp_end; ++cp) sk_flags[2 * cp + rank] = 0;
+          }
+        }
       }
     }
     if (lane == 0) BulkWaitAll();
@@ -1089,6 +1205,53 @@ int KSplitPair(const GemmArgs& g, int bn) {
   return best;
 }
 
+// Stream-K for the CTA-pair kernel (opt-in: RH_GEMM_STREAMK=1): when whole pair tiles leave
+// >= 8% of the pairs idle in the last wave (e.g. 128 tiles on 74 pairs: 1.73 waves run as 2),
+// and every pair still gets >= 16 k-blocks.  Needs the caller's flags and scratch
+// (StreamKScratchBytes).  Measured slower than the tile-stepping schedule on every C3/C5 shape
+// (profiles/r2/streamk_ab.txt): without the fixup the k-balanced main loop is 10-16% faster
+// (2048^3: 14.4 -> 13.2 us class), but the finisher's partial reads run in the 4-warp
+// epilogue's serial chunk loop (128 KB per CTA and contributor, L2-latency-bound: +8 us) and the
+// contributors' writes +5 us; long-K shapes also lose the L2 reuse of the lock-step k order
+// (2048x16384x4096: 183 -> 272 us).
+int StreamKPairs() { return NumSms() / 2; }
+bool UseStreamK(const GemmArgs& g) {
+  static const int on = EnvInt("RH_GEMM_STREAMK", 0);
+  if (!on || !g.sk_flags || !UsePair(g) || g.n % 256) return false;
+  const int64_t tiles = (g.m / (2 * BM)) * (g.n / 256), kb = g.k / BK, pairs = StreamKPairs();
+  const int64_t waves = (tiles + pairs - 1) / pairs;
+  if (tiles * 100 >= waves * pairs * 92) return false;
+  return tiles * kb >= pairs * 16;
+}
+size_t StreamKScratchBytes() { return static_cast<size_t>(2 * StreamKPairs()) * BM * 256 * 4; }
+
+// Pairs of the CTA-pair kernel that can be resident at once (stream-K requires co-residency:
+// a finishing pair waits for later pairs' partials).  Cached per device.
+template <int BN, bool kBK, bool kAK, bool kG, int kEpi>
+int MaxPairs() {
+  static int cache[64] = {};
+  int dev = 0;
+  RH_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && cache[dev]) return cache[dev];
+  using Cfg = Tc2Cfg<BN, kBK, kAK, kEpi>;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * StreamKPairs());
+  cfg.blockDim = dim3(128 + 32 * kEpi);
+  cfg.dynamicSmemBytes = Cfg::kSmem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  RH_CUDA(cudaOccupancyMaxActiveClusters(&n, GemmTcPairKernel<BN, kBK, kAK, kG, kEpi>, &cfg));
+  n = std::max(1, std::min(n, StreamKPairs()));
+  if (dev < 64) cache[dev] = n;
+  return n;
+}
+
 // A grouped launch (GemmTcGroup): problem 0's maps as the kernel-param maps (the shared A),
 // the device table, and the problem count.
 struct GroupLaunch {
@@ -1149,10 +1312,19 @@ void LaunchPair(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullp
   }
   const Maps& mp = kG ? gl->m0 : GetMaps(g, BN / 2);  // B box: half of the pair's columns per CTA
   const int64_t n = kG ? g.n * gl->n_prob : g.n;
-  const int ks = g.scratch && !kG ? KSplitPair(g, BN) : 1;
+  const bool sk = !kG && UseStreamK(g);
+  if (sk && !g.scratch) Fail("internal: stream-K GEMM without scratch (GemmTcScratchBytes)");
+  const int ks = g.scratch && !kG && !sk ? KSplitPair(g, BN) : 1;
   const int tiles = static_cast<int>((g.m / (2 * BM)) * (n / BN)) * ks;
-  const int pairs = std::min(tiles, NumSms() / 2);
-  float* ws = ks > 1 ? static_cast<float*>(g.scratch) : nullptr;
+  int pairs = std::min(tiles, NumSms() / 2);
+  if (sk) {
+    static const int force = EnvInt("RH_GEMM_SK_PAIRS", 0);
+    pairs = std::min<int64_t>(int64_t{tiles} * (g.k / BK), force ? force : MaxPairs<BN, kBK, kAK, kG, kEpi>());
+    static const int dbg = EnvInt("RH_GEMM_SK_DEBUG", 0);
+    if (dbg) fprintf(stderr, "[stream-k] m %lld n %lld k %lld tiles %d pairs %d (max %d)\n", (long long)g.m,
+                     (long long)g.n, (long long)g.k, tiles, pairs, MaxPairs<BN, kBK, kAK, kG, kEpi>());
+  }
+  float* ws = ks > 1 || sk ? static_cast<float*>(g.scratch) : nullptr;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(128 + 32 * kEpi);
@@ -1169,8 +1341,8 @@ void LaunchPair(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullp
   cfg.numAttrs = PdlEnabled() ? 2 : 1;
   RH_CUDA(cudaLaunchKernelEx(&cfg, GemmTcPairKernel<BN, kBK, kAK, kG, kEpi>, mp.a, mp.b, mp.c,
                              static_cast<int>(g.m), static_cast<int>(n), static_cast<int>(g.k), g.epi, ks, ws,
-                             kG ? gl->dev : GroupDev{}));
-  if (ws) {
+                             kG ? gl->dev : GroupDev{}, sk ? g.sk_flags : nullptr));
+  if (ws && !sk) {
     const int64_t n4 = g.m * g.n / 4;
     const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, SmCount() * 8)));
     LaunchPdl(SplitReduceBf16, blocks, 256, 0, s, static_cast<__nv_bfloat16*>(g.c), reinterpret_cast<const float4*>(ws),
@@ -1254,6 +1426,7 @@ namespace {
 struct Sched {
   bool pair;
   int bn, ks;
+  bool sk = false;  // stream-K (pair kernel)
 };
 // Measured (profiles/gemm_shapes.py, B200, bf16): the CTA-pair kernel with 256 x 256 pair
 // tiles wins once they fill a wave (2048x4096 output, K 4096: 46.8 vs 49.4 us; K 16384: 174 vs
@@ -1261,6 +1434,7 @@ struct Sched {
 // 77 us); below a wave, and with 256 x 128 pair tiles, the single-CTA kernel is faster (2048^3:
 // 14.7 vs 15.6 us; 512x4096 output, K 4096: 19.3 vs 23.4 us).
 Sched ScheduleOf(const GemmArgs& g) {
+  if (UseStreamK(g)) return {true, 256, 1, true};
   if (UsePair(g) && g.n % 256 == 0) {
     static const int force = EnvInt("RH_GEMM_BN", 0);
     const int64_t ctas = (g.m / BM) * (g.n / 256);
@@ -1276,6 +1450,7 @@ Sched ScheduleOf(const GemmArgs& g) {
 size_t GemmTcScratchBytes(const GemmArgs& g) {
   if (g.dtype == RH_F32) return GemmTf32x3ScratchBytes(g);
   const Sched sc = ScheduleOf(g);
+  if (sc.sk) return StreamKScratchBytes();
   return sc.ks > 1 ? static_cast<size_t>(sc.ks) * g.m * g.n * 4 : 0;
 }
 
@@ -1297,6 +1472,7 @@ bool GemmTcSupported(const GemmArgs& g) {
 const char* GemmTcSchedule(const GemmArgs& g) {
   if (g.dtype == RH_F32) return "";
   const Sched sc = ScheduleOf(g);
+  if (sc.sk) return " [pair, stream-k]";
   if (sc.pair) return sc.ks > 1 ? " [pair, split-k]" : " [pair]";
   return sc.ks > 1 ? " [split-k]" : "";
 }

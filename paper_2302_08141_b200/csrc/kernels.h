@@ -207,7 +207,12 @@ struct GemmArgs {
   // fp32 tensor-core path (3xTF32): device scratch for the hi/lo splits of A and B
   // (GemmTf32x3ScratchBytes bytes, reused by every GEMM of a program: they run in stream order).
   void* scratch = nullptr;
+  // bf16 stream-K (CTA-pair kernel): kGemmSkFlagBytes of zeroed flags, owned by the caller and
+  // left zeroed by every launch; the partial accumulators live in `scratch`.  nullptr: no
+  // stream-K.
+  uint32_t* sk_flags = nullptr;
 };
+constexpr size_t kGemmSkFlagBytes = 4096;
 size_t GemmTf32x3ScratchBytes(const GemmArgs& g);
 // Scratch the tensor-core path wants for this GEMM (3xTF32 splits, or bf16 split-K partials).
 size_t GemmTcScratchBytes(const GemmArgs& g);
