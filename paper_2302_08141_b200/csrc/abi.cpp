@@ -187,14 +187,15 @@ int64_t RunOnce(rh_program* p, std::vector<cudaEvent_t>* prof) {
       continue;
     }
     if (st.p2p && st.sync_slot < 0) GroupSync(p, st.axis);
-    // PDL (launch.cuh) after a compute kernel only: for the next compute kernel, and for a
-    // peer-memory pull (its CTAs become resident while the producer drains and publish their
-    // arrival at the fused barrier as soon as griddepcontrol.wait returns).  Never after a
-    // transition (a kernel must not wait on a grid whose CTAs spin on peers), a cross-stream
-    // join or a profiling event; RH_PDL_PULL=0 keeps pulls on plain launches.
+    // PDL (launch.cuh) after a compute kernel only: for the next compute kernel, and (opt-in,
+    // RH_PDL_PULL=1) for a peer-memory pull, whose CTAs then become resident while the producer
+    // drains and publish their arrival at the fused barrier as soon as griddepcontrol.wait
+    // returns (measured: no change at N=2/4, profiles/r2/README).  Never after a transition (a
+    // kernel must not wait on a grid whose CTAs spin on peers), a cross-stream join or a
+    // profiling event.
     static const bool pdl_pull = [] {
       const char* e = std::getenv("RH_PDL_PULL");
-      return !(e && e[0] == '0');
+      return e && e[0] == '1';
     }();
     const bool pdl = !(p->flags & RH_FLAG_NO_PDL) && !prof && prev_kernel && p->joins_at[si].empty() &&
                      (st.kind == rh::Step::kKernel ||
