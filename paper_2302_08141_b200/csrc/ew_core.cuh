@@ -298,12 +298,15 @@ __device__ __forceinline__ void EwStep(const EwArgs& a, int64_t i, const uint16_
 }
 
 // Loads vector i's inputs (kExact: exactly kIn inputs, else the first a.n_in <= kIn) and, for
-// rematerializing programs, the base's ladder rows; clears acc / keep.
-template <bool kBf16, bool kRemat, bool kHalf, int kIn, bool kExact>
+// rematerializing programs, the base's ladder rows; clears acc / keep.  kPre: the inputs are
+// already in v.raw (loaded one iteration ahead).
+template <bool kBf16, bool kRemat, bool kHalf, int kIn, bool kExact, bool kPre = false>
 __device__ __forceinline__ void EwVecBegin(const EwArgs& a, int64_t i, const uint4* vlad_s, EwVec<kIn>& v) {
+  if constexpr (!kPre) {
 #pragma unroll
-  for (int k = 0; k < kIn; ++k)
-    if (kExact || k < a.n_in) v.raw[k] = reinterpret_cast<const uint4*>(a.in[k])[i];
+    for (int k = 0; k < kIn; ++k)
+      if (kExact || k < a.n_in) v.raw[k] = reinterpret_cast<const uint4*>(a.in[k])[i];
+  }
   v.vbase = make_uint4(0, 0, 0, 0);
   if constexpr (kBf16 && kRemat) {
     v.vbase = EwPickN<kIn>(v.raw, a.vlad_in);
@@ -385,6 +388,24 @@ __device__ __noinline__ void EwRunScalar(const EwArgs& a, int64_t i, const uint1
   }
 }
 
+// Block-wide copy of n table entries global -> shared with every thread's loads issued before
+// its stores (the tables are L2-resident: one round trip instead of n / blockDim dependent ones).
+// Assumes blockDim.x == 256 and n <= 8 * 256.
+template <typename T>
+__device__ __forceinline__ void StageTable(T* __restrict__ dst, const T* __restrict__ src, int n, int src_stride = 1) {
+  T v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int i = threadIdx.x + j * 256;
+    if (i < n) v[j] = src[static_cast<int64_t>(i) * src_stride];
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int i = threadIdx.x + j * 256;
+    if (i < n) dst[i] = v[j];
+  }
+}
+
 // Kernel body of a chain program: stage the tanh-run tables (and the rematerialization ladder)
 // in shared memory, then one vector per thread-iteration through `prog` (EwInterp, or a
 // specialized instruction sequence), then the scalar tail.
@@ -395,12 +416,10 @@ __device__ __forceinline__ void EwProgBody(const EwArgs& a, const Prog& prog) {
   extern __shared__ uint4 vlad_s[];  // rematerialization ladder (vlad_n > 0); kHalf: half rows
   if constexpr (kBf16) {
     for (int t = 0; t < a.n_tab; ++t)
-      for (int i = threadIdx.x; i < kTanhRunEntries; i += blockDim.x) tab_s[t * kTanhRunEntries + i] = a.tab[t][i];
+      StageTable(tab_s + t * kTanhRunEntries, a.tab[t], kTanhRunEntries);
     if (kRemat) {
-      if (kHalf)
-        for (int i = threadIdx.x; i < kTanhRunEntries; i += blockDim.x) vlad_s[i] = a.vlad[2 * i];
-      else
-        for (int i = threadIdx.x; i < kTanhRunEntries * 2; i += blockDim.x) vlad_s[i] = a.vlad[i];
+      if (kHalf) StageTable(vlad_s, a.vlad, kTanhRunEntries, 2);
+      else StageTable(vlad_s, a.vlad, kTanhRunEntries * 2);
     }
     __syncthreads();
   }
@@ -408,6 +427,42 @@ __device__ __forceinline__ void EwProgBody(const EwArgs& a, const Prog& prog) {
   constexpr int E = kBf16 ? 8 : 4;
   const int64_t nv = a.n / E;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+#ifndef RH_EW_PAIR_VECTORS
+#define RH_EW_PAIR_VECTORS 1
+#endif
+  if constexpr (kExact && !kRemat && kIn <= 4 && RH_EW_PAIR_VECTORS) {
+    // specialized programs with few inputs: two vectors per iteration, the second one's inputs
+    // loaded before the first one's program runs (two loads per input in flight per thread;
+    // measured -5..10% on the C5 forward chains, neutral on the rematerializing ones, whose
+    // ladder rows double the live registers: profiles/r2/ew_jit_c5.txt)
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nv; i += 2 * stride) {
+      const int64_t i2 = i + stride;
+      uint4 nxt[kIn];
+      if (i2 < nv) {
+#pragma unroll
+        for (int k = 0; k < kIn; ++k) nxt[k] = reinterpret_cast<const uint4*>(a.in[k])[i2];
+      }
+      if constexpr (kRemat) {
+        const int64_t nx = i + 2 * stride;
+        if (nx < nv)
+#pragma unroll
+          for (int k = 0; k < kIn; ++k)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint4*>(a.in[k]) + nx));
+      }
+      {
+        EwVec<kIn> v;
+        EwVecBegin<kBf16, kRemat, kHalf, kIn, kExact>(a, i, vlad_s, v);
+        prog(a, i, tab_s, v);
+      }
+      if (i2 < nv) {
+        EwVec<kIn> v;
+#pragma unroll
+        for (int k = 0; k < kIn; ++k) v.raw[k] = nxt[k];
+        EwVecBegin<kBf16, kRemat, kHalf, kIn, kExact, true>(a, i2, vlad_s, v);
+        prog(a, i2, tab_s, v);
+      }
+    }
+  } else {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nv; i += stride) {
     if constexpr (kRemat) {
       // few warps per SM: L2-prefetch the next iteration's vectors so their loads do not wait
@@ -420,6 +475,7 @@ __device__ __forceinline__ void EwProgBody(const EwArgs& a, const Prog& prog) {
     EwVec<kIn> v;
     EwVecBegin<kBf16, kRemat, kHalf, kIn, kExact>(a, i, vlad_s, v);
     prog(a, i, tab_s, v);
+  }
   }
   for (int64_t i = nv * E + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < a.n; i += stride)
     EwRunScalar<kBf16>(a, i, tab_s);
@@ -436,11 +492,11 @@ __device__ __forceinline__ void EwLadderBody(const EwArgs& a, const Prog& prog) 
   extern __shared__ uint4 lad_s[];  // kTanhRunEntries rows x 2 uint4
   __shared__ uint16_t tab_s[kMaxTanhRuns * kTanhRunEntries];
   for (int t = 0; t < a.n_tab; ++t)
-    for (int i = threadIdx.x; i < kTanhRunEntries; i += blockDim.x) tab_s[t * kTanhRunEntries + i] = a.tab[t][i];
-  for (int i = threadIdx.x; i < kTanhRunEntries * 2; i += blockDim.x) lad_s[i] = a.lad[i];
+    StageTable(tab_s + t * kTanhRunEntries, a.tab[t], kTanhRunEntries);
+  StageTable(lad_s, a.lad, kTanhRunEntries * 2);
   uint4* vlad_s = lad_s + kTanhRunEntries * 2;  // rematerialization ladder (vlad_n > 0)
   if (kRemat)
-    for (int i = threadIdx.x; i < kTanhRunEntries * 2; i += blockDim.x) vlad_s[i] = a.vlad[i];
+    StageTable(vlad_s, a.vlad, kTanhRunEntries * 2);
   __syncthreads();
   PdlWait();
   constexpr uint32_t kLo = 122u << 7, kSpan = 0x7f80u - (122u << 7), kLast = kTanhRunEntries - 1;

@@ -88,7 +88,9 @@ std::string KernelSource(const JitEntry& e, int id) {
 }
 
 std::string Prelude() {
-  std::string s =
+  // RH_EW_PAIR=0: one vector per thread-iteration (A/B of EwProgBody's two-vector loop)
+  const char* pair = getenv("RH_EW_PAIR");
+  std::string s = std::string("#define RH_EW_PAIR_VECTORS ") + (pair && pair[0] == '0' ? "0" : "1") + "\n" +
       "#include <cuda_bf16.h>\n#include <cuda/std/cstdint>\n"
       "using cuda::std::int8_t; using cuda::std::uint8_t; using cuda::std::int16_t; using cuda::std::uint16_t;\n"
       "using cuda::std::int32_t; using cuda::std::uint32_t; using cuda::std::int64_t; using cuda::std::uint64_t;\n";
