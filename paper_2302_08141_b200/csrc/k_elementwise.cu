@@ -28,9 +28,7 @@ __device__ __forceinline__ float ApplyChain(const ChainArgs& c, float x) {
 // The chain's T^k tables (kernel arguments, arena-resident) staged into shared memory once per
 // block: n_tab x 897 x 2 bytes.
 __device__ __forceinline__ void LoadRunTables(const ChainArgs& c, uint16_t* smem) {
-  for (int t = 0; t < c.n_tab; ++t)
-    for (int i = threadIdx.x; i < kTanhRunEntries; i += blockDim.x)
-      smem[t * kTanhRunEntries + i] = c.tab[t][i];
+  for (int t = 0; t < c.n_tab; ++t) StageTable(smem + t * kTanhRunEntries, c.tab[t], kTanhRunEntries);
   __syncthreads();
 }
 
@@ -391,7 +389,10 @@ void LaunchUnaryChain(void* out, const void* in, int64_t n, const ChainArgs& c, 
                       cudaStream_t s) {
   if (n == 0) return;
   if (dtype == RH_BF16) {
-    LaunchPdl(UnaryChainKernel<true>, Blocks(n, 8), 256, 0, s, out, in, n, c);
+    // blocks that stage T^k tables: a persistent-ish grid, so each block's staging is amortized
+    // over several iterations (16 blocks per SM did ~1 vector pair per thread after staging)
+    const int blocks = c.n_tab ? std::min(Blocks(n, 16), SmCount() * 4) : Blocks(n, 8);
+    LaunchPdl(UnaryChainKernel<true>, blocks, 256, 0, s, out, in, n, c);
   } else {
     LaunchPdl(UnaryChainKernel<false>, Blocks(n, 4), 256, 0, s, out, in, n, c);
   }
@@ -442,7 +443,7 @@ void LaunchEwProg(const EwArgs& a, int dtype, cudaStream_t s) {
       blocks = std::min(Blocks(a.n, 8), SmCount() * 2);
       smem = kLadSmem;
       break;
-    case kEwKindBf16: blocks = Blocks(a.n, 8); break;
+    case kEwKindBf16: blocks = a.n_tab ? std::min(Blocks(a.n, 8), SmCount() * 4) : Blocks(a.n, 8); break;
     default: blocks = Blocks(a.n, 4);
   }
   if (a.jit && EwJitLaunch(a, blocks, smem, s)) return;
@@ -470,7 +471,8 @@ void LaunchBinary(void* out, const void* a, const void* b, int64_t n, bool mul, 
                   int dtype, cudaStream_t s) {
   if (n == 0) return;
   if (dtype == RH_BF16) {
-    LaunchPdl(BinaryKernel<true>, Blocks(n, 8), 256, 0, s, out, a, b, n, mul, c);
+    const int blocks = c.n_tab ? std::min(Blocks(n, 8), SmCount() * 4) : Blocks(n, 8);
+    LaunchPdl(BinaryKernel<true>, blocks, 256, 0, s, out, a, b, n, mul, c);
   } else {
     LaunchPdl(BinaryKernel<false>, Blocks(n, 4), 256, 0, s, out, a, b, n, mul, c);
   }
