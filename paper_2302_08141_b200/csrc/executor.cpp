@@ -349,7 +349,7 @@ class Lowerer {
         continue;
       }
       EmitOp(i);
-      if (eager) EagerTransitions(chain_[i].empty() ? i : chain_[i].back());
+      if (eager) EagerTransitions(Tail(i));
     }
     if ((p_->flags & RH_FLAG_REDUCE_OUTPUTS) && !(p_->flags & RH_FLAG_NO_MATERIALIZE)) {
       // training-step outputs: reduce Partial axes (the gradient all-reduce / reduce of a
@@ -914,6 +914,7 @@ class Lowerer {
     const int n = static_cast<int>(p_->ops.size());
     absorbed_.assign(n, false);
     chain_.assign(n, {});
+    resid_.assign(n, Resid{});
     if (p_->flags & RH_FLAG_NO_FUSION) return;
     std::vector<int> uses(n, 0);
     std::vector<int> consumer(n, -1);
@@ -936,6 +937,8 @@ class Lowerer {
         if (x.kind == RH_PARTIAL) return false;
       return true;
     };
+    std::vector<int> pos(n, 0);
+    for (size_t k = 0; k < p_->order.size(); ++k) pos[p_->order[k]] = static_cast<int>(k);
     for (int h : p_->order) {
       const rh_op& op = p_->ops[h];
       if (op.kind != RH_OP_MATMUL || absorbed_[h]) continue;  // elementwise heads: PlanEwChains
@@ -981,6 +984,26 @@ class Lowerer {
       if (op.kind == RH_OP_MATMUL && !epi_ok) {
         for (int v : chain_[h]) absorbed_[v] = false;
         chain_[h].clear();
+      }
+      // Residual add after the GEMM (and its epilogue chain): bf16, the add's other operand in
+      // the same layout, no other reader of the pre-add value -> the GEMM's epilogue adds it
+      // (GemmArgs::resid; the separate add kernel re-read the GEMM output from HBM).
+      static const bool no_resid = getenv("RH_NO_RESID_FUSION") != nullptr;  // A/B knob
+      const int t = chain_[h].empty() ? h : chain_[h].back();
+      if (!no_resid && op.dtype == RH_BF16 && uses[t] == 1 && !is_out[t] &&
+          (group_of_.empty() || group_of_[h] < 0)) {
+        const int v = consumer[t];
+        const rh_op& a = p_->ops[v];
+        if (a.kind == RH_OP_ADD && a.dtype == op.dtype && SameTask(v, h) && p_->inputs[v].size() == 2) {
+          const int slot = p_->inputs[v][0] == t ? 1 : 0;
+          const int x = p_->inputs[v][slot];
+          if (x != t && pos[x] < pos[h] && SpecsEq(p_->in_specs[v][0], p_->out_specs[t]) && SpecsEq(p_->in_specs[v][1], p_->out_specs[t]) &&
+              SpecsEq(p_->out_specs[v], p_->out_specs[t]) && no_partial(p_->out_specs[t]) && natural_ok(t) &&
+              natural_ok(v) && GDims(x) == GDims(v) && GDims(v) == GDims(t)) {
+            resid_[h] = Resid{v, x, slot};
+            absorbed_[v] = true;
+          }
+        }
       }
     }
     PlanTransposeFold(uses, consumer, is_out);
@@ -1206,7 +1229,7 @@ class Lowerer {
     // rematerialized value: the pre-epilogue value does not exist)
     std::vector<bool> epi_tail(n, false);
     for (int h = 0; h < n; ++h)
-      if (!chain_[h].empty()) epi_tail[chain_[h].back()] = true;
+      if (Tail(h) != h) epi_tail[Tail(h)] = true;
     std::vector<int> base_of(n, -1), pow_of(n, 0);
     for (int m : p_->order) {
       if (!IsElementwiseUnary(m) || UnaryFn(m) != RH_FN_TANH || p_->ops[m].dtype != RH_BF16) continue;
@@ -1652,9 +1675,9 @@ class Lowerer {
     for (int s = 0; s < nin && s < 2; ++s)
       if (!fold_t_.empty() && fold_t_[i][s]) p_->in_tensor[i][s] = -1;  // not materialized
     const Specs nat = NaturalSpecs(i, p_->in_specs[i]);
-    const int tail = chain_[i].empty() ? i : chain_[i].back();
+    const int tail = Tail(i);
     const bool direct = SpecsEq(nat, p_->out_specs[i]);
-    if (!chain_[i].empty() && !direct) Fail("internal: fused head without a natural spec");
+    if (tail != i && !direct) Fail("internal: fused head without a natural spec");
     // Reshape: pass-through layouts keep the local buffer byte-identical -> alias, no kernel.
     if (op.kind == RH_OP_RESHAPE) {
       int t = NewTensor(i, nat, /*alloc=*/false);
@@ -1909,6 +1932,11 @@ class Lowerer {
     rh_program* P = p_;
     const rh_op& op = P->ops[i];
     const int first = rt_->first_rank;
+    // fused residual add operand (matmul, PlanFusion): fetched before T is referenced (GetTensor
+    // may emit transitions and grow the tensor table)
+    int resid_t = -1;
+    if (op.kind == RH_OP_MATMUL && !resid_.empty() && resid_[i].v >= 0)
+      resid_t = GetTensor(resid_[i].x, p_->in_specs[resid_[i].v][resid_[i].slot], "edge");
     const Tensor& T = P->tensors[out_t];
     const int dtype = op.dtype;
     const int eb = ElemBytes(dtype);
@@ -1931,6 +1959,13 @@ class Lowerer {
         g.n = etb ? bd[0] : bd[1];
         if ((etb ? bd[1] : bd[0]) != g.k) Fail("matmul " + id + ": local k mismatch");
         if (T.ldims[0] != g.m || T.ldims[1] != g.n) Fail("matmul " + id + ": local output shape mismatch");
+        if (resid_t >= 0) {  // fused residual add (PlanFusion)
+          const Resid& R = resid_[i];
+          if (P->tensors[resid_t].ldims != T.ldims) Fail("matmul " + id + ": residual shape mismatch");
+          p_->in_tensor[R.v].assign(2, -1);  // the pre-add operand is not materialized
+          p_->in_tensor[R.v][R.slot] = resid_t;
+          st.alg_bytes += static_cast<double>(P->tensors[resid_t].bytes);
+        }
         g.ta = eta;
         g.tb = etb;
         g.dtype = dtype;
@@ -1947,12 +1982,15 @@ class Lowerer {
                   (fa || fb ? " [T-folded]" : "");
         st.alg_flops = 2.0 * g.m * g.n * g.k;
         const int ta = in_t[0], tb = in_t[1];
-        st.run = [P, g, ta, tb, out_t, first, tc](int li, cudaStream_t s) {
+        const int rs = resid_t;
+        if (rs >= 0) st.name += " +add " + OpName(resid_[i].v);
+        st.run = [P, g, ta, tb, out_t, first, tc, rs](int li, cudaStream_t s) {
           GemmArgs a = g;
           const int r = first + li;
           a.a = P->Ptr(P->tensors[ta], r);
           a.b = P->Ptr(P->tensors[tb], r);
           a.c = P->Ptr(P->tensors[out_t], r);
+          if (rs >= 0) a.resid = P->Ptr(P->tensors[rs], r);
           a.epi = Patch(P, g.epi, r);
           if (P->gemm_scratch_bytes) a.scratch = P->peer_base[r] + P->gemm_scratch_off;
           a.sk_flags = reinterpret_cast<uint32_t*>(P->peer_base[r] + P->gemm_flags_off);
@@ -2101,6 +2139,7 @@ class Lowerer {
     }
     (void)eb;
     st.reads = in_t;
+    if (resid_t >= 0) st.reads.push_back(resid_t);
     st.writes = {out_t};
     AddStep(std::move(st));
   }
@@ -2529,6 +2568,16 @@ class Lowerer {
   size_t arena_ = 0;
   std::map<std::string, int> cache_;
   std::vector<bool> absorbed_;
+  // GEMM head -> the add fused into its epilogue (v), the add's other operand (x, input slot)
+  struct Resid {
+    int v = -1, x = -1, slot = -1;
+  };
+  std::vector<Resid> resid_;
+  // The op whose value a GEMM head's kernel writes: the fused add, else its chain's tail.
+  int Tail(int i) const {
+    if (!resid_.empty() && resid_[i].v >= 0) return resid_[i].v;
+    return chain_[i].empty() ? i : chain_[i].back();
+  }
   std::vector<std::array<bool, 2>> fold_t_;  // matmul slot reads a folded 2-D transpose
   std::vector<std::vector<int>> chain_;
   std::map<int, size_t> tanh_tables_;

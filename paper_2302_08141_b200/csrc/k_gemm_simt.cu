@@ -52,7 +52,8 @@ template <typename T, bool TA, bool TB>
 __global__ void __launch_bounds__(256) GemmSimtKernel(T* __restrict__ C, const T* __restrict__ A,
                                                       const T* __restrict__ B, int64_t M,
                                                       int64_t N, int64_t K, ChainArgs epi,
-                                                      int64_t kchunk, float* __restrict__ ws) {
+                                                      int64_t kchunk, float* __restrict__ ws,
+                                                      const T* __restrict__ resid) {
   PdlTrigger();
   PdlWait();
   __shared__ __align__(16) float As[BK][BM];
@@ -138,6 +139,7 @@ __global__ void __launch_bounds__(256) GemmSimtKernel(T* __restrict__ C, const T
       }
       if constexpr (sizeof(T) == 2) v = RoundBf16(v);
       v = EpiChain<T>(epi, v);
+      if (resid) v = __fadd_rn(v, Ld<T>(resid, gm * N + gn));  // fused add (rounded below)
       if constexpr (sizeof(T) == 2) {
         C[gm * N + gn] = __float2bfloat16_rn(v);
       } else {
@@ -149,7 +151,8 @@ __global__ void __launch_bounds__(256) GemmSimtKernel(T* __restrict__ C, const T
 
 template <typename T>
 __global__ void __launch_bounds__(256) SplitReduceKernel(T* __restrict__ C, const float* __restrict__ ws,
-                                                         int64_t n, int splits, ChainArgs epi) {
+                                                         int64_t n, int splits, ChainArgs epi,
+                                                         const T* __restrict__ resid) {
   PdlTrigger();
   PdlWait();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
@@ -157,6 +160,7 @@ __global__ void __launch_bounds__(256) SplitReduceKernel(T* __restrict__ C, cons
     for (int z = 1; z < splits; ++z) v = __fadd_rn(v, ws[int64_t(z) * n + i]);
     if constexpr (sizeof(T) == 2) v = RoundBf16(v);
     v = EpiChain<T>(epi, v);
+    if (resid) v = __fadd_rn(v, Ld<T>(resid, i));  // fused add (rounded below)
     if constexpr (sizeof(T) == 2) {
       C[i] = __float2bfloat16_rn(v);
     } else {
@@ -184,14 +188,15 @@ int Dispatch(const GemmArgs& g, cudaStream_t s) {
   T* c = static_cast<T*>(g.c);
   const T* a = static_cast<const T*>(g.a);
   const T* b = static_cast<const T*>(g.b);
-  if (!g.ta && !g.tb) LaunchPdl(GemmSimtKernel<T, false, false>, grid, 256, 0, s, c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws);
-  else if (!g.ta && g.tb) LaunchPdl(GemmSimtKernel<T, false, true>, grid, 256, 0, s, c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws);
-  else if (g.ta && !g.tb) LaunchPdl(GemmSimtKernel<T, true, false>, grid, 256, 0, s, c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws);
-  else LaunchPdl(GemmSimtKernel<T, true, true>, grid, 256, 0, s, c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws);
+  const T* rs = static_cast<const T*>(g.resid);
+  if (!g.ta && !g.tb) LaunchPdl(GemmSimtKernel<T, false, false>, grid, 256, 0, s, c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws, rs);
+  else if (!g.ta && g.tb) LaunchPdl(GemmSimtKernel<T, false, true>, grid, 256, 0, s, c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws, rs);
+  else if (g.ta && !g.tb) LaunchPdl(GemmSimtKernel<T, true, false>, grid, 256, 0, s, c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws, rs);
+  else LaunchPdl(GemmSimtKernel<T, true, true>, grid, 256, 0, s, c, a, b, g.m, g.n, g.k, g.epi, kchunk, ws, rs);
   if (!ws) return 1;
   const int64_t n = g.m * g.n;
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, SmCount() * 8)));
-  LaunchPdl(SplitReduceKernel<T>, blocks, 256, 0, s, c, ws, n, z, g.epi);
+  LaunchPdl(SplitReduceKernel<T>, blocks, 256, 0, s, c, ws, n, z, g.epi, rs);
   return 2;
 }
 

@@ -33,6 +33,14 @@ namespace {
 constexpr int BM = 128, BK = 64;
 constexpr int kThreads = 256;
 
+// Residual add of the fused `add` op: the same add.rn.bf16x2 as the chain kernels (ew_core.cuh),
+// so the fused result is bit-identical to the separate add kernel's.
+__device__ __forceinline__ uint32_t AddBf16x2Epi(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
 __device__ __forceinline__ uint32_t SmemU32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -154,7 +162,8 @@ __device__ __forceinline__ void TmemLd32(uint32_t taddr, uint32_t (&r)[32]) {
 
 // Split-K finish: sum the fp32 partials in split order, round to bf16, apply the chain.
 __global__ void __launch_bounds__(256) SplitReduceBf16(__nv_bfloat16* __restrict__ C, const float4* __restrict__ ws,
-                                                       int64_t n4, int splits, ChainArgs epi);
+                                                       int64_t n4, int splits, ChainArgs epi,
+                                                       const __nv_bfloat16* __restrict__ resid);
 
 // The packed bf16 ops the lowering lets into a bf16 GEMM epilogue (executor.cpp: relu / neg /
 // identity, and tanh runs = one T^k table lookup; LaunchGemmTc rejects anything else).
@@ -192,7 +201,8 @@ __device__ __forceinline__ void StageEpiTables(const ChainArgs& epi, uint16_t* t
 constexpr int kEpiTabBytes = 8192;  // >= kMaxTanhRuns * kTanhRunEntries * 2
 
 __global__ void __launch_bounds__(256) SplitReduceBf16(__nv_bfloat16* __restrict__ C, const float4* __restrict__ ws,
-                                                       int64_t n4, int splits, ChainArgs epi) {
+                                                       int64_t n4, int splits, ChainArgs epi,
+                                                       const __nv_bfloat16* __restrict__ resid) {
   PdlTrigger();
   PdlWait();
   const uint16_t* tabs[kMaxTanhRuns];
@@ -209,6 +219,11 @@ __global__ void __launch_bounds__(256) SplitReduceBf16(__nv_bfloat16* __restrict
     }
     uint32_t p[2] = {PackBf16x2(v.x, v.y), PackBf16x2(v.z, v.w)};
     EpiPackedBf16(epi, p, tabs);
+    if (resid) {
+      const uint2 r = reinterpret_cast<const uint2*>(resid)[i];
+      p[0] = AddBf16x2Epi(p[0], r.x);
+      p[1] = AddBf16x2Epi(p[1], r.y);
+    }
     reinterpret_cast<uint2*>(C)[i] = make_uint2(p[0], p[1]);
   }
 }
@@ -247,7 +262,7 @@ template <int BN, bool kBKMajor, bool kAKMajor, int KB, bool kGroup = false>
 __global__ void __launch_bounds__(kThreads, 1)
     GemmTcKernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                  const __grid_constant__ CUtensorMap tma_c, int M, int N, int K, ChainArgs epi, int ksplit,
-                 float* __restrict__ ws, GroupDev grp) {
+                 float* __restrict__ ws, GroupDev grp, const __nv_bfloat16* __restrict__ resid) {
   PdlTrigger();
   // Work unit = (m tile, n tile, k split).  ksplit > 1 (few tiles: the sharded GEMMs at N >= 4)
   // writes fp32 partial tiles to ws[split][M][N]; SplitReduceBf16 finishes them.
@@ -394,8 +409,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       FenceAfter();
       const int row = m_blk * BM + ew * 32 + lane;
       float* wrow = ws ? ws + (static_cast<int64_t>(ks) * M + row) * N + n_blk * BN : nullptr;
+      // residual (fused add): 64 bytes of the thread's row per 32-column chunk, loaded one chunk
+      // ahead so the loads overlap the previous chunk's TMEM load, chain and store
+      const uint4* rrow = resid && !wrow ? reinterpret_cast<const uint4*>(resid + static_cast<int64_t>(row) * N + n_blk * BN)
+                                         : nullptr;
+      uint4 rn[4];
+      if (rrow) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rn[q] = rrow[q];
+      }
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
+        uint4 rv[4];
+        if (rrow) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) rv[q] = rn[q];
+          if (c + 1 < BN / 32) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) rn[q] = rrow[(c + 1) * 4 + q];
+          }
+        }
         uint32_t r[32];
         TmemLd32(tmem + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
         if (wrow) {  // split-K partial (fp32, unrounded)
@@ -413,6 +446,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) p[j] = PackBf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
         EpiPackedBf16(epi, p, tp);
+        if (rrow) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            p[4 * q] = AddBf16x2Epi(p[4 * q], rv[q].x);
+            p[4 * q + 1] = AddBf16x2Epi(p[4 * q + 1], rv[q].y);
+            p[4 * q + 2] = AddBf16x2Epi(p[4 * q + 2], rv[q].z);
+            p[4 * q + 3] = AddBf16x2Epi(p[4 * q + 3], rv[q].w);
+          }
+        }
         int col = n_blk * BN + c * 32;
         const CUtensorMap* cmap = &tma_c;
         if constexpr (kGroup) {  // this 32-column chunk's problem and column within it
@@ -594,7 +636,8 @@ template <int BN, bool kBKMajor, bool kAKMajor, bool kGroup = false, int kEpi = 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpi, 1)
     GemmTcPairKernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                      const __grid_constant__ CUtensorMap tma_c, int M, int N, int K, ChainArgs epi, int ksplit,
-                     float* __restrict__ ws, GroupDev grp, uint32_t* __restrict__ sk_flags) {
+                     float* __restrict__ ws, GroupDev grp, uint32_t* __restrict__ sk_flags,
+                     const __nv_bfloat16* __restrict__ resid) {
   PdlTrigger();
   using Cfg = Tc2Cfg<BN, kBKMajor, kAKMajor, kEpi>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -759,8 +802,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpi, 1)
       const int row0 = m_blk * 2 * BM + static_cast<int>(rank) * BM + quarter * 32;
       const int row = row0 + lane;
       float* wrow = ws && !sk ? ws + (static_cast<int64_t>(ks) * M + row) * N + n_blk * BN : nullptr;
+      // residual (fused add): 64 bytes of the thread's row per 32-column chunk, loaded one chunk
+      // ahead so the loads overlap the previous chunk's TMEM load, chain and store
+      const bool radd = resid && !wrow && !contrib;
+      const uint4* rrow = radd ? reinterpret_cast<const uint4*>(resid + static_cast<int64_t>(row) * N + n_blk * BN)
+                               : nullptr;
+      uint4 rn[4];
+      if (radd) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rn[q] = rrow[half * 4 + q];
+      }
 #pragma unroll 1
       for (int c = half; c < BN / 32; c += kEpi / 4) {
+        uint4 rv[4];
+        if (radd) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) rv[q] = rn[q];
+          if (c + kEpi / 4 < BN / 32) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) rn[q] = rrow[(c + kEpi / 4) * 4 + q];
+          }
+        }
         uint32_t r[32];
         TmemLd32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c * 32, r);
         const int64_t so = (static_cast<int64_t>(c) * BM + quarter * 32 + lane) * 32;
@@ -797,6 +859,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpi, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) p[j] = PackBf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
         EpiPackedBf16(epi, p, tp);
+        if (radd) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            p[4 * q] = AddBf16x2Epi(p[4 * q], rv[q].x);
+            p[4 * q + 1] = AddBf16x2Epi(p[4 * q + 1], rv[q].y);
+            p[4 * q + 2] = AddBf16x2Epi(p[4 * q + 2], rv[q].z);
+            p[4 * q + 3] = AddBf16x2Epi(p[4 * q + 3], rv[q].w);
+          }
+        }
         int col = n_blk * BN + c * 32;
         const CUtensorMap* cmap = &tma_c;
         if constexpr (kGroup) {
@@ -1279,13 +1350,14 @@ void LaunchKB(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullptr
   float* ws = ks > 1 ? static_cast<float*>(g.scratch) : nullptr;
   LaunchPdl(GemmTcKernel<BN, kBK, kAK, KB, kG>, grid, kThreads, Cfg::kSmem, s,
       mp.a, mp.b, mp.c, static_cast<int>(g.m), static_cast<int>(n),
-      static_cast<int>(g.k), g.epi, ks, ws, kG ? gl->dev : GroupDev{});
+      static_cast<int>(g.k), g.epi, ks, ws, kG ? gl->dev : GroupDev{},
+      kG ? nullptr : static_cast<const __nv_bfloat16*>(g.resid));
   RH_CUDA(cudaGetLastError());
   if (ws) {
     const int64_t n4 = g.m * g.n / 4;
     const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, SmCount() * 8)));
     LaunchPdl(SplitReduceBf16, blocks, 256, 0, s, static_cast<__nv_bfloat16*>(g.c), reinterpret_cast<const float4*>(ws),
-                                           n4, ks, g.epi);
+              n4, ks, g.epi, static_cast<const __nv_bfloat16*>(g.resid));
     RH_CUDA(cudaGetLastError());
   }
 }
@@ -1341,12 +1413,13 @@ void LaunchPair(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullp
   cfg.numAttrs = PdlEnabled() ? 2 : 1;
   RH_CUDA(cudaLaunchKernelEx(&cfg, GemmTcPairKernel<BN, kBK, kAK, kG, kEpi>, mp.a, mp.b, mp.c,
                              static_cast<int>(g.m), static_cast<int>(n), static_cast<int>(g.k), g.epi, ks, ws,
-                             kG ? gl->dev : GroupDev{}, sk ? g.sk_flags : nullptr));
+                             kG ? gl->dev : GroupDev{}, sk ? g.sk_flags : nullptr,
+                             kG ? nullptr : static_cast<const __nv_bfloat16*>(g.resid)));
   if (ws && !sk) {
     const int64_t n4 = g.m * g.n / 4;
     const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, SmCount() * 8)));
     LaunchPdl(SplitReduceBf16, blocks, 256, 0, s, static_cast<__nv_bfloat16*>(g.c), reinterpret_cast<const float4*>(ws),
-              n4, ks, g.epi);
+              n4, ks, g.epi, static_cast<const __nv_bfloat16*>(g.resid));
     RH_CUDA(cudaGetLastError());
   }
 }

@@ -211,6 +211,10 @@ struct GemmArgs {
   // left zeroed by every launch; the partial accumulators live in `scratch`.  nullptr: no
   // stream-K.
   uint32_t* sk_flags = nullptr;
+  // Fused residual add (bf16): C = round(GEMM [+ chain]) + resid, resid [m, n] row-major like C
+  // (the add op after the GEMM, executor PlanFusion), every kernel and the split-K reduce
+  // included.  nullptr: none.
+  const void* resid = nullptr;
 };
 constexpr size_t kGemmSkFlagBytes = 4096;
 size_t GemmTf32x3ScratchBytes(const GemmArgs& g);
