@@ -997,7 +997,11 @@ class Lowerer {
         if (a.kind == RH_OP_ADD && a.dtype == op.dtype && SameTask(v, h) && p_->inputs[v].size() == 2) {
           const int slot = p_->inputs[v][0] == t ? 1 : 0;
           const int x = p_->inputs[v][slot];
-          if (x != t && pos[x] < pos[h] && SpecsEq(p_->in_specs[v][0], p_->out_specs[t]) && SpecsEq(p_->in_specs[v][1], p_->out_specs[t]) &&
+          // x must be read in the layout it is produced in: a residual that needs a transition
+          // would move that transition's join up to the GEMM's start (C5 at N=2: +0.5 ms
+          // exposed transition time when it did)
+          if (x != t && pos[x] < pos[h] && SpecsEq(p_->in_specs[v][slot], p_->out_specs[x]) &&
+              SpecsEq(p_->in_specs[v][0], p_->out_specs[t]) && SpecsEq(p_->in_specs[v][1], p_->out_specs[t]) &&
               SpecsEq(p_->out_specs[v], p_->out_specs[t]) && no_partial(p_->out_specs[t]) && natural_ok(t) &&
               natural_ok(v) && GDims(x) == GDims(v) && GDims(v) == GDims(t)) {
             resid_[h] = Resid{v, x, slot};
