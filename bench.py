@@ -480,7 +480,7 @@ def main():
         # pipelined path: a fully replicated input in a multi-process run is scattered over PCIe
         # (1/world per process) and all-gathered over NVLink (ScatterPart, abi.cpp)
         def scattered(x):
-            return (world > 1 and os.environ.get("RH_E2E_SCATTER", "0") == "1"
+            return (world > 1 and world <= 8 and os.environ.get("RH_E2E_SCATTER", "1") != "0"
                     and all(sp.kind == RH_REPLICATED for sp in prog.ops[x].out_spec)
                     and prog.full_bytes(x) % (world * 16) == 0)
         h2d = sum(prog.full_bytes(x) * (1 if scattered(x) else world) for x in xs)
@@ -523,7 +523,8 @@ def main():
             "e2e": {"value": tok / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "rh_program_run_host (pinned host buffers; copies of neighbouring steps overlap)",
-                    "inputs": "replicated inputs: 1/world slice per process over PCIe + NVLink all-gather"
+                    "inputs": "replicated inputs: 1/world slice per process over PCIe + NVLink all-gather "
+                              "(gather stream, overlapping the previous step's run)"
                               if any(scattered(x) for x in xs) else "every process copies its inputs whole",
                     "serial": {"value": tok / (e2e_serial_ms * 1e-3), "ms_per_step": e2e_serial_ms,
                                "api": "rh_program_step_host (H2D, run, D2H back to back)"}},

@@ -851,6 +851,33 @@ int rh_program_profile(rh_program* p, int iters, double* ms_per_iter) {
   });
 }
 
+// Every rank's copy of a symmetric device buffer, mapped here (CUDA IPC handles all-gathered
+// over the world communicator); entry `first_rank` is `mine` itself.
+std::vector<char*> ExchangeIpc(rh_runtime* rt, char* mine) {
+  cudaIpcMemHandle_t h;
+  RH_CUDA(cudaIpcGetMemHandle(&h, mine));
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  char* dev = nullptr;
+  RH_CUDA(cudaMalloc(&dev, hb * (rt->world + 1)));
+  RH_CUDA(cudaMemcpy(dev + hb * rt->world, &h, hb, cudaMemcpyHostToDevice));
+  RH_NCCL(ncclAllGather(dev + hb * rt->world, dev, hb, ncclChar, rt->world_comm, rt->streams[0]));
+  RH_CUDA(cudaStreamSynchronize(rt->streams[0]));
+  std::vector<cudaIpcMemHandle_t> all(rt->world);
+  RH_CUDA(cudaMemcpy(all.data(), dev, hb * rt->world, cudaMemcpyDeviceToHost));
+  cudaFree(dev);
+  std::vector<char*> out(rt->world, nullptr);
+  for (int r = 0; r < rt->world; ++r) {
+    if (r == rt->first_rank) {
+      out[r] = mine;
+      continue;
+    }
+    void* ptr = nullptr;
+    RH_CUDA(cudaIpcOpenMemHandle(&ptr, all[r], cudaIpcMemLazyEnablePeerAccess));
+    out[r] = static_cast<char*>(ptr);
+  }
+  return out;
+}
+
 // Host read of output k: a materialized (replicated) output in a multi-process run is read as
 // this process's 1/world contiguous slice (the processes' slices together are the full tensor;
 // every rank copying the whole replicated tensor would multiply the PCIe traffic by world).
@@ -865,16 +892,16 @@ std::pair<size_t, size_t> OutSlice(const rh_program* p, int op, const rh::Tensor
 
 // A fully replicated input in a multi-process run: each process copies only its 1/world
 // contiguous slice over PCIe and the slices are all-gathered over NVLink (every process copying
-// the whole tensor multiplies the host->device traffic by world).  Returns the slice bytes,
-// 0 when the input is copied whole.  Opt-in (RH_E2E_SCATTER=1): measured on C3 (r1d), the
-// barriers and the gather on the compute stream cost more than the PCIe bytes they save
-// (N=2 e2e 0.518 -> 0.634 ms, N=4 0.465 -> 0.465 ms): the whole-tensor H2D on the copy-in
-// stream overlaps the previous step's run.
+// the whole tensor multiplies the host->device traffic by world: at N=4 the 16 MiB C3 input per
+// process and step made e2e PCIe-bound, 0.60 ms against a 0.31 ms run).  The gather runs on its
+// own stream between the H2D and the step that consumes it, so it overlaps the previous step's
+// run (round 1 had it, with host-ordered world barriers, on the compute stream: slower).
+// Returns the slice bytes, 0 when the input is copied whole.  RH_E2E_SCATTER=0 disables.
 size_t ScatterPart(const rh_program* p, const rh::Tensor& t) {
   const rh_runtime* rt = p->mesh->rt;
-  if (!rt->dist || rt->world <= 1) return 0;
+  if (!rt->dist || rt->world <= 1 || rt->world > rh::kMaxGroup || !p->e2e_epoch_off) return 0;
   const char* env = std::getenv("RH_E2E_SCATTER");
-  if (!env || env[0] != '1') return 0;
+  if (env && env[0] == '0') return 0;
   for (int a = 0; a < p->n_axes; ++a)
     if (t.specs[a].kind != RH_REPLICATED) return 0;
   if (t.bytes % (static_cast<size_t>(rt->world) * 16) != 0) return 0;
@@ -902,6 +929,7 @@ int rh_program_run_host(rh_program* p, int iters, int n_in, const int* in_ops, c
       size_t bytes;
       void* stage[2];
       size_t part;  // > 0: scattered (this process copies bytes [part*g, part*(g+1)) over PCIe)
+      std::vector<char*> peer_stage[2];  // scattered: every rank's stage[b] (IPC-mapped)
     };
     struct Out {
       const rh::Tensor* t;
@@ -910,12 +938,37 @@ int rh_program_run_host(rh_program* p, int iters, int n_in, const int* in_ops, c
     };
     std::vector<In> ins(n_in);
     std::vector<Out> outs(n_outs);
+    bool any_part = false;
     for (int k = 0; k < n_in; ++k) {
       const rh::Tensor& t = p->tensors[p->out_tensor[in_ops[k]]];
       ins[k].t = &t;
       ins[k].bytes = static_cast<size_t>(Prod(t.gdims)) * rh::ElemBytes(t.dtype);
       ins[k].part = ScatterPart(p, t);
+      any_part = any_part || ins[k].part;
       for (int b = 0; b < 2; ++b) RH_CUDA(cudaMalloc(&ins[k].stage[b], ins[k].bytes));
+    }
+    // scattered inputs: map every rank's stage buffers (CUDA IPC over the world communicator)
+    std::vector<char*> opened;
+    for (auto& x : ins) {
+      if (!x.part) continue;
+      for (int b = 0; b < 2; ++b) {
+        x.peer_stage[b] = ExchangeIpc(rt, static_cast<char*>(x.stage[b]));
+        for (int q = 0; q < rt->world; ++q)
+          if (q != g) opened.push_back(x.peer_stage[b][q]);
+      }
+    }
+    rh::PeerSync gsync{};
+    if (any_part) {
+      gsync.d = rt->world;
+      gsync.me = g;
+      for (int q = 0; q < rt->world; ++q) {
+        gsync.members[q] = q;
+        gsync.peer_slot[q] = reinterpret_cast<uint32_t*>(p->peer_base[q] + p->e2e_sync_off);
+      }
+      gsync.my_slot = reinterpret_cast<uint32_t*>(p->base[0] + p->e2e_sync_off);
+      gsync.epoch = reinterpret_cast<const uint32_t*>(p->base[0] + p->e2e_epoch_off);
+      gsync.err = reinterpret_cast<uint32_t*>(p->base[0] + p->err_off);
+      gsync.timeout_ns = rh::SyncTimeoutNs();
     }
     for (int k = 0; k < n_outs; ++k) {
       const int op = p->outputs[k];
@@ -925,11 +978,14 @@ int rh_program_run_host(rh_program* p, int iters, int n_in, const int* in_ops, c
       std::tie(outs[k].off, outs[k].bytes) = OutSlice(p, op, *outs[k].t);
       for (int b = 0; b < 2; ++b) RH_CUDA(cudaMalloc(&outs[k].stage[b], outs[k].bytes));
     }
-    cudaStream_t sin = nullptr, sout = nullptr;
+    cudaStream_t sin = nullptr, sout = nullptr, sg = nullptr;
     RH_CUDA(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking));
     RH_CUDA(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking));
-    cudaEvent_t in_ready[2], in_free[2], out_ready[2], out_free[2], e0, e1;
+    RH_CUDA(cudaStreamCreateWithFlags(&sg, cudaStreamNonBlocking));
+    cudaEvent_t in_ready[2], in_free[2], out_ready[2], out_free[2], h2d_done[2], gathered[2], e0, e1;
     for (int b = 0; b < 2; ++b) {
+      RH_CUDA(cudaEventCreateWithFlags(&h2d_done[b], cudaEventDisableTiming));
+      RH_CUDA(cudaEventCreateWithFlags(&gathered[b], cudaEventDisableTiming));
       RH_CUDA(cudaEventCreateWithFlags(&in_ready[b], cudaEventDisableTiming));
       RH_CUDA(cudaEventCreateWithFlags(&in_free[b], cudaEventDisableTiming));
       RH_CUDA(cudaEventCreateWithFlags(&out_ready[b], cudaEventDisableTiming));
@@ -939,13 +995,23 @@ int rh_program_run_host(rh_program* p, int iters, int n_in, const int* in_ops, c
     RH_CUDA(cudaEventCreate(&e1));
     auto cleanup = [&] {
       cudaStreamSynchronize(sin);
+      cudaStreamSynchronize(sg);
       cudaStreamSynchronize(sout);
       cudaStreamSynchronize(cs);
+      if (!opened.empty()) {
+        try {
+          HostBarrier(rt);  // no peer still reads this rank's stage buffers
+        } catch (...) {
+        }
+        for (char* q : opened) cudaIpcCloseMemHandle(q);
+      }
       for (auto& x : ins)
         for (void* q : x.stage) cudaFree(q);
       for (auto& x : outs)
         for (void* q : x.stage) cudaFree(q);
       for (int b = 0; b < 2; ++b) {
+        cudaEventDestroy(h2d_done[b]);
+        cudaEventDestroy(gathered[b]);
         cudaEventDestroy(in_ready[b]);
         cudaEventDestroy(in_free[b]);
         cudaEventDestroy(out_ready[b]);
@@ -955,6 +1021,7 @@ int rh_program_run_host(rh_program* p, int iters, int n_in, const int* in_ops, c
       cudaEventDestroy(e1);
       cudaStreamDestroy(sin);
       cudaStreamDestroy(sout);
+      cudaStreamDestroy(sg);
     };
     try {
       if (UseGraph(p) && !p->graph) {  // capture outside the timed region
@@ -965,9 +1032,13 @@ int rh_program_run_host(rh_program* p, int iters, int n_in, const int* in_ops, c
       WorldSync(p);
       RH_CUDA(cudaEventRecord(e0, cs));
       RH_CUDA(cudaStreamWaitEvent(sin, e0, 0));
+      RH_CUDA(cudaStreamWaitEvent(sg, e0, 0));
       for (int it = 0; it < iters; ++it) {
         const int b = it & 1;
         RH_CUDA(cudaStreamWaitEvent(sin, in_free[b], 0));
+        // scattered inputs: stage[b] is rewritten only after this rank's previous gather, whose
+        // barrier every peer passed after finishing the gather that read stage[b] two steps ago
+        if (any_part && it > 0) RH_CUDA(cudaStreamWaitEvent(sin, gathered[b ^ 1], 0));
         for (auto& x : ins) {
           const size_t off = x.part * static_cast<size_t>(g), n = x.part ? x.part : x.bytes;
           RH_CUDA(cudaMemcpyAsync(static_cast<char*>(x.stage[b]) + off,
@@ -975,7 +1046,16 @@ int rh_program_run_host(rh_program* p, int iters, int n_in, const int* in_ops, c
                                   cudaMemcpyHostToDevice, sin));
         }
         RH_CUDA(cudaEventRecord(in_ready[b], sin));
-        RH_CUDA(cudaStreamWaitEvent(cs, in_ready[b], 0));
+        if (any_part) {  // gather stream: world barrier fused into the pull of the peers' pieces
+          RH_CUDA(cudaStreamWaitEvent(sg, in_ready[b], 0));
+          rh::LaunchEpochTick(reinterpret_cast<uint32_t*>(p->base[0] + p->e2e_epoch_off), sg);
+          for (auto& x : ins)
+            if (x.part) rh::LaunchGatherSlices(x.peer_stage[b].data(), rt->world, g, x.part, gsync, sg);
+          RH_CUDA(cudaEventRecord(gathered[b], sg));
+          RH_CUDA(cudaStreamWaitEvent(cs, gathered[b], 0));
+        } else {
+          RH_CUDA(cudaStreamWaitEvent(cs, in_ready[b], 0));
+        }
         for (auto& x : ins) {
           const rh::Tensor& t = *x.t;
           bool all_rep = true, partial_zero = false;
@@ -984,22 +1064,7 @@ int rh_program_run_host(rh_program* p, int iters, int n_in, const int* in_ops, c
             all_rep = all_rep && t.specs[a].kind == RH_REPLICATED;
             if (t.specs[a].kind == RH_PARTIAL && c[a] != 0) partial_zero = true;
           }
-          if (x.part) {
-            // own slice into the arena; world barrier (every rank's slice landed, and every
-            // peer finished reading the previous step's slices); pull the peers' slices over
-            // NVLink; world barrier (no rank rewrites its slice while a peer still reads it)
-            const size_t off = x.part * static_cast<size_t>(g);
-            RH_CUDA(cudaMemcpyAsync(p->base[0] + t.offset + off, static_cast<char*>(x.stage[b]) + off, x.part,
-                                    cudaMemcpyDeviceToDevice, cs));
-            WorldSync(p);
-            for (int k = 1; k < rt->world; ++k) {
-              const int q = (g + k) % rt->world;  // rotated: no single source hot spot
-              const size_t qo = x.part * static_cast<size_t>(q);
-              RH_CUDA(cudaMemcpyAsync(p->base[0] + t.offset + qo, p->peer_base[q] + t.offset + qo, x.part,
-                                      cudaMemcpyDeviceToDevice, cs));
-            }
-            WorldSync(p);
-          } else if (all_rep) {
+          if (all_rep) {  // (a scattered input's stage is whole again after its gather)
             RH_CUDA(cudaMemcpyAsync(p->base[0] + t.offset, x.stage[b], x.bytes, cudaMemcpyDeviceToDevice, cs));
           } else if (partial_zero) {
             rh::LaunchZero(p->base[0] + t.offset, t.bytes, cs);

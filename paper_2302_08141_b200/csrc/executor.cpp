@@ -311,6 +311,10 @@ class Lowerer {
     p_->flags_off = Alloc(static_cast<size_t>(rt_->world) * 4);
     p_->counter_off = Alloc(4);
     p_->err_off = Alloc(4);
+    if (rt_->dist && rt_->world > 1) {  // rh_program_run_host's overlapped input gather
+      p_->e2e_sync_off = Alloc(static_cast<size_t>(rt_->world) * 4);
+      p_->e2e_epoch_off = Alloc(4);
+    }
     ValidateSpecs();
     const bool pipeline = p_->pipeline_axis >= 0;
     const bool eager = rt_->dist && rt_->world > 1 && !(p_->flags & RH_FLAG_NO_OVERLAP) &&

@@ -125,6 +125,7 @@ struct rh_program {
   size_t flags_off = 0, counter_off = 0;
   size_t err_off = 0;  // bounded cross-GPU waits: first timed-out (me, member) pair (PeerSync)
   size_t sync_off = 0, epoch_off = 0;  // fused-barrier flag rows [slots][world] + run counter
+  size_t e2e_sync_off = 0, e2e_epoch_off = 0;  // rh_program_run_host input gather: flag row + counter
   int n_sync_slots = 0;
   std::vector<char*> base;       // per local rank
   std::vector<char*> peer_base;  // per global rank (dist: IPC-mapped; local: = base)

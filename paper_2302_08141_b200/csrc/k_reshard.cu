@@ -140,6 +140,28 @@ __global__ void EpochTickKernel(uint32_t* epoch) { *epoch += 1; }
 
 __global__ void PeerSyncKernel(PeerSync s) { ArriveAndWait(s); }
 
+struct GatherArgs {
+  char* src[kMaxGroup];
+  int world, me;
+  uint64_t part16;  // 16-byte chunks per piece
+  PeerSync sync;
+};
+
+// Peer q's piece comes from peer (me + 1 + k) % world for k = 0..world-2: at any moment the
+// ranks read from different peers.
+__global__ void __launch_bounds__(256) GatherSlicesKernel(const __grid_constant__ GatherArgs a) {
+  ArriveAndWait(a.sync);
+  const uint64_t total = a.part16 * static_cast<uint64_t>(a.world - 1);
+  uint4* dst = reinterpret_cast<uint4*>(a.src[a.me]);
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(i / a.part16);
+    const uint64_t j = i - static_cast<uint64_t>(k) * a.part16;
+    const int q = (a.me + 1 + k) % a.world;
+    const uint64_t o = static_cast<uint64_t>(q) * a.part16 + j;
+    dst[o] = reinterpret_cast<const uint4*>(a.src[q])[o];
+  }
+}
+
 __device__ __forceinline__ uint32_t DstToGlobal(const PullDev& a, uint32_t i) {
   if (!a.to_shard) return i;
   const uint32_t p = Div(a.qst, i);
@@ -942,6 +964,24 @@ uint64_t SyncTimeoutNs() {
 
 void LaunchBarrier(const BarrierArgs& b, cudaStream_t s) {
   BarrierKernel<<<1, 32, 0, s>>>(b);
+  RH_CUDA(cudaGetLastError());
+}
+
+void LaunchGatherSlices(char* const* src, int world, int me, size_t part, const PeerSync& sync, cudaStream_t s) {
+  if (world > kMaxGroup || part % 16) Fail("gather slices: unsupported world / piece size");
+  GatherArgs a{};
+  for (int q = 0; q < world; ++q) a.src[q] = src[q];
+  a.world = world;
+  a.me = me;
+  a.part16 = part / 16;
+  a.sync = sync;
+  const uint64_t total = a.part16 * static_cast<uint64_t>(world - 1);
+  static const int cap = [] {  // grid cap (A/B knob; profiles/r2/e2e_scatter_ab.txt: 148 best)
+    const char* e = getenv("RH_E2E_GATHER_BLOCKS");
+    return e && *e ? std::max(1, atoi(e)) : SmCount();
+  }();
+  const int blocks = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, cap)));
+  GatherSlicesKernel<<<blocks, 256, 0, s>>>(a);
   RH_CUDA(cudaGetLastError());
 }
 

@@ -191,6 +191,11 @@ void LaunchZero(void* dst, size_t bytes, cudaStream_t s);
 void LaunchSgd(void* w, const void* g, int64_t n, float lr, int dtype, cudaStream_t s);
 // A fused-barrier rendezvous on its own (one CTA): the sending side of a cross-stage transfer.
 void LaunchPeerSync(const PeerSync& sync, cudaStream_t s);
+// End-to-end input gather (rh_program_run_host): every member q of the world holds its piece
+// [q*part, (q+1)*part) of a replicated input in its stage buffer src[q] (mapped); behind the
+// fused barrier `sync` (every member's H2D of this step landed) this rank pulls the peers'
+// pieces into the same offsets of dst = src[me].  part % 16 == 0.
+void LaunchGatherSlices(char* const* src, int world, int me, size_t part, const PeerSync& sync, cudaStream_t s);
 
 // ------------------------------------------ GEMM (K1) ----------------------------------------
 // C[m,n] = op(A)[m,k] . op(B)[k,n]; A stored [m,k] (ta=0) or [k,m] (ta=1), B stored [k,n]
