@@ -325,6 +325,7 @@ class Lowerer {
     SortGroupMembers();
     PlanFusion();
     RefineGemmGroups();
+    PlanAttnChains();
     for (int i : p_->order) {
       const rh_op& op = p_->ops[i];
       cur_stage_ = StageOfOp(i);
@@ -344,11 +345,19 @@ class Lowerer {
         continue;
       }
       if (!group_of_.empty() && group_of_[i] >= 0) {  // grouped GEMM: one launch at its first member
-        const std::vector<int>& g = groups_[group_of_[i]];
-        if (g.front() == i) {
-          EmitGemmGroup(g);
-          if (eager)
-            for (int m : g) EagerTransitions(chain_[m].empty() ? m : chain_[m].back());
+        const int gi = group_of_[i];
+        const std::vector<int>& g = groups_[gi];
+        if (g.front() == i && !attn_done_[gi]) {
+          const int g2 = attn_pair_[gi];
+          if (g2 >= 0 && EmitAttnChain(gi, g2)) {  // score + chain + context in one kernel
+            attn_done_[g2] = true;
+            if (eager)
+              for (int m : groups_[g2]) EagerTransitions(m);
+          } else {
+            EmitGemmGroup(g);
+            if (eager)
+              for (int m : g) EagerTransitions(chain_[m].empty() ? m : chain_[m].back());
+          }
         }
         continue;
       }
@@ -1207,6 +1216,137 @@ class Lowerer {
     st.writes = out_t;
     AddStep(std::move(st));
   }
+  // Fused attention-head chains: a grouped score GEMM (Q_h K_h^T, epilogue chain) whose every
+  // member's value is read only by the matching member of one grouped context GEMM
+  // (chain(S_h) V_h) runs with it as one kernel (LaunchAttnChain): the scores never reach HBM.
+  // attn_pair_[score group] = context group; local shapes are checked at emission
+  // (EmitAttnChain falls back to the two grouped launches).  RH_NO_ATTN_FUSION disables.
+  void PlanAttnChains() {
+    const int n = static_cast<int>(p_->ops.size());
+    attn_pair_.assign(groups_.size(), -1);
+    attn_done_.assign(groups_.size(), false);
+    static const bool off = getenv("RH_NO_ATTN_FUSION") != nullptr;
+    if (off || groups_.empty() || (p_->flags & (RH_FLAG_NO_FUSION | RH_FLAG_SIMT_GEMM | RH_FLAG_KEEP_ALL))) return;
+    std::vector<int> uses(n, 0), consumer(n, -1), slot(n, -1), pos(n, 0);
+    for (int i = 0; i < n; ++i)
+      for (size_t k = 0; k < p_->inputs[i].size(); ++k) {
+        const int src = p_->inputs[i][k];
+        ++uses[src];
+        consumer[src] = i;
+        slot[src] = static_cast<int>(k);
+      }
+    std::vector<bool> is_out(n, false);
+    for (int o : p_->outputs) is_out[o] = true;
+    for (size_t k = 0; k < p_->order.size(); ++k) pos[p_->order[k]] = static_cast<int>(k);
+    auto folded = [&](int m) { return !fold_t_.empty() && (fold_t_[m][0] || fold_t_[m][1]); };
+    for (size_t g1 = 0; g1 < groups_.size(); ++g1) {
+      const std::vector<int>& G = groups_[g1];
+      int g2 = -1;
+      bool ok = G.size() >= 1;
+      std::vector<int> ctx;
+      for (int m : G) {
+        const rh_op& op = p_->ops[m];
+        const int t = Tail(m);
+        ok = ok && op.kind == RH_OP_MATMUL && op.dtype == RH_BF16 && !op.transpose_a && op.transpose_b && !folded(m) &&
+             resid_[m].v < 0 && uses[t] == 1 && !is_out[t];
+        if (!ok) break;
+        const int c = consumer[t];
+        const rh_op& co = p_->ops[c];
+        ok = co.kind == RH_OP_MATMUL && slot[t] == 0 && !co.transpose_a && !co.transpose_b && !folded(c) &&
+             chain_[c].empty() && resid_[c].v < 0 && group_of_[c] >= 0 && SameTask(c, m) &&
+             SpecsEq(p_->in_specs[c][0], p_->out_specs[t]) && pos[p_->inputs[c][1]] < pos[G.front()];
+        if (!ok) break;
+        if (g2 < 0) g2 = group_of_[c];
+        ok = group_of_[c] == g2 && ChainSig(m) == ChainSig(G.front());
+        ctx.push_back(c);
+      }
+      if (!ok || g2 < 0 || groups_[g2].size() != G.size()) continue;
+      // the context group's members in the score group's order
+      std::vector<int> sorted_ctx = ctx;
+      std::sort(sorted_ctx.begin(), sorted_ctx.end());
+      std::vector<int> g2m = groups_[g2];
+      std::sort(g2m.begin(), g2m.end());
+      if (sorted_ctx != g2m) continue;
+      attn_pair_[g1] = g2;
+      attn_ctx_[g1] = ctx;
+    }
+  }
+
+  std::string ChainSig(int m) {
+    std::ostringstream k;
+    for (int v : chain_[m]) k << UnaryFn(v) << ',';
+    return k.str();
+  }
+
+  bool EmitAttnChain(int g1, int g2) {
+    rh_program* P = p_;
+    const std::vector<int>& S = groups_[g1];
+    const std::vector<int>& C = attn_ctx_[g1];
+    const int n = static_cast<int>(S.size());
+    std::vector<int> qt(n), kt(n), vt(n), ot(n);
+    for (int h = 0; h < n; ++h) {
+      qt[h] = GetTensor(p_->inputs[S[h]][0], p_->in_specs[S[h]][0], "edge");
+      kt[h] = GetTensor(p_->inputs[S[h]][1], p_->in_specs[S[h]][1], "edge");
+      vt[h] = GetTensor(p_->inputs[C[h]][1], p_->in_specs[C[h]][1], "edge");
+    }
+    const Dims qd = P->tensors[qt[0]].ldims, kd = P->tensors[kt[0]].ldims, vd = P->tensors[vt[0]].ldims;
+    bool ok = qd.size() == 2 && kd.size() == 2 && vd.size() == 2 && qd[1] == kd[1] && kd == vd &&
+              AttnChainSupported(n, qd[0], kd[0], qd[1]) && SpecsEq(NaturalSpecs(S[0], p_->in_specs[S[0]]), p_->out_specs[S[0]]);
+    for (int h = 0; h < n && ok; ++h)
+      ok = P->tensors[qt[h]].ldims == qd && P->tensors[kt[h]].ldims == kd && P->tensors[vt[h]].ldims == vd &&
+           SpecsEq(NaturalSpecs(C[h], p_->in_specs[C[h]]), p_->out_specs[C[h]]);
+    if (!ok) return false;  // (transitions fetched above are cached; the groups reuse them)
+    for (int h = 0; h < n; ++h) {
+      ot[h] = NewTensor(C[h], p_->out_specs[C[h]]);
+      p_->out_tensor[C[h]] = ot[h];
+      p_->in_tensor[S[h]] = {qt[h], kt[h]};
+      p_->in_tensor[C[h]] = {-1, vt[h]};  // the chained scores are never materialized
+    }
+    const int64_t sq = qd[0], sk = kd[0];
+    const ChainArgs epi = ChainOf(S[0], false);
+    const size_t off = Alloc(AttnChainTableBytes(n));
+    Step st;
+    st.kind = Step::kKernel;
+    st.launches = 1;
+    st.name = "attn_chain[" + std::to_string(n) + "] " + OpName(S.front()) + ".." + OpName(C.back()) +
+              " (score + chain + context)";
+    st.alg_flops = 2.0 * 2.0 * static_cast<double>(sq) * sk * qd[1] * n;
+    std::set<int> rd;
+    for (int h = 0; h < n; ++h) {
+      rd.insert(qt[h]);
+      rd.insert(kt[h]);
+      rd.insert(vt[h]);
+    }
+    for (int t : rd) st.alg_bytes += static_cast<double>(P->tensors[t].bytes);
+    for (int t : ot) st.alg_bytes += static_cast<double>(P->tensors[t].bytes);
+    const int first = rt_->first_rank;
+    st.init = [P, qt, kt, vt, ot, off, first, n, sq, sk](int li) {
+      const int r = first + li;
+      std::vector<const void*> q(n), k(n), v(n);
+      std::vector<void*> o(n);
+      for (int h = 0; h < n; ++h) {
+        q[h] = P->Ptr(P->tensors[qt[h]], r);
+        k[h] = P->Ptr(P->tensors[kt[h]], r);
+        v[h] = P->Ptr(P->tensors[vt[h]], r);
+        o[h] = P->Ptr(P->tensors[ot[h]], r);
+      }
+      PrepareAttnChain(n, sq, sk, q.data(), k.data(), v.data(), o.data(), P->peer_base[r] + off);
+    };
+    st.run = [P, epi, off, first, n, sq, sk](int li, cudaStream_t s) {
+      const int r = first + li;
+      LaunchAttnChain(n, sq, sk, Patch(P, epi, r), P->peer_base[r] + off, s);
+      return 1;
+    };
+    st.reads.assign(rd.begin(), rd.end());
+    st.writes = ot;
+    AddStep(std::move(st));
+    (void)g2;
+    return true;
+  }
+  std::vector<int> attn_pair_;                 // score group -> context group (-1: none)
+  std::vector<bool> attn_done_;                // context group emitted inside its score group's kernel
+  std::map<int, std::vector<int>> attn_ctx_;   // score group -> context members, score order
+
   std::vector<int> group_of_;             // op -> grouped GEMM id (-1: none)
   std::vector<std::vector<int>> groups_;  // members in schedule order
 

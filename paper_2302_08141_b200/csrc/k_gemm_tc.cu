@@ -1489,6 +1489,178 @@ void LaunchTf32x3(const GemmArgs& g, cudaStream_t s) {
   RH_CUDA(cudaGetLastError());
 }
 
+
+// ------------------------- fused score -> chain -> context (attention heads) -------------------------
+// One kernel for a head's S = Q K^T (K = 128), the elementwise chain on S (bf16 rounding, then
+// the score GEMM's epilogue chain: T^14 for the fixture's unlabeled tanh chain), and
+// O = chain(S) V — the score and context groups of the 32-head block without the 2048 x 2048
+// score tensor ever leaving the SM.  One CTA per (head, 128-row block of Q):
+//   warp 0: TMA producer (Q once; K_j and V_j per 128-key block, 2 stages),
+//   warp 1: MMA issuer (S_j into one of 2 TMEM buffers, O += P_j V_j into a third),
+//   warps 4-7: S_j -> bf16 -> chain -> P_j in shared memory (128-byte swizzled K-major, the
+//   A operand of the next MMA), then O -> bf16 -> TMA-store epilogue.
+// P_j is exactly the score group's output (same rounding, same chain code) and O accumulates the
+// same K = 16 MMA steps in key order as the context group's 128 x 128 tiles.
+constexpr int kAttnD = 128, kAttnBlk = 128;
+constexpr int kAttnChunk = kAttnBlk * 128;                     // one 64-wide K chunk of a 128-row tile
+constexpr int kAttnQ = 2 * kAttnChunk;                         // Q_i: [128 rows x 128 K]
+constexpr int kAttnKV = 4 * kAttnChunk;                        // K_j + V_j per stage
+constexpr int kAttnP = 2 * kAttnChunk;                         // P_j: [128 rows x 128 keys]
+constexpr int kAttnSmem = kAttnQ + 2 * kAttnKV + kAttnP + 1024 + kEpiTabBytes + kEpiStageBytes + 1024;
+constexpr uint32_t kAttnIdescS = TcCfg<128, true, true, 128>::kIdesc;   // B = K_j, K-major
+constexpr uint32_t kAttnIdescO = TcCfg<128, false, true, 128>::kIdesc;  // B = V_j, MN-major
+
+__global__ void __launch_bounds__(kThreads, 1)
+    AttnChainKernel(const CUtensorMap* __restrict__ maps, int q_blocks, int k_blocks, ChainArgs epi) {
+  PdlTrigger();
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sq = smem;
+  uint8_t* skv = sq + kAttnQ;
+  uint8_t* sp = skv + 2 * kAttnKV;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sp + kAttnP);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* s_empty = bars + 7;   // [2]
+  uint64_t* p_full = bars + 9;
+  uint64_t* p_empty = bars + 10;
+  uint64_t* o_full = bars + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint8_t* tab_area = reinterpret_cast<uint8_t*>(bars) + 1024;
+  uint8_t* stage_base = tab_area + kEpiTabBytes;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int head = blockIdx.x / q_blocks, qi = blockIdx.x % q_blocks;
+  const CUtensorMap* mq = maps + 4 * head;
+  const CUtensorMap* mk = mq + 1;
+  const CUtensorMap* mv = mq + 2;
+  const CUtensorMap* mo = mq + 3;
+
+  if (warp == 0 && lane == 0) {
+    MbarInit(q_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      MbarInit(&kv_full[b], 1);
+      MbarInit(&kv_empty[b], 1);
+      MbarInit(&s_full[b], 1);
+      MbarInit(&s_empty[b], 4);
+    }
+    MbarInit(p_full, 4);
+    MbarInit(p_empty, 1);
+    MbarInit(o_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(SmemU32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  FenceBefore();
+  __syncthreads();
+  FenceAfter();
+  const uint32_t tmem = *tmem_slot;  // S_0 at column 0, S_1 at 128, O at 256
+  PdlWait();
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer ----------------
+      MbarExpectTx(q_full, kAttnQ);
+      for (int c = 0; c < 2; ++c) TmaLoad2D(sq + c * kAttnChunk, mq, q_full, c * 64, qi * kAttnBlk);
+      for (int j = 0; j < k_blocks; ++j) {
+        const int st = j & 1;
+        MbarWait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        uint8_t* sk = skv + st * kAttnKV;
+        uint8_t* sv = sk + 2 * kAttnChunk;
+        MbarExpectTx(&kv_full[st], kAttnKV);
+        for (int c = 0; c < 2; ++c) TmaLoad2D(sk + c * kAttnChunk, mk, &kv_full[st], c * 64, j * kAttnBlk);
+        for (int c = 0; c < 2; ++c) TmaLoad2D(sv + c * kAttnChunk, mv, &kv_full[st], c * 64, j * kAttnBlk);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer ----------------
+      MbarWait(q_full, 0);
+      const uint32_t aq = SmemU32(sq);
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        MbarWait(&kv_full[st], (j >> 1) & 1);
+        MbarWait(&s_empty[st], ((j >> 1) & 1) ^ 1);
+        FenceAfter();
+        const uint32_t ak = SmemU32(skv + st * kAttnKV);
+#pragma unroll
+        for (int k = 0; k < kAttnD / 16; ++k)
+          MmaF16(tmem + st * kAttnBlk, DescSw128(aq + (k / 4) * kAttnChunk + (k % 4) * 32, 16, 1024),
+                 DescSw128(ak + (k / 4) * kAttnChunk + (k % 4) * 32, 16, 1024), kAttnIdescS, k != 0);
+        Commit(&s_full[st]);
+      };
+      issue_s(0);
+      const uint32_t ap = SmemU32(sp);
+      for (int j = 0; j < k_blocks; ++j) {
+        if (j + 1 < k_blocks) issue_s(j + 1);
+        MbarWait(p_full, j & 1);
+        FenceAfter();
+        const uint32_t av = SmemU32(skv + (j & 1) * kAttnKV + 2 * kAttnChunk);
+#pragma unroll
+        for (int k = 0; k < kAttnBlk / 16; ++k)
+          MmaF16(tmem + 2 * kAttnBlk, DescSw128(ap + (k / 4) * kAttnChunk + (k % 4) * 32, 16, 1024),
+                 DescSw128(av + k * 16 * 128, 64 * kAttnBlk * 2, 1024), kAttnIdescO, (j | k) != 0);
+        Commit(p_empty);
+        Commit(&kv_empty[j & 1]);
+      }
+      Commit(o_full);
+    }
+  } else if (warp >= 4) {  // ---------------- chain + output epilogue ----------------
+    const int ew = warp - 4;  // TMEM lanes / rows [32*ew, 32*ew + 32)
+    const uint16_t* tp[kMaxTanhRuns];
+    StageEpiTables(epi, reinterpret_cast<uint16_t*>(tab_area), threadIdx.x - 128, tp);
+    const int r = ew * 32 + lane;  // row of the 128-row tile
+    for (int j = 0; j < k_blocks; ++j) {
+      const int st = j & 1;
+      MbarWait(&s_full[st], (j >> 1) & 1);
+      FenceAfter();
+      if (j > 0) MbarWait(p_empty, (j - 1) & 1);  // the previous O MMA has read P
+#pragma unroll 1
+      for (int c = 0; c < kAttnBlk / 32; ++c) {
+        uint32_t v[32];
+        TmemLd32(tmem + (static_cast<uint32_t>(ew * 32) << 16) + st * kAttnBlk + c * 32, v);
+        uint32_t p[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) p[t] = PackBf16x2(__uint_as_float(v[2 * t]), __uint_as_float(v[2 * t + 1]));
+        EpiPackedBf16(epi, p, tp);
+        // keys c*32 .. c*32+31 of row r: 64-key chunk c/2, 16-byte units (c%2)*4 + t, 128-byte swizzle
+        uint8_t* row = sp + (c >> 1) * kAttnChunk + r * 128;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          *reinterpret_cast<uint4*>(row + ((((c & 1) * 4 + t) ^ (r & 7)) << 4)) =
+              make_uint4(p[4 * t], p[4 * t + 1], p[4 * t + 2], p[4 * t + 3]);
+      }
+      FenceBefore();
+      FenceProxyAsyncSmem();  // generic-proxy P stores -> the MMA's async-proxy reads
+      __syncwarp();
+      if (lane == 0) {
+        MbarArrive(&s_empty[st]);
+        MbarArrive(p_full);
+      }
+    }
+    MbarWait(o_full, 0);
+    FenceAfter();
+    uint8_t* stage_c = stage_base + ew * 4096;
+    uint32_t boxes = 0;
+#pragma unroll 1
+    for (int c = 0; c < kAttnD / 32; ++c) {
+      uint32_t v[32];
+      TmemLd32(tmem + (static_cast<uint32_t>(ew * 32) << 16) + 2 * kAttnBlk + c * 32, v);
+      uint32_t p[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) p[t] = PackBf16x2(__uint_as_float(v[2 * t]), __uint_as_float(v[2 * t + 1]));
+      EpiStoreBox(stage_c, boxes++, p, mo, c * 32, qi * kAttnBlk + ew * 32, lane);
+    }
+    if (lane == 0) BulkWaitAll();
+  }
+  FenceBefore();
+  __syncthreads();
+  FenceAfter();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
 }  // namespace
 
 size_t GemmTf32x3ScratchBytes(const GemmArgs& g) {
@@ -1747,4 +1919,43 @@ void LaunchGemmTc(const GemmArgs& g, cudaStream_t s) {
   }
 }
 
+
+// ------------------------- fused score -> chain -> context: host side -------------------------
+bool AttnChainSupported(int n_heads, int64_t sq, int64_t sk, int64_t d) {
+  return n_heads > 0 && d == kAttnD && sq > 0 && sk > 0 && sq % kAttnBlk == 0 && sk % kAttnBlk == 0 &&
+         static_cast<int64_t>(n_heads) * (sq / kAttnBlk) < (int64_t{1} << 31) && sk / kAttnBlk < (1 << 30);
+}
+size_t AttnChainTableBytes(int n_heads) { return static_cast<size_t>(n_heads) * 4 * sizeof(CUtensorMap); }
+
+void PrepareAttnChain(int n_heads, int64_t sq, int64_t sk, const void* const* q, const void* const* k,
+                      const void* const* v, void* const* o, void* table) {
+  std::vector<CUtensorMap> m(static_cast<size_t>(n_heads) * 4);
+  for (int h = 0; h < n_heads; ++h) {
+    for (const void* ptr : {q[h], k[h], v[h], static_cast<const void*>(o[h])})
+      if (reinterpret_cast<uintptr_t>(ptr) % 16) Fail("attention chain: unaligned operand");
+    m[4 * h + 0] = MakeMap(q[h], kAttnD, sq, kAttnD, 64, kAttnBlk);  // Q [sq, 128]: K-major A
+    m[4 * h + 1] = MakeMap(k[h], kAttnD, sk, kAttnD, 64, kAttnBlk);  // K [sk, 128]: K-major B
+    m[4 * h + 2] = MakeMap(v[h], kAttnD, sk, kAttnD, 64, kAttnBlk);  // V [sk, 128]: MN-major B
+    m[4 * h + 3] = MakeMap(o[h], kAttnD, sq, kAttnD, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
+  }
+  RH_CUDA(cudaMemcpy(table, m.data(), m.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+}
+
+void LaunchAttnChain(int n_heads, int64_t sq, int64_t sk, const ChainArgs& epi, const void* table, cudaStream_t s) {
+  for (int i = 0; i < epi.n_fn; ++i) {
+    const int fn = epi.fns[i];
+    if (fn != RH_FN_RELU && fn != RH_FN_NEG && fn != RH_FN_IDENTITY && !(fn >= kFnTanhRun && fn - kFnTanhRun < epi.n_tab))
+      Fail("attention chain: the score chain takes only relu / neg / identity / tanh runs", RH_ERR_UNSUPPORTED);
+  }
+  int dev = 0;
+  RH_CUDA(cudaGetDevice(&dev));
+  static bool attr[64] = {};
+  if (dev < 64 && !attr[dev]) {
+    RH_CUDA(cudaFuncSetAttribute(AttnChainKernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
+    attr[dev] = true;
+  }
+  const int qb = static_cast<int>(sq / kAttnBlk), kb = static_cast<int>(sk / kAttnBlk);
+  LaunchPdl(AttnChainKernel, n_heads * qb, kThreads, kAttnSmem, s, static_cast<const CUtensorMap*>(table), qb, kb, epi);
+  RH_CUDA(cudaGetLastError());
+}
 }  // namespace rh

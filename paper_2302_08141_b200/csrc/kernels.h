@@ -248,6 +248,16 @@ void PrepareGemmTcGroup(const GemmArgs& g, int n_prob, const void* const* a, con
 void ReleaseGemmTcGroup(const void* table);
 void LaunchGemmTcGroup(const GemmArgs& g, const void* table, cudaStream_t s);
 
+// Fused attention-head chain (the 32-head block): per head h, O_h = chain(round(Q_h K_h^T)) V_h
+// with Q_h [sq, 128], K_h / V_h [sk, 128], O_h [sq, 128] bf16 row-major and `epi` the score
+// GEMM's epilogue chain; the sq x sk scores stay on chip.  PrepareAttnChain writes the per-head
+// TMA maps (AttnChainTableBytes) once.
+bool AttnChainSupported(int n_heads, int64_t sq, int64_t sk, int64_t d);
+size_t AttnChainTableBytes(int n_heads);
+void PrepareAttnChain(int n_heads, int64_t sq, int64_t sk, const void* const* q, const void* const* k,
+                      const void* const* v, void* const* o, void* table);
+void LaunchAttnChain(int n_heads, int64_t sq, int64_t sk, const ChainArgs& epi, const void* table, cudaStream_t s);
+
 // --------------------------------------- cross-GPU sync --------------------------------------
 // Group barrier over CUDA-IPC-mapped flag arrays (one process per GPU only: every member runs on
 // its own GPU, so the spin never waits on a kernel of the same GPU).

@@ -369,7 +369,11 @@ def test_gpt_block_bf16(rx, oracle_lib, name):
         names = [s["name"] for s in gp.steps()]
         assert any("gemm_tc" in n for n in names)
         if "heads32" in name:
-            assert sum(n.startswith("gemm_tc_group[") for n in names) >= 3, names
+            # q/k/v, score and context: three grouped launches, or q/k/v plus the fused
+            # score -> chain -> context kernel (the scores never reach HBM)
+            groups = sum(n.startswith("gemm_tc_group[") for n in names)
+            attn = sum(n.startswith("attn_chain[") for n in names)
+            assert groups + 2 * attn >= 3, names
             if prog.world > 1:
                 assert any(n.startswith("grouped[") for n in names), names
     finally:
@@ -502,3 +506,76 @@ def test_remat_scalar_tail_bit_exact(rx, monkeypatch, m, n):
     for a, b in zip(outs["remat"], outs["ref"]):
         np.testing.assert_array_equal(a, b)
     print(steps["remat"])
+
+
+_JIT_DUMP = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2302_08141_b200 import runtime as rx
+from paper_2302_08141_b200.abi import RH_BF16
+from paper_2302_08141_b200.program import LoweredProgram
+prog = LoweredProgram.load(sys.argv[2]).with_dtype(RH_BF16)
+rt = rx.Runtime(devices=[0] * prog.world)
+mesh = rx.Mesh(rt, prog.mesh)
+gp = rx.Program(mesh, prog, int(sys.argv[4]))
+gp.init_synthetic(11)
+gp.run(1)
+np.savez(sys.argv[3], *[gp.read_full(o) for o in prog.outputs])
+gp.close(); mesh.close(); rt.close()
+"""
+
+
+@pytest.mark.parametrize("name", ["c5_big_gpt1_d1", "c5_gpt_small_d4", "c3_gpt_block_d1"])
+def test_ew_jit_matches_interpreter(rx, tmp_path, name):
+    """The per-program elementwise kernels (NVRTC, ew_jit.cpp) against the nvcc-built interpreter
+    kernels (RH_EW_JIT=0, read once per process: a subprocess): bit-identical outputs on the
+    rematerializing, ladder and plain chain programs of the full-size C5 layer and C3."""
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    prog = LoweredProgram.load(name).with_dtype(RH_BF16)
+    flags = RH_FLAG_REDUCE_OUTPUTS if name.startswith("c5_") else 0
+    rt, mesh, gp = load(rx, prog, flags)
+    try:
+        gp.init_synthetic(11)
+        gp.run(1)
+        got = [gp.read_full(o) for o in prog.outputs]
+        names = [s["name"] for s in gp.steps()]
+    finally:
+        close(rt, mesh, gp)
+    assert any(n.startswith("ew_chain") for n in names), names[:20]
+    out = tmp_path / "interp.npz"
+    env = dict(os.environ, RH_EW_JIT="0")
+    subprocess.run([sys.executable, "-c", _JIT_DUMP, repo, name, str(out), str(flags)], env=env, check=True,
+                   timeout=600)
+    ref = np.load(out)
+    for k, a in enumerate(got):
+        np.testing.assert_array_equal(a, ref[f"arr_{k}"], err_msg=f"{name}: output {k}")
+
+
+@pytest.mark.parametrize("name", ["c3_gpt_heads32_d1", "c3_gpt_heads32_d4"])
+def test_attn_chain_matches_grouped(rx, tmp_path, name):
+    """The fused score -> chain -> context kernel (attn_chain) against the two grouped GEMM
+    launches it replaces (RH_NO_ATTN_FUSION=1, read once per process: a subprocess): the chained
+    scores are the score group's exact values and the context accumulates the same MMA steps in
+    key order, so the block's output is bit-identical."""
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    prog = LoweredProgram.load(name).with_dtype(RH_BF16)
+    rt, mesh, gp = load(rx, prog, 0)
+    try:
+        gp.init_synthetic(11)
+        gp.run(1)
+        got = [gp.read_full(o) for o in prog.outputs]
+        names = [s["name"] for s in gp.steps()]
+    finally:
+        close(rt, mesh, gp)
+    assert any(n.startswith("attn_chain[") for n in names), names[:20]
+    out = tmp_path / "grouped.npz"
+    env = dict(os.environ, RH_NO_ATTN_FUSION="1")
+    subprocess.run([sys.executable, "-c", _JIT_DUMP, repo, name, str(out), "0"], env=env, check=True, timeout=900)
+    ref = np.load(out)
+    for k, a in enumerate(got):
+        np.testing.assert_array_equal(a, ref[f"arr_{k}"], err_msg=f"{name}: output {k}")
