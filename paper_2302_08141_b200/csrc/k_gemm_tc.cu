@@ -1506,11 +1506,14 @@ constexpr int kAttnChunk = kAttnBlk * 128;                     // one 64-wide K 
 constexpr int kAttnQ = 2 * kAttnChunk;                         // Q_i: [128 rows x 128 K]
 constexpr int kAttnKV = 4 * kAttnChunk;                        // K_j + V_j per stage
 constexpr int kAttnP = 2 * kAttnChunk;                         // P_j: [128 rows x 128 keys]
-constexpr int kAttnSmem = kAttnQ + 2 * kAttnKV + kAttnP + 1024 + kEpiTabBytes + kEpiStageBytes + 1024;
+constexpr int kAttnEpi = 8;                                    // epilogue warps: 2 per TMEM lane quarter
+constexpr int kAttnThreads = 128 + 32 * kAttnEpi;
+// (the output staging of the final epilogue reuses the P buffer: the last MMA has read it)
+constexpr int kAttnSmem = kAttnQ + 2 * kAttnKV + kAttnP + 1024 + kEpiTabBytes + 1024;
 constexpr uint32_t kAttnIdescS = TcCfg<128, true, true, 128>::kIdesc;   // B = K_j, K-major
 constexpr uint32_t kAttnIdescO = TcCfg<128, false, true, 128>::kIdesc;  // B = V_j, MN-major
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kAttnThreads, 1)
     AttnChainKernel(const CUtensorMap* __restrict__ maps, int q_blocks, int k_blocks, ChainArgs epi) {
   PdlTrigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1529,7 +1532,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* o_full = bars + 11;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
   uint8_t* tab_area = reinterpret_cast<uint8_t*>(bars) + 1024;
-  uint8_t* stage_base = tab_area + kEpiTabBytes;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int head = blockIdx.x / q_blocks, qi = blockIdx.x % q_blocks;
@@ -1544,9 +1546,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       MbarInit(&kv_full[b], 1);
       MbarInit(&kv_empty[b], 1);
       MbarInit(&s_full[b], 1);
-      MbarInit(&s_empty[b], 4);
+      MbarInit(&s_empty[b], kAttnEpi);
     }
-    MbarInit(p_full, 4);
+    MbarInit(p_full, kAttnEpi);
     MbarInit(p_empty, 1);
     MbarInit(o_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1609,50 +1611,58 @@ __global__ void __launch_bounds__(kThreads, 1)
       Commit(o_full);
     }
   } else if (warp >= 4) {  // ---------------- chain + output epilogue ----------------
-    const int ew = warp - 4;  // TMEM lanes / rows [32*ew, 32*ew + 32)
+    // warp ew: TMEM lane quarter ew % 4 (rows [32*q, 32*q + 32)), 32-column chunks ew / 4 + 2i
+    const int ew = warp - 4, quarter = ew % 4, half = ew / 4;
     const uint16_t* tp[kMaxTanhRuns];
-    StageEpiTables(epi, reinterpret_cast<uint16_t*>(tab_area), threadIdx.x - 128, tp);
-    const int r = ew * 32 + lane;  // row of the 128-row tile
+    StageEpiTables(epi, reinterpret_cast<uint16_t*>(tab_area), threadIdx.x - 128, tp, 32 * kAttnEpi);
+    const int r = quarter * 32 + lane;  // row of the 128-row tile
+    constexpr int kCh = kAttnBlk / 32 / (kAttnEpi / 4);  // 32-column chunks per warp and block
     for (int j = 0; j < k_blocks; ++j) {
       const int st = j & 1;
       MbarWait(&s_full[st], (j >> 1) & 1);
       FenceAfter();
-      if (j > 0) MbarWait(p_empty, (j - 1) & 1);  // the previous O MMA has read P
-#pragma unroll 1
-      for (int c = 0; c < kAttnBlk / 32; ++c) {
-        uint32_t v[32];
-        TmemLd32(tmem + (static_cast<uint32_t>(ew * 32) << 16) + st * kAttnBlk + c * 32, v);
-        uint32_t p[16];
+      // S_j -> bf16 -> chain into registers first: this overlaps the previous O MMA, and the S
+      // buffer goes back to the MMA warp before P is written
+      uint32_t pk[kCh][16];
 #pragma unroll
-        for (int t = 0; t < 16; ++t) p[t] = PackBf16x2(__uint_as_float(v[2 * t]), __uint_as_float(v[2 * t + 1]));
-        EpiPackedBf16(epi, p, tp);
+      for (int ci = 0; ci < kCh; ++ci) {
+        const int c = half + ci * (kAttnEpi / 4);
+        uint32_t v[32];
+        TmemLd32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + st * kAttnBlk + c * 32, v);
+#pragma unroll
+        for (int t = 0; t < 16; ++t) pk[ci][t] = PackBf16x2(__uint_as_float(v[2 * t]), __uint_as_float(v[2 * t + 1]));
+        EpiPackedBf16(epi, pk[ci], tp);
+      }
+      FenceBefore();
+      __syncwarp();
+      if (lane == 0) MbarArrive(&s_empty[st]);
+      if (j > 0) MbarWait(p_empty, (j - 1) & 1);  // the previous O MMA has read P
+#pragma unroll
+      for (int ci = 0; ci < kCh; ++ci) {
+        const int c = half + ci * (kAttnEpi / 4);
         // keys c*32 .. c*32+31 of row r: 64-key chunk c/2, 16-byte units (c%2)*4 + t, 128-byte swizzle
         uint8_t* row = sp + (c >> 1) * kAttnChunk + r * 128;
 #pragma unroll
         for (int t = 0; t < 4; ++t)
           *reinterpret_cast<uint4*>(row + ((((c & 1) * 4 + t) ^ (r & 7)) << 4)) =
-              make_uint4(p[4 * t], p[4 * t + 1], p[4 * t + 2], p[4 * t + 3]);
+              make_uint4(pk[ci][4 * t], pk[ci][4 * t + 1], pk[ci][4 * t + 2], pk[ci][4 * t + 3]);
       }
-      FenceBefore();
       FenceProxyAsyncSmem();  // generic-proxy P stores -> the MMA's async-proxy reads
       __syncwarp();
-      if (lane == 0) {
-        MbarArrive(&s_empty[st]);
-        MbarArrive(p_full);
-      }
+      if (lane == 0) MbarArrive(p_full);
     }
-    MbarWait(o_full, 0);
+    MbarWait(o_full, 0);  // every MMA done: P is free for the output staging
     FenceAfter();
-    uint8_t* stage_c = stage_base + ew * 4096;
+    uint8_t* stage_c = sp + ew * 4096;
     uint32_t boxes = 0;
 #pragma unroll 1
-    for (int c = 0; c < kAttnD / 32; ++c) {
+    for (int c = half; c < kAttnD / 32; c += kAttnEpi / 4) {
       uint32_t v[32];
-      TmemLd32(tmem + (static_cast<uint32_t>(ew * 32) << 16) + 2 * kAttnBlk + c * 32, v);
+      TmemLd32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + 2 * kAttnBlk + c * 32, v);
       uint32_t p[16];
 #pragma unroll
       for (int t = 0; t < 16; ++t) p[t] = PackBf16x2(__uint_as_float(v[2 * t]), __uint_as_float(v[2 * t + 1]));
-      EpiStoreBox(stage_c, boxes++, p, mo, c * 32, qi * kAttnBlk + ew * 32, lane);
+      EpiStoreBox(stage_c, boxes++, p, mo, c * 32, qi * kAttnBlk + quarter * 32, lane);
     }
     if (lane == 0) BulkWaitAll();
   }
@@ -1955,7 +1965,7 @@ void LaunchAttnChain(int n_heads, int64_t sq, int64_t sk, const ChainArgs& epi, 
     attr[dev] = true;
   }
   const int qb = static_cast<int>(sq / kAttnBlk), kb = static_cast<int>(sk / kAttnBlk);
-  LaunchPdl(AttnChainKernel, n_heads * qb, kThreads, kAttnSmem, s, static_cast<const CUtensorMap*>(table), qb, kb, epi);
+  LaunchPdl(AttnChainKernel, n_heads * qb, kAttnThreads, kAttnSmem, s, static_cast<const CUtensorMap*>(table), qb, kb, epi);
   RH_CUDA(cudaGetLastError());
 }
 }  // namespace rh
