@@ -1506,7 +1506,7 @@ constexpr int kAttnChunk = kAttnBlk * 128;                     // one 64-wide K 
 constexpr int kAttnQ = 2 * kAttnChunk;                         // Q_i: [128 rows x 128 K]
 constexpr int kAttnKV = 4 * kAttnChunk;                        // K_j + V_j per stage
 constexpr int kAttnP = 2 * kAttnChunk;                         // P_j: [128 rows x 128 keys]
-constexpr int kAttnEpi = 8;                                    // epilogue warps: 2 per TMEM lane quarter
+constexpr int kAttnEpi = 16;  // epilogue warps: 4 per TMEM lane quarter, one 32-column chunk each per block
 constexpr int kAttnThreads = 128 + 32 * kAttnEpi;
 // (the output staging of the final epilogue reuses the P buffer: the last MMA has read it)
 constexpr int kAttnSmem = kAttnQ + 2 * kAttnKV + kAttnP + 1024 + kEpiTabBytes + 1024;
@@ -1522,15 +1522,19 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint8_t* skv = sq + kAttnQ;
   uint8_t* sp = skv + 2 * kAttnKV;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sp + kAttnP);
+  // K_j and V_j have their own stages: K_j is free once S_j is computed, V_j only after O += P_j V_j,
+  // so K can be fetched two blocks ahead of its use (one shared stage serialized the TMA latency)
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* s_empty = bars + 7;   // [2]
-  uint64_t* p_full = bars + 9;
-  uint64_t* p_empty = bars + 10;
-  uint64_t* o_full = bars + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* k_full = bars + 1;   // [2]
+  uint64_t* k_empty = bars + 3;  // [2]
+  uint64_t* v_full = bars + 5;   // [2]
+  uint64_t* v_empty = bars + 7;  // [2]
+  uint64_t* s_full = bars + 9;   // [2]
+  uint64_t* s_empty = bars + 11; // [2]
+  uint64_t* p_full = bars + 13;
+  uint64_t* p_empty = bars + 14;
+  uint64_t* o_full = bars + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
   uint8_t* tab_area = reinterpret_cast<uint8_t*>(bars) + 1024;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -1543,8 +1547,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   if (warp == 0 && lane == 0) {
     MbarInit(q_full, 1);
     for (int b = 0; b < 2; ++b) {
-      MbarInit(&kv_full[b], 1);
-      MbarInit(&kv_empty[b], 1);
+      MbarInit(&k_full[b], 1);
+      MbarInit(&k_empty[b], 1);
+      MbarInit(&v_full[b], 1);
+      MbarInit(&v_empty[b], 1);
       MbarInit(&s_full[b], 1);
       MbarInit(&s_empty[b], kAttnEpi);
     }
@@ -1568,14 +1574,24 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     if (lane == 0) {  // ---------------- TMA producer ----------------
       MbarExpectTx(q_full, kAttnQ);
       for (int c = 0; c < 2; ++c) TmaLoad2D(sq + c * kAttnChunk, mq, q_full, c * 64, qi * kAttnBlk);
-      for (int j = 0; j < k_blocks; ++j) {
+      auto load_k = [&](int j) {
         const int st = j & 1;
-        MbarWait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        MbarWait(&k_empty[st], ((j >> 1) & 1) ^ 1);
         uint8_t* sk = skv + st * kAttnKV;
-        uint8_t* sv = sk + 2 * kAttnChunk;
-        MbarExpectTx(&kv_full[st], kAttnKV);
-        for (int c = 0; c < 2; ++c) TmaLoad2D(sk + c * kAttnChunk, mk, &kv_full[st], c * 64, j * kAttnBlk);
-        for (int c = 0; c < 2; ++c) TmaLoad2D(sv + c * kAttnChunk, mv, &kv_full[st], c * 64, j * kAttnBlk);
+        MbarExpectTx(&k_full[st], 2 * kAttnChunk);
+        for (int c = 0; c < 2; ++c) TmaLoad2D(sk + c * kAttnChunk, mk, &k_full[st], c * 64, j * kAttnBlk);
+      };
+      auto load_v = [&](int j) {
+        const int st = j & 1;
+        MbarWait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        uint8_t* sv = skv + st * kAttnKV + 2 * kAttnChunk;
+        MbarExpectTx(&v_full[st], 2 * kAttnChunk);
+        for (int c = 0; c < 2; ++c) TmaLoad2D(sv + c * kAttnChunk, mv, &v_full[st], c * 64, j * kAttnBlk);
+      };
+      // K runs one block ahead of V: K0 K1 V0 K2 V1 ... (a V wait never delays the next K)
+      for (int j = 0; j <= k_blocks; ++j) {
+        if (j < k_blocks) load_k(j);
+        if (j > 0) load_v(j - 1);
       }
     }
   } else if (warp == 1) {
@@ -1584,7 +1600,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const uint32_t aq = SmemU32(sq);
       auto issue_s = [&](int j) {
         const int st = j & 1;
-        MbarWait(&kv_full[st], (j >> 1) & 1);
+        MbarWait(&k_full[st], (j >> 1) & 1);
         MbarWait(&s_empty[st], ((j >> 1) & 1) ^ 1);
         FenceAfter();
         const uint32_t ak = SmemU32(skv + st * kAttnKV);
@@ -1593,12 +1609,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           MmaF16(tmem + st * kAttnBlk, DescSw128(aq + (k / 4) * kAttnChunk + (k % 4) * 32, 16, 1024),
                  DescSw128(ak + (k / 4) * kAttnChunk + (k % 4) * 32, 16, 1024), kAttnIdescS, k != 0);
         Commit(&s_full[st]);
+        Commit(&k_empty[st]);
       };
       issue_s(0);
       const uint32_t ap = SmemU32(sp);
       for (int j = 0; j < k_blocks; ++j) {
         if (j + 1 < k_blocks) issue_s(j + 1);
         MbarWait(p_full, j & 1);
+        MbarWait(&v_full[j & 1], (j >> 1) & 1);
         FenceAfter();
         const uint32_t av = SmemU32(skv + (j & 1) * kAttnKV + 2 * kAttnChunk);
 #pragma unroll
@@ -1606,7 +1624,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           MmaF16(tmem + 2 * kAttnBlk, DescSw128(ap + (k / 4) * kAttnChunk + (k % 4) * 32, 16, 1024),
                  DescSw128(av + k * 16 * 128, 64 * kAttnBlk * 2, 1024), kAttnIdescO, (j | k) != 0);
         Commit(p_empty);
-        Commit(&kv_empty[j & 1]);
+        Commit(&v_empty[j & 1]);
       }
       Commit(o_full);
     }
@@ -1653,7 +1671,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     }
     MbarWait(o_full, 0);  // every MMA done: P is free for the output staging
     FenceAfter();
-    uint8_t* stage_c = sp + ew * 4096;
+    // one or two 2 KB boxes per warp: kAttnEpi warps x that fit in the 32 KB P buffer
+    constexpr int kBoxes = kAttnD / 32 / (kAttnEpi / 4);
+    static_assert(kAttnEpi * (kBoxes > 1 ? 4096 : 2048) <= kAttnP, "output staging exceeds the P buffer");
+    uint8_t* stage_c = sp + ew * (kBoxes > 1 ? 4096 : 2048);
     uint32_t boxes = 0;
 #pragma unroll 1
     for (int c = half; c < kAttnD / 32; c += kAttnEpi / 4) {
