@@ -219,3 +219,39 @@ bool EwJitLaunch(const EwArgs& a, int blocks, size_t smem, cudaStream_t s) {
 }
 
 }  // namespace rh
+
+// Test hook (not part of include/rhino_exec.h): NVRTC-compiles one program of every kernel
+// family from the embedded headers — no GPU needed — so the CPU suite catches a header the
+// run-time compiler rejects.  Returns the cubin size, 0 on a compile failure (log printed).
+extern "C" long long rh_test_ew_jit_compile() {
+  using namespace rh;
+  auto I = [](int op, int arg) { return op | (arg << 8); };
+  std::vector<JitEntry> es(6);
+  es[0].kind = kEwKindRematHalf;
+  es[0].n_in = 2;
+  es[0].code = {I(kEwLoad, 0), I(kEwTanhBwdLad, 6 | (7 << 4)), I(kEwStore, 0)};
+  es[1].kind = kEwKindBf16;
+  es[1].n_in = 2;
+  es[1].code = {I(kEwLoad, 0), I(kEwUnary, kFnTanhRun), I(kEwStore, 0), I(kEwUnary, kFnTanhRun + 1), I(kEwKeep, 0),
+                I(kEwAdd, 1), I(kEwStore, 1), I(kEwUnary, RH_FN_GELU)};
+  es[2].kind = kEwKindF32;
+  es[2].n_in = 2;
+  es[2].code = {I(kEwLoad, 0), I(kEwUnary, RH_FN_TANH), I(kEwTanhBwd, 1), I(kEwStore, 0), I(kEwMul, kEwSrcKeep)};
+  es[3].kind = kEwKindLadder;
+  es[3].n_in = 1;
+  es[3].code = {I(kEwLoad, 0), I(kEwUnary, kFnTanhRun)};
+  es[4].kind = kEwKindRematFull;
+  es[4].n_in = 3;
+  es[4].code = {I(kEwLoad, 0), I(kEwTanhBwd, kEwSrcVirt + 1), I(kEwTanhBwdLad, 12 | (3 << 4)), I(kEwAdd, 1),
+                I(kEwMul, kEwSrcVirt + 8), I(kEwStore, 0)};
+  es[5].kind = kEwKindLadderRemat;
+  es[5].n_in = 2;
+  es[5].code = {I(kEwLoad, 1), I(kEwMul, kEwSrcVirt)};
+  std::vector<int> ids;
+  std::vector<std::string> bodies;
+  for (int i = 0; i < static_cast<int>(es.size()); ++i) {
+    ids.push_back(i);
+    bodies.push_back(KernelSource(es[i], i));
+  }
+  return static_cast<long long>(Compile(ids, bodies).size());
+}
