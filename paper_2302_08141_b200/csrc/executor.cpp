@@ -298,6 +298,35 @@ FinePlan ClassifyFine(const AxisView& f, const AxisView& t, int eb, int d, int64
   return p;
 }
 
+// The fused-barrier arguments of flag row `slot` for local rank li's group on `axis` (the pull
+// kernels' PeerSync, also used by the GEMM output push and its post-barrier).
+PeerSync SyncOf(const rh_program* P, int axis, int slot, int li) {
+  PeerSync y{};
+  if (slot < 0) return y;
+  const int g = P->mesh->rt->first_rank + li;
+  const std::vector<int> members = P->mesh->Group(axis, g);
+  const size_t row = P->sync_off + static_cast<size_t>(slot) * P->mesh->rt->world * 4;
+  y.d = static_cast<int>(members.size());
+  y.me = g;
+  for (size_t k = 0; k < members.size(); ++k) {
+    y.members[k] = members[k];
+    y.peer_slot[k] = reinterpret_cast<uint32_t*>(P->peer_base[members[k]] + row);
+  }
+  y.my_slot = reinterpret_cast<uint32_t*>(P->peer_base[g] + row);
+  y.epoch = reinterpret_cast<const uint32_t*>(P->peer_base[g] + P->epoch_off);
+  y.err = reinterpret_cast<uint32_t*>(P->peer_base[g] + P->err_off);
+  y.timeout_ns = SyncTimeoutNs();
+  return y;
+}
+
+// A GEMM step's output push (GemmPush), filled in when the output's materialization is fused
+// into it (TryPushMaterialize), after the step was emitted.
+struct PushPlan {
+  int dst_t = -1;  // the replicated copy every member's kernel writes into
+  int axis = 0, slot = -1;
+  int64_t rows_local = 0;
+};
+
 class Lowerer {
  public:
   explicit Lowerer(rh_program* p) : p_(p), mesh_(p->mesh->dims), rt_(p->mesh->rt) {}
@@ -381,6 +410,7 @@ class Lowerer {
     } else if (!(p_->flags & RH_FLAG_NO_MATERIALIZE)) {
       for (int o : p_->outputs) {
         cur_stage_ = StageOfOp(o);
+        if (TryPushMaterialize(o)) continue;
         Specs rep(p_->n_axes, Rep());
         p_->mat_tensor[o] = GetTensor(o, rep, "materialize");
       }
@@ -1343,6 +1373,67 @@ class Lowerer {
     (void)g2;
     return true;
   }
+  // Output materialization fused into the producing GEMM (dist runs): a bf16 tcgen05 GEMM (no
+  // split-K) whose output is sharded by contiguous row blocks on one mesh axis and replicated on
+  // the others pushes every output tile, from its epilogue, into the replicated copy of every
+  // member of that axis (GemmPush; the GEMM's own barrier, fused into it, orders the pushes
+  // after every member's copy is free).  The pull all-gather after the GEMM becomes a barrier
+  // step (every push landed).  RH_NO_PUSH_MATERIALIZE disables.
+  bool TryPushMaterialize(int o) {
+    static const bool off = getenv("RH_NO_PUSH_MATERIALIZE") != nullptr;
+    if (off || !rt_->dist || rt_->world <= 1 || p_->pipeline_axis >= 0) return false;
+    auto it = gemm_push_.find(o);
+    if (it == gemm_push_.end() || p_->out_tensor[o] < 0) return false;
+    const Tensor T = p_->tensors[p_->out_tensor[o]];
+    if (T.alias >= 0 || T.gdims.size() != 2) return false;
+    int axis = -1;
+    for (int a = 0; a < p_->n_axes; ++a) {
+      const rh_spec& sp = T.specs[a];
+      if (sp.kind == RH_REPLICATED) continue;
+      if (sp.kind != RH_SHARD || sp.dim != 0 || axis >= 0) return false;
+      if (sp.stride * mesh_[a] != T.gdims[0]) return false;  // one contiguous row block per rank
+      axis = a;
+    }
+    if (axis < 0 || mesh_[axis] > kMaxGroup) return false;
+    GemmArgs g = it->second.g;
+    if (!GemmTcPushSupported(g) || g.m != T.ldims[0] || g.n != T.gdims[1]) return false;
+    Specs rep(p_->n_axes, Rep());
+    const int dst = NewTensor(o, rep);
+    p_->mat_tensor[o] = dst;
+    PushPlan& pp = *it->second.plan;
+    pp.dst_t = dst;
+    pp.axis = axis;
+    pp.slot = p_->n_sync_slots++;
+    pp.rows_local = T.ldims[0];
+    p_->steps[it->second.step].name += " [+all_gather push]";
+    p_->steps[it->second.step].writes.push_back(dst);
+    Step st;
+    st.kind = Step::kTransition;
+    st.axis = axis;
+    st.p2p = true;
+    st.no_async = true;
+    st.post_mode = 2;  // itself the barrier after the pushes
+    st.sync_slot = p_->n_sync_slots++;
+    st.name = "all_gather op" + std::to_string(o) + " " + SpecStr(T.specs[axis]) + "->R@" + std::to_string(axis) +
+              " (materialize) [pushed by the GEMM; barrier]";
+    st.launches = 1;
+    rh_program* P = p_;
+    const int slot = st.sync_slot;
+    st.run = [P, axis, slot](int li, cudaStream_t s) {
+      LaunchPeerSync(SyncOf(P, axis, slot, li), s);
+      return 1;
+    };
+    st.writes = {dst};
+    AddStep(std::move(st));
+    return true;
+  }
+  struct GemmPushRef {
+    std::shared_ptr<PushPlan> plan;
+    GemmArgs g;
+    int step;
+  };
+  std::map<int, GemmPushRef> gemm_push_;  // op whose value a tcgen05 GEMM step writes -> its push plan
+
   std::vector<int> attn_pair_;                 // score group -> context group (-1: none)
   std::vector<bool> attn_done_;                // context group emitted inside its score group's kernel
   std::map<int, std::vector<int>> attn_ctx_;   // score group -> context members, score order
@@ -2132,13 +2223,22 @@ class Lowerer {
         const int ta = in_t[0], tb = in_t[1];
         const int rs = resid_t;
         if (rs >= 0) st.name += " +add " + OpName(resid_[i].v);
-        st.run = [P, g, ta, tb, out_t, first, tc, rs](int li, cudaStream_t s) {
+        auto pp = std::make_shared<PushPlan>();
+        if (tc && dtype == RH_BF16) gemm_push_[Tail(i)] = {pp, g, static_cast<int>(p_->steps.size())};
+        st.run = [P, g, ta, tb, out_t, first, tc, rs, pp](int li, cudaStream_t s) {
           GemmArgs a = g;
           const int r = first + li;
           a.a = P->Ptr(P->tensors[ta], r);
           a.b = P->Ptr(P->tensors[tb], r);
           a.c = P->Ptr(P->tensors[out_t], r);
           if (rs >= 0) a.resid = P->Ptr(P->tensors[rs], r);
+          if (pp->dst_t >= 0) {  // the output all-gather, fused (TryPushMaterialize)
+            a.push.sync = SyncOf(P, pp->axis, pp->slot, li);
+            a.push.n = a.push.sync.d;
+            for (int k = 0; k < a.push.n; ++k) a.push.dst[k] = P->Ptr(P->tensors[pp->dst_t], a.push.sync.members[k]);
+            a.push.row_off = P->mesh->Coords(r)[pp->axis] * pp->rows_local;
+            a.push.rows_full = P->tensors[pp->dst_t].gdims[0];
+          }
           a.epi = Patch(P, g.epi, r);
           if (P->gemm_scratch_bytes) a.scratch = P->peer_base[r] + P->gemm_scratch_off;
           a.sk_flags = reinterpret_cast<uint32_t*>(P->peer_base[r] + P->gemm_flags_off);

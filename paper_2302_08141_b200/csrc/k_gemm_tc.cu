@@ -41,6 +41,51 @@ __device__ __forceinline__ uint32_t AddBf16x2Epi(uint32_t a, uint32_t b) {
   return d;
 }
 
+// Output push (GemmPush): the fused barrier's arrival and wait (the same flag protocol as the
+// resharding kernels' PeerSync, k_reshard.cu) and the pushed rows.
+__device__ __forceinline__ uint32_t PushLdAcquireSys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// block 0, threads < d: this rank's destination copy is free (every earlier reader of it is
+// done: stream order), signalled into every member's flag row
+// kernel-side form of GemmPush: a 32 x 32 box tensor map of every member's replicated copy
+// (LaunchGemmTc builds them from the pointers); the epilogue's staged output box is stored
+// through each of them right after the local store (bulk NVLink writes to the peers).
+struct PushDev {
+  int n;
+  int row_off;
+  PeerSync sync;
+  CUtensorMap map[kMaxGroup];
+};
+__device__ __forceinline__ void PushArrive(const PushDev& p) {
+  if (p.n == 0 || blockIdx.x != 0 || static_cast<int>(threadIdx.x) >= p.sync.d) return;
+  const uint32_t e = *reinterpret_cast<const volatile uint32_t*>(p.sync.epoch);
+  __threadfence_system();
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p.sync.peer_slot[threadIdx.x] + p.sync.me), "r"(e)
+               : "memory");
+}
+// one lane: every member arrived (bounded: a missing peer records the error and gives up)
+__device__ __forceinline__ void PushWaitAll(const PushDev& p) {
+  const uint32_t e = *reinterpret_cast<const volatile uint32_t*>(p.sync.epoch);
+  for (int t = 0; t < p.sync.d; ++t) {
+    const uint32_t* f = p.sync.my_slot + p.sync.members[t];
+    if (static_cast<int32_t>(PushLdAcquireSys(f) - e) >= 0) continue;
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (uint32_t n = 1; static_cast<int32_t>(PushLdAcquireSys(f) - e) < 0; ++n) {
+      if ((n & 1023) == 0 && p.sync.timeout_ns) {
+        uint64_t t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > p.sync.timeout_ns) {
+          if (p.sync.err) atomicCAS(p.sync.err, 0u, SyncErrorCode(p.sync.me, p.sync.members[t]));
+          break;
+        }
+      }
+    }
+  }
+}
 __device__ __forceinline__ uint32_t SmemU32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -98,8 +143,19 @@ constexpr int kEpiStageBytes = 4 * 2 * 2048;  // 4 epilogue warps x 2 buffers x 
 // One 32-row x 32-column bf16 box of the epilogue (lane = row, p = its 16 packed pairs) through
 // staging buffer `buf` (of 2, alternating) and a TMA store at (c0, c1).  `cnt` = boxes this warp
 // stored before: the buffer's previous store must have been read out before it is rewritten.
+struct PushDev;
 __device__ __forceinline__ void EpiStoreBox(uint8_t* stage, uint32_t cnt, const uint32_t (&p)[16],
-                                            const CUtensorMap* map, int c0, int c1, int lane) {
+                                            const CUtensorMap* map, int c0, int c1, int lane,
+                                            const PushDev* push = nullptr, bool* push_ready = nullptr);
+
+// One 32-row x 32-column bf16 box of the epilogue (lane = row, p = its 16 packed pairs) through
+// staging buffer `buf` (of 2, alternating) and a TMA store at (c0, c1) — and, with `push`, the
+// same box into every member's replicated copy (rows offset by push->row_off), after the fused
+// barrier (first box only).  `cnt` = boxes this warp stored before: the buffer's previous
+// stores must have been read out before it is rewritten.
+__device__ __forceinline__ void EpiStoreBox(uint8_t* stage, uint32_t cnt, const uint32_t (&p)[16],
+                                            const CUtensorMap* map, int c0, int c1, int lane,
+                                            const PushDev* push, bool* push_ready) {
   uint8_t* sb = stage + (cnt & 1) * 2048;
   if (lane == 0 && cnt >= 2) BulkWaitRead<1>();
   __syncwarp();
@@ -111,9 +167,18 @@ __device__ __forceinline__ void EpiStoreBox(uint8_t* stage, uint32_t cnt, const 
   __syncwarp();
   if (lane == 0) {
     TmaStore2D(map, sb, c0, c1);
+    if (push && push->n) {
+      if (!*push_ready) {
+        PushWaitAll(*push);
+        *push_ready = true;
+      }
+      for (int k = 0; k < push->n; ++k) TmaStore2D(&push->map[k], sb, c0, c1 + push->row_off);
+    }
     BulkCommit();
   }
 }
+
+
 
 __device__ __forceinline__ void FenceBefore() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void FenceAfter() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -262,7 +327,8 @@ template <int BN, bool kBKMajor, bool kAKMajor, int KB, bool kGroup = false>
 __global__ void __launch_bounds__(kThreads, 1)
     GemmTcKernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                  const __grid_constant__ CUtensorMap tma_c, int M, int N, int K, ChainArgs epi, int ksplit,
-                 float* __restrict__ ws, GroupDev grp, const __nv_bfloat16* __restrict__ resid) {
+                 float* __restrict__ ws, GroupDev grp, const __nv_bfloat16* __restrict__ resid,
+                 const __grid_constant__ PushDev push) {
   PdlTrigger();
   // Work unit = (m tile, n tile, k split).  ksplit > 1 (few tiles: the sharded GEMMs at N >= 4)
   // writes fp32 partial tiles to ws[split][M][N]; SplitReduceBf16 finishes them.
@@ -304,6 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   FenceAfter();
   const uint32_t tmem = *tmem_slot;
   PdlWait();  // prologue above overlaps the previous kernel's tail (launch.cuh)
+  PushArrive(push);
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer ----------------
@@ -402,6 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t boxes = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    bool push_ready = false;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       const int t = tile % mn, ks = tile / mn;
       const int m_blk = t % num_m, n_blk = t / num_m;
@@ -461,7 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           cmap = grp.cm + col / grp.seg_n;
           col %= grp.seg_n;
         }
-        EpiStoreBox(stage_c, boxes++, p, cmap, col, m_blk * BM + ew * 32, lane);
+        EpiStoreBox(stage_c, boxes++, p, cmap, col, m_blk * BM + ew * 32, lane, &push, &push_ready);
       }
       FenceBefore();
       __syncwarp();
@@ -637,7 +705,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpi, 1)
     GemmTcPairKernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                      const __grid_constant__ CUtensorMap tma_c, int M, int N, int K, ChainArgs epi, int ksplit,
                      float* __restrict__ ws, GroupDev grp, uint32_t* __restrict__ sk_flags,
-                     const __nv_bfloat16* __restrict__ resid) {
+                     const __nv_bfloat16* __restrict__ resid, const __grid_constant__ PushDev push) {
   PdlTrigger();
   using Cfg = Tc2Cfg<BN, kBKMajor, kAKMajor, kEpi>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -681,6 +749,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpi, 1)
   FenceAfter();
   const uint32_t tmem = *tmem_slot;
   PdlWait();
+  PushArrive(push);
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs) ----------------
@@ -782,6 +851,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpi, 1)
     uint32_t acc_phase = 0;
     PairWork w = PairWorkOf(pair, n_pairs, tiles, kblocks, sk);
     const int64_t sk_total = static_cast<int64_t>(tiles) * kblocks;
+    bool push_ready = false;
     constexpr int kSlot = BM * BN;  // floats per CTA slot: [BN/32 chunks][128 rows][32]
     int tile, k0, k1;
     while (NextPairWork(w, tile, k0, k1)) {
@@ -874,7 +944,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpi, 1)
           cmap = grp.cm + col / grp.seg_n;
           col %= grp.seg_n;
         }
-        EpiStoreBox(stage_c, boxes++, p, cmap, col, row0, lane);
+        EpiStoreBox(stage_c, boxes++, p, cmap, col, row0, lane, &push, &push_ready);
       }
       FenceBefore();
       __syncwarp();
@@ -1276,6 +1346,28 @@ int KSplitPair(const GemmArgs& g, int bn) {
   return best;
 }
 
+// Kernel-side push arguments: a 32 x 32 box (64-byte swizzle) tensor map of every member's
+// replicated copy; nothing when g.push.n == 0 or when the schedule cannot push (split-K).
+PushDev MakePushDev(const GemmArgs& g, bool allowed) {
+  PushDev d{};
+  if (!g.push.n) return d;
+  if (!allowed) Fail("internal: GEMM output push with split-K / stream-K / grouped launch");
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int64_t, int64_t>, CUtensorMap> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  d.n = g.push.n;
+  d.row_off = static_cast<int>(g.push.row_off);
+  d.sync = g.push.sync;
+  for (int k = 0; k < g.push.n; ++k) {
+    const auto key = std::make_tuple(static_cast<const void*>(g.push.dst[k]), g.push.rows_full, g.n);
+    auto it = cache.find(key);
+    if (it == cache.end())
+      it = cache.emplace(key, MakeMap(g.push.dst[k], g.n, g.push.rows_full, g.n, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B)).first;
+    d.map[k] = it->second;
+  }
+  return d;
+}
+
 // Stream-K for the CTA-pair kernel (opt-in: RH_GEMM_STREAMK=1): when whole pair tiles leave
 // >= 8% of the pairs idle in the last wave (e.g. 128 tiles on 74 pairs: 1.73 waves run as 2),
 // and every pair still gets >= 16 k-blocks.  Needs the caller's flags and scratch
@@ -1351,7 +1443,7 @@ void LaunchKB(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullptr
   LaunchPdl(GemmTcKernel<BN, kBK, kAK, KB, kG>, grid, kThreads, Cfg::kSmem, s,
       mp.a, mp.b, mp.c, static_cast<int>(g.m), static_cast<int>(n),
       static_cast<int>(g.k), g.epi, ks, ws, kG ? gl->dev : GroupDev{},
-      kG ? nullptr : static_cast<const __nv_bfloat16*>(g.resid));
+      kG ? nullptr : static_cast<const __nv_bfloat16*>(g.resid), MakePushDev(g, ks == 1 && !kG));
   RH_CUDA(cudaGetLastError());
   if (ws) {
     const int64_t n4 = g.m * g.n / 4;
@@ -1414,7 +1506,8 @@ void LaunchPair(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullp
   RH_CUDA(cudaLaunchKernelEx(&cfg, GemmTcPairKernel<BN, kBK, kAK, kG, kEpi>, mp.a, mp.b, mp.c,
                              static_cast<int>(g.m), static_cast<int>(n), static_cast<int>(g.k), g.epi, ks, ws,
                              kG ? gl->dev : GroupDev{}, sk ? g.sk_flags : nullptr,
-                             kG ? nullptr : static_cast<const __nv_bfloat16*>(g.resid)));
+                             kG ? nullptr : static_cast<const __nv_bfloat16*>(g.resid),
+                             MakePushDev(g, ks == 1 && !sk && !kG)));
   if (ws && !sk) {
     const int64_t n4 = g.m * g.n / 4;
     const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, SmCount() * 8)));
@@ -1751,6 +1844,12 @@ const char* GemmTcSchedule(const GemmArgs& g) {
   if (sc.sk) return " [pair, stream-k]";
   if (sc.pair) return sc.ks > 1 ? " [pair, split-k]" : " [pair]";
   return sc.ks > 1 ? " [split-k]" : "";
+}
+
+bool GemmTcPushSupported(const GemmArgs& g) {
+  if (g.dtype != RH_BF16 || !GemmTcSupported(g)) return false;
+  const Sched sc = ScheduleOf(g);
+  return sc.ks == 1 && !sc.sk;
 }
 
 int GemmTcLaunches(const GemmArgs& g) {

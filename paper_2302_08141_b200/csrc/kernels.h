@@ -201,6 +201,17 @@ void LaunchGatherSlices(char* const* src, int world, int me, size_t part, const 
 // C[m,n] = op(A)[m,k] . op(B)[k,n]; A stored [m,k] (ta=0) or [k,m] (ta=1), B stored [k,n]
 // (tb=0) or [n,k] (tb=1); fp32 accumulation; C row-major in `dtype`; optional unary chain
 // applied in the epilogue.
+// The output all-gather of a row-sharded GEMM output, fused into the GEMM's epilogue (executor
+// TryPushMaterialize): every output row r of this rank's C also goes to dst[k] + (row_off + r)
+// * n for each of the n group members k (this rank included), behind a barrier fused into the
+// kernel (block 0 arrives at the start: this rank's copy is free; every epilogue warp waits for
+// all members before its first push).  n = 0: none.
+struct GemmPush {
+  int n;
+  void* dst[kMaxGroup];  // member k's replicated copy: [rows_full, GemmArgs::n] row-major
+  int64_t row_off, rows_full;
+  PeerSync sync;
+};
 struct GemmArgs {
   void* c;
   const void* a;
@@ -220,7 +231,11 @@ struct GemmArgs {
   // (the add op after the GEMM, executor PlanFusion), every kernel and the split-K reduce
   // included.  nullptr: none.
   const void* resid = nullptr;
+  GemmPush push{};
 };
+// A push epilogue is available when the GEMM runs without split-K / stream-K (one kernel writes
+// the final values).
+bool GemmTcPushSupported(const GemmArgs& g);
 constexpr size_t kGemmSkFlagBytes = 4096;
 size_t GemmTf32x3ScratchBytes(const GemmArgs& g);
 // Scratch the tensor-core path wants for this GEMM (3xTF32 splits, or bf16 split-K partials).
