@@ -48,8 +48,6 @@ __device__ __forceinline__ uint32_t PushLdAcquireSys(const uint32_t* p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-// block 0, threads < d: this rank's destination copy is free (every earlier reader of it is
-// done: stream order), signalled into every member's flag row
 // kernel-side form of GemmPush: a 32 x 32 box tensor map of every member's replicated copy
 // (LaunchGemmTc builds them from the pointers); the epilogue's staged output box is stored
 // through each of them right after the local store (bulk NVLink writes to the peers).
@@ -59,33 +57,39 @@ struct PushDev {
   PeerSync sync;
   CUtensorMap map[kMaxGroup];
 };
-__device__ __forceinline__ void PushArrive(const PushDev& p) {
-  if (p.n == 0 || blockIdx.x != 0 || static_cast<int>(threadIdx.x) >= p.sync.d) return;
-  const uint32_t e = *reinterpret_cast<const volatile uint32_t*>(p.sync.epoch);
+// block 0, threads < d: this rank's destination copy is free (every earlier reader of it is
+// done: stream order), signalled into every member's flag row
+__device__ __forceinline__ void SyncArrive(const PeerSync& y) {
+  if (y.d == 0 || blockIdx.x != 0 || static_cast<int>(threadIdx.x) >= y.d) return;
+  const uint32_t e = *reinterpret_cast<const volatile uint32_t*>(y.epoch);
   __threadfence_system();
-  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p.sync.peer_slot[threadIdx.x] + p.sync.me), "r"(e)
-               : "memory");
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(y.peer_slot[threadIdx.x] + y.me), "r"(e) : "memory");
 }
-// one lane: every member arrived (bounded: a missing peer records the error and gives up)
-__device__ __forceinline__ void PushWaitAll(const PushDev& p) {
-  const uint32_t e = *reinterpret_cast<const volatile uint32_t*>(p.sync.epoch);
-  for (int t = 0; t < p.sync.d; ++t) {
-    const uint32_t* f = p.sync.my_slot + p.sync.members[t];
+__device__ __forceinline__ void PushArrive(const PushDev& p) {
+  if (p.n) SyncArrive(p.sync);
+}
+// one thread: every member arrived (bounded: a missing peer records the error and gives up)
+__device__ __forceinline__ void SyncWaitAll(const PeerSync& y) {
+  const uint32_t e = *reinterpret_cast<const volatile uint32_t*>(y.epoch);
+  for (int t = 0; t < y.d; ++t) {
+    const uint32_t* f = y.my_slot + y.members[t];
     if (static_cast<int32_t>(PushLdAcquireSys(f) - e) >= 0) continue;
     uint64_t t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (uint32_t n = 1; static_cast<int32_t>(PushLdAcquireSys(f) - e) < 0; ++n) {
-      if ((n & 1023) == 0 && p.sync.timeout_ns) {
+      if ((n & 1023) == 0 && y.timeout_ns) {
         uint64_t t1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        if (t1 - t0 > p.sync.timeout_ns) {
-          if (p.sync.err) atomicCAS(p.sync.err, 0u, SyncErrorCode(p.sync.me, p.sync.members[t]));
+        if (t1 - t0 > y.timeout_ns) {
+          if (y.err) atomicCAS(y.err, 0u, SyncErrorCode(y.me, y.members[t]));
           break;
         }
       }
     }
   }
 }
+__device__ __forceinline__ void PushWaitAll(const PushDev& p) { SyncWaitAll(p.sync); }
+
 __device__ __forceinline__ uint32_t SmemU32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -226,9 +230,17 @@ __device__ __forceinline__ void TmemLd32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 
 // Split-K finish: sum the fp32 partials in split order, round to bf16, apply the chain.
+// Output push of a split-K GEMM: the reduce writes every final 4-element group into each
+// member's replicated copy too (dst[k] = the copy + this rank's row offset), behind the barrier.
+struct ReducePush {
+  int n;
+  uint2* dst[kMaxGroup];
+  PeerSync sync;
+};
 __global__ void __launch_bounds__(256) SplitReduceBf16(__nv_bfloat16* __restrict__ C, const float4* __restrict__ ws,
                                                        int64_t n4, int splits, ChainArgs epi,
-                                                       const __nv_bfloat16* __restrict__ resid);
+                                                       const __nv_bfloat16* __restrict__ resid,
+                                                       const __grid_constant__ ReducePush rp);
 
 // The packed bf16 ops the lowering lets into a bf16 GEMM epilogue (executor.cpp: relu / neg /
 // identity, and tanh runs = one T^k table lookup; LaunchGemmTc rejects anything else).
@@ -267,9 +279,15 @@ constexpr int kEpiTabBytes = 8192;  // >= kMaxTanhRuns * kTanhRunEntries * 2
 
 __global__ void __launch_bounds__(256) SplitReduceBf16(__nv_bfloat16* __restrict__ C, const float4* __restrict__ ws,
                                                        int64_t n4, int splits, ChainArgs epi,
-                                                       const __nv_bfloat16* __restrict__ resid) {
+                                                       const __nv_bfloat16* __restrict__ resid,
+                                                       const __grid_constant__ ReducePush rp) {
   PdlTrigger();
   PdlWait();
+  if (rp.n) {  // block 0 arrives (this rank's copy is free); every block waits for all members
+    SyncArrive(rp.sync);
+    if (threadIdx.x == 0) SyncWaitAll(rp.sync);
+    __syncthreads();
+  }
   const uint16_t* tabs[kMaxTanhRuns];
 #pragma unroll
   for (int k = 0; k < kMaxTanhRuns; ++k) tabs[k] = epi.tab[k];
@@ -290,6 +308,7 @@ __global__ void __launch_bounds__(256) SplitReduceBf16(__nv_bfloat16* __restrict
       p[1] = AddBf16x2Epi(p[1], r.y);
     }
     reinterpret_cast<uint2*>(C)[i] = make_uint2(p[0], p[1]);
+    for (int k = 0; k < rp.n; ++k) rp.dst[k][i] = make_uint2(p[0], p[1]);
   }
 }
 
@@ -1350,8 +1369,7 @@ int KSplitPair(const GemmArgs& g, int bn) {
 // replicated copy; nothing when g.push.n == 0 or when the schedule cannot push (split-K).
 PushDev MakePushDev(const GemmArgs& g, bool allowed) {
   PushDev d{};
-  if (!g.push.n) return d;
-  if (!allowed) Fail("internal: GEMM output push with split-K / stream-K / grouped launch");
+  if (!g.push.n || !allowed) return d;  // (split-K: the reduce pushes, MakeReducePush)
   static std::mutex mu;
   static std::map<std::tuple<const void*, int64_t, int64_t>, CUtensorMap> cache;
   std::lock_guard<std::mutex> lk(mu);
@@ -1366,6 +1384,16 @@ PushDev MakePushDev(const GemmArgs& g, bool allowed) {
     d.map[k] = it->second;
   }
   return d;
+}
+
+ReducePush MakeReducePush(const GemmArgs& g) {
+  ReducePush r{};
+  if (!g.push.n) return r;
+  r.n = g.push.n;
+  r.sync = g.push.sync;
+  for (int k = 0; k < g.push.n; ++k)
+    r.dst[k] = reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(g.push.dst[k]) + g.push.row_off * g.n);
+  return r;
 }
 
 // Stream-K for the CTA-pair kernel (opt-in: RH_GEMM_STREAMK=1): when whole pair tiles leave
@@ -1449,7 +1477,7 @@ void LaunchKB(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullptr
     const int64_t n4 = g.m * g.n / 4;
     const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, SmCount() * 8)));
     LaunchPdl(SplitReduceBf16, blocks, 256, 0, s, static_cast<__nv_bfloat16*>(g.c), reinterpret_cast<const float4*>(ws),
-              n4, ks, g.epi, static_cast<const __nv_bfloat16*>(g.resid));
+              n4, ks, g.epi, static_cast<const __nv_bfloat16*>(g.resid), MakeReducePush(g));
     RH_CUDA(cudaGetLastError());
   }
 }
@@ -1512,7 +1540,7 @@ void LaunchPair(const GemmArgs& g, cudaStream_t s, const GroupLaunch* gl = nullp
     const int64_t n4 = g.m * g.n / 4;
     const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, SmCount() * 8)));
     LaunchPdl(SplitReduceBf16, blocks, 256, 0, s, static_cast<__nv_bfloat16*>(g.c), reinterpret_cast<const float4*>(ws),
-              n4, ks, g.epi, static_cast<const __nv_bfloat16*>(g.resid));
+              n4, ks, g.epi, static_cast<const __nv_bfloat16*>(g.resid), MakeReducePush(g));
     RH_CUDA(cudaGetLastError());
   }
 }
@@ -1848,8 +1876,7 @@ const char* GemmTcSchedule(const GemmArgs& g) {
 
 bool GemmTcPushSupported(const GemmArgs& g) {
   if (g.dtype != RH_BF16 || !GemmTcSupported(g)) return false;
-  const Sched sc = ScheduleOf(g);
-  return sc.ks == 1 && !sc.sk;
+  return !ScheduleOf(g).sk;  // single pass: the epilogue pushes; split-K: the reduce pushes
 }
 
 int GemmTcLaunches(const GemmArgs& g) {
