@@ -438,7 +438,19 @@ def main():
         # pipelined (rh_program_run_host): every step's H2D and D2H inside the timed region,
         # step i's H2D overlapping step i-1's run and step i-2's D2H (a loop that prefetches)
         D.barrier()
-        e2e_ms = D.max_over_ranks(gp.run_host(max(args.steps, 2), xs, ptrs, [yout.data_ptr()]))
+        # a failed pipelined pass (e.g. a cross-GPU barrier timeout, RH_ERR_TIMEOUT) must not take
+        # the whole line down on some ranks while the others wait in the max-over-ranks: every
+        # rank reports, and the serial end-to-end value stands in (said so in "e2e.note")
+        e2e_note = None
+        try:
+            e2e_local = gp.run_host(max(args.steps, 2), xs, ptrs, [yout.data_ptr()])
+        except Exception as ex:  # noqa: BLE001
+            print(f"[bench] rank {rank}: pipelined end-to-end pass failed: {ex}", file=sys.stderr)
+            e2e_local = float("inf")
+        e2e_ms = D.max_over_ranks(e2e_local)
+        if not math.isfinite(e2e_ms):
+            e2e_ms = e2e_serial_ms
+            e2e_note = "pipelined pass failed on a rank (stderr); the serial end-to-end value is reported"
 
         pk = peaks()
         clk_sum = clk.summary()
@@ -526,6 +538,7 @@ def main():
                     "inputs": "replicated inputs: 1/world slice per process over PCIe + NVLink all-gather "
                               "(gather stream, overlapping the previous step's run)"
                               if any(scattered(x) for x in xs) else "every process copies its inputs whole",
+                    "note": e2e_note,
                     "serial": {"value": tok / (e2e_serial_ms * 1e-3), "ms_per_step": e2e_serial_ms,
                                "api": "rh_program_step_host (H2D, run, D2H back to back)"}},
             "gpu_launches": launches,

@@ -325,6 +325,10 @@ struct PushPlan {
   int dst_t = -1;  // the replicated copy every member's kernel writes into
   int axis = 0, slot = -1;
   int64_t rows_local = 0;
+  // reduce-scatter form (TryPushReduceScatter): partial tiles go to their owner's staging
+  int scatter_dim = -1;
+  int64_t part = 0;
+  size_t stage_off = 0, slot_bytes = 0;
 };
 
 class Lowerer {
@@ -1427,6 +1431,78 @@ class Lowerer {
     AddStep(std::move(st));
     return true;
   }
+  // Reduce-scatter of a GEMM's Partial output fused into the GEMM (dist runs): a bf16 tcgen05
+  // GEMM without split-K whose output goes Partial -> Shard(t, s) with one contiguous block per
+  // rank (t = 0 or 1) on one axis (the others replicated) stores each partial output box, from
+  // its epilogue, into the box owner's staging slot for this rank (TMA bulk stores over NVLink,
+  // behind a barrier fused into the GEMM).  The transition becomes a local rank-order sum of
+  // the d slots behind the usual fused barrier (every member's pushes landed): the same fp32
+  // rank-order reduction and single bf16 rounding as the pull-sum, so bit-identical.
+  // RH_NO_PUSH_REDUCE_SCATTER disables.
+  bool TryPushReduceScatter(int src, int dst, int axis, const Specs& to_specs, const char* why) {
+    static const bool off = getenv("RH_NO_PUSH_REDUCE_SCATTER") != nullptr;
+    if (off || !rt_->dist || rt_->world <= 1 || p_->pipeline_axis >= 0 || (p_->flags & RH_FLAG_TRANSPORT_NCCL))
+      return false;
+    const Tensor X = p_->tensors[src];
+    const Tensor Y = p_->tensors[dst];
+    const int d = mesh_[axis];
+    if (X.dtype != RH_BF16 || X.ldims.size() != 2 || d > kMaxGroup) return false;
+    if (X.specs[axis].kind != RH_PARTIAL || to_specs[axis].kind != RH_SHARD) return false;
+    for (int a = 0; a < p_->n_axes; ++a)
+      if (a != axis && (X.specs[a].kind != RH_REPLICATED || to_specs[a].kind != RH_REPLICATED)) return false;
+    const int t = to_specs[axis].dim;
+    if (t < 0 || t > 1 || to_specs[axis].stride * d != X.ldims[t]) return false;
+    const int64_t part = X.ldims[t] / d;
+    if (part % 32 || X.ldims[1 - t] % 32) return false;
+    auto it = gemm_push_.find(X.op);
+    if (it == gemm_push_.end() || p_->out_tensor[X.op] != src) return false;
+    PushPlan& pp = *it->second.plan;
+    if (pp.dst_t >= 0 || pp.scatter_dim >= 0) return false;
+    const GemmArgs& g = it->second.g;
+    if (!GemmTcPushSupported(g, /*single_pass=*/true) || g.m != X.ldims[0] || g.n != X.ldims[1]) return false;
+    pp.scatter_dim = t;
+    pp.part = part;
+    pp.axis = axis;
+    pp.slot = p_->n_sync_slots++;
+    pp.slot_bytes = static_cast<size_t>(Prod(X.ldims)) / d * ElemBytes(X.dtype);
+    pp.stage_off = Alloc(pp.slot_bytes * d);
+    p_->steps[it->second.step].name += " [+reduce_scatter push]";
+    // the transition: sum of the d staged slots (local memory) in rank order into Y
+    Step st;
+    st.kind = Step::kTransition;
+    st.axis = axis;
+    st.p2p = true;
+    st.no_async = true;
+    st.post_mode = 2;  // peers rewrite this rank's staging only after its next GEMM's barrier
+    if (rt_->dist && rt_->world > 1) st.sync_slot = p_->n_sync_slots++;
+    st.name = std::string("reduce_scatter op") + std::to_string(X.op) + " P->" + SpecStr(to_specs[axis]) + "@" +
+              std::to_string(axis) + " (" + why + ") [pushed by the GEMM; local sum]";
+    st.alg_bytes = static_cast<double>(Y.elems()) * ElemBytes(X.dtype) * (d + 1);
+    st.launches = 1;
+    rh_program* P = p_;
+    const Dims YD = Y.ldims;
+    const rh_spec rp{RH_PARTIAL, -1, 0}, rr = Rep();
+    const AxisView pv = MakeAxisView(rp, static_cast<int>(YD.size()), YD.data(), d);
+    const AxisView rv = MakeAxisView(rr, static_cast<int>(YD.size()), YD.data(), d);
+    const size_t soff = pp.stage_off, sb = pp.slot_bytes;
+    const int dtype = X.dtype;
+    st.pulls.push_back([P, dst, axis, soff, sb, pv, rv, dtype, d](int li) {
+      const int g2 = P->mesh->rt->first_rank + li;
+      PullArgs a{};
+      a.dst = P->Ptr(P->tensors[dst], g2);
+      for (int k = 0; k < d; ++k) a.src[k] = P->peer_base[g2] + soff + static_cast<size_t>(k) * sb;  // local slots
+      a.from = pv;
+      a.to = rv;
+      a.coord = P->mesh->Coords(g2)[axis];
+      a.n_dst = P->tensors[dst].elems();
+      a.dtype = dtype;
+      return a;
+    });
+    st.reads = {};
+    st.writes = {dst};
+    AddStep(std::move(st));
+    return true;
+  }
   struct GemmPushRef {
     std::shared_ptr<PushPlan> plan;
     GemmArgs g;
@@ -2238,6 +2314,14 @@ class Lowerer {
             for (int k = 0; k < a.push.n; ++k) a.push.dst[k] = P->Ptr(P->tensors[pp->dst_t], a.push.sync.members[k]);
             a.push.row_off = P->mesh->Coords(r)[pp->axis] * pp->rows_local;
             a.push.rows_full = P->tensors[pp->dst_t].gdims[0];
+          } else if (pp->scatter_dim >= 0) {  // the reduce-scatter, fused (TryPushReduceScatter)
+            a.push.sync = SyncOf(P, pp->axis, pp->slot, li);
+            a.push.n = a.push.sync.d;
+            const int64_t me = P->mesh->Coords(r)[pp->axis];
+            for (int k = 0; k < a.push.n; ++k)
+              a.push.dst[k] = P->peer_base[a.push.sync.members[k]] + pp->stage_off + me * pp->slot_bytes;
+            a.push.scatter_dim = pp->scatter_dim;
+            a.push.part = pp->part;
           }
           a.epi = Patch(P, g.epi, r);
           if (P->gemm_scratch_bytes) a.scratch = P->peer_base[r] + P->gemm_scratch_off;
@@ -2688,6 +2772,7 @@ class Lowerer {
     const AxisView tv = MakeAxisView(to, static_cast<int>(D.size()), D.data(), d);
     const int eb = ElemBytes(X.dtype);
     const double S = static_cast<double>(Prod(D)) * eb;
+    if (TryPushReduceScatter(src, dst, axis, to_specs, why)) return dst;
     {
       static const bool no_fine = getenv("RH_NO_FINE") != nullptr;  // A/B knob (profiles/)
       const bool nccl_t = (p_->flags & RH_FLAG_TRANSPORT_NCCL) && rt_->dist;

@@ -54,6 +54,7 @@ __device__ __forceinline__ uint32_t PushLdAcquireSys(const uint32_t* p) {
 struct PushDev {
   int n;
   int row_off;
+  int scatter_dim, part;  // scatter_dim >= 0: one owner per box (GemmPush)
   PeerSync sync;
   CUtensorMap map[kMaxGroup];
 };
@@ -176,7 +177,15 @@ __device__ __forceinline__ void EpiStoreBox(uint8_t* stage, uint32_t cnt, const 
         PushWaitAll(*push);
         *push_ready = true;
       }
-      for (int k = 0; k < push->n; ++k) TmaStore2D(&push->map[k], sb, c0, c1 + push->row_off);
+      if (push->scatter_dim == 1) {
+        const int k = c0 / push->part;
+        TmaStore2D(&push->map[k], sb, c0 - k * push->part, c1);
+      } else if (push->scatter_dim == 0) {
+        const int k = c1 / push->part;
+        TmaStore2D(&push->map[k], sb, c0, c1 - k * push->part);
+      } else {
+        for (int k = 0; k < push->n; ++k) TmaStore2D(&push->map[k], sb, c0, c1 + push->row_off);
+      }
     }
     BulkCommit();
   }
@@ -1375,12 +1384,17 @@ PushDev MakePushDev(const GemmArgs& g, bool allowed) {
   std::lock_guard<std::mutex> lk(mu);
   d.n = g.push.n;
   d.row_off = static_cast<int>(g.push.row_off);
+  d.scatter_dim = g.push.scatter_dim;
+  d.part = static_cast<int>(g.push.part);
   d.sync = g.push.sync;
+  // destination [rows, cols]: the replicated copy, or the owner's slot of its staging
+  const int64_t cols = g.push.scatter_dim == 1 ? g.push.part : g.n;
+  const int64_t rows = g.push.scatter_dim == 0 ? g.push.part : g.push.scatter_dim == 1 ? g.m : g.push.rows_full;
   for (int k = 0; k < g.push.n; ++k) {
-    const auto key = std::make_tuple(static_cast<const void*>(g.push.dst[k]), g.push.rows_full, g.n);
+    const auto key = std::make_tuple(static_cast<const void*>(g.push.dst[k]), rows, cols);
     auto it = cache.find(key);
     if (it == cache.end())
-      it = cache.emplace(key, MakeMap(g.push.dst[k], g.n, g.push.rows_full, g.n, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B)).first;
+      it = cache.emplace(key, MakeMap(g.push.dst[k], cols, rows, cols, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B)).first;
     d.map[k] = it->second;
   }
   return d;
@@ -1389,6 +1403,7 @@ PushDev MakePushDev(const GemmArgs& g, bool allowed) {
 ReducePush MakeReducePush(const GemmArgs& g) {
   ReducePush r{};
   if (!g.push.n) return r;
+  if (g.push.scatter_dim >= 0) Fail("internal: scatter push from a split-K reduce");
   r.n = g.push.n;
   r.sync = g.push.sync;
   for (int k = 0; k < g.push.n; ++k)
@@ -1874,9 +1889,11 @@ const char* GemmTcSchedule(const GemmArgs& g) {
   return sc.ks > 1 ? " [split-k]" : "";
 }
 
-bool GemmTcPushSupported(const GemmArgs& g) {
+bool GemmTcPushSupported(const GemmArgs& g, bool single_pass) {
   if (g.dtype != RH_BF16 || !GemmTcSupported(g)) return false;
-  return !ScheduleOf(g).sk;  // single pass: the epilogue pushes; split-K: the reduce pushes
+  const Sched sc = ScheduleOf(g);
+  if (sc.sk) return false;
+  return !single_pass || sc.ks == 1;  // single pass: the epilogue pushes; split-K: the reduce
 }
 
 int GemmTcLaunches(const GemmArgs& g) {

@@ -211,6 +211,11 @@ struct GemmPush {
   void* dst[kMaxGroup];  // member k's replicated copy: [rows_full, GemmArgs::n] row-major
   int64_t row_off, rows_full;
   PeerSync sync;
+  // scatter_dim >= 0 (the reduce-scatter of a Partial output, executor TryPushReduceScatter):
+  // output box (row, col) goes only to its owner k = (scatter_dim ? col : row) / part, into
+  // dst[k] = this rank's slot of k's staging, [m, part] (dim 1) or [part, n] (dim 0).
+  int scatter_dim = -1;
+  int64_t part = 0;
 };
 struct GemmArgs {
   void* c;
@@ -235,7 +240,7 @@ struct GemmArgs {
 };
 // A push epilogue is available when the GEMM runs without split-K / stream-K (one kernel writes
 // the final values).
-bool GemmTcPushSupported(const GemmArgs& g);
+bool GemmTcPushSupported(const GemmArgs& g, bool single_pass = false);
 constexpr size_t kGemmSkFlagBytes = 4096;
 size_t GemmTf32x3ScratchBytes(const GemmArgs& g);
 // Scratch the tensor-core path wants for this GEMM (3xTF32 splits, or bf16 split-K partials).
