@@ -1438,9 +1438,14 @@ class Lowerer {
   // behind a barrier fused into the GEMM).  The transition becomes a local rank-order sum of
   // the d slots behind the usual fused barrier (every member's pushes landed): the same fp32
   // rank-order reduction and single bf16 rounding as the pull-sum, so bit-identical.
-  // RH_NO_PUSH_REDUCE_SCATTER disables.
+  // Opt-in (RH_PUSH_REDUCE_SCATTER=1): the fused form runs on the main stream, so in programs
+  // whose reduce-scatters PlanAsync overlaps with compute (C5's backward at N=2/4) it lost more
+  // than it saved (16.45 -> 18.87 ms); on C3 it saved 2 us at N=4.
   bool TryPushReduceScatter(int src, int dst, int axis, const Specs& to_specs, const char* why) {
-    static const bool off = getenv("RH_NO_PUSH_REDUCE_SCATTER") != nullptr;
+    static const bool off = [] {
+      const char* e = getenv("RH_PUSH_REDUCE_SCATTER");
+      return !(e && e[0] == '1');
+    }();
     if (off || !rt_->dist || rt_->world <= 1 || p_->pipeline_axis >= 0 || (p_->flags & RH_FLAG_TRANSPORT_NCCL))
       return false;
     const Tensor X = p_->tensors[src];
