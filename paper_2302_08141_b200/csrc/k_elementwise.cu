@@ -142,17 +142,35 @@ __global__ void __launch_bounds__(256) UnaryChainKernel(void* out, const void* i
   }
   PdlWait();  // the tables are program constants; inputs come from the previous kernel
   const int64_t nv = n / E;
-  const int64_t npair = nv / 2;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npair; i += stride) {
-    const uint4 u0 = reinterpret_cast<const uint4*>(in)[2 * i];
-    const uint4 u1 = reinterpret_cast<const uint4*>(in)[2 * i + 1];
-    if constexpr (kBf16) {
-      uint32_t p[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
-      ApplyChainPackedBf16<8>(c.fns, c.n_fn, p, tab);
-      reinterpret_cast<uint4*>(out)[2 * i] = make_uint4(p[0], p[1], p[2], p[3]);
-      reinterpret_cast<uint4*>(out)[2 * i + 1] = make_uint4(p[4], p[5], p[6], p[7]);
-    } else {
+  if constexpr (kBf16) {
+    // four 16-byte vectors per thread in flight (vectors i + q * stride: every load instruction
+    // coalesced); the persistent-ish grid otherwise keeps too few bytes in flight to cover HBM
+    // latency (one C3 step's 1-lookup chain ran at 2.2 TB/s)
+    int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    for (; i + 3 * stride < nv; i += 4 * stride) {
+      uint4 u[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) u[q] = reinterpret_cast<const uint4*>(in)[i + q * stride];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t p[4] = {u[q].x, u[q].y, u[q].z, u[q].w};
+        ApplyChainPackedBf16<4>(c.fns, c.n_fn, p, tab);
+        reinterpret_cast<uint4*>(out)[i + q * stride] = make_uint4(p[0], p[1], p[2], p[3]);
+      }
+    }
+    for (; i < nv; i += stride) {
+      const uint4 u0 = reinterpret_cast<const uint4*>(in)[i];
+      uint32_t p[4] = {u0.x, u0.y, u0.z, u0.w};
+      ApplyChainPackedBf16<4>(c.fns, c.n_fn, p, tab);
+      reinterpret_cast<uint4*>(out)[i] = make_uint4(p[0], p[1], p[2], p[3]);
+    }
+  }
+  const int64_t npair = nv / 2;
+  if constexpr (!kBf16) {  // fp32: two 16-byte packets per thread-iteration
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < npair; i += stride) {
+      const uint4 u0 = reinterpret_cast<const uint4*>(in)[2 * i];
+      const uint4 u1 = reinterpret_cast<const uint4*>(in)[2 * i + 1];
       float v[8] = {__uint_as_float(u0.x), __uint_as_float(u0.y), __uint_as_float(u0.z),
                     __uint_as_float(u0.w), __uint_as_float(u1.x), __uint_as_float(u1.y),
                     __uint_as_float(u1.z), __uint_as_float(u1.w)};
@@ -161,7 +179,8 @@ __global__ void __launch_bounds__(256) UnaryChainKernel(void* out, const void* i
       reinterpret_cast<float4*>(out)[2 * i + 1] = make_float4(v[4], v[5], v[6], v[7]);
     }
   }
-  for (int64_t i = npair * 2 * E + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
+  const int64_t done = kBf16 ? nv * E : npair * 2 * E;  // elements the vector loops covered
+  for (int64_t i = done + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
     if constexpr (kBf16) {
       uint32_t p[1] = {static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(in)[i])};
       ApplyChainPackedBf16<1>(c.fns, c.n_fn, p, tab);
